@@ -1,0 +1,195 @@
+/*
+ * ilans_b200.h -- C ABI of the B200-native interleaved-rANS (word16) codec.
+ *
+ * Plain pointers and sizes only; no C++ exceptions and no torch types cross
+ * this boundary. Every entry point returns an ilans_rc (0 = ILANS_OK) and,
+ * where the reference raises, fills an ilans_status with the error kind so
+ * the Python host layer can raise the reference's exception types
+ * (pkg/src/ilans/errors.py:4-33).
+ *
+ * Two families:
+ *  1. HOST-BUFFER DROP-INS for the reference kernel boundary
+ *     (pkg/src/ilans/backend.py:16-21 -> pkg/src/ilans/_core.pyx). Same
+ *     argument meaning as the Cython functions; inputs are host arrays, the
+ *     library copies them to HBM, runs the sm_100a kernels and copies back.
+ *  2. DEVICE-POINTER, STREAM-ORDERED entry points for the chunked,
+ *     HBM-resident pipeline (histogram -> quantize/table -> chunked encode ->
+ *     framing; chunked decode). All `d_*` pointers are device memory; the
+ *     `stream` argument is a cudaStream_t (NULL = legacy default stream).
+ *     They launch asynchronously and never synchronize.
+ *
+ * Word16 only (WORD16 = 16-bit digits, L = 2^16, rans.py:87): states are
+ * u32 in [2^16, 2^32), scale_bits in [1, 16], alphabet <= 256.
+ */
+#ifndef ILANS_B200_H
+#define ILANS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ILANS_B200_ABI_VERSION 1
+
+typedef enum ilans_rc {
+    ILANS_OK = 0,
+    ILANS_ERR_VALUE = 1,        /* ValueError (bad argument)                  */
+    ILANS_ERR_UNENCODABLE = 2,  /* UnencodableSymbolError (f == 0)            */
+    ILANS_ERR_TRUNCATED = 3,    /* TruncatedStreamError (payload exhausted)   */
+    ILANS_ERR_UNSUPPORTED = 4,  /* UnsupportedVariantError                    */
+    ILANS_ERR_CUDA = 5,         /* CUDA runtime failure / no device           */
+} ilans_rc;
+
+typedef struct ilans_status {
+    int32_t code;       /* ilans_rc of the failure, ILANS_OK otherwise           */
+    int32_t cuda_error; /* cudaError_t when code == ILANS_ERR_CUDA               */
+    int64_t stream;     /* chunk/stream index of the first failing stream, or -1 */
+    int64_t index;      /* message index of the offending symbol, or -1          */
+    int32_t symbol;     /* offending symbol value (unencodable), or -1           */
+    int32_t reserved;
+    int64_t consumed;   /* words consumed (single-stream decode)                 */
+    char message[128];  /* human-readable detail                                 */
+} ilans_status;
+
+/* -------------------------------------------------------------------------
+ * Library / device
+ * ---------------------------------------------------------------------- */
+int ilans_abi_version(void);
+/* Number of visible CUDA devices (0 when none); never fails. */
+int ilans_device_count(void);
+/* Select the device subsequent host-buffer calls run on (per host thread). */
+int ilans_set_device(int device, ilans_status *st);
+/* Number of kernel launches issued by this library since load (counter used
+ * by bench.py's gpu_launches evidence). */
+uint64_t ilans_launch_count(void);
+
+/* -------------------------------------------------------------------------
+ * 1. Host-buffer drop-ins (reference: pkg/src/ilans/_core.pyx)
+ * ---------------------------------------------------------------------- */
+
+/* Replaces _core.encode_interleaved_u16(msg, freq, cum, scale_bits, n_lanes)
+ * (_core.pyx:14-43; contract _pure.py:15-39). freq/cum have n_freq and
+ * n_freq+1 entries; symbols >= n_freq have frequency 0. payload_out must
+ * hold n words; on success words [0, *payload_words) are the payload in
+ * decoder read order and states_out[0, n_lanes) the final lane states.
+ * n_lanes in [1, 65535]. Errors: ILANS_ERR_UNENCODABLE (f == 0, reported
+ * for the highest message index, matching the reference's backward walk). */
+int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const uint32_t *freq,
+                                 int32_t n_freq, const uint32_t *cum, int32_t scale_bits,
+                                 int32_t n_lanes, uint16_t *payload_out,
+                                 int64_t *payload_words, uint32_t *states_out,
+                                 ilans_status *st);
+
+/* Replaces _core.decode_interleaved_u16(payload, states, slot_sym, freq, cum,
+ * scale_bits, msg_len, n_lanes) (_core.pyx:46-127; _pure.py:42-66).
+ * slot_sym has n_slots >= 2^scale_bits entries. Writes msg_len bytes to out
+ * and the number of payload words read to *consumed. n_lanes in
+ * [1, 65535]. Errors: ILANS_ERR_TRUNCATED. */
+int ilans_decode_interleaved_u16(const uint16_t *payload, int64_t pay_len,
+                                 const uint32_t *states, const uint8_t *slot_sym,
+                                 int64_t n_slots, const uint32_t *freq, const uint32_t *cum,
+                                 int32_t n_freq, int32_t scale_bits, int64_t msg_len,
+                                 int32_t n_lanes, uint8_t *out, int64_t *consumed,
+                                 ilans_status *st);
+
+/* Replaces _core.decode_lanes_u16 (_core.pyx:130-173; _pure.py:69-101):
+ * same signature and byte-identical results; rejects n_lanes > 32 with
+ * ILANS_ERR_VALUE (the reference's ValueError, _core.pyx:144-145). */
+int ilans_decode_lanes_u16(const uint16_t *payload, int64_t pay_len, const uint32_t *states,
+                           const uint8_t *slot_sym, int64_t n_slots, const uint32_t *freq,
+                           const uint32_t *cum, int32_t n_freq, int32_t scale_bits,
+                           int64_t msg_len, int32_t n_lanes, uint8_t *out,
+                           int64_t *consumed, ilans_status *st);
+
+/* Replaces rans.quantize(counts, scale_bits) (rans.py:171-211), computed on
+ * the device. counts has n <= 256 entries; freq_out receives n entries.
+ * Errors (ILANS_ERR_VALUE, with the reference's message): scale_bits not in
+ * [1,16]; n > 256; all counts zero; more present symbols than 2^scale_bits. */
+int ilans_quantize(const uint64_t *counts, int32_t n, int32_t scale_bits, uint32_t *freq_out,
+                   ilans_status *st);
+
+/* Replaces np.bincount(msg, minlength=256) at the model-building call sites
+ * (cli.py:31-37, bench.py:47-51). counts_out has 256 entries; *alphabet =
+ * max symbol + 1 (0 for an empty message). */
+int ilans_histogram_u8(const uint8_t *msg, int64_t n, uint64_t *counts_out, int32_t *alphabet,
+                       ilans_status *st);
+
+/* -------------------------------------------------------------------------
+ * 2. Device-pointer, stream-ordered pipeline (chunk framing)
+ *
+ * A "table" is an opaque device blob of ilans_table_bytes() bytes holding
+ * freq/cum, the encoder's per-symbol reciprocals and the decoder's slot
+ * lookup. A "status" is an opaque device blob of ilans_dstatus_bytes().
+ * Chunk k of an n-byte message covers bytes [k*C, min((k+1)*C, n)) and is an
+ * independent N-lane stream (N <= 32): its payload and final states equal
+ * the reference encode_interleaved(msg[kC:(k+1)C], table, N, WORD16).
+ * ---------------------------------------------------------------------- */
+size_t ilans_table_bytes(void);
+size_t ilans_dstatus_bytes(void);
+
+/* Zero d_counts[256] (u64) on `stream`. */
+int ilans_counts_zero_dev(uint64_t *d_counts, void *stream);
+/* d_counts[b] += #{i : d_msg[i] == b}. Accumulates (call counts_zero first),
+ * so shards/batches can share one histogram. */
+int ilans_histogram_u8_dev(const uint8_t *d_msg, int64_t n, uint64_t *d_counts, void *stream);
+/* Model build: alphabet = highest nonzero bin + 1 (an all-zero histogram
+ * maps to counts [1,1], cli.py:32-34), quantize (bit-exact rans.quantize)
+ * and all lookup tables, into d_table. Validation errors are recorded in the
+ * table blob; read them with ilans_table_read_host. */
+int ilans_table_from_counts_dev(const uint64_t *d_counts, int32_t scale_bits, void *d_table,
+                                void *stream);
+/* Build a table from given frequencies (device pointer, n_freq entries). */
+int ilans_table_from_freq_dev(const uint32_t *d_freq, int32_t n_freq, int32_t scale_bits,
+                              void *d_table, void *stream);
+/* Copy the table header back (synchronizes `stream`): status, alphabet and
+ * the quantized frequencies (freq_out: 256 entries, may be NULL). */
+int ilans_table_read_host(const void *d_table, int32_t *alphabet, int32_t *scale_bits,
+                          uint32_t *freq_out, void *stream, ilans_status *st);
+
+/* Reset a device status blob to "no error". */
+int ilans_dstatus_reset_dev(void *d_status, void *stream);
+/* Read a device status blob (synchronizes `stream`). */
+int ilans_dstatus_read_host(const void *d_status, void *stream, ilans_status *st);
+
+/* Chunked encode. d_scratch holds n words (chunk k uses words
+ * [k*C, k*C + len_k), filled from the end); d_chunk_words[k] receives the
+ * payload length of chunk k and d_states[k*N + l] its final lane states.
+ * C must be a positive multiple of 16. */
+int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
+                            int32_t n_lanes, const void *d_table, uint16_t *d_scratch,
+                            uint32_t *d_chunk_words, uint32_t *d_states, void *d_status,
+                            void *stream);
+/* Framing: d_word_offsets[0..n_chunks] = exclusive prefix sum of chunk
+ * words, and the chunk payloads packed back to back into d_payload
+ * (capacity n words). */
+int ilans_frame_chunks_dev(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
+                           const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
+                           uint16_t *d_payload, void *stream);
+/* Chunked decode of a framed stream: d_out receives n bytes, d_consumed[k]
+ * the words chunk k consumed (== its payload length on valid input), and
+ * d_final_states (optional, n_chunks*N) the lane states after decoding.
+ * scale_bits must equal the table's (the launch is sized on the host without
+ * a device round trip; a mismatch is recorded in d_status as a value error).
+ * Truncation is recorded in d_status. Reads of d_payload are 16-byte
+ * granular and never pass d_payload + d_word_offsets[n_chunks] rounded up to
+ * 16 bytes. */
+int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t *d_word_offsets,
+                            const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                            int32_t n_lanes, const void *d_table, int32_t scale_bits,
+                            uint8_t *d_out,
+                            uint64_t *d_consumed, uint32_t *d_final_states, void *d_status,
+                            void *stream);
+
+/* Deterministic synthetic source used by the benches: byte i is
+ * the inverse-CDF of a counter-based hash, u = splitmix64(seed ^ i) >> 32,
+ * against d_cdf[256] (u32, non-decreasing, last entry is treated as 2^32).
+ * Symbol = #{k : d_cdf[k] <= u}, clamped to 255. */
+int ilans_synth_bytes_dev(uint8_t *d_out, int64_t n, uint64_t seed, int64_t first_index,
+                          const uint32_t *d_cdf, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ILANS_B200_H */

@@ -1,0 +1,129 @@
+"""Kernel backend: the drop-in for the reference plugin boundary.
+
+Reference: pkg/src/ilans/backend.py:16-78 -- a frozen ``Backend`` with the
+three word16 kernel callables, resolved by ``get(name)`` with the default
+chosen by ``ILANS_BACKEND``. Here there is exactly one backend, "b200",
+whose callables have the reference signatures (_core.pyx:14, :46-47,
+:130-131) and run on the B200 through libilans_b200.so. "ext" resolves to
+it too (it is the compiled backend); the reference's pure-Python backend is
+not shipped -- its behaviour is the test oracle (oracle/), never a runtime
+fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import warnings
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class Backend:
+    name: str
+    encode_interleaved_u16: Callable
+    decode_interleaved_u16: Callable
+    decode_lanes_u16: Callable
+
+
+def _u32(a):
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def encode_interleaved_u16(msg, freq, cum, scale_bits: int, n_lanes: int):
+    """Backward interleaved encode on the B200. Returns (payload u16 array in
+    decoder read order, final lane states u32 array) -- contract of
+    _pure.encode_interleaved_u16 (_pure.py:15-39)."""
+    m = np.ascontiguousarray(msg, dtype=np.uint8)
+    f = _u32(freq)
+    c = _u32(cum)
+    if len(c) < len(f) + 1:
+        raise ValueError("cum must have len(freq) + 1 entries")
+    payload = np.empty(max(1, len(m)), dtype=np.uint16)
+    states = np.empty(n_lanes, dtype=np.uint32) if n_lanes > 0 else np.empty(0, np.uint32)
+    words = ctypes.c_int64(0)
+    st = _lib.Status()
+    rc = _lib.lib.ilans_encode_interleaved_u16(
+        _lib.ptr(m), len(m), _lib.ptr(f), len(f), _lib.ptr(c), int(scale_bits), int(n_lanes),
+        _lib.ptr(payload), ctypes.byref(words), _lib.ptr(states), ctypes.byref(st))
+    _lib.raise_for(rc, st, "encode_interleaved_u16")
+    return payload[: words.value].copy(), states
+
+
+def _decode(fn, payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):
+    pay = np.ascontiguousarray(payload, dtype=np.uint16)
+    xs = np.array(states, dtype=np.uint32)  # copied: inputs are never mutated
+    slot = np.ascontiguousarray(slot_sym, dtype=np.uint8)
+    f = _u32(freq)
+    c = _u32(cum)
+    if len(c) < len(f) + 1:
+        raise ValueError("cum must have len(freq) + 1 entries")
+    if len(xs) < n_lanes:
+        raise ValueError("one state per lane required")
+    out = np.empty(max(1, msg_len), dtype=np.uint8)
+    consumed = ctypes.c_int64(0)
+    st = _lib.Status()
+    rc = fn(_lib.ptr(pay), len(pay), _lib.ptr(xs), _lib.ptr(slot), len(slot), _lib.ptr(f),
+            _lib.ptr(c), len(f), int(scale_bits), int(msg_len), int(n_lanes), _lib.ptr(out),
+            ctypes.byref(consumed), ctypes.byref(st))
+    _lib.raise_for(rc, st, "decode")
+    return out[:msg_len], int(consumed.value)
+
+
+_dec_serial = _lib.lib.ilans_decode_interleaved_u16
+_dec_lanes = _lib.lib.ilans_decode_lanes_u16
+
+
+def decode_interleaved_u16(payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):
+    """Forward interleaved decode on the B200. Returns (message u8 array,
+    words read) -- contract of _pure.decode_interleaved_u16 (_pure.py:42-66)."""
+    return _decode(_dec_serial, payload, states, slot_sym, freq, cum, scale_bits, msg_len,
+                   n_lanes)
+
+
+def decode_lanes_u16(payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):
+    """Group-at-a-time lane decode on the B200; byte-identical to
+    decode_interleaved_u16 (_pure.py:69-101). At most 32 lanes."""
+    if n_lanes > 32:
+        raise ValueError("at most 32 lanes")
+    return _decode(_dec_lanes, payload, states, slot_sym, freq, cum, scale_bits, msg_len,
+                   n_lanes)
+
+
+B200 = Backend("b200", encode_interleaved_u16, decode_interleaved_u16, decode_lanes_u16)
+EXT = B200  # the compiled backend, under the reference's name for it
+PURE = None  # not shipped: the pure-Python kernels are the test oracle
+
+
+def _pick_default() -> Backend:
+    forced = os.environ.get("ILANS_BACKEND", "").strip().lower()
+    if forced in ("", "b200", "ext", "auto"):
+        return B200
+    warnings.warn(
+        f"ILANS_BACKEND={forced!r} is not available in ilans-b200; using 'b200'",
+        RuntimeWarning,
+    )
+    return B200
+
+
+ACTIVE = _pick_default()
+
+
+def get(name: str | None = None) -> Backend:
+    """Resolve a backend by name; None / "auto" mean the import-time default."""
+    if name is None or name == "auto":
+        return ACTIVE
+    if name in ("b200", "ext"):
+        return B200
+    if name == "pure":
+        raise ValueError("the pure-Python backend is not part of ilans-b200 (no CPU fallback)")
+    raise ValueError(f"unknown backend {name!r}")
+
+
+def available() -> list[str]:
+    return ["b200"]

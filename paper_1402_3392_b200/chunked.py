@@ -1,0 +1,335 @@
+"""Chunk framing and the HBM-resident codec pipeline.
+
+A message is cut into fixed-size chunks (boundaries depend only on the
+chunk length, never on the GPU count); chunk k is an independent N-lane
+word16 stream under ONE global table, so its payload and final states are
+exactly the reference's ``encode_interleaved(msg[kC:(k+1)C], table, N,
+WORD16)`` and it re-wraps as a standalone IEC1 ``Container``
+(``ChunkedContainer.chunk(k)``).
+
+``DeviceCodec`` keeps everything in HBM: histogram -> (optional NCCL
+all-reduce) -> quantize + tables -> one encode launch over all chunks ->
+framing (offset scan + payload compaction); decode is one launch over all
+chunks. Torch provides device memory and the stream; all compute is
+libilans_b200.so.
+
+ICH1 wire format (little-endian), the on-disk form of a chunked stream:
+
+    0   4      magic "ICH1"
+    4   1      version (1)
+    5   1      variant (1 = word16)
+    6   2      lane_count N (u16)
+    8   8      message_length (u64)
+    16  8      chunk_len C (u64)
+    24  3+2n   table (rans.serialize_table)
+    -   4K     payload words per chunk (u32), K = ceil(len / C)
+    -   4KN    final lane states, chunk-major (u32)
+    -   rest   payloads back to back (u16 LE)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, rans
+from .errors import FormatError, TruncatedStreamError
+from .interleave import Container, _as_symbols
+from .rans import WORD16, SymbolTable
+
+CHUNK_MAGIC = b"ICH1"
+DEFAULT_CHUNK = 64 * 1024
+
+__all__ = ["ChunkedContainer", "DeviceCodec", "encode_chunked", "decode_chunked"]
+
+
+def n_chunks_for(n: int, chunk_len: int) -> int:
+    return 0 if n == 0 else -(-n // chunk_len)
+
+
+def _check_chunking(chunk_len: int, lane_count: int) -> None:
+    if chunk_len <= 0 or chunk_len % 16:
+        raise ValueError("chunk_len must be a positive multiple of 16")
+    if not 1 <= lane_count <= 32:
+        raise ValueError("chunked streams use 1..32 lanes (one warp per chunk)")
+
+
+@dataclass
+class ChunkedContainer:
+    lane_count: int
+    chunk_len: int
+    message_length: int
+    table: SymbolTable
+    states: np.ndarray        # u32 [n_chunks, N]
+    word_offsets: np.ndarray  # u64 [n_chunks + 1]
+    payload: np.ndarray       # u16 [word_offsets[-1]]
+
+    @property
+    def n_chunks(self) -> int:
+        return n_chunks_for(self.message_length, self.chunk_len)
+
+    def chunk_length(self, k: int) -> int:
+        return min(self.chunk_len, self.message_length - k * self.chunk_len)
+
+    def chunk(self, k: int) -> Container:
+        """Chunk k as a standalone IEC1 container (reference-decodable)."""
+        a, b = int(self.word_offsets[k]), int(self.word_offsets[k + 1])
+        return Container(WORD16, self.lane_count, self.chunk_length(k), self.table,
+                         tuple(int(x) for x in self.states[k]), self.payload[a:b].copy())
+
+    def to_bytes(self) -> bytes:
+        head = CHUNK_MAGIC + struct.pack("<BBHQQ", 1, 1, self.lane_count, self.message_length,
+                                         self.chunk_len)
+        words = np.diff(self.word_offsets.astype(np.uint64)).astype("<u4")
+        return (head + rans.serialize_table(self.table) + words.tobytes()
+                + np.ascontiguousarray(self.states, dtype="<u4").tobytes()
+                + np.ascontiguousarray(self.payload, dtype="<u2").tobytes())
+
+    @classmethod
+    def from_bytes(cls, raw: bytes) -> "ChunkedContainer":
+        raw = bytes(raw)
+        if len(raw) < 24:
+            raise TruncatedStreamError("chunked container shorter than fixed header")
+        if raw[:4] != CHUNK_MAGIC:
+            raise FormatError("bad magic; not an ilans chunked container")
+        version, variant, lanes, n, chunk_len = struct.unpack_from("<BBHQQ", raw, 4)
+        if version != 1:
+            raise FormatError(f"unsupported container version {version}")
+        if variant != 1:
+            raise FormatError(f"unknown variant byte {variant}")
+        if not 1 <= lanes <= 32 or chunk_len == 0 or chunk_len % 16:
+            raise FormatError("invalid lane_count / chunk_len")
+        table, off = rans.parse_table(raw, 24)
+        k = n_chunks_for(n, chunk_len)
+        need = off + 4 * k + 4 * k * lanes
+        if len(raw) < need:
+            raise TruncatedStreamError("chunk directory truncated")
+        words = np.frombuffer(raw, dtype="<u4", count=k, offset=off).astype(np.uint64)
+        off += 4 * k
+        states = np.frombuffer(raw, dtype="<u4", count=k * lanes, offset=off).astype(
+            np.uint32).reshape(k, lanes)
+        off += 4 * k * lanes
+        if ((states < WORD16.lower_bound)).any():
+            raise FormatError("lane state outside the coder interval")
+        offsets = np.zeros(k + 1, dtype=np.uint64)
+        np.cumsum(words, out=offsets[1:])
+        tail = raw[off:]
+        if len(tail) % 2:
+            raise FormatError("word16 payload has odd byte length")
+        if len(tail) // 2 < int(offsets[-1]):
+            raise TruncatedStreamError("payload truncated")
+        payload = np.frombuffer(tail, dtype="<u2").astype(np.uint16)
+        return cls(lanes, chunk_len, n, table, states, offsets, payload)
+
+
+# ---------------------------------------------------------------------------
+# HBM-resident pipeline
+# ---------------------------------------------------------------------------
+def _torch():
+    import torch  # torch: device memory, streams, NCCL plumbing only
+
+    return torch
+
+
+class DeviceCodec:
+    """Chunked word16 codec resident on one GPU.
+
+    Buffers are allocated once for ``capacity`` message bytes and reused;
+    every method is asynchronous on ``stream`` (default: torch's current
+    stream) except the explicit ``*_host`` read-backs.
+    """
+
+    def __init__(self, capacity: int, chunk_len: int = DEFAULT_CHUNK, lane_count: int = 32,
+                 scale_bits: int = 14, device=None, stream=None):
+        torch = _torch()
+        _check_chunking(chunk_len, lane_count)
+        if not 1 <= scale_bits <= 16:
+            raise ValueError("scale_bits must be in [1, 16]")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.capacity = int(capacity)
+        self.chunk_len = int(chunk_len)
+        self.lane_count = int(lane_count)
+        self.scale_bits = int(scale_bits)
+        self.stream = stream
+        kmax = max(1, n_chunks_for(self.capacity, chunk_len))
+        dev = self.device
+        e = lambda n, dt: torch.empty(n, dtype=dt, device=dev)  # noqa: E731
+        self.table = e(int(_lib.lib.ilans_table_bytes()), torch.uint8)
+        self.status = e(int(_lib.lib.ilans_dstatus_bytes()), torch.uint8)
+        self.counts = torch.zeros(256, dtype=torch.int64, device=dev)
+        self.scratch = e(max(1, self.capacity) + 8, torch.int16)
+        self.payload = e(max(1, self.capacity) + 8, torch.int16)
+        self.chunk_words = e(kmax, torch.int32)
+        self.offsets = e(kmax + 1, torch.int64)
+        self.states = e(kmax * lane_count, torch.int32)
+        self.consumed = e(kmax, torch.int64)
+        self.final_states = e(kmax * lane_count, torch.int32)
+
+    # -- plumbing ---------------------------------------------------------
+    def _s(self) -> int:
+        torch = _torch()
+        s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+        return int(s.cuda_stream)
+
+    @staticmethod
+    def _p(t) -> int:
+        return int(t.data_ptr())
+
+    # -- model ------------------------------------------------------------
+    def histogram(self, d_msg, n: int, accumulate: bool = False):
+        """counts[b] (+)= #{i < n : d_msg[i] == b} (int64 view of u64)."""
+        s = self._s()
+        if not accumulate:
+            _lib.check_dev(_lib.lib.ilans_counts_zero_dev(self._p(self.counts), s), "counts_zero")
+        _lib.check_dev(_lib.lib.ilans_histogram_u8_dev(self._p(d_msg), int(n),
+                                                       self._p(self.counts), s), "histogram")
+        return self.counts
+
+    def build_table_from_counts(self):
+        _lib.check_dev(_lib.lib.ilans_table_from_counts_dev(
+            self._p(self.counts), self.scale_bits, self._p(self.table), self._s()), "table")
+
+    def build_table_from_freq(self, table: SymbolTable):
+        torch = _torch()
+        if table.scale_bits != self.scale_bits:
+            raise ValueError("table scale_bits differs from the codec's")
+        f = torch.from_numpy(table.freq_u32.view(np.int32).copy()).to(self.device,
+                                                                      non_blocking=False)
+        self._freq_keepalive = f
+        _lib.check_dev(_lib.lib.ilans_table_from_freq_dev(
+            self._p(f), table.alphabet_size, table.scale_bits, self._p(self.table), self._s()),
+            "table_from_freq")
+
+    def read_table(self) -> SymbolTable:
+        """Synchronizing read-back of the device model as a SymbolTable."""
+        alpha = ctypes.c_int32(0)
+        sb = ctypes.c_int32(0)
+        freq = np.zeros(256, dtype=np.uint32)
+        st = _lib.Status()
+        rc = _lib.lib.ilans_table_read_host(self._p(self.table), ctypes.byref(alpha),
+                                            ctypes.byref(sb), _lib.ptr(freq), self._s(),
+                                            ctypes.byref(st))
+        _lib.raise_for(rc, st, "table")
+        return SymbolTable(freq[: alpha.value].tolist(), sb.value)
+
+    # -- coding -----------------------------------------------------------
+    def reset_status(self):
+        _lib.check_dev(_lib.lib.ilans_dstatus_reset_dev(self._p(self.status), self._s()),
+                       "status")
+
+    def check_status(self):
+        st = _lib.Status()
+        rc = _lib.lib.ilans_dstatus_read_host(self._p(self.status), self._s(), ctypes.byref(st))
+        _lib.raise_for(rc, st, "device status")
+
+    def encode(self, d_msg, n: int, frame: bool = True):
+        """Encode n bytes at d_msg with the current table: one launch for all
+        chunks, then (frame=True) the offset scan + payload compaction."""
+        if n > self.capacity:
+            raise ValueError("message larger than codec capacity")
+        s = self._s()
+        _lib.check_dev(_lib.lib.ilans_encode_chunks_dev(
+            self._p(d_msg), int(n), self.chunk_len, self.lane_count, self._p(self.table),
+            self._p(self.scratch), self._p(self.chunk_words), self._p(self.states),
+            self._p(self.status), s), "encode")
+        if frame:
+            _lib.check_dev(_lib.lib.ilans_frame_chunks_dev(
+                self._p(self.scratch), int(n), self.chunk_len, self._p(self.chunk_words),
+                self._p(self.offsets), self._p(self.payload), s), "frame")
+
+    def decode(self, d_out, n: int, payload=None, offsets=None, states=None,
+               final_states: bool = False):
+        """Decode n bytes into d_out from (payload, offsets, states) -- by
+        default the codec's own framed encode output."""
+        payload = self.payload if payload is None else payload
+        offsets = self.offsets if offsets is None else offsets
+        states = self.states if states is None else states
+        _lib.check_dev(_lib.lib.ilans_decode_chunks_dev(
+            self._p(payload), self._p(offsets), self._p(states), int(n), self.chunk_len,
+            self.lane_count, self._p(self.table), self.scale_bits, self._p(d_out),
+            self._p(self.consumed), self._p(self.final_states) if final_states else None,
+            self._p(self.status), self._s()), "decode")
+
+    # -- read-back --------------------------------------------------------
+    def encoded_host(self, n: int, table: SymbolTable) -> ChunkedContainer:
+        torch = _torch()
+        k = n_chunks_for(n, self.chunk_len)
+        torch.cuda.current_stream(self.device).synchronize() if self.stream is None \
+            else self.stream.synchronize()
+        offs = self.offsets[: k + 1].cpu().numpy().view(np.uint64).copy()
+        words = int(offs[-1]) if k else 0
+        payload = self.payload[:words].cpu().numpy().view(np.uint16).copy()
+        states = self.states[: k * self.lane_count].cpu().numpy().view(np.uint32).reshape(
+            k, self.lane_count).copy()
+        if k == 0:
+            offs = np.zeros(1, dtype=np.uint64)
+        return ChunkedContainer(self.lane_count, self.chunk_len, n, table, states, offs, payload)
+
+
+def encode_chunked(message, table: SymbolTable | None = None, lane_count: int = 32,
+                   chunk_len: int = DEFAULT_CHUNK, scale_bits: int = 14) -> ChunkedContainer:
+    """Encode host bytes as independent N-lane chunks under one table. With
+    table=None the model is built on the device (histogram + quantize), as
+    cli._build_table does on the host (cli.py:31-37)."""
+    torch = _torch()
+    _check_chunking(chunk_len, lane_count)
+    if table is not None:
+        msg = _as_symbols(message, table)
+        WORD16.check_table(table)
+        scale_bits = table.scale_bits
+    else:
+        msg = np.frombuffer(message, dtype=np.uint8) if isinstance(
+            message, (bytes, bytearray, memoryview)) else np.asarray(message, dtype=np.uint8)
+    n = len(msg)
+    codec = DeviceCodec(max(16, n), chunk_len, lane_count, scale_bits)
+    d_msg = torch.empty(max(16, n), dtype=torch.uint8, device=codec.device)
+    if n:
+        d_msg[:n].copy_(torch.from_numpy(np.ascontiguousarray(msg)))
+    if table is None:
+        codec.histogram(d_msg, n)
+        codec.build_table_from_counts()
+        table = codec.read_table()
+    else:
+        codec.build_table_from_freq(table)
+    codec.reset_status()
+    codec.encode(d_msg, n)
+    codec.check_status()
+    return codec.encoded_host(n, table)
+
+
+def decode_chunked(cc: ChunkedContainer) -> np.ndarray:
+    """Decode a ChunkedContainer on the device (one launch for all chunks)."""
+    torch = _torch()
+    _check_chunking(cc.chunk_len, cc.lane_count)
+    n = cc.message_length
+    if n == 0:
+        return np.zeros(0, dtype=np.uint8)
+    k = cc.n_chunks
+    if cc.states.shape != (k, cc.lane_count) or len(cc.word_offsets) != k + 1:
+        raise FormatError("chunk directory does not match the message length")
+    codec = DeviceCodec(n, cc.chunk_len, cc.lane_count, cc.table.scale_bits)
+    dev = codec.device
+    pay = torch.from_numpy(np.ascontiguousarray(cc.payload).view(np.int16)).to(dev)
+    if pay.numel() == 0:
+        pay = torch.zeros(8, dtype=torch.int16, device=dev)
+    offs = torch.from_numpy(np.ascontiguousarray(cc.word_offsets, dtype=np.uint64).view(
+        np.int64)).to(dev)
+    states = torch.from_numpy(np.ascontiguousarray(cc.states, dtype=np.uint32).view(
+        np.int32).reshape(-1)).to(dev)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    codec.build_table_from_freq(cc.table)
+    codec.reset_status()
+    codec.decode(out, n, pay, offs, states)
+    codec.check_status()
+    consumed = codec.consumed[:k].cpu().numpy()
+    if (consumed != np.diff(cc.word_offsets.astype(np.int64))).any():
+        import warnings
+
+        from .errors import TrailingGarbageWarning
+
+        warnings.warn("unread digits after chunk decode", TrailingGarbageWarning, stacklevel=2)
+    return out.cpu().numpy()

@@ -1,0 +1,585 @@
+// capi.cu -- the extern "C" boundary (include/ilans_b200.h).
+//
+// Host-buffer drop-ins mirror pkg/src/ilans/_core.pyx one for one: the host
+// arrays are copied to HBM, the sm_100a kernels run on a library-owned
+// stream, results come back. There is no CPU compute fallback: without a
+// CUDA device every entry point returns ILANS_ERR_CUDA.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+static std::atomic<unsigned long long> g_launches{0};
+void ilans_note_launch(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n)); }
+
+namespace ilans {
+
+__global__ void dstatus_reset_kernel(DStatus *s) {
+    s->trunc_stream = ~0ull;
+    s->unenc_index = -1;
+    s->unenc_symbol = 0;
+    s->value_error = 0;
+}
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
+}
+
+cudaError_t launch_histogram(const uint8_t *d_msg, int64_t n, unsigned long long *d_counts,
+                             cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int smem = 256 * 256;
+    if (!attr_set[dev & 63]) {
+        cudaFuncSetAttribute(histogram_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem);
+        attr_set[dev & 63] = true;
+    }
+    // 3 CTAs x 64 KB per SM; a block needs >= 15 x 4 KB of input per round
+    int64_t blocks = int64_t(sm_count()) * 3;
+    const int64_t want = (n + 256 * 16 * 15 - 1) / (256 * 16 * 15);
+    if (blocks > want) blocks = want < 1 ? 1 : want;
+    histogram_u8_kernel<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(d_msg, n, d_counts);
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_table(const unsigned long long *d_counts, const uint32_t *d_freq,
+                               int n_freq, const uint32_t *d_cum, const uint8_t *d_slot,
+                               int scale_bits, TableDev *d_table, cudaStream_t stream) {
+    build_table_kernel<<<1, kMaxSym, 0, stream>>>(d_counts, d_freq, n_freq, d_cum, d_slot,
+                                                  scale_bits, d_table);
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace ilans
+
+using namespace ilans;
+
+// ---------------------------------------------------------------------------
+// status helpers
+// ---------------------------------------------------------------------------
+static void st_clear(ilans_status *st) {
+    if (!st) return;
+    std::memset(st, 0, sizeof(*st));
+    st->stream = -1;
+    st->index = -1;
+    st->symbol = -1;
+}
+
+static int st_fail(ilans_status *st, int code, const char *fmt, ...) {
+    if (st) {
+        st->code = code;
+        va_list ap;
+        va_start(ap, fmt);
+        std::vsnprintf(st->message, sizeof(st->message), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+static int st_cuda(ilans_status *st, cudaError_t e, const char *where) {
+    if (st) st->cuda_error = static_cast<int32_t>(e);
+    return st_fail(st, ILANS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(expr)                                              \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return st_cuda(st, _e, #expr); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// per-device context for the host-buffer drop-ins
+// ---------------------------------------------------------------------------
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes < 64) bytes = 64;
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = bytes + bytes / 4;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    template <typename T>
+    T *as() const { return static_cast<T *>(p); }
+};
+
+struct Ctx {
+    std::mutex mu;
+    bool init = false;
+    cudaStream_t stream = nullptr;
+    DevBuf msg, scratch, payload, out, states, ws, slot, freq, cum, table, status, counts,
+        offsets, consumed, words;
+};
+
+Ctx g_ctx[64];
+thread_local int t_device = -1;
+
+int current_device(ilans_status *st, Ctx **out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return st_fail(st, ILANS_ERR_CUDA, "no CUDA device available (%s)",
+                       e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    int dev = t_device;
+    if (dev < 0) {
+        e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return st_cuda(st, e, "cudaGetDevice");
+    }
+    if (dev >= n || dev >= 64) return st_fail(st, ILANS_ERR_VALUE, "bad device %d", dev);
+    e = cudaSetDevice(dev);
+    if (e != cudaSuccess) return st_cuda(st, e, "cudaSetDevice");
+    Ctx &c = g_ctx[dev];
+    *out = &c;
+    return ILANS_OK;
+}
+
+int ctx_init(Ctx &c, ilans_status *st) {
+    if (c.init) return ILANS_OK;
+    CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    CK(c.table.ensure(sizeof(TableDev)));
+    CK(c.status.ensure(sizeof(DStatus)));
+    c.init = true;
+    return ILANS_OK;
+}
+
+int read_dstatus(const DStatus *d, cudaStream_t s, DStatus *h, ilans_status *st) {
+    CK(cudaMemcpyAsync(h, d, sizeof(DStatus), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ILANS_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// library
+// ---------------------------------------------------------------------------
+extern "C" int ilans_abi_version(void) { return ILANS_B200_ABI_VERSION; }
+
+extern "C" int ilans_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+extern "C" int ilans_set_device(int device, ilans_status *st) {
+    st_clear(st);
+    int n = ilans_device_count();
+    if (device < 0 || device >= n || device >= 64)
+        return st_fail(st, ILANS_ERR_VALUE, "device %d out of range (%d visible)", device, n);
+    t_device = device;
+    CK(cudaSetDevice(device));
+    return ILANS_OK;
+}
+
+extern "C" uint64_t ilans_launch_count(void) { return g_launches.load(); }
+
+extern "C" size_t ilans_table_bytes(void) { return sizeof(TableDev); }
+extern "C" size_t ilans_dstatus_bytes(void) { return sizeof(DStatus); }
+
+// ---------------------------------------------------------------------------
+// 1. host-buffer drop-ins
+// ---------------------------------------------------------------------------
+extern "C" int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const uint32_t *freq,
+                                            int32_t n_freq, const uint32_t *cum,
+                                            int32_t scale_bits, int32_t n_lanes,
+                                            uint16_t *payload_out, int64_t *payload_words,
+                                            uint32_t *states_out, ilans_status *st) {
+    st_clear(st);
+    if (n < 0) return st_fail(st, ILANS_ERR_VALUE, "negative message length");
+    if (n_lanes < 1 || n_lanes > 0xFFFF)
+        return st_fail(st, ILANS_ERR_VALUE, "lane_count must be in [1, 65535]");
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits)
+        return st_fail(st, ILANS_ERR_VALUE, "scale_bits must be in [1, 16]");
+    if (n_freq < 0 || n_freq > kMaxSym)
+        return st_fail(st, ILANS_ERR_VALUE, "alphabet size must be in [1, 256]");
+    Ctx *cp = nullptr;
+    if (int rc = current_device(st, &cp)) return rc;
+    Ctx &c = *cp;
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (int rc = ctx_init(c, st)) return rc;
+    if (n == 0) {  // states stay at L, empty payload (_core.pyx:28-29)
+        for (int l = 0; l < n_lanes; ++l) states_out[l] = kLow;
+        *payload_words = 0;
+        return ILANS_OK;
+    }
+    cudaStream_t s = c.stream;
+    CK(c.msg.ensure(size_t(n)));
+    CK(c.scratch.ensure(size_t(n) * 2));
+    CK(c.states.ensure(size_t(n_lanes) * 4));
+    CK(c.ws.ensure(size_t(n_lanes) * 4));
+    CK(c.freq.ensure(kMaxSym * 4));
+    CK(c.cum.ensure((kMaxSym + 1) * 4));
+    CK(c.words.ensure(8));
+    uint32_t hf[kMaxSym] = {0}, hc[kMaxSym + 1] = {0};
+    std::memcpy(hf, freq, size_t(n_freq) * 4);
+    std::memcpy(hc, cum, size_t(n_freq + 1) * 4);
+    CK(cudaMemcpyAsync(c.msg.p, msg, size_t(n), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.freq.p, hf, sizeof(hf), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.cum.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    CK(launch_build_table(nullptr, c.freq.as<uint32_t>(), n_freq, c.cum.as<uint32_t>(), nullptr,
+                          scale_bits, c.table.as<TableDev>(), s));
+    dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
+    ilans_note_launch();
+    CK(launch_encode(c.msg.as<uint8_t>(), n, n, n_lanes, c.table.as<TableDev>(),
+                     c.scratch.as<uint16_t>(), c.words.as<uint32_t>(), c.states.as<uint32_t>(),
+                     c.status.as<DStatus>(), c.ws.as<uint32_t>(), s));
+    DStatus hs;
+    if (int rc = read_dstatus(c.status.as<DStatus>(), s, &hs, st)) return rc;
+    if (hs.unenc_index >= 0) {
+        st->index = hs.unenc_index;
+        st->symbol = msg[hs.unenc_index];
+        return st_fail(st, ILANS_ERR_UNENCODABLE, "symbol %d has frequency 0", st->symbol);
+    }
+    uint32_t w = 0;
+    CK(cudaMemcpyAsync(&w, c.words.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (w)
+        CK(cudaMemcpyAsync(payload_out, c.scratch.as<uint16_t>() + (n - w), size_t(w) * 2,
+                           cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(states_out, c.states.p, size_t(n_lanes) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *payload_words = w;
+    return ILANS_OK;
+}
+
+// sb <= 12 packed LUT is valid only for self-consistent tables (every slot's
+// symbol s has 1 <= f[s] <= 4096 and 0 <= slot - cum[s] < 4096).
+static bool host_packable(const uint8_t *slot_sym, const uint32_t *f, const uint32_t *cum,
+                          int scale_bits) {
+    if (scale_bits > kPackedMaxBits) return false;
+    const uint32_t m = 1u << scale_bits;
+    for (uint32_t j = 0; j < m; ++j) {
+        const uint32_t s = slot_sym[j];
+        if (f[s] < 1 || f[s] > 4096 || j - cum[s] >= 4096u) return false;
+    }
+    return true;
+}
+
+static int decode_common(const uint16_t *payload, int64_t pay_len, const uint32_t *states,
+                         const uint8_t *slot_sym, int64_t n_slots, const uint32_t *freq,
+                         const uint32_t *cum, int32_t n_freq, int32_t scale_bits,
+                         int64_t msg_len, int32_t n_lanes, uint8_t *out, int64_t *consumed,
+                         ilans_status *st) {
+    if (msg_len < 0 || pay_len < 0) return st_fail(st, ILANS_ERR_VALUE, "negative length");
+    if (n_lanes < 1 || n_lanes > 0xFFFF)
+        return st_fail(st, ILANS_ERR_VALUE, "lane_count must be in [1, 65535]");
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits)
+        return st_fail(st, ILANS_ERR_VALUE, "scale_bits must be in [1, 16]");
+    if (n_freq < 0 || n_freq > kMaxSym)
+        return st_fail(st, ILANS_ERR_VALUE, "alphabet size must be in [1, 256]");
+    const int64_t m = int64_t(1) << scale_bits;
+    if (n_slots < m) return st_fail(st, ILANS_ERR_VALUE, "slot table shorter than 2^scale_bits");
+    Ctx *cp = nullptr;
+    if (int rc = current_device(st, &cp)) return rc;
+    Ctx &c = *cp;
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (int rc = ctx_init(c, st)) return rc;
+    if (msg_len == 0) {
+        *consumed = 0;
+        st->consumed = 0;
+        return ILANS_OK;
+    }
+    cudaStream_t s = c.stream;
+    CK(c.payload.ensure(size_t(pay_len) * 2 + 16));
+    CK(c.offsets.ensure(16));
+    CK(c.states.ensure(size_t(n_lanes) * 4));
+    CK(c.ws.ensure(size_t(n_lanes) * 4));
+    CK(c.slot.ensure(size_t(m)));
+    CK(c.freq.ensure(kMaxSym * 4));
+    CK(c.cum.ensure((kMaxSym + 1) * 4));
+    CK(c.out.ensure(size_t(msg_len)));
+    CK(c.consumed.ensure(8));
+    uint32_t hf[kMaxSym] = {0}, hc[kMaxSym + 1] = {0};
+    std::memcpy(hf, freq, size_t(n_freq) * 4);
+    std::memcpy(hc, cum, size_t(n_freq + 1) * 4);
+    const uint64_t offs[2] = {0, uint64_t(pay_len)};
+    if (pay_len)
+        CK(cudaMemcpyAsync(c.payload.p, payload, size_t(pay_len) * 2, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.offsets.p, offs, sizeof(offs), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.states.p, states, size_t(n_lanes) * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.slot.p, slot_sym, size_t(m), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.freq.p, hf, sizeof(hf), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.cum.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    CK(launch_build_table(nullptr, c.freq.as<uint32_t>(), n_freq, c.cum.as<uint32_t>(),
+                          c.slot.as<uint8_t>(), scale_bits, c.table.as<TableDev>(), s));
+    dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
+    ilans_note_launch();
+    const bool packed = host_packable(slot_sym, hf, hc, scale_bits);
+    CK(launch_decode(c.payload.as<uint16_t>(), c.offsets.as<uint64_t>(), c.states.as<uint32_t>(),
+                     msg_len, msg_len, n_lanes, c.table.as<TableDev>(), scale_bits, packed,
+                     c.out.as<uint8_t>(), c.consumed.as<uint64_t>(), nullptr,
+                     c.status.as<DStatus>(), c.ws.as<uint32_t>(), s));
+    DStatus hs;
+    if (int rc = read_dstatus(c.status.as<DStatus>(), s, &hs, st)) return rc;
+    uint64_t used = 0;
+    CK(cudaMemcpyAsync(&used, c.consumed.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hs.trunc_stream != ~0ull) {
+        st->stream = int64_t(hs.trunc_stream);
+        st->consumed = int64_t(used);
+        return st_fail(st, ILANS_ERR_TRUNCATED, "payload exhausted mid-decode");
+    }
+    CK(cudaMemcpyAsync(out, c.out.p, size_t(msg_len), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *consumed = int64_t(used);
+    st->consumed = int64_t(used);
+    return ILANS_OK;
+}
+
+extern "C" int ilans_decode_interleaved_u16(const uint16_t *payload, int64_t pay_len,
+                                            const uint32_t *states, const uint8_t *slot_sym,
+                                            int64_t n_slots, const uint32_t *freq,
+                                            const uint32_t *cum, int32_t n_freq,
+                                            int32_t scale_bits, int64_t msg_len,
+                                            int32_t n_lanes, uint8_t *out, int64_t *consumed,
+                                            ilans_status *st) {
+    st_clear(st);
+    return decode_common(payload, pay_len, states, slot_sym, n_slots, freq, cum, n_freq,
+                         scale_bits, msg_len, n_lanes, out, consumed, st);
+}
+
+extern "C" int ilans_decode_lanes_u16(const uint16_t *payload, int64_t pay_len,
+                                      const uint32_t *states, const uint8_t *slot_sym,
+                                      int64_t n_slots, const uint32_t *freq, const uint32_t *cum,
+                                      int32_t n_freq, int32_t scale_bits, int64_t msg_len,
+                                      int32_t n_lanes, uint8_t *out, int64_t *consumed,
+                                      ilans_status *st) {
+    st_clear(st);
+    if (n_lanes > 32) return st_fail(st, ILANS_ERR_VALUE, "at most 32 lanes");
+    return decode_common(payload, pay_len, states, slot_sym, n_slots, freq, cum, n_freq,
+                         scale_bits, msg_len, n_lanes, out, consumed, st);
+}
+
+extern "C" int ilans_quantize(const uint64_t *counts, int32_t n, int32_t scale_bits,
+                              uint32_t *freq_out, ilans_status *st) {
+    st_clear(st);
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits)
+        return st_fail(st, ILANS_ERR_VALUE, "scale_bits must be in [1, %d]", kMaxScaleBits);
+    if (n > kMaxSym) return st_fail(st, ILANS_ERR_VALUE, "alphabet size must be <= %d", kMaxSym);
+    bool any = false;
+    for (int i = 0; i < n; ++i) any |= counts[i] != 0;
+    if (!any) return st_fail(st, ILANS_ERR_VALUE, "at least one count must be positive");
+    Ctx *cp = nullptr;
+    if (int rc = current_device(st, &cp)) return rc;
+    Ctx &c = *cp;
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (int rc = ctx_init(c, st)) return rc;
+    cudaStream_t s = c.stream;
+    CK(c.counts.ensure(kMaxSym * 8));
+    uint64_t hc[kMaxSym] = {0};
+    std::memcpy(hc, counts, size_t(n) * 8);
+    CK(cudaMemcpyAsync(c.counts.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    CK(launch_build_table(c.counts.as<unsigned long long>(), nullptr, 0, nullptr, nullptr,
+                          scale_bits, c.table.as<TableDev>(), s));
+    TableDev *h = static_cast<TableDev *>(std::malloc(sizeof(TableDev)));
+    if (!h) return st_fail(st, ILANS_ERR_VALUE, "host allocation failed");
+    cudaError_t e = cudaMemcpyAsync(h, c.table.p, offsetof(TableDev, cum), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        std::free(h);
+        return st_cuda(st, e, "quantize readback");
+    }
+    int rc = ILANS_OK;
+    if (h->status != ILANS_OK) {
+        if (h->err_detail[0] == 2)
+            rc = st_fail(st, ILANS_ERR_VALUE,
+                         "alphabet too large for scale: %u present symbols, only %u slots",
+                         h->err_detail[1], h->err_detail[2]);
+        else
+            rc = st_fail(st, ILANS_ERR_VALUE, "quantize failed (%u)", h->err_detail[0]);
+    } else {
+        std::memcpy(freq_out, h->freq, size_t(n) * 4);
+    }
+    std::free(h);
+    return rc;
+}
+
+extern "C" int ilans_histogram_u8(const uint8_t *msg, int64_t n, uint64_t *counts_out,
+                                  int32_t *alphabet, ilans_status *st) {
+    st_clear(st);
+    if (n < 0) return st_fail(st, ILANS_ERR_VALUE, "negative length");
+    Ctx *cp = nullptr;
+    if (int rc = current_device(st, &cp)) return rc;
+    Ctx &c = *cp;
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (int rc = ctx_init(c, st)) return rc;
+    cudaStream_t s = c.stream;
+    CK(c.counts.ensure(kMaxSym * 8));
+    CK(cudaMemsetAsync(c.counts.p, 0, kMaxSym * 8, s));
+    if (n > 0) {
+        CK(c.msg.ensure(size_t(n)));
+        CK(cudaMemcpyAsync(c.msg.p, msg, size_t(n), cudaMemcpyHostToDevice, s));
+        CK(launch_histogram(c.msg.as<uint8_t>(), n, c.counts.as<unsigned long long>(), s));
+    }
+    CK(cudaMemcpyAsync(counts_out, c.counts.p, kMaxSym * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int a = 0;
+    for (int i = 0; i < kMaxSym; ++i)
+        if (counts_out[i]) a = i + 1;
+    if (alphabet) *alphabet = a;
+    return ILANS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// 2. device-pointer pipeline
+// ---------------------------------------------------------------------------
+#define ST(x) static_cast<cudaStream_t>(x)
+
+extern "C" int ilans_counts_zero_dev(uint64_t *d_counts, void *stream) {
+    return cudaMemsetAsync(d_counts, 0, kMaxSym * 8, ST(stream)) == cudaSuccess ? ILANS_OK
+                                                                               : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_histogram_u8_dev(const uint8_t *d_msg, int64_t n, uint64_t *d_counts,
+                                      void *stream) {
+    return launch_histogram(d_msg, n, reinterpret_cast<unsigned long long *>(d_counts),
+                            ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_table_from_counts_dev(const uint64_t *d_counts, int32_t scale_bits,
+                                           void *d_table, void *stream) {
+    return launch_build_table(reinterpret_cast<const unsigned long long *>(d_counts), nullptr, 0,
+                              nullptr, nullptr, scale_bits, static_cast<TableDev *>(d_table),
+                              ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_table_from_freq_dev(const uint32_t *d_freq, int32_t n_freq,
+                                         int32_t scale_bits, void *d_table, void *stream) {
+    if (n_freq < 1 || n_freq > kMaxSym) return ILANS_ERR_VALUE;
+    return launch_build_table(nullptr, d_freq, n_freq, nullptr, nullptr, scale_bits,
+                              static_cast<TableDev *>(d_table), ST(stream)) == cudaSuccess
+               ? ILANS_OK
+               : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_table_read_host(const void *d_table, int32_t *alphabet, int32_t *scale_bits,
+                                     uint32_t *freq_out, void *stream, ilans_status *st) {
+    st_clear(st);
+    TableDev *h = static_cast<TableDev *>(std::malloc(offsetof(TableDev, cum)));
+    if (!h) return st_fail(st, ILANS_ERR_VALUE, "host allocation failed");
+    cudaError_t e = cudaMemcpyAsync(h, d_table, offsetof(TableDev, cum), cudaMemcpyDeviceToHost,
+                                    ST(stream));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ST(stream));
+    if (e != cudaSuccess) {
+        std::free(h);
+        return st_cuda(st, e, "table readback");
+    }
+    if (alphabet) *alphabet = int32_t(h->n_sym);
+    if (scale_bits) *scale_bits = int32_t(h->scale_bits);
+    if (freq_out) std::memcpy(freq_out, h->freq, sizeof(h->freq));
+    int rc = ILANS_OK;
+    if (h->status != ILANS_OK) {
+        if (h->err_detail[0] == 2)
+            rc = st_fail(st, ILANS_ERR_VALUE,
+                         "alphabet too large for scale: %u present symbols, only %u slots",
+                         h->err_detail[1], h->err_detail[2]);
+        else
+            rc = st_fail(st, ILANS_ERR_VALUE, "invalid model (%u)", h->err_detail[0]);
+    }
+    std::free(h);
+    return rc;
+}
+
+extern "C" int ilans_dstatus_reset_dev(void *d_status, void *stream) {
+    dstatus_reset_kernel<<<1, 1, 0, ST(stream)>>>(static_cast<DStatus *>(d_status));
+    ilans_note_launch();
+    return cudaGetLastError() == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_dstatus_read_host(const void *d_status, void *stream, ilans_status *st) {
+    st_clear(st);
+    DStatus h;
+    cudaError_t e = cudaMemcpyAsync(&h, d_status, sizeof(h), cudaMemcpyDeviceToHost, ST(stream));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ST(stream));
+    if (e != cudaSuccess) return st_cuda(st, e, "status readback");
+    if (h.trunc_stream != ~0ull) {
+        st->stream = int64_t(h.trunc_stream);
+        return st_fail(st, ILANS_ERR_TRUNCATED, "payload exhausted mid-decode (chunk %lld)",
+                       static_cast<long long>(h.trunc_stream));
+    }
+    if (h.value_error) {
+        return st_fail(st, ILANS_ERR_VALUE, "table does not match the launch (scale_bits / layout)");
+    }
+    if (h.unenc_index >= 0) {
+        st->index = h.unenc_index;
+        return st_fail(st, ILANS_ERR_UNENCODABLE, "zero-frequency symbol at index %lld",
+                       static_cast<long long>(h.unenc_index));
+    }
+    return ILANS_OK;
+}
+
+extern "C" int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
+                                       int32_t n_lanes, const void *d_table,
+                                       uint16_t *d_scratch, uint32_t *d_chunk_words,
+                                       uint32_t *d_states, void *d_status, void *stream) {
+    if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    if (reinterpret_cast<uintptr_t>(d_msg) & 15) return ILANS_ERR_VALUE;
+    return launch_encode(d_msg, n, chunk_len, n_lanes, static_cast<const TableDev *>(d_table),
+                         d_scratch, d_chunk_words, d_states, static_cast<DStatus *>(d_status),
+                         nullptr, ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_frame_chunks_dev(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
+                                      const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
+                                      uint16_t *d_payload, void *stream) {
+    if (chunk_len <= 0) return ILANS_ERR_VALUE;
+    return launch_frame(d_scratch, n, chunk_len, d_chunk_words, d_word_offsets, d_payload,
+                        ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t *d_word_offsets,
+                                       const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                       int32_t n_lanes, const void *d_table, int32_t scale_bits,
+                                       uint8_t *d_out, uint64_t *d_consumed,
+                                       uint32_t *d_final_states, void *d_status, void *stream) {
+    if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits) return ILANS_ERR_VALUE;
+    if ((reinterpret_cast<uintptr_t>(d_payload) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
+        return ILANS_ERR_VALUE;
+    // tables built by the model builder are self-consistent, so the packed
+    // LUT applies whenever scale_bits <= 12; the kernel re-checks the table
+    // header on the device (scale_bits match, packed flag) and records a
+    // value error instead of decoding with a mismatched layout.
+    const bool packed = scale_bits <= kPackedMaxBits;
+    return launch_decode(d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes,
+                         static_cast<const TableDev *>(d_table), scale_bits, packed, d_out,
+                         d_consumed, d_final_states, static_cast<DStatus *>(d_status), nullptr,
+                         ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_synth_bytes_dev(uint8_t *d_out, int64_t n, uint64_t seed,
+                                     int64_t first_index, const uint32_t *d_cdf, void *stream) {
+    if (reinterpret_cast<uintptr_t>(d_out) & 15) return ILANS_ERR_VALUE;
+    return launch_synth(d_out, n, seed, first_index, d_cdf, ST(stream)) == cudaSuccess
+               ? ILANS_OK
+               : ILANS_ERR_CUDA;
+}

@@ -1,0 +1,325 @@
+// decode.cu -- word16 interleaved-rANS decoders for sm_100a.
+//
+// Replaces _core.decode_interleaved_u16 (_core.pyx:46-127) and
+// _core.decode_lanes_u16 (_core.pyx:130-173); both produce byte-identical
+// output (_pure.py:69-72), so one group-at-a-time kernel serves both.
+//
+// Warp kernel (N <= 32): one warp per stream (chunk), lane l = rANS lane l.
+// Per group of N symbols (lanes.decode_step, lanes.py:138-151):
+//   pop:     slot = x & (m-1); s = LUT[slot]; x = f*(x >> sb) + slot - cum
+//   ballot:  mask = __ballot_sync(x < 2^16)            (lanes.ballot)
+//   refill:  x = x << 16 | payload[pos + popc(mask & lanemask_lt)]
+//                                                      (lanes.packed_load)
+//   pos += popc(mask)
+// The payload is staged into a per-warp shared-memory ring by cp.async
+// (4 x 512-byte segments, 3 segments = ~66 groups ahead of the reader), so
+// the refill read is a conflict-free LDS, never an HBM round trip. Decoded
+// bytes are staged in a 1 KB per-warp buffer and written to HBM as 16-byte
+// vectors (512 B per warp store).
+//
+// Block kernel (N > 32, up to 65535 lanes): one CTA per stream, contiguous
+// lane ranges per thread and a CTA-wide exclusive scan of refill counts in
+// place of the warp ballot. Correct for every N, used for
+// the wide single-stream calls the reference allows (interleave.py:197-200).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ilans {
+
+constexpr int kSegWords = 256;            // 512 B per cp.async warp-copy
+constexpr int kRingWords = 4 * kSegWords; // 2 KB payload ring per warp
+constexpr int kObufBytes = 1024;          // 2 x 512 B output halves per warp
+constexpr int kWarpSmem = kRingWords * 2 + kObufBytes;
+
+__device__ __forceinline__ void issue_payload_segment(uint16_t *ring, const uint16_t *g_aligned,
+                                                      uint64_t rel_words_avail, uint32_t seg,
+                                                      int lane) {
+    const uint64_t w0 = static_cast<uint64_t>(seg) * kSegWords + static_cast<uint64_t>(lane) * 8u;
+    uint32_t bytes = 0;
+    if (rel_words_avail > w0) {
+        const uint64_t left = (rel_words_avail - w0) * 2u;
+        bytes = left >= 16u ? 16u : static_cast<uint32_t>(left);
+    }
+    const uint16_t *src = bytes ? g_aligned + w0 : g_aligned;
+    cp_async16(ring + (seg & 3u) * kSegWords + lane * 8, src, bytes);
+}
+
+template <bool PACKED>
+__global__ void __launch_bounds__(1024)
+decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                   const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                   int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                   uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
+                   uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
+                   int launch_sb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int sb = static_cast<int>(tab->scale_bits);
+    if (sb != launch_sb || (PACKED && !(tab->flags & kTabPacked)) || tab->status != ILANS_OK) {
+        if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
+        return;
+    }
+    const uint32_t m = 1u << sb;
+    const uint32_t mask = m - 1u;
+
+    // ---- stage the lookup tables in shared memory ------------------------
+    uint32_t *lut32 = reinterpret_cast<uint32_t *>(smem);
+    uint2 *dec = reinterpret_cast<uint2 *>(smem);
+    uint8_t *sym = smem + kMaxSym * sizeof(uint2);
+    uint32_t lut_bytes;
+    if (PACKED) {
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) lut32[i] = tab->packed[i];
+        lut_bytes = m * 4u;
+    } else {
+        for (uint32_t i = threadIdx.x; i < kMaxSym; i += blockDim.x) dec[i] = tab->dec[i];
+        if (m >= 4) {
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(tab->slot_sym);
+            uint32_t *dst = reinterpret_cast<uint32_t *>(sym);
+            for (uint32_t i = threadIdx.x; i < m / 4; i += blockDim.x) dst[i] = src[i];
+        } else {
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) sym[i] = tab->slot_sym[i];
+        }
+        lut_bytes = kMaxSym * sizeof(uint2) + (m < 16 ? 16u : m);
+    }
+    lut_bytes = (lut_bytes + 15u) & ~15u;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    uint16_t *ring = reinterpret_cast<uint16_t *>(smem + lut_bytes + wib * kWarpSmem);
+    uint8_t *obuf = smem + lut_bytes + wib * kWarpSmem + kRingWords * 2;
+    const uint32_t lt = lanemask_lt();
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; k < n_chunks;
+         k += warps_total) {
+        const int64_t cbase = k * chunk_len;
+        const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+        const uint64_t woff = offsets[k];
+        const uint64_t wlen = offsets[k + 1] - woff;
+        const uint64_t a_words = woff & ~7ull;  // 16-byte aligned segment base
+        const uint32_t delta = static_cast<uint32_t>(woff & 7u);
+        const uint16_t *g_al = payload + a_words;
+        const uint64_t avail = wlen + delta;  // readable words from g_al
+#pragma unroll
+        for (uint32_t s = 0; s < 4; ++s) {
+            issue_payload_segment(ring, g_al, avail, s, lane);
+            cp_async_commit();
+        }
+        cp_async_wait<2>();
+        __syncwarp();
+
+        uint64_t cur = 0;
+        uint32_t x = lane < n_lanes ? states[k * n_lanes + lane] : 0u;
+        uint64_t pos = 0;
+        bool truncated = false;
+        uint8_t *out_k = out + cbase;
+        for (int64_t base = 0; base < len; base += n_lanes) {
+            const int64_t left = len - base;
+            const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
+            const bool on = lane < active;
+            uint32_t s = 0;
+            if (on) {
+                const uint32_t slot = x & mask;
+                if (PACKED) {
+                    const uint32_t e = lut32[slot];
+                    s = e & 0xFFu;
+                    x = (((e >> 8) & 0xFFFu) + 1u) * (x >> sb) + (e >> 20);
+                } else {
+                    s = sym[slot];
+                    const uint2 d = dec[s];
+                    x = d.x * (x >> sb) + slot - d.y;
+                }
+            }
+            const bool need = on && x < kLow;
+            const uint32_t mk = __ballot_sync(0xffffffffu, need);
+            const uint32_t cnt = __popc(mk);
+            if (pos + cnt > wlen) {
+                truncated = true;
+                break;
+            }
+            if (need) {
+                const uint64_t v = delta + pos + __popc(mk & lt);
+                x = (x << 16) | ring[v & (kRingWords - 1)];
+            }
+            pos += cnt;
+            if (on) obuf[(base + lane) & (kObufBytes - 1)] = static_cast<uint8_t>(s);
+            const int64_t nb = base + active;
+            if ((nb >> 9) != (base >> 9)) {  // a 512-byte half is complete
+                __syncwarp();
+                const int64_t blk = base >> 9;
+                const uint4 v = reinterpret_cast<const uint4 *>(obuf + (blk & 1) * 512)[lane];
+                reinterpret_cast<uint4 *>(out_k + (blk << 9))[lane] = v;
+                __syncwarp();
+            }
+            const uint64_t seg = (delta + pos) >> 8;
+            if (seg != cur) {  // segment cur-1 fully read: refill its slot
+                cur = seg;
+                __syncwarp();
+                issue_payload_segment(ring, g_al, avail, static_cast<uint32_t>(cur + 3), lane);
+                cp_async_commit();
+                cp_async_wait<2>();
+                __syncwarp();
+            }
+        }
+        if (truncated) {
+            if (lane == 0) atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
+        } else {
+            __syncwarp();
+            const int64_t tail0 = (len >> 9) << 9;
+            const uint8_t *half = obuf + ((len >> 9) & 1) * 512;
+            for (int64_t i = tail0 + lane; i < len; i += 32) out_k[i] = half[i - tail0];
+        }
+        if (lane == 0 && consumed) consumed[k] = pos;
+        if (final_states && lane < n_lanes) final_states[k * n_lanes + lane] = x;
+        cp_async_wait<0>();
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-wide exclusive scan (blockDim multiple of 32, <= 1024)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *total,
+                                                    uint32_t *sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+    }
+    if (lane == 31) sh[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < nw ? sh[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += u;
+        }
+        sh[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t off = wid ? sh[wid - 1] : 0u;
+    *total = sh[nw - 1];
+    __syncthreads();
+    return off + inc - v;
+}
+
+// One CTA per stream; thread t owns lanes [t*k, min(N, t*k + k)), k <= 64.
+__global__ void __launch_bounds__(1024)
+decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                    const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                    int n_lanes, const TableDev *__restrict__ tab, uint8_t *__restrict__ out,
+                    uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
+                    DStatus *__restrict__ status, uint32_t *__restrict__ ws_all) {
+    __shared__ uint32_t scan_sh[32];
+    const int64_t k = blockIdx.x;
+    const int64_t cbase = k * chunk_len;
+    const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+    const uint64_t woff = offsets[k];
+    const uint64_t wlen = offsets[k + 1] - woff;
+    const uint16_t *pay = payload + woff;
+    uint32_t *ws = ws_all + k * n_lanes;
+    const int sb = static_cast<int>(tab->scale_bits);
+    const uint32_t mask = (1u << sb) - 1u;
+    const int per = (n_lanes + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per;
+    for (int l = lo; l < lo + per && l < n_lanes; ++l) ws[l] = states[k * n_lanes + l];
+    uint64_t pos = 0;
+    bool truncated = false;
+    for (int64_t base = 0; base < len; base += n_lanes) {
+        const int64_t left = len - base;
+        const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
+        const int hi = lo + per < active ? lo + per : active;
+        uint64_t pend = 0;
+        uint32_t cnt = 0;
+        for (int l = lo; l < hi; ++l) {
+            uint32_t x = ws[l];
+            const uint32_t slot = x & mask;
+            const uint32_t s = tab->slot_sym[slot];
+            const uint2 d = tab->dec[s];
+            x = d.x * (x >> sb) + slot - d.y;
+            out[cbase + base + l] = static_cast<uint8_t>(s);
+            ws[l] = x;
+            if (x < kLow) {
+                pend |= 1ull << (l - lo);
+                ++cnt;
+            }
+        }
+        uint32_t total;
+        const uint32_t excl = block_excl_scan(cnt, &total, scan_sh);
+        if (pos + total > wlen) {
+            truncated = true;
+            break;
+        }
+        uint32_t r = 0;
+        while (pend) {
+            const int j = __ffsll(static_cast<long long>(pend)) - 1;
+            pend &= pend - 1;
+            const int l = lo + j;
+            ws[l] = (ws[l] << 16) | pay[pos + excl + r];
+            ++r;
+        }
+        pos += total;
+    }
+    if (threadIdx.x == 0) {
+        if (truncated) atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
+        if (consumed) consumed[k] = pos;
+    }
+    if (final_states)
+        for (int l = lo; l < lo + per && l < n_lanes; ++l) final_states[k * n_lanes + l] = ws[l];
+}
+
+static size_t decode_lut_bytes(int scale_bits, bool packed) {
+    const size_t m = size_t(1) << scale_bits;
+    size_t b = packed ? m * 4 : kMaxSym * sizeof(uint2) + (m < 16 ? 16 : m);
+    return (b + 15) & ~size_t(15);
+}
+
+cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offsets,
+                          const uint32_t *d_states, int64_t n, int64_t chunk_len, int n_lanes,
+                          const TableDev *d_table, int scale_bits, bool packed,
+                          uint8_t *d_out, uint64_t *d_consumed, uint32_t *d_final_states,
+                          DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
+    if (n_lanes > 32) {
+        const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
+        decode_block_kernel<<<static_cast<unsigned>(n_chunks), threads, 0, stream>>>(
+            d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table, d_out,
+            d_consumed, d_final_states, d_status, d_lane_ws);
+        ilans_note_launch();
+        return cudaGetLastError();
+    }
+    const bool use_packed = packed && scale_bits <= kPackedMaxBits;
+    const size_t lut = decode_lut_bytes(scale_bits, use_packed);
+    // warps per CTA: fill the SM (up to 64 warps) given the per-CTA LUT copy
+    int warps = 8;
+    const size_t smem_cap = 227 * 1024;
+    if (lut > 48 * 1024) warps = 32;
+    else if (lut > 16 * 1024) warps = 16;
+    while (warps > 1 && lut + size_t(warps) * kWarpSmem > smem_cap) warps >>= 1;
+    const size_t smem = lut + size_t(warps) * kWarpSmem;
+    int64_t blocks = (n_chunks + warps - 1) / warps;
+    const int64_t max_blocks = int64_t(sm_count()) * 64;
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (use_packed) {
+        cudaFuncSetAttribute(decode_warp_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        decode_warp_kernel<true><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
+            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
+            d_out, d_consumed, d_final_states, d_status, scale_bits);
+    } else {
+        cudaFuncSetAttribute(decode_warp_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        decode_warp_kernel<false><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
+            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
+            d_out, d_consumed, d_final_states, d_status, scale_bits);
+    }
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace ilans

@@ -1,0 +1,317 @@
+// encode.cu -- word16 interleaved-rANS encoders for sm_100a, plus framing.
+//
+// Replaces _core.encode_interleaved_u16 (_core.pyx:14-43). The reference
+// walks the message backwards (i = n-1 .. 0, lane = i mod N), spills one
+// 16-bit digit when x >= f << (32 - sb), then pushes
+// x -> (x / f << sb) + cum + x % f, stacking digits from the end of an
+// n-word buffer. Group form (lanes.encode_step / packed_store,
+// lanes.py:124-181; encode_lanes_full, lanes.py:235-252): the tail group
+// first, then full groups backwards; inside a group the spilling lanes'
+// digits occupy the next popc(mask) stack slots so that, read forwards, they
+// appear in ascending lane order -- lane i writes at
+// top - popc(mask) + popc(mask & lanemask_lt(i)).
+//
+// Warp kernel (N <= 32): one warp per chunk; message bytes are staged
+// backwards into a per-warp 2 KB shared ring by cp.async (4 x 512 B
+// segments); the per-symbol record {f, cum, magic, shifts} lives in shared
+// memory, and x / f is an exact multiply-high (Granlund-Montgomery), no
+// hardware divide. Block kernel (N > 32): one CTA per stream with a
+// CTA-wide scan over spill counts.
+//
+// Framing: chunk k's payload sits at scratch[k*C + len_k - w_k, k*C + len_k);
+// an exclusive scan of w_k gives word offsets and a compaction kernel packs
+// the payloads back to back (SURVEY A12 chunk framing).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ilans {
+
+constexpr int kInSeg = 512;            // bytes per cp.async warp-copy
+constexpr int kInRing = 4 * kInSeg;    // 2 KB per warp
+
+__device__ __forceinline__ void issue_msg_segment(uint8_t *ring, const uint8_t *g, int64_t len,
+                                                  int64_t seg, int lane) {
+    const int64_t b0 = seg * kInSeg + lane * 16;
+    uint32_t bytes = 0;
+    if (seg >= 0 && b0 < len) bytes = (len - b0) >= 16 ? 16u : static_cast<uint32_t>(len - b0);
+    const uint8_t *src = bytes ? g + b0 : g;
+    cp_async16(ring + (static_cast<uint32_t>(seg) & 3u) * kInSeg + lane * 16, src, bytes);
+}
+
+__global__ void __launch_bounds__(256)
+encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
+                   int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                   uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
+                   uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
+    __shared__ uint4 enc[kMaxSym];
+    __shared__ __align__(16) uint8_t rings[8][kInRing];
+    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
+    __syncthreads();
+    const int sb = static_cast<int>(tab->scale_bits);
+    const int thr_shift = 32 - sb;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    uint8_t *ring = rings[wib];
+    const uint32_t lt = lanemask_lt();
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; k < n_chunks;
+         k += warps_total) {
+        const int64_t cbase = k * chunk_len;
+        const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+        const uint8_t *g = msg + cbase;
+        uint16_t *out = scratch + cbase;
+        int64_t cur = (len - 1) >> 9;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            issue_msg_segment(ring, g, len, cur - s, lane);
+            cp_async_commit();
+        }
+        cp_async_wait<2>();
+        __syncwarp();
+
+        uint32_t x = kLow;
+        int64_t top = len;
+        const int64_t groups = (len + n_lanes - 1) / n_lanes;
+        bool bad = false;
+        for (int64_t gi = groups - 1; gi >= 0; --gi) {
+            const int64_t base = gi * n_lanes;
+            const int64_t left = len - base;
+            const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
+            const int64_t hi = (base + active - 1) >> 9;
+            if (hi != cur) {  // segment cur fully consumed: recycle its slot
+                cur = hi;
+                __syncwarp();
+                issue_msg_segment(ring, g, len, cur - 3, lane);
+                cp_async_commit();
+                cp_async_wait<2>();
+                __syncwarp();
+            }
+            const bool on = lane < active;
+            const uint32_t s = on ? ring[(base + lane) & (kInRing - 1)] : 0u;
+            const uint4 e = enc[s];
+            const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.x == 0u);
+            if (badmask) {
+                if (lane == 0)
+                    atomicMax(&status->unenc_index,
+                              static_cast<long long>(cbase + base + 31 - __clz(badmask)));
+                bad = true;
+                break;
+            }
+            const bool spill = on && (x >> thr_shift) >= e.x;
+            const uint32_t mk = __ballot_sync(0xffffffffu, spill);
+            const int cnt = __popc(mk);
+            if (spill) {
+                out[top - cnt + __popc(mk & lt)] = static_cast<uint16_t>(x & 0xFFFFu);
+                x >>= 16;
+            }
+            top -= cnt;
+            if (on) {
+                const uint32_t q = div_magic(x, e.z, e.w & 0xFFu, (e.w >> 8) & 0xFFu);
+                x = (q << sb) + e.y + (x - q * e.x);
+            }
+        }
+        if (!bad) {
+            if (lane == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
+            if (lane < n_lanes) states_out[k * n_lanes + lane] = x;
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+    }
+}
+
+__device__ __forceinline__ uint32_t block_excl_scan_e(uint32_t v, uint32_t *total,
+                                                      uint32_t *sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+    }
+    if (lane == 31) sh[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < nw ? sh[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += u;
+        }
+        sh[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t off = wid ? sh[wid - 1] : 0u;
+    *total = sh[nw - 1];
+    __syncthreads();
+    return off + inc - v;
+}
+
+// One CTA per stream, N > 32: thread t owns lanes [t*k, t*k + k), k <= 64.
+__global__ void __launch_bounds__(1024)
+encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
+                    int n_lanes, const TableDev *__restrict__ tab,
+                    uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
+                    uint32_t *__restrict__ states_out, DStatus *__restrict__ status,
+                    uint32_t *__restrict__ ws_all) {
+    __shared__ uint32_t scan_sh[32];
+    __shared__ uint4 enc[kMaxSym];
+    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
+    __syncthreads();
+    const int64_t k = blockIdx.x;
+    const int64_t cbase = k * chunk_len;
+    const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+    const uint8_t *g = msg + cbase;
+    uint16_t *out = scratch + cbase;
+    uint32_t *ws = ws_all + k * n_lanes;
+    const int sb = static_cast<int>(tab->scale_bits);
+    const int thr_shift = 32 - sb;
+    const int per = (n_lanes + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per;
+    for (int l = lo; l < lo + per && l < n_lanes; ++l) ws[l] = kLow;
+    int64_t top = len;
+    const int64_t groups = (len + n_lanes - 1) / n_lanes;
+    bool bad = false;
+    for (int64_t gi = groups - 1; gi >= 0; --gi) {
+        const int64_t base = gi * n_lanes;
+        const int64_t left = len - base;
+        const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
+        const int hi = lo + per < active ? lo + per : active;
+        uint64_t spill = 0;
+        uint32_t cnt = 0;
+        long long my_bad = -1;
+        for (int l = lo; l < hi; ++l) {
+            const uint32_t f = enc[g[base + l]].x;
+            if (f == 0u) my_bad = base + l;
+            else if ((ws[l] >> thr_shift) >= f) {
+                spill |= 1ull << (l - lo);
+                ++cnt;
+            }
+        }
+        if (__syncthreads_or(my_bad >= 0)) {
+            if (my_bad >= 0) atomicMax(&status->unenc_index, static_cast<long long>(cbase + my_bad));
+            bad = true;
+            break;
+        }
+        uint32_t total;
+        const uint32_t excl = block_excl_scan_e(cnt, &total, scan_sh);
+        uint32_t r = 0;
+        while (spill) {
+            const int j = __ffsll(static_cast<long long>(spill)) - 1;
+            spill &= spill - 1;
+            const int l = lo + j;
+            out[top - total + excl + r] = static_cast<uint16_t>(ws[l] & 0xFFFFu);
+            ws[l] >>= 16;
+            ++r;
+        }
+        top -= total;
+        for (int l = lo; l < hi; ++l) {
+            const uint4 e = enc[g[base + l]];
+            const uint32_t x = ws[l];
+            const uint32_t q = div_magic(x, e.z, e.w & 0xFFu, (e.w >> 8) & 0xFFu);
+            ws[l] = (q << sb) + e.y + (x - q * e.x);
+        }
+    }
+    if (!bad) {
+        if (threadIdx.x == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
+        for (int l = lo; l < lo + per && l < n_lanes; ++l) states_out[k * n_lanes + l] = ws[l];
+    }
+}
+
+cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, int n_lanes,
+                          const TableDev *d_table, uint16_t *d_scratch,
+                          uint32_t *d_chunk_words, uint32_t *d_states, DStatus *d_status,
+                          uint32_t *d_lane_ws, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
+    if (n_lanes > 32) {
+        const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
+        encode_block_kernel<<<static_cast<unsigned>(n_chunks), threads, 0, stream>>>(
+            d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states,
+            d_status, d_lane_ws);
+    } else {
+        constexpr int warps = 8;
+        int64_t blocks = (n_chunks + warps - 1) / warps;
+        const int64_t max_blocks = int64_t(sm_count()) * 32;
+        if (blocks > max_blocks) blocks = max_blocks;
+        encode_warp_kernel<<<static_cast<unsigned>(blocks), warps * 32, 0, stream>>>(
+            d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_chunk_words,
+            d_states, d_status);
+    }
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Framing
+// ---------------------------------------------------------------------------
+// Single CTA exclusive scan of n_chunks word counts -> offsets[n_chunks + 1].
+__global__ void __launch_bounds__(1024)
+chunk_offsets_kernel(const uint32_t *__restrict__ words, int64_t n_chunks,
+                     uint64_t *__restrict__ offsets) {
+    __shared__ unsigned long long wsum[32];
+    __shared__ unsigned long long carry;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n_chunks; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const unsigned long long v = i < n_chunks ? words[i] : 0ull;
+        unsigned long long inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) wsum[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            unsigned long long w = lane < int(blockDim.x >> 5) ? wsum[lane] : 0ull;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long u = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += u;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const unsigned long long excl = carry + (wid ? wsum[wid - 1] : 0ull) + inc - v;
+        if (i < n_chunks) offsets[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += wsum[(blockDim.x >> 5) - 1];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) offsets[n_chunks] = carry;
+}
+
+// One CTA per chunk: move its payload from the end of its scratch region to
+// the packed position.
+__global__ void __launch_bounds__(256)
+compact_kernel(const uint16_t *__restrict__ scratch, int64_t n, int64_t chunk_len,
+               const uint32_t *__restrict__ words, const uint64_t *__restrict__ offsets,
+               uint16_t *__restrict__ payload) {
+    const int64_t k = blockIdx.x;
+    const int64_t cbase = k * chunk_len;
+    const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+    const uint32_t w = words[k];
+    const uint16_t *src = scratch + cbase + len - w;
+    uint16_t *dst = payload + offsets[k];
+    for (uint32_t i = threadIdx.x; i < w; i += blockDim.x) dst[i] = __ldcs(src + i);
+}
+
+cudaError_t launch_frame(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
+                         const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
+                         uint16_t *d_payload, cudaStream_t stream) {
+    const int64_t n_chunks = n <= 0 ? 0 : (n + chunk_len - 1) / chunk_len;
+    chunk_offsets_kernel<<<1, 1024, 0, stream>>>(d_chunk_words, n_chunks, d_word_offsets);
+    ilans_note_launch();
+    if (n_chunks > 0) {
+        compact_kernel<<<static_cast<unsigned>(n_chunks), 256, 0, stream>>>(
+            d_scratch, n, chunk_len, d_chunk_words, d_word_offsets, d_payload);
+        ilans_note_launch();
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace ilans

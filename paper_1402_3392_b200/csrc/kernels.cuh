@@ -1,0 +1,48 @@
+// kernels.cuh -- kernel declarations and host-side launchers shared between
+// the translation units of libilans_b200.so.
+#pragma once
+
+#include "common.cuh"
+
+namespace ilans {
+
+// table.cu
+__global__ void histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
+                                    unsigned long long *__restrict__ counts);
+__global__ void build_table_kernel(const unsigned long long *__restrict__ counts,
+                                   const uint32_t *freq_in, int n_freq, const uint32_t *cum_in,
+                                   const uint8_t *slot_in, int scale_bits, TableDev *t);
+
+// Host launchers (all asynchronous on `stream`; return cudaError_t).
+cudaError_t launch_histogram(const uint8_t *d_msg, int64_t n, unsigned long long *d_counts,
+                             cudaStream_t stream);
+cudaError_t launch_build_table(const unsigned long long *d_counts, const uint32_t *d_freq,
+                               int n_freq, const uint32_t *d_cum, const uint8_t *d_slot,
+                               int scale_bits, TableDev *d_table, cudaStream_t stream);
+
+// encode.cu -- chunked encode (N <= 32: one warp per chunk; N > 32: one CTA
+// per stream), then framing (scan + compaction).
+cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, int n_lanes,
+                          const TableDev *d_table, uint16_t *d_scratch,
+                          uint32_t *d_chunk_words, uint32_t *d_states, DStatus *d_status,
+                          uint32_t *d_lane_ws, cudaStream_t stream);
+cudaError_t launch_frame(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
+                         const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
+                         uint16_t *d_payload, cudaStream_t stream);
+
+// decode.cu
+cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offsets,
+                          const uint32_t *d_states, int64_t n, int64_t chunk_len, int n_lanes,
+                          const TableDev *d_table, int scale_bits, bool packed,
+                          uint8_t *d_out, uint64_t *d_consumed, uint32_t *d_final_states,
+                          DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream);
+
+// synth.cu
+cudaError_t launch_synth(uint8_t *d_out, int64_t n, uint64_t seed, int64_t first_index,
+                         const uint32_t *d_cdf, cudaStream_t stream);
+
+__global__ void dstatus_reset_kernel(DStatus *s);
+
+int sm_count();
+
+}  // namespace ilans

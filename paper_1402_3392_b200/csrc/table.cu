@@ -1,0 +1,364 @@
+// table.cu -- model builder on the device: byte histogram, bit-exact
+// quantize (rans.quantize, rans.py:171-211) and the lookup tables the coders
+// use (SymbolTable, rans.py:99-146).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ilans {
+
+// ---------------------------------------------------------------------------
+// Histogram (np.bincount at cli.py:31-37 / bench.py:47-51)
+//
+// HBM-bound streaming read. Every thread owns a private column of 8-bit
+// counters (256 bins x 256 threads = 64 KB of shared memory), laid out so a
+// warp's 32 increments always hit 32 distinct banks whatever the byte values
+// (bank = lane): byte (bin, w, l) lives at bin*256 + ((w>>2)*32 + l)*4 + (w&3).
+// No atomics, so a 1-bit-entropy source (80% of bytes in one bin) costs the
+// same as a uniform one. Counters flush every 240 bytes per thread (before an
+// 8-bit counter can wrap): thread t sums bin t's 256 counters with
+// dp4a, reading the 64 words in a per-thread staggered order (conflict-free),
+// and zeroes them.
+// ---------------------------------------------------------------------------
+constexpr int kHistThreads = 256;
+constexpr int kHistVecPerRound = 15;  // 15 x 16 B = 240 bytes < 256 per counter
+
+__device__ __forceinline__ uint32_t hist_byte_offset(uint32_t bin, uint32_t tid) {
+    const uint32_t w = tid >> 5, l = tid & 31;
+    return bin * 256u + (((w >> 2) * 32u + l) << 2) + (w & 3u);
+}
+
+__device__ __forceinline__ void hist_bump(uint8_t *h, uint32_t tid, uint32_t b) {
+    uint8_t *p = h + hist_byte_offset(b, tid);
+    *p = static_cast<uint8_t>(*p + 1);
+}
+
+__device__ __forceinline__ void hist_bump16(uint8_t *h, uint32_t tid, uint4 v) {
+    const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) hist_bump(h, tid, (words[q] >> (8 * j)) & 0xFFu);
+    }
+}
+
+// thread t: add the 256 counters of bin t into acc and zero them.
+__device__ __forceinline__ void hist_flush(uint8_t *h, uint32_t tid, unsigned long long &acc) {
+    uint32_t *row = reinterpret_cast<uint32_t *>(h + tid * 256u);
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (int k = 0; k < 64; ++k) {
+        const int idx = (k + static_cast<int>(tid)) & 63;
+        sum = __dp4a(row[idx], 0x01010101u, sum);
+        row[idx] = 0;
+    }
+    acc += sum;
+}
+
+__global__ void __launch_bounds__(kHistThreads)
+histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
+                    unsigned long long *__restrict__ counts) {
+    extern __shared__ __align__(16) uint8_t hist_smem[];
+    const uint32_t tid = threadIdx.x;
+    uint32_t *z = reinterpret_cast<uint32_t *>(hist_smem);
+    for (uint32_t i = tid; i < 256u * 256u / 4u; i += kHistThreads) z[i] = 0;
+    __syncthreads();
+
+    // unaligned head / tail bytes: block 0, thread 0 (its own counters)
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(msg);
+    int64_t head = static_cast<int64_t>((16 - (addr & 15)) & 15);
+    if (head > n) head = n;
+    const int64_t nvec = (n - head) >> 4;
+    const int64_t tail_start = head + (nvec << 4);
+    unsigned long long acc = 0;
+    if (blockIdx.x == 0 && tid == 0) {
+        for (int64_t i = 0; i < head; ++i) hist_bump(hist_smem, 0, msg[i]);
+        for (int64_t i = tail_start; i < n; ++i) hist_bump(hist_smem, 0, msg[i]);
+    }
+    __syncthreads();
+    hist_flush(hist_smem, tid, acc);
+    __syncthreads();
+
+    const uint4 *vec = reinterpret_cast<const uint4 *>(msg + head);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kHistThreads;
+    int64_t i = static_cast<int64_t>(blockIdx.x) * kHistThreads + tid;
+    // rounds: every thread does <= 15 vectors, then the block flushes
+    const int64_t per_round = stride * kHistVecPerRound;
+    for (int64_t round_base = 0; round_base < nvec; round_base += per_round) {
+#pragma unroll 1
+        for (int r = 0; r < kHistVecPerRound; ++r) {
+            const int64_t j = i + round_base + static_cast<int64_t>(r) * stride;
+            if (j < nvec) hist_bump16(hist_smem, tid, __ldcs(vec + j));
+        }
+        __syncthreads();
+        hist_flush(hist_smem, tid, acc);
+        __syncthreads();
+    }
+    if (acc) atomicAdd(counts + tid, acc);
+}
+
+// ---------------------------------------------------------------------------
+// Quantize + tables: one CTA of 256 threads, thread i owns symbol i.
+// ---------------------------------------------------------------------------
+typedef unsigned __int128 u128;
+
+struct I128 {  // signed 128-bit comparison key as (hi:int64, lo:uint64)
+    long long hi;
+    unsigned long long lo;
+};
+__device__ __forceinline__ I128 to_i128(u128 a_minus_b_pos, bool neg) {
+    u128 v = neg ? (u128)0 - a_minus_b_pos : a_minus_b_pos;
+    I128 r;
+    r.hi = static_cast<long long>(static_cast<unsigned long long>(v >> 64));
+    r.lo = static_cast<unsigned long long>(v);
+    return r;
+}
+__device__ __forceinline__ bool gt(const I128 &a, const I128 &b) {
+    return a.hi != b.hi ? a.hi > b.hi : a.lo > b.lo;
+}
+__device__ __forceinline__ bool eq(const I128 &a, const I128 &b) {
+    return a.hi == b.hi && a.lo == b.lo;
+}
+// a - b for unsigned 128-bit a, b as a signed key
+__device__ __forceinline__ I128 sub_key(u128 a, u128 b) {
+    return a >= b ? to_i128(a - b, false) : to_i128(b - a, true);
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum_256(T v, T *red) {
+    const int tid = threadIdx.x;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    T s = 0;
+#pragma unroll
+    for (int w = 0; w < kMaxSym / 32; ++w) s += red[w];
+    __syncthreads();
+    return s;
+}
+
+__device__ __forceinline__ int block_max_256(int v, int *red) {
+    const int tid = threadIdx.x;
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    int s = red[0];
+#pragma unroll
+    for (int w = 1; w < kMaxSym / 32; ++w) s = max(s, red[w]);
+    __syncthreads();
+    return s;
+}
+
+// floor(c * m / T) for c*m < 2^81, result <= m <= 2^16: binary search on q.
+__device__ __forceinline__ uint32_t floor_cm_over_t(unsigned long long c, uint32_t m,
+                                                    u128 total) {
+    const u128 cm = (u128)c * m;
+    uint32_t lo = 0, hi = m;  // answer in [0, m]
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if ((u128)mid * total <= cm) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Writes freq/cum/enc/dec/slot/packed for the table described by t->freq,
+// t->cum (already in shared `freq`, `cum`). Runs on the whole CTA.
+__device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *cum,
+                            const uint8_t *slot_in, int scale_bits, int *red) {
+    const int tid = threadIdx.x;
+    const uint32_t m = 1u << scale_bits;
+    {
+        const uint32_t f = freq[tid];
+        uint32_t magic = 0, sh1 = 0, sh2 = 0;
+        if (f) divmagic(f, &magic, &sh1, &sh2);
+        t->freq[tid] = f;
+        t->enc[tid] = make_uint4(f, cum[tid], magic, sh1 | (sh2 << 8));
+        t->dec[tid] = make_uint2(f, cum[tid]);
+    }
+    if (tid == 0) t->cum[kMaxSym] = cum[kMaxSym];
+    t->cum[tid] = cum[tid];
+    // slot -> symbol; consistent (packable) check for the sb <= 12 LUT
+    int ok = scale_bits <= kPackedMaxBits ? 1 : 0;
+    for (uint32_t j = tid; j < m; j += kMaxSym) {
+        uint32_t s;
+        if (slot_in) {
+            s = slot_in[j];
+        } else {  // largest s with cum[s] <= j and f[s] > 0
+            int lo = 0, hi = kMaxSym - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (cum[mid] <= j) lo = mid; else hi = mid - 1;
+            }
+            s = static_cast<uint32_t>(lo);
+        }
+        t->slot_sym[j] = static_cast<uint8_t>(s);
+        if (scale_bits <= kPackedMaxBits) {
+            const uint32_t f = freq[s];
+            const uint32_t bias = j - cum[s];
+            if (f < 1 || f > 4096 || bias >= 4096) ok = 0;
+            t->packed[j] = s | ((f - 1u) & 0xFFFu) << 8 | (bias & 0xFFFu) << 20;
+        }
+    }
+    __syncthreads();
+    const int all_ok = -block_max_256(-ok, red);  // min over threads
+    if (tid == 0) t->flags = all_ok ? kTabPacked : 0u;
+}
+
+// mode: counts != nullptr -> quantize(counts) first (alphabet = max+1).
+//       otherwise freq_in/cum_in/slot_in as given (drop-in decode/encode).
+__global__ void __launch_bounds__(kMaxSym)
+build_table_kernel(const unsigned long long *__restrict__ counts, const uint32_t *freq_in,
+                   int n_freq, const uint32_t *cum_in, const uint8_t *slot_in, int scale_bits,
+                   TableDev *t) {
+    __shared__ uint32_t freq[kMaxSym];
+    __shared__ uint32_t cum[kMaxSym + 1];
+    __shared__ I128 keys[kMaxSym];
+    __shared__ unsigned long long red64[8];
+    __shared__ int red[8];
+    __shared__ int status_sh;
+    const int tid = threadIdx.x;
+    if (tid == 0) status_sh = ILANS_OK;
+    if (tid < 4) t->err_detail[tid] = 0;
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits) {
+        if (tid == 0) { t->status = ILANS_ERR_VALUE; t->err_detail[0] = 1; t->scale_bits = scale_bits; }
+        return;
+    }
+    const uint32_t m = 1u << scale_bits;
+    int n_sym;
+    if (counts) {
+        // ---- rans.quantize (rans.py:171-211), bit-exact ------------------
+        unsigned long long c = counts[tid];
+        const int alpha = block_max_256(c ? tid + 1 : 0, red);
+        n_sym = alpha;
+        if (alpha == 0) {  // empty message -> counts [1, 1] (cli.py:32-34)
+            n_sym = 2;
+            c = tid < 2 ? 1ull : 0ull;
+        }
+        const int present = block_sum_256<int>(c ? 1 : 0, red);
+        u128 total = 0;
+        {
+            // 128-bit sum as two 64-bit halves
+            const unsigned long long lo = block_sum_256<unsigned long long>(c & 0xFFFFFFFFull, red64);
+            const unsigned long long hi = block_sum_256<unsigned long long>(c >> 32, red64);
+            total = ((u128)hi << 32) + lo;
+        }
+        if (static_cast<uint32_t>(present) > m) {
+            if (tid == 0) {
+                t->status = ILANS_ERR_VALUE;
+                t->err_detail[0] = 2;
+                t->err_detail[1] = present;
+                t->err_detail[2] = m;
+                t->n_sym = n_sym;
+                t->scale_bits = scale_bits;
+            }
+            return;
+        }
+        uint32_t f = 0;
+        if (c) {
+            f = floor_cm_over_t(c, m, total);
+            if (f < 1) f = 1;
+        }
+        const long long diff =
+            static_cast<long long>(m) - block_sum_256<long long>(static_cast<long long>(f), reinterpret_cast<long long *>(red64));
+        const u128 cm = (u128)c * m;
+        if (diff > 0) {
+            // picks are the top-`diff` present symbols by (c*m - f*T, -i):
+            // with diff > 0 every key is < T and >= diff+1 keys are > 0, so
+            // no symbol is picked twice.
+            keys[tid] = sub_key(cm, (u128)f * total);
+            freq[tid] = c ? 1u : 0u;  // presence flag
+            __syncthreads();
+            if (c) {
+                const I128 my = keys[tid];
+                int rank = 0;
+                for (int j = 0; j < kMaxSym; ++j) {
+                    if (!freq[j]) continue;
+                    const I128 o = keys[j];
+                    rank += (gt(o, my) || (eq(o, my) && j < tid)) ? 1 : 0;
+                }
+                if (rank < diff) f += 1;
+            }
+            __syncthreads();
+        } else if (diff < 0) {
+            // -1 rounds: round r takes every symbol with f >= r+2, ordered by
+            // (f*T - c*m, -i); all keys of round r exceed all keys of round
+            // r+1, so R full rounds take sum(min(R, f-1)) units.
+            const long long need = -diff;
+            uint32_t lo = 0, hi = m;  // largest R with P(R) <= need
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                const long long take = (c && f > 1) ? static_cast<long long>(min(mid, f - 1)) : 0;
+                const long long P = block_sum_256<long long>(take, reinterpret_cast<long long *>(red64));
+                if (P <= need) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t R = lo;
+            const long long took = (c && f > 1) ? static_cast<long long>(min(R, f - 1)) : 0;
+            const long long rem = need - block_sum_256<long long>(took, reinterpret_cast<long long *>(red64));
+            keys[tid] = sub_key((u128)f * total, cm);
+            freq[tid] = (c && f >= R + 2) ? 1u : 0u;  // eligible in round R
+            __syncthreads();
+            uint32_t dec = static_cast<uint32_t>(took);
+            if (freq[tid]) {
+                const I128 my = keys[tid];
+                int rank = 0;
+                for (int j = 0; j < kMaxSym; ++j) {
+                    if (!freq[j]) continue;
+                    const I128 o = keys[j];
+                    rank += (gt(o, my) || (eq(o, my) && j < tid)) ? 1 : 0;
+                }
+                if (rank < rem) dec += 1;
+            }
+            __syncthreads();
+            f -= dec;
+        }
+        freq[tid] = tid < n_sym ? f : 0u;
+        __syncthreads();
+    } else {
+        n_sym = n_freq;
+        freq[tid] = (tid < n_freq && freq_in) ? freq_in[tid] : 0u;
+        __syncthreads();
+        if (!cum_in) {  // model from frequencies alone: must sum to 2^sb (rans.py:110-112)
+            const long long sum = block_sum_256<long long>(static_cast<long long>(freq[tid]),
+                                                           reinterpret_cast<long long *>(red64));
+            if (sum != static_cast<long long>(m)) {
+                if (tid == 0) {
+                    t->status = ILANS_ERR_VALUE;
+                    t->err_detail[0] = 3;
+                    t->n_sym = n_sym;
+                    t->scale_bits = scale_bits;
+                }
+                return;
+            }
+        }
+    }
+    // cum: given (drop-in calls) or exclusive prefix of freq
+    if (cum_in) {
+        cum[tid] = tid <= n_sym ? cum_in[tid] : 0u;
+        if (tid == 0) cum[kMaxSym] = n_sym >= kMaxSym ? cum_in[kMaxSym] : 0u;
+        __syncthreads();
+    } else {
+        // inclusive warp scan then warp offsets
+        uint32_t v = freq[tid];
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if ((tid & 31) >= o) v += u;
+        }
+        __shared__ uint32_t wsum[8];
+        if ((tid & 31) == 31) wsum[tid >> 5] = v;
+        __syncthreads();
+        uint32_t off = 0;
+        for (int w = 0; w < (tid >> 5); ++w) off += wsum[w];
+        cum[tid + 1] = v + off;
+        if (tid == 0) cum[0] = 0;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        t->scale_bits = scale_bits;
+        t->n_sym = n_sym;
+        t->status = status_sh;
+    }
+    fill_tables(t, freq, cum, slot_in, scale_bits, red);
+}
+
+}  // namespace ilans

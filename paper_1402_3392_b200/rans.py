@@ -1,0 +1,209 @@
+"""rANS model objects: renorm variants, the quantized symbol table, quantize.
+
+API-compatible with the reference module (pkg/src/ilans/rans.py). The
+numeric work -- quantize (rans.py:171-211) and, in the chunked pipeline,
+the histogram and every lookup table -- runs on the B200 through
+libilans_b200.so. SymbolTable keeps the reference's host-side fields
+(freq / cum lists, slot view) because callers read them; the device builds
+its own tables from the same frequencies.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+from functools import cached_property
+
+import numpy as np
+
+from . import _lib
+from .errors import FormatError, TruncatedStreamError, UnencodableSymbolError
+
+MAX_ALPHABET = 256
+MAX_SCALE_BITS = 16
+
+__all__ = [
+    "RenormVariant",
+    "BYTE8",
+    "WORD16",
+    "SymbolTable",
+    "quantize",
+    "encode_threshold",
+    "serialize_table",
+    "parse_table",
+    "variant_by_tag",
+]
+
+
+@dataclass(frozen=True)
+class RenormVariant:
+    """Digit width plus the lower bound L of the normalized state interval
+    (reference rans.py:45-83). The B200 kernels implement WORD16 (16-bit
+    digits, L = 2^16), where one spill / refill per symbol always suffices."""
+
+    tag: str
+    digit_bits: int
+    lower_bound: int
+
+    def __post_init__(self):
+        if not 1 <= self.digit_bits <= 16:
+            raise ValueError("digit_bits must be in [1, 16]")
+        if self.lower_bound < 1:
+            raise ValueError("lower_bound must be >= 1")
+        if (1 << self.digit_bits) * self.lower_bound > 1 << 32:
+            raise ValueError("radix * lower_bound must fit in 32 bits")
+
+    @property
+    def radix(self) -> int:
+        return 1 << self.digit_bits
+
+    @property
+    def digit_mask(self) -> int:
+        return self.radix - 1
+
+    @property
+    def state_limit(self) -> int:
+        return self.radix * self.lower_bound
+
+    def check_table(self, table: "SymbolTable") -> None:
+        if self.lower_bound % table.total:
+            raise ValueError(
+                f"lower_bound {self.lower_bound} is not a multiple of the table total "
+                f"{table.total}; renormalized coding would not be b-unique"
+            )
+
+
+BYTE8 = RenormVariant("byte8", 8, 1 << 23)
+WORD16 = RenormVariant("word16", 16, 1 << 16)
+_BY_TAG = {v.tag: v for v in (BYTE8, WORD16)}
+
+
+def variant_by_tag(tag: str) -> RenormVariant:
+    if tag not in _BY_TAG:
+        raise ValueError(f"unknown renorm variant {tag!r}")
+    return _BY_TAG[tag]
+
+
+def quantize(counts, scale_bits: int) -> list[int]:
+    """Counts -> integer frequencies summing to 2**scale_bits, bit-identical
+    to the reference largest-remainder quantizer (rans.py:171-211), computed
+    by the device model builder (csrc/table.cu, build_table_kernel)."""
+    counts = [int(c) for c in counts]
+    if not 1 <= scale_bits <= MAX_SCALE_BITS:
+        raise ValueError(f"scale_bits must be in [1, {MAX_SCALE_BITS}]")
+    if len(counts) > MAX_ALPHABET:
+        raise ValueError(f"alphabet size must be <= {MAX_ALPHABET}")
+    if any(c < 0 for c in counts):
+        raise ValueError("counts must be non-negative")
+    if any(c >= 1 << 64 for c in counts):
+        raise ValueError("counts must fit in 64 bits")
+    arr = np.ascontiguousarray(counts, dtype=np.uint64)
+    out = np.zeros(max(1, len(counts)), dtype=np.uint32)
+    st = _lib.Status()
+    rc = _lib.lib.ilans_quantize(_lib.ptr(arr), len(counts), scale_bits, _lib.ptr(out),
+                                 _lib.ctypes.byref(st))
+    _lib.raise_for(rc, st, "quantize")
+    return out[: len(counts)].tolist()
+
+
+class SymbolTable:
+    """Quantized frequencies plus cumulative offsets and slot lookup
+    (reference rans.py:99-168). Equality is (scale_bits, freq list)."""
+
+    def __init__(self, freqs, scale_bits: int):
+        if not 1 <= scale_bits <= MAX_SCALE_BITS:
+            raise ValueError(f"scale_bits must be in [1, {MAX_SCALE_BITS}]")
+        freqs = [int(f) for f in freqs]
+        if not 1 <= len(freqs) <= MAX_ALPHABET:
+            raise ValueError(f"alphabet size must be in [1, {MAX_ALPHABET}]")
+        if min(freqs) < 0:
+            raise ValueError("frequencies must be non-negative")
+        if sum(freqs) != 1 << scale_bits:
+            raise ValueError(f"frequencies must sum to {1 << scale_bits}, got {sum(freqs)}")
+        self.scale_bits = scale_bits
+        self.freq = freqs
+        self.cum = [0, *np.cumsum(freqs).tolist()]
+
+    @classmethod
+    def from_counts(cls, counts, scale_bits: int = 14) -> "SymbolTable":
+        return cls(quantize(counts, scale_bits), scale_bits)
+
+    @property
+    def total(self) -> int:
+        return 1 << self.scale_bits
+
+    @property
+    def alphabet_size(self) -> int:
+        return len(self.freq)
+
+    @cached_property
+    def freq_u32(self) -> np.ndarray:
+        return np.asarray(self.freq, dtype=np.uint32)
+
+    @cached_property
+    def cum_u32(self) -> np.ndarray:
+        return np.asarray(self.cum, dtype=np.uint32)
+
+    @cached_property
+    def slot_u8(self) -> np.ndarray:
+        """Dense slot -> symbol view (rans.py:119-121) passed to decode calls."""
+        return np.repeat(np.arange(self.alphabet_size, dtype=np.uint8), self.freq_u32)
+
+    @property
+    def slot_to_symbol(self) -> list[int]:
+        return self.slot_u8.tolist()
+
+    def model_entropy_bits(self) -> float:
+        """Entropy of the quantized distribution, bits per symbol."""
+        f = self.freq_u32[self.freq_u32 > 0].astype(np.float64) / self.total
+        return float(-(f * np.log2(f)).sum())
+
+    def ideal_bits(self, symbols) -> float:
+        """Sum of -log2(f_s / m) over a message (rans.py:153-158)."""
+        f = self.freq_u32[np.asarray(symbols, dtype=np.uint8)].astype(np.float64)
+        if (f == 0).any():
+            raise UnencodableSymbolError("message contains zero-frequency symbols")
+        return float((self.scale_bits - np.log2(f)).sum())
+
+    def __eq__(self, other):
+        return (
+            isinstance(other, SymbolTable)
+            and self.scale_bits == other.scale_bits
+            and self.freq == other.freq
+        )
+
+    __hash__ = None
+
+    def __repr__(self):
+        return f"SymbolTable(n={self.alphabet_size}, scale_bits={self.scale_bits})"
+
+
+def encode_threshold(table: SymbolTable, variant: RenormVariant, symbol: int) -> int:
+    """Exclusive upper state bound before pushing ``symbol`` (rans.py:229-232)."""
+    return table.freq[symbol] * (variant.state_limit >> table.scale_bits)
+
+
+def serialize_table(table: SymbolTable) -> bytes:
+    """scale_bits u8, alphabet u16 LE, then u16 LE frequencies (rans.py:332-338)."""
+    if max(table.freq) > 0xFFFF:
+        raise FormatError("frequency 65536 does not fit the u16 table field")
+    return struct.pack("<BH", table.scale_bits, table.alphabet_size) + table.freq_u32.astype(
+        "<u2"
+    ).tobytes()
+
+
+def parse_table(buf: bytes, offset: int = 0) -> tuple[SymbolTable, int]:
+    """Inverse of serialize_table (rans.py:341-355)."""
+    if len(buf) < offset + 3:
+        raise TruncatedStreamError("table header truncated")
+    scale_bits, n = struct.unpack_from("<BH", buf, offset)
+    offset += 3
+    if len(buf) < offset + 2 * n:
+        raise TruncatedStreamError("frequency table truncated")
+    freqs = np.frombuffer(buf, dtype="<u2", count=n, offset=offset).tolist()
+    offset += 2 * n
+    try:
+        table = SymbolTable(freqs, scale_bits)
+    except ValueError as exc:
+        raise FormatError(f"invalid frequency table: {exc}") from exc
+    return table, offset

@@ -1,0 +1,265 @@
+"""Parity of the B200 path against the oracle and the reference's golden
+fixtures. Every call here goes through libilans_b200.so (C ABI) into the
+sm_100a kernels; results must be bit-exact: identical tables, payloads,
+final states, consumed counts and decoded bytes."""
+
+import hashlib
+import warnings
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1402_3392_b200 as ilb
+from conftest import ZIPF_1MIB_DIGESTS, zipf_1mib
+from paper_1402_3392_b200 import _lib, backend, rans
+from paper_1402_3392_b200.errors import (
+    FormatError,
+    TrailingGarbageWarning,
+    TruncatedStreamError,
+    UnencodableSymbolError,
+)
+from paper_1402_3392_b200.interleave import Container
+from paper_1402_3392_b200.rans import WORD16, SymbolTable
+
+pytestmark = pytest.mark.gpu
+
+B = backend.B200
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device: the -m gpu suite must run on a B200")
+
+
+def random_table(rng, max_n=256, max_sb=16):
+    n = int(rng.integers(1, max_n + 1))
+    sb = int(rng.integers(max(1, (n - 1).bit_length()), max_sb + 1))
+    counts = rng.integers(0, 1000, size=n)
+    counts[int(rng.integers(0, n))] += 1
+    return SymbolTable(oracle.quantize(counts, sb), sb)
+
+
+def random_message(rng, table, n):
+    return rng.choice(table.alphabet_size, size=n, p=table.freq_u32 / table.total).astype(np.uint8)
+
+
+# ---------------------------------------------------------------- golden ---
+def test_kernels_match_reference_fixtures(golden_codec, golden_meta):
+    for case in golden_meta["codec"]:
+        k, lanes, sb = case["case"], case["lanes"], case["scale_bits"]
+        msg = golden_codec[f"c{k}_msg"]
+        t = SymbolTable(golden_codec[f"c{k}_freq"].tolist(), sb)
+        payload, states = B.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, lanes)
+        assert np.array_equal(payload, golden_codec[f"c{k}_payload"]), case
+        assert np.array_equal(states, golden_codec[f"c{k}_states"]), case
+        out, consumed = B.decode_interleaved_u16(payload, states, t.slot_u8, t.freq_u32,
+                                                 t.cum_u32, sb, len(msg), lanes)
+        assert np.array_equal(out, msg) and consumed == len(payload), case
+        if lanes <= 32:
+            out2, consumed2 = B.decode_lanes_u16(payload, states, t.slot_u8, t.freq_u32,
+                                                 t.cum_u32, sb, len(msg), lanes)
+            assert np.array_equal(out2, msg) and consumed2 == len(payload), case
+        if case["sha256"] is not None:
+            c = Container(WORD16, lanes, len(msg), t, tuple(int(x) for x in states), payload)
+            assert hashlib.sha256(c.to_bytes()).hexdigest() == case["sha256"]
+
+
+def test_quantize_matches_reference_fixtures(golden_quantize, golden_meta):
+    for case in golden_meta["quantize"]:
+        k = case["case"]
+        counts = golden_quantize[f"q{k}_counts"]
+        want = golden_quantize[f"q{k}_freq"].tolist()
+        assert rans.quantize(counts.tolist(), case["scale_bits"]) == want, case
+
+
+def test_quantize_known_answers_and_errors():
+    assert rans.quantize([1, 3], 2) == [1, 3]
+    assert rans.quantize([9, 9, 9, 9], 2) == [1, 1, 1, 1]
+    assert rans.quantize([10**6, 1], 14) == [16383, 1]
+    assert rans.quantize([3, 0, 0], 4) == [16, 0, 0]
+    for bad, match in ((([0, 0], 4), "positive"), (([1, 2], 0), "scale_bits"),
+                       (([1] * 300, 12), "alphabet"), (([1] * 5, 2), "too large")):
+        with pytest.raises(ValueError, match=match):
+            rans.quantize(*bad)
+
+
+def test_quantize_fuzz_vs_oracle():
+    rng = np.random.default_rng(11)
+    for _ in range(300):
+        n = int(rng.integers(1, 257))
+        sb = int(rng.integers(max(1, (n - 1).bit_length()), 17))
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            counts = rng.integers(0, 1000, size=n)
+        elif kind == 1:  # forced-to-one heavy (several -1 rounds)
+            counts = np.ones(n, dtype=np.int64)
+            counts[int(rng.integers(0, n))] = int(rng.integers(1, 10**12))
+        else:  # huge totals (> 2^32, u64 counts)
+            counts = rng.integers(0, 2**40, size=n)
+        counts[int(rng.integers(0, n))] += 1
+        assert rans.quantize(counts.tolist(), sb) == oracle.quantize(counts, sb)
+
+
+def test_baseline_md_digests_through_product_api():
+    msg = zipf_1mib()
+    counts, alpha = oracle.histogram(msg)
+    for (lanes, sb), digest in ZIPF_1MIB_DIGESTS.items():
+        t = SymbolTable.from_counts(counts[:alpha].tolist(), sb)
+        c = ilb.encode_interleaved(msg, t, lanes, WORD16)
+        assert hashlib.sha256(c.to_bytes()).hexdigest()[:16] == digest, (lanes, sb)
+        assert np.array_equal(ilb.decode_interleaved(c), msg)
+        if lanes <= 32:
+            assert np.array_equal(ilb.decode_lanes_full(c), msg)
+
+
+# ------------------------------------------------------------ histogram ---
+def test_histogram_matches_bincount():
+    from paper_1402_3392_b200 import chunked  # noqa: F401  (torch-free host path below)
+    import ctypes
+
+    rng = np.random.default_rng(5)
+    cases = [np.zeros(0, np.uint8), np.array([7], np.uint8),
+             rng.integers(0, 256, size=1_000_003).astype(np.uint8),
+             np.full(3_000_001, 200, dtype=np.uint8),  # 1-symbol source
+             (rng.random(2_000_000) < 0.8).astype(np.uint8) * 77]
+    for msg in cases:
+        for off in (0, 1, 5, 15):
+            m = msg[off:] if len(msg) > off else msg
+            counts = np.zeros(256, np.uint64)
+            alpha = ctypes.c_int32(0)
+            st = _lib.Status()
+            rc = _lib.lib.ilans_histogram_u8(_lib.ptr(np.ascontiguousarray(m)), len(m),
+                                             _lib.ptr(counts), ctypes.byref(alpha),
+                                             ctypes.byref(st))
+            _lib.raise_for(rc, st)
+            ref, ref_alpha = oracle.histogram(m)
+            assert np.array_equal(counts, ref) and alpha.value == ref_alpha
+
+
+# ------------------------------------------------------- API behaviour ---
+def test_round_trips_many_shapes():
+    rng = np.random.default_rng(2026)
+    for lanes in (1, 2, 3, 5, 8, 16, 17, 31, 32, 33, 64, 100, 1024, 1500):
+        t = random_table(rng)
+        for n in sorted({0, 1, lanes - 1, lanes, lanes + 1, 2 * lanes + 1, 513, 4097,
+                         int(rng.integers(1000, 20000))}):
+            msg = random_message(rng, t, n)
+            c = ilb.encode_interleaved(msg, t, lanes, WORD16)
+            ref_p, ref_s = oracle.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32,
+                                                         t.scale_bits, lanes)
+            assert np.array_equal(c.payload, ref_p) and c.final_states == tuple(ref_s.tolist())
+            assert np.array_equal(ilb.decode_interleaved(c), msg)
+            if lanes <= 32:
+                assert np.array_equal(ilb.decode_lanes_full(c), msg)
+                assert ilb.encode_lanes_full(msg, t, lanes).to_bytes() == c.to_bytes()
+
+
+def test_max_lanes_65535():
+    rng = np.random.default_rng(9)
+    t = random_table(rng, max_n=20)
+    msg = random_message(rng, t, 200_000)
+    c = ilb.encode_interleaved(msg, t, 65535, WORD16)
+    ref_p, ref_s = oracle.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, t.scale_bits, 65535)
+    assert np.array_equal(c.payload, ref_p) and c.final_states == tuple(ref_s.tolist())
+    assert np.array_equal(ilb.decode_interleaved(c), msg)
+
+
+def test_truncation_raises_like_reference():
+    rng = np.random.default_rng(63)
+    t = random_table(rng)
+    for lanes in (1, 2, 4, 32, 40):
+        msg = random_message(rng, t, 1500)
+        c = ilb.encode_interleaved(msg, t, lanes, WORD16)
+        if len(c.payload) == 0:
+            continue
+        for cut in (0, len(c.payload) // 3, len(c.payload) - 1):
+            c2 = Container(c.variant, c.lane_count, c.message_length, c.table, c.final_states,
+                           c.payload[:cut])
+            with pytest.raises(TruncatedStreamError):
+                ilb.decode_interleaved(c2)
+            if lanes <= 32:
+                with pytest.raises(TruncatedStreamError):
+                    ilb.decode_lanes_full(c2)
+
+
+def test_unencodable_symbol():
+    t = SymbolTable([4, 0], 2)
+    with pytest.raises(UnencodableSymbolError, match="symbol 1"):
+        ilb.encode_interleaved([0, 1, 0], t, 2, WORD16)
+    with pytest.raises(UnencodableSymbolError):
+        ilb.encode_interleaved([0, 1, 0], t, 40, WORD16)
+    with pytest.raises(UnencodableSymbolError):
+        B.encode_interleaved_u16(np.array([0, 1], np.uint8), [4, 0], [0, 4, 4], 2, 1)
+
+
+def test_trailing_garbage_warns():
+    t = SymbolTable([1, 3], 2)
+    c = ilb.encode_interleaved([1, 0, 1, 1, 0] * 20, t, 1, WORD16)
+    c.payload = np.concatenate([c.payload, np.asarray([123], dtype=np.uint16)])
+    with pytest.warns(TrailingGarbageWarning):
+        out = ilb.decode_interleaved(c)
+    assert out.tolist() == [1, 0, 1, 1, 0] * 20
+
+
+def test_golden_container_through_gpu():
+    t = SymbolTable([1, 3], 2)
+    c = ilb.encode_interleaved([1], t, 1, WORD16)
+    assert c.final_states == (87382,) and len(c.payload) == 0
+    assert ilb.decode_interleaved(Container.from_bytes(c.to_bytes())).tolist() == [1]
+
+
+def test_wrong_lane_count_never_silently_matches():
+    rng = np.random.default_rng(23)
+    t = random_table(rng)
+    msg = random_message(rng, t, 5000)
+    blob = bytearray(ilb.encode_interleaved(msg, t, 4, WORD16).to_bytes())
+    blob[6] = 5
+    tampered = Container.from_bytes(bytes(blob))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        try:
+            out = ilb.decode_interleaved(tampered)
+        except (TruncatedStreamError, FormatError):
+            return
+    assert not np.array_equal(out, msg)
+
+
+# -------------------------------------------------------- chunk framing ---
+def test_chunked_matches_reference_per_chunk(golden_chunks, golden_meta):
+    from paper_1402_3392_b200.chunked import decode_chunked, encode_chunked
+
+    for case in golden_meta["chunks"]:
+        k, sb, C = case["case"], case["scale_bits"], case["chunk"]
+        msg = golden_chunks[f"k{k}_msg"]
+        t = SymbolTable(golden_chunks[f"k{k}_freq"].tolist(), sb)
+        cc = encode_chunked(msg, t, 32, C)
+        assert np.array_equal(cc.payload, golden_chunks[f"k{k}_payload"])
+        assert np.array_equal(cc.word_offsets, golden_chunks[f"k{k}_offsets"])
+        assert np.array_equal(cc.states, golden_chunks[f"k{k}_states"])
+        assert np.array_equal(decode_chunked(cc), msg)
+        # device model build == host reference model (bincount + quantize)
+        cc2 = encode_chunked(msg, None, 32, C, sb)
+        assert cc2.table == SymbolTable.from_counts(
+            np.bincount(msg, minlength=int(msg.max()) + 1).tolist(), sb)
+        # every chunk is a standalone IEC1 container
+        for j in (0, cc.n_chunks - 1):
+            one = Container.from_bytes(cc.chunk(j).to_bytes())
+            assert np.array_equal(ilb.decode_interleaved(one), msg[j * C:(j + 1) * C])
+
+
+def test_chunked_edge_shapes():
+    from paper_1402_3392_b200.chunked import ChunkedContainer, decode_chunked, encode_chunked
+
+    rng = np.random.default_rng(4)
+    for n, C, lanes in ((0, 1024, 32), (1, 16, 1), (17, 16, 3), (4096, 1024, 32),
+                        (100_000, 1008, 7), (65536 * 3 + 5, 65536, 32)):
+        t = random_table(rng)
+        msg = random_message(rng, t, n)
+        cc = encode_chunked(msg, t, lanes, C)
+        ref_p, ref_o, ref_s = oracle.encode_chunks_u16(msg, C, t.freq_u32, t.cum_u32,
+                                                       t.scale_bits, lanes)
+        assert np.array_equal(cc.payload, ref_p) and np.array_equal(cc.states, ref_s)
+        back = ChunkedContainer.from_bytes(cc.to_bytes())
+        assert np.array_equal(decode_chunked(back), msg)
