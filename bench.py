@@ -1,0 +1,518 @@
+"""Benchmark: word16 32-lane interleaved rANS round trip on B200.
+
+Workload (BASELINE.json configs[1]): 256 MiB of
+synthetic Zipf(s=1.1) bytes per GPU, N=32 lanes, 16-bit word renorm,
+64 KiB chunks (4096 independent streams), scale_bits 12. One STEP is the
+whole path over that batch, inputs resident in HBM:
+
+    histogram -> [NCCL all-reduce of 256 x u64 when N>1] -> quantize + tables
+    -> chunked encode -> framing (offset scan + compaction) -> chunked decode
+
+value = raw bytes of all ranks / step time (GB/s = 1e9 B/s), max over
+ranks. Inputs (256 MiB) exceed the 126 MB L2, so no explicit flush.
+Decode and encode GB/s are also reported separately (per-phase CUDA events
+on the launching stream). `e2e` is the same round trip through the public
+HostCodec API from pinned host memory (H2D + D2H inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+`--impl reference` times the unmodified reference (oracle/_ref: ilans with
+its compiled Cython kernels) on the host cores, fork pool over all cores,
+on a bounded sample of the same chunks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MIB = 1 << 20
+METRIC = "rANS decode & encode GB/s per B200 and 8xB200; compression ratio vs entropy"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--mib", type=int, default=256, help="MiB per GPU")
+    ap.add_argument("--chunk", type=int, default=64 * 1024)
+    ap.add_argument("--lanes", type=int, default=32)
+    ap.add_argument("--scale-bits", type=int, default=12)
+    ap.add_argument("--zipf-s", type=float, default=1.1)
+    ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="config 4: entropy x precision sweep")
+    return ap.parse_args()
+
+
+def config_of(a, world):
+    return {
+        "workload": f"config2: {a.mib} MiB/GPU synthetic Zipf(s={a.zipf_s}) bytes, "
+                    f"N={a.lanes} lanes word16, {a.chunk // 1024} KiB chunks, sb={a.scale_bits}, "
+                    "round trip (model build + encode + framing + decode)",
+        "bytes_per_gpu": a.mib * MIB,
+        "global_bytes": a.mib * MIB * world,
+        "chunk_len": a.chunk,
+        "lanes": a.lanes,
+        "scale_bits": a.scale_bits,
+        "zipf_s": a.zipf_s,
+        "seed": a.seed,
+        "parallelism": f"chunk-sharded x{world} (weak), histogram all-reduce" if world > 1
+        else "single GPU",
+        "l2": "inputs (256 MiB) larger than the 126 MB L2; no flush",
+    }
+
+
+# ---------------------------------------------------------------- clocks ---
+REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+class Clocks:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/ilans_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def wait_lines(self, k: int, timeout: float = 5.0) -> None:
+        """Block until the sampler has written k more lines (so short timed
+        regions are still bracketed by samples)."""
+        if self.proc is None:
+            return
+        def count():
+            try:
+                return self.path.read_text().count("\n")
+            except OSError:
+                return 0
+        start = count()
+        t0 = time.time()
+        while count() < start + k and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm, mx, active = [], [], set()
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(REASONS, parts[2:6]):
+                if v.lower().startswith("active"):
+                    active.add(name)
+        self.path.unlink(missing_ok=True)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(active), "samples": len(sm)}
+
+
+# --------------------------------------------------------- CPU reference ---
+def _ref_worker(args):
+    """Fork-pool worker: round-trip a contiguous range of chunks with the
+    reference ext kernels on fork-inherited data; returns (seconds, ok)."""
+    lo, hi = args
+    from ilans.interleave import decode_interleaved, encode_interleaved
+    from ilans.rans import WORD16
+
+    msg, table, C, lanes = _REF_STATE
+    t0 = time.perf_counter()
+    ok = True
+    for k in range(lo, hi):
+        chunk = msg[k * C:(k + 1) * C]
+        c = encode_interleaved(chunk, table, lanes, WORD16, backend="ext")
+        out = decode_interleaved(c, backend="ext")
+        ok &= bool(np.array_equal(out, chunk))
+    return time.perf_counter() - t0, ok
+
+
+_REF_STATE = None
+
+
+def cpu_reference(msg: np.ndarray, freqs: list, sb: int, C: int, lanes: int,
+                  per_core_mib: int = 8):
+    """Time the reference CPU path on a bounded sample: all host cores, each
+    core round-trips per_core_mib of the same chunks. Returns dict."""
+    global _REF_STATE
+    import multiprocessing as mp
+
+    ref_dir = ROOT / "oracle" / "_ref"
+    kind = "reference"
+    if (ref_dir / "ilans" / "__init__.py").exists():
+        sys.path.insert(0, str(ref_dir))
+        os.environ["ILANS_BACKEND"] = "ext"
+        from ilans import backend as ref_backend
+        from ilans.rans import SymbolTable as RefTable
+
+        if ref_backend.EXT is None:
+            kind = "port"
+    else:
+        kind = "port"
+    cores = len(os.sched_getaffinity(0))
+    chunks_per_core = max(1, (per_core_mib * MIB) // C)
+    total_chunks = len(msg) // C
+    n_chunks = min(total_chunks, chunks_per_core * cores)
+    if kind == "reference":
+        table = RefTable(freqs, sb)
+        _REF_STATE = (msg, table, C, lanes)
+        ranges = np.array_split(np.arange(n_chunks), cores)
+        jobs = [(int(r[0]), int(r[-1]) + 1) for r in ranges if len(r)]
+        ctx = mp.get_context("fork")
+        t0 = time.perf_counter()
+        with ctx.Pool(len(jobs)) as pool:
+            res = pool.map(_ref_worker, jobs)
+        wall = time.perf_counter() - t0
+        busy = max(r[0] for r in res)
+        ok = all(r[1] for r in res)
+        workers = len(jobs)
+    else:  # oracle port (C restatement), single core
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle
+
+        f, cum, slot = oracle.table_views(freqs, sb)
+        n_chunks = min(total_chunks, chunks_per_core)
+        t0 = time.perf_counter()
+        ok = True
+        for k in range(n_chunks):
+            chunk = msg[k * C:(k + 1) * C]
+            p, s = oracle.encode_interleaved_u16(chunk, f, cum, sb, lanes)
+            out, _ = oracle.decode_interleaved_u16(p, s, slot, f, cum, sb, len(chunk), lanes)
+            ok &= bool(np.array_equal(out, chunk))
+        wall = busy = time.perf_counter() - t0
+        workers = 1
+    sample = n_chunks * C
+    return {
+        "value": sample / busy / 1e9,
+        "unit": "GB/s",
+        "cores": workers,
+        "kind": kind,
+        "sample": f"{n_chunks} x {C // 1024} KiB chunks ({sample / MIB:.0f} MiB) of the same "
+                  f"workload, encode+decode round trip per chunk, reference ext backend, "
+                  f"fork pool of {workers} workers (slowest worker's time; wall incl. fork "
+                  f"{wall:.2f}s)",
+        "round_trip_ok": ok,
+        "wall_s": wall,
+    }
+
+
+# ---------------------------------------------------------------- b200 ---
+def run_b200(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1402_3392_b200 import _lib
+    from paper_1402_3392_b200.chunked import DeviceCodec, HostCodec, n_chunks_for
+    from paper_1402_3392_b200.synth import synth_device, zipf_probs, entropy_bits
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = a.mib * MIB
+    C, N, sb = a.chunk, a.lanes, a.scale_bits
+    k_chunks = n_chunks_for(n, C)
+
+    d_msg = synth_device(n, a.zipf_s, a.seed, first=rank * n, device=dev)
+    d_out = torch.empty(n, dtype=torch.uint8, device=dev)
+    codec = DeviceCodec(n, C, N, sb, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def allreduce(counts):
+        if world > 1:
+            dist.all_reduce(counts)  # int64 sum == u64 sum bit-for-bit
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(marks=None):
+        if marks: marks[0].record(stream)
+        codec.histogram(d_msg, n)
+        allreduce(codec.counts)
+        codec.build_table_from_counts()
+        if marks: marks[1].record(stream)
+        codec.encode(d_msg, n, frame=False)
+        if marks: marks[2].record(stream)
+        _lib.check_dev(_lib.lib.ilans_frame_chunks_dev(
+            codec.scratch.data_ptr(), n, C, codec.chunk_words.data_ptr(),
+            codec.offsets.data_ptr(), codec.payload.data_ptr(), stream.cuda_stream), "frame")
+        if marks: marks[3].record(stream)
+        codec.decode(d_out, n)
+        if marks: marks[4].record(stream)
+
+    # round-trip gate before timing (reference bench.py:92-93)
+    codec.reset_status()
+    step()
+    codec.check_status()
+    torch.cuda.synchronize(dev)
+    if not torch.equal(d_out, d_msg[:n]):
+        raise SystemExit("bench round-trip mismatch")
+    consumed = codec.consumed[:k_chunks]
+    offs = codec.offsets[: k_chunks + 1]
+    if not torch.equal(consumed, offs[1:] - offs[:-1]):
+        raise SystemExit("decoder did not consume every payload word")
+    total_words = int(offs[-1])
+    for _ in range(max(0, a.warmup - 1)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    marks = [[ev() for _ in range(5)] for _ in range(a.steps)]
+    l0 = _lib.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with Clocks(local) as clk:
+        clk.wait_lines(1)
+        t0 = ev(); t1 = ev()
+        t0.record(stream)
+        for i in range(a.steps):
+            step(marks[i])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        clk.wait_lines(1)
+    if world > 1:
+        dist.barrier()
+    launches = _lib.launch_count() - l0
+    total_ms = t0.elapsed_time(t1)
+    phase = np.array([[m[j].elapsed_time(m[j + 1]) for j in range(4)] for m in marks])
+    t = torch.tensor([total_ms, *phase.mean(0).tolist()], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, model_ms, enc_ms, frame_ms, dec_ms = t.tolist()
+    ms_step = total_ms / a.steps
+    gbs = lambda b, ms: b / (ms * 1e-3) / 1e9  # noqa: E731
+
+    # compression ratio (framed ICH1 size) vs empirical entropy
+    counts = codec.counts.cpu().numpy().astype(np.float64)
+    H = entropy_bits(counts / counts.sum())
+    table = codec.read_table()
+    framed = 24 + 3 + 2 * table.alphabet_size + 4 * k_chunks + 4 * k_chunks * N + 2 * total_words
+    single_hdr = 16 + 3 + 2 * table.alphabet_size + 4 * N
+    bpb = 8 * framed / n
+
+    # roofline for the dominant kernels: algorithmic bytes per launch
+    dec_bytes = 2 * total_words + 4 * N * k_chunks + n          # payload + states read, raw written
+    enc_bytes = n + 2 * total_words + 4 * N * k_chunks          # raw read, payload + states written
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (
+        ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback 6.65 TB/s"
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text())
+    dom = "decode" if dec_ms >= enc_ms else "encode"
+    dom_ms = max(dec_ms, enc_ms)
+    dom_bytes = dec_bytes if dom == "decode" else enc_bytes
+    achieved = gbs(dom_bytes, dom_ms)
+
+    out = {
+        "metric": METRIC,
+        "value": gbs(n * world, ms_step),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8 symbols / u32 states / u16 digits (integer)",
+        "data": "synthetic (counter-based splitmix64 Zipf sampler, csrc/synth.cu)",
+        "config": config_of(a, world),
+        "decode": {"GBps": gbs(n, dec_ms), "ms": dec_ms,
+                   "roofline_frac": gbs(dec_bytes, dec_ms) / hbm},
+        "encode": {"GBps": gbs(n, enc_ms + frame_ms), "ms": enc_ms + frame_ms,
+                   "kernel_ms": enc_ms, "frame_ms": frame_ms,
+                   "roofline_frac": gbs(enc_bytes, enc_ms) / hbm},
+        "model_build": {"ms": model_ms, "GBps": gbs(n, model_ms)},
+        "ratio": {"bits_per_byte": bpb, "entropy_bpb": H, "vs_entropy": bpb / H,
+                  "single_stream_bits_per_byte": 8 * (single_hdr + 2 * total_words
+                                                      - 4 * N * (k_chunks - 1)) / n,
+                  "framed_bytes": framed, "payload_words": total_words},
+        "roofline": {"bound": "hbm", "kernel": f"{dom}_warp_kernel", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": (traffic or {}).get(dom), "algorithmic_bytes": dom_bytes,
+                     "peak_source": peak_src},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+    if not a.no_e2e:
+        hc = HostCodec(n, C, N, sb, dev, counts_allreduce=allreduce)
+        h_msg = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        h_msg.copy_(d_msg[:n])
+        h_out = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        def e2e_step():
+            p, o, s = hc.encode(h_msg, n)
+            hc.decode(p, o, s, n, h_out)
+            return hc
+        e2e_step()
+        if not torch.equal(h_out, h_msg):
+            raise SystemExit("e2e round-trip mismatch")
+        h2d = d2h = 0
+        steps = max(3, min(a.steps, 5))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            hc.encode(h_msg, n)
+            h2d += hc.h2d_bytes; d2h += hc.d2h_bytes
+            p, o, s = hc.h_payload[: int(hc.h_offsets[k_chunks])], \
+                hc.h_offsets[: k_chunks + 1], hc.h_states[: k_chunks * N]
+            hc.decode(p, o, s, n, h_out)
+            h2d += hc.h2d_bytes; d2h += hc.d2h_bytes
+        torch.cuda.synchronize(dev)
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        out["e2e"] = {"value": n * world * steps / float(el.item()) / 1e9, "unit": "GB/s",
+                      "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
+                      "api": "chunked.HostCodec encode()+decode() from pinned host memory",
+                      "steps": steps}
+
+    if rank == 0 and world == 1 and not a.no_cpu:
+        msg_h = d_msg[:n].cpu().numpy()
+        out["cpu_baseline"] = cpu_reference(msg_h, table.freq, sb, C, N)
+        out["cpu_baseline"].pop("wall_s", None)
+
+    if a.sweep and rank == 0:
+        out["sweep"] = sweep(a, dev)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out))
+
+
+def sweep(a, dev):
+    """Config 4: entropy x precision sweep (decode / encode GB/s, ratio)."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import DeviceCodec, n_chunks_for
+    from paper_1402_3392_b200.synth import ZIPF_S_FOR_ENTROPY, synth_device
+
+    n = min(a.mib, 256) * MIB
+    rows = []
+    for H, s in ZIPF_S_FOR_ENTROPY.items():
+        d_msg = synth_device(n, s, a.seed, device=dev)
+        d_out = torch.empty(n, dtype=torch.uint8, device=dev)
+        for sb in range(11, 16):
+            codec = DeviceCodec(n, a.chunk, a.lanes, sb, dev)
+            codec.histogram(d_msg, n)
+            codec.build_table_from_counts()
+            codec.reset_status()
+            codec.encode(d_msg, n)
+            codec.decode(d_out, n)
+            codec.check_status()
+            assert torch.equal(d_out, d_msg[:n])
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            reps = 3
+            ev[0].record()
+            for _ in range(reps):
+                codec.encode(d_msg, n)
+            ev[1].record()
+            for _ in range(reps):
+                codec.decode(d_out, n)
+            ev[2].record()
+            torch.cuda.synchronize(dev)
+            k = n_chunks_for(n, a.chunk)
+            words = int(codec.offsets[k])
+            rows.append({"H_target": H, "zipf_s": s, "scale_bits": sb,
+                         "encode_GBps": n * reps / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9,
+                         "decode_GBps": n * reps / (ev[1].elapsed_time(ev[2]) * 1e-3) / 1e9,
+                         "payload_bits_per_byte": 16 * words / n})
+    return rows
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from paper_1402_3392_b200.synth import synth_host
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+
+    n = a.mib * MIB
+    cores = len(os.sched_getaffinity(0))
+    per_core = 4  # MiB per core per step -> a bounded sample of the workload
+    sample = min(n, cores * per_core * MIB)
+    msg = synth_host(sample, a.zipf_s, a.seed)
+    # the model is built from the full workload's histogram, as the b200 arm
+    # does; on the sample alone it would differ slightly -- use the sample's
+    # histogram computed by the reference's own call site (np.bincount)
+    counts = np.bincount(msg, minlength=int(msg.max()) + 1)
+    freqs = oracle.quantize(counts, a.scale_bits)
+    vals = []
+    for i in range(a.warmup + a.steps):
+        r = cpu_reference(msg, freqs, a.scale_bits, a.chunk, a.lanes, per_core_mib=per_core)
+        if i >= a.warmup:
+            vals.append(r)
+    v = statistics.median([r["value"] for r in vals])
+    ms = 1e3 * sample / (v * 1e9)
+    base = vals[-1]
+    base["value"] = v
+    base.pop("wall_s", None)
+    print(json.dumps({
+        "metric": METRIC, "impl": "reference", "value": v, "unit": "GB/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8 symbols / u32 states / u16 digits",
+        "data": "synthetic (same sampler, host twin)", "config": config_of(a, world),
+        "cpu_baseline": base,
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)
+
+
+if __name__ == "__main__":
+    main()

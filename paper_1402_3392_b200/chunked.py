@@ -333,3 +333,63 @@ def decode_chunked(cc: ChunkedContainer) -> np.ndarray:
 
         warnings.warn("unread digits after chunk decode", TrailingGarbageWarning, stacklevel=2)
     return out.cpu().numpy()
+
+
+class HostCodec:
+    """End-to-end chunked codec over pinned host buffers: the public call a
+    user makes with data in host memory. encode(): H2D message -> device
+    model build -> encode -> framing -> D2H (offsets, states, payload).
+    decode(): H2D (payload, offsets, states) -> decode -> D2H message.
+    Buffers (device and pinned host) are allocated once for ``capacity``."""
+
+    def __init__(self, capacity: int, chunk_len: int = DEFAULT_CHUNK, lane_count: int = 32,
+                 scale_bits: int = 14, device=None, counts_allreduce=None):
+        torch = _torch()
+        self.codec = DeviceCodec(capacity, chunk_len, lane_count, scale_bits, device)
+        dev = self.codec.device
+        self.d_msg = torch.empty(max(16, capacity), dtype=torch.uint8, device=dev)
+        self.d_out = torch.empty(max(16, capacity), dtype=torch.uint8, device=dev)
+        k = max(1, n_chunks_for(capacity, chunk_len))
+        pin = lambda n, dt: torch.empty(n, dtype=dt, pin_memory=True)  # noqa: E731
+        self.h_offsets = pin(k + 1, torch.int64)
+        self.h_states = pin(k * lane_count, torch.int32)
+        self.h_payload = pin(max(1, capacity) + 8, torch.int16)
+        self.counts_allreduce = counts_allreduce
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def encode(self, h_msg, n: int):
+        """h_msg: pinned uint8 tensor. Returns (payload, offsets, states) as
+        views of the pinned host buffers (valid until the next encode)."""
+        c = self.codec
+        k = n_chunks_for(n, c.chunk_len)
+        self.d_msg[:n].copy_(h_msg[:n], non_blocking=True)
+        c.histogram(self.d_msg, n)
+        if self.counts_allreduce is not None:
+            self.counts_allreduce(c.counts)
+        c.build_table_from_counts()
+        c.encode(self.d_msg, n)
+        self.h_offsets[: k + 1].copy_(c.offsets[: k + 1], non_blocking=True)
+        self.h_states[: k * c.lane_count].copy_(c.states[: k * c.lane_count], non_blocking=True)
+        _torch().cuda.current_stream(c.device).synchronize()
+        words = int(self.h_offsets[k]) if k else 0
+        self.h_payload[:words].copy_(c.payload[:words], non_blocking=True)
+        _torch().cuda.current_stream(c.device).synchronize()
+        self.h2d_bytes = n
+        self.d2h_bytes = 8 * (k + 1) + 4 * k * c.lane_count + 2 * words
+        return self.h_payload[:words], self.h_offsets[: k + 1], self.h_states[: k * c.lane_count]
+
+    def decode(self, h_payload, h_offsets, h_states, n: int, h_out):
+        """Decode into pinned uint8 tensor h_out (device table = last model)."""
+        c = self.codec
+        k = n_chunks_for(n, c.chunk_len)
+        words = h_payload.numel()
+        c.payload[:words].copy_(h_payload, non_blocking=True)
+        c.offsets[: k + 1].copy_(h_offsets, non_blocking=True)
+        c.states[: k * c.lane_count].copy_(h_states, non_blocking=True)
+        c.decode(self.d_out, n)
+        h_out[:n].copy_(self.d_out[:n], non_blocking=True)
+        _torch().cuda.current_stream(c.device).synchronize()
+        self.h2d_bytes = 2 * words + 8 * (k + 1) + 4 * k * c.lane_count
+        self.d2h_bytes = n
+        return h_out[:n]

@@ -70,25 +70,54 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Granlund-Montgomery exact unsigned division by an invariant d in [1, 2^16]
-// for every 32-bit numerator ("Division by invariant integers using
-// multiplication", PLDI'94, fig. 4.1): q = (t + ((n - t) >> sh1)) >> sh2,
-// t = umulhi(magic, n). Verified exhaustively per d on the host oracle side
-// (tests/test_division.py) and on device (tests/test_gpu_parity.py).
-__host__ __device__ inline void divmagic(uint32_t d, uint32_t *magic, uint32_t *sh1,
-                                         uint32_t *sh2) {
+// Exact unsigned division by an invariant d in [1, 2^16] for every 32-bit
+// numerator with a 33-bit magic (Granlund & Montgomery, "Division by
+// invariant integers using multiplication", PLDI'94, sec. 4):
+//   l = ceil(log2 d), m = floor(2^(32+l) / d) + 1 = 2^32 + magic,
+//   q = floor(m * n / 2^(32+l)) = (umulhi(magic, n) + n) >> l   (33-bit sum).
+// m*d - 2^(32+l) lies in (0, 2^l], which makes q exact for all n < 2^32;
+// magic < 2^32 because 2^(l-1) < d. tests/test_host.py checks every d.
+__host__ __device__ inline void divmagic(uint32_t d, uint32_t *magic, uint32_t *l_out) {
     uint32_t l = 0;
     while ((1ull << l) < d) ++l;  // l = ceil(log2 d)
-    uint64_t m = ((((1ull << l) - d) << 32) / d) + 1;
-    *magic = static_cast<uint32_t>(m);
-    *sh1 = l < 1 ? l : 1;
-    *sh2 = l > 0 ? l - 1 : 0;
+    const uint64_t m = ((1ull << (32 + l)) / d) + 1;  // in (2^32, 2^33)
+    *magic = static_cast<uint32_t>(m - (1ull << 32));
+    *l_out = l;
 }
 
-__device__ __forceinline__ uint32_t div_magic(uint32_t n, uint32_t magic, uint32_t sh1,
-                                              uint32_t sh2) {
-    uint32_t t = __umulhi(magic, n);
-    return (t + ((n - t) >> sh1)) >> sh2;
+// q = (umulhi(magic, n) + n) >> l, the sum kept as 33 bits: a funnel shift
+// of (carry:lo). `shift` may carry other data above bit 4 (.wrap uses & 31).
+__device__ __forceinline__ uint32_t div_magic(uint32_t n, uint32_t magic, uint32_t shift) {
+    const uint32_t t = __umulhi(magic, n);
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, 0, 0;" : "=r"(lo), "=r"(hi) : "r"(t), "r"(n));
+    uint32_t q;
+    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(lo), "r"(hi), "r"(shift));
+    return q;
+}
+
+// Encoder record per symbol (16 bytes, one LDS.128):
+//   .x = spill bound  (f << (32 - sb)) - 1   (x > .x  <=>  x >= f << (32-sb))
+//   .y = magic        (0 marks f == 0: unencodable)
+//   .z = m - f        (push: x' = q*(m - f) + x + cum, since x - q*f + q*m)
+//   .w = cum << 8 | l
+struct EncSym {
+    __host__ __device__ static uint4 make(uint32_t f, uint32_t cum, int scale_bits) {
+        if (f == 0) return make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+        uint32_t magic, l;
+        divmagic(f, &magic, &l);
+        uint64_t bound = (static_cast<uint64_t>(f) << (32 - scale_bits)) - 1;
+        if (bound > 0xFFFFFFFFull) bound = 0xFFFFFFFFull;  // f > m: never spills
+        const uint32_t m = 1u << scale_bits;
+        return make_uint4(static_cast<uint32_t>(bound), magic, m - f, (cum << 8) | l);
+    }
+};
+
+// One rANS push of symbol record e onto state x (after the spill):
+// x' = (x / f) * m + cum + x % f = q*(m - f) + x + cum.
+__device__ __forceinline__ uint32_t enc_push(uint32_t x, const uint4 &e) {
+    const uint32_t q = div_magic(x, e.y, e.w);
+    return q * e.z + x + (e.w >> 8);
 }
 
 }  // namespace ilans

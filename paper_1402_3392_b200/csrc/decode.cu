@@ -12,10 +12,15 @@
 //                                                      (lanes.packed_load)
 //   pos += popc(mask)
 // The payload is staged into a per-warp shared-memory ring by cp.async
-// (4 x 512-byte segments, 3 segments = ~66 groups ahead of the reader), so
-// the refill read is a conflict-free LDS, never an HBM round trip. Decoded
-// bytes are staged in a 1 KB per-warp buffer and written to HBM as 16-byte
-// vectors (512 B per warp store).
+// (4 segments x 512 words; two segments = ~88 groups ahead of the reader),
+// so the refill read is a conflict-free LDS, never an HBM round trip.
+//
+// N = 32 fast path: 16 groups (512 symbols) per batch, fully unrolled; the
+// ring is advanced and the 512 decoded bytes are written (one 16-byte
+// vector store per lane) once per batch, and truncation is checked once per
+// batch (pos is monotone, so "some group overran" == "pos > len at the end
+// of the batch"; reads past the payload hit zero-filled ring words and are
+// never used). Other N and the < 512-symbol tail run the per-group loop.
 //
 // Block kernel (N > 32, up to 65535 lanes): one CTA per stream, contiguous
 // lane ranges per thread and a CTA-wide exclusive scan of refill counts in
@@ -26,23 +31,54 @@
 
 namespace ilans {
 
-constexpr int kSegWords = 256;            // 512 B per cp.async warp-copy
-constexpr int kRingWords = 4 * kSegWords; // 2 KB payload ring per warp
-constexpr int kObufBytes = 1024;          // 2 x 512 B output halves per warp
+constexpr int kSegWords = 512;             // 1 KB per cp.async warp-copy (2 x 16 B / lane)
+constexpr int kRingWords = 4 * kSegWords;  // 4 KB payload ring per warp
+constexpr int kBatch = 16;                 // groups per fast-path batch (N = 32)
+constexpr int kObufBytes = 1024;           // 2 x 512 B output halves per warp
 constexpr int kWarpSmem = kRingWords * 2 + kObufBytes;
 
-__device__ __forceinline__ void issue_payload_segment(uint16_t *ring, const uint16_t *g_aligned,
-                                                      uint64_t rel_words_avail, uint32_t seg,
-                                                      int lane) {
-    const uint64_t w0 = static_cast<uint64_t>(seg) * kSegWords + static_cast<uint64_t>(lane) * 8u;
-    uint32_t bytes = 0;
-    if (rel_words_avail > w0) {
-        const uint64_t left = (rel_words_avail - w0) * 2u;
-        bytes = left >= 16u ? 16u : static_cast<uint32_t>(left);
+struct SegSrc {
+    const uint16_t *g;    // 16-byte aligned base of the chunk's payload
+    uint64_t avail;       // readable words from g
+};
+
+__device__ __forceinline__ void issue_segment(uint16_t *ring, const SegSrc &src, uint32_t seg,
+                                              int lane) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint64_t w0 = static_cast<uint64_t>(seg) * kSegWords + h * 256 + lane * 8;
+        uint32_t bytes = 0;
+        if (src.avail > w0) {
+            const uint64_t left = (src.avail - w0) * 2u;
+            bytes = left >= 16u ? 16u : static_cast<uint32_t>(left);
+        }
+        cp_async16(ring + (seg & 3u) * kSegWords + h * 256 + lane * 8, bytes ? src.g + w0 : src.g,
+                   bytes);
     }
-    const uint16_t *src = bytes ? g_aligned + w0 : g_aligned;
-    cp_async16(ring + (seg & 3u) * kSegWords + lane * 8, src, bytes);
 }
+
+template <bool PACKED>
+struct Lut {
+    const uint32_t *packed;  // PACKED: sym | (f-1) << 8 | bias << 20
+    const uint8_t *sym;      // else: slot -> symbol
+    const uint2 *dec;        //       symbol -> {f, cum}
+    uint32_t mask;
+    uint32_t sb;
+
+    __device__ __forceinline__ uint32_t pop(uint32_t &x) const {
+        const uint32_t slot = x & mask;
+        if (PACKED) {
+            const uint32_t e = packed[slot];
+            x = (((e >> 8) & 0xFFFu) + 1u) * (x >> sb) + (e >> 20);
+            return e & 0xFFu;
+        } else {
+            const uint32_t s = sym[slot];
+            const uint2 d = dec[s];
+            x = d.x * (x >> sb) + slot - d.y;
+            return s;
+        }
+    }
+};
 
 template <bool PACKED>
 __global__ void __launch_bounds__(1024)
@@ -59,25 +95,30 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         return;
     }
     const uint32_t m = 1u << sb;
-    const uint32_t mask = m - 1u;
 
     // ---- stage the lookup tables in shared memory ------------------------
-    uint32_t *lut32 = reinterpret_cast<uint32_t *>(smem);
-    uint2 *dec = reinterpret_cast<uint2 *>(smem);
-    uint8_t *sym = smem + kMaxSym * sizeof(uint2);
+    Lut<PACKED> lut;
+    lut.mask = m - 1u;
+    lut.sb = static_cast<uint32_t>(sb);
     uint32_t lut_bytes;
     if (PACKED) {
-        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) lut32[i] = tab->packed[i];
+        uint32_t *p = reinterpret_cast<uint32_t *>(smem);
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) p[i] = tab->packed[i];
+        lut.packed = p;
         lut_bytes = m * 4u;
     } else {
-        for (uint32_t i = threadIdx.x; i < kMaxSym; i += blockDim.x) dec[i] = tab->dec[i];
+        uint2 *d = reinterpret_cast<uint2 *>(smem);
+        uint8_t *s = smem + kMaxSym * sizeof(uint2);
+        for (uint32_t i = threadIdx.x; i < kMaxSym; i += blockDim.x) d[i] = tab->dec[i];
         if (m >= 4) {
             const uint32_t *src = reinterpret_cast<const uint32_t *>(tab->slot_sym);
-            uint32_t *dst = reinterpret_cast<uint32_t *>(sym);
+            uint32_t *dst = reinterpret_cast<uint32_t *>(s);
             for (uint32_t i = threadIdx.x; i < m / 4; i += blockDim.x) dst[i] = src[i];
         } else {
-            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) sym[i] = tab->slot_sym[i];
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) s[i] = tab->slot_sym[i];
         }
+        lut.dec = d;
+        lut.sym = s;
         lut_bytes = kMaxSym * sizeof(uint2) + (m < 16 ? 16u : m);
     }
     lut_bytes = (lut_bytes + 15u) & ~15u;
@@ -96,66 +137,83 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
         const uint64_t woff = offsets[k];
         const uint64_t wlen = offsets[k + 1] - woff;
-        const uint64_t a_words = woff & ~7ull;  // 16-byte aligned segment base
         const uint32_t delta = static_cast<uint32_t>(woff & 7u);
-        const uint16_t *g_al = payload + a_words;
-        const uint64_t avail = wlen + delta;  // readable words from g_al
+        SegSrc src{payload + (woff & ~7ull), wlen + delta};
 #pragma unroll
         for (uint32_t s = 0; s < 4; ++s) {
-            issue_payload_segment(ring, g_al, avail, s, lane);
+            issue_segment(ring, src, s, lane);
             cp_async_commit();
         }
         cp_async_wait<2>();
         __syncwarp();
 
-        uint64_t cur = 0;
+        uint64_t cur = 0;            // ring segment holding the read cursor
+        uint64_t v = delta;          // read cursor in words from src.g
         uint32_t x = lane < n_lanes ? states[k * n_lanes + lane] : 0u;
-        uint64_t pos = 0;
-        bool truncated = false;
         uint8_t *out_k = out + cbase;
-        for (int64_t base = 0; base < len; base += n_lanes) {
+        int64_t base = 0;
+
+        if (n_lanes == 32) {
+            // ---------------- fast path: batches of 16 full groups ----------
+            const int64_t full = len >> 9;
+            uint32_t vv = static_cast<uint32_t>(v);  // low 32 bits suffice for ring indexing
+            for (int64_t b = 0; b < full; ++b) {
+#pragma unroll
+                for (int g = 0; g < kBatch; ++g) {
+                    const uint32_t s = lut.pop(x);
+                    const bool need = x < kLow;
+                    const uint32_t mk = __ballot_sync(0xffffffffu, need);
+                    if (need) x = (x << 16) | ring[(vv + __popc(mk & lt)) & (kRingWords - 1)];
+                    vv += __popc(mk);
+                    obuf[g * 32 + lane] = static_cast<uint8_t>(s);
+                }
+                __syncwarp();
+                const uint4 o = reinterpret_cast<const uint4 *>(obuf)[lane];
+                reinterpret_cast<uint4 *>(out_k + (b << 9))[lane] = o;
+                // advance the ring: the cursor moved by <= 512 words
+                v += static_cast<uint32_t>(vv - static_cast<uint32_t>(v));
+                const uint64_t seg = v / kSegWords;
+                if (seg != cur) {
+                    cur = seg;
+                    issue_segment(ring, src, static_cast<uint32_t>(cur + 3), lane);
+                    cp_async_commit();
+                    cp_async_wait<2>();
+                }
+                __syncwarp();
+            }
+            base = full << 9;
+        }
+        // ---------------- generic per-group loop (any N <= 32, tails) ------
+        bool truncated = (v - delta) > wlen;
+        for (; !truncated && base < len; base += n_lanes) {
             const int64_t left = len - base;
             const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
             const bool on = lane < active;
             uint32_t s = 0;
-            if (on) {
-                const uint32_t slot = x & mask;
-                if (PACKED) {
-                    const uint32_t e = lut32[slot];
-                    s = e & 0xFFu;
-                    x = (((e >> 8) & 0xFFFu) + 1u) * (x >> sb) + (e >> 20);
-                } else {
-                    s = sym[slot];
-                    const uint2 d = dec[s];
-                    x = d.x * (x >> sb) + slot - d.y;
-                }
-            }
+            if (on) s = lut.pop(x);
             const bool need = on && x < kLow;
             const uint32_t mk = __ballot_sync(0xffffffffu, need);
             const uint32_t cnt = __popc(mk);
-            if (pos + cnt > wlen) {
+            if (v - delta + cnt > wlen) {
                 truncated = true;
                 break;
             }
-            if (need) {
-                const uint64_t v = delta + pos + __popc(mk & lt);
-                x = (x << 16) | ring[v & (kRingWords - 1)];
-            }
-            pos += cnt;
+            if (need) x = (x << 16) | ring[(v + __popc(mk & lt)) & (kRingWords - 1)];
+            v += cnt;
             if (on) obuf[(base + lane) & (kObufBytes - 1)] = static_cast<uint8_t>(s);
             const int64_t nb = base + active;
             if ((nb >> 9) != (base >> 9)) {  // a 512-byte half is complete
                 __syncwarp();
                 const int64_t blk = base >> 9;
-                const uint4 v = reinterpret_cast<const uint4 *>(obuf + (blk & 1) * 512)[lane];
-                reinterpret_cast<uint4 *>(out_k + (blk << 9))[lane] = v;
+                const uint4 o = reinterpret_cast<const uint4 *>(obuf + (blk & 1) * 512)[lane];
+                reinterpret_cast<uint4 *>(out_k + (blk << 9))[lane] = o;
                 __syncwarp();
             }
-            const uint64_t seg = (delta + pos) >> 8;
+            const uint64_t seg = v / kSegWords;
             if (seg != cur) {  // segment cur-1 fully read: refill its slot
                 cur = seg;
                 __syncwarp();
-                issue_payload_segment(ring, g_al, avail, static_cast<uint32_t>(cur + 3), lane);
+                issue_segment(ring, src, static_cast<uint32_t>(cur + 3), lane);
                 cp_async_commit();
                 cp_async_wait<2>();
                 __syncwarp();
@@ -169,7 +227,7 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
             const uint8_t *half = obuf + ((len >> 9) & 1) * 512;
             for (int64_t i = tail0 + lane; i < len; i += 32) out_k[i] = half[i - tail0];
         }
-        if (lane == 0 && consumed) consumed[k] = pos;
+        if (lane == 0 && consumed) consumed[k] = v - delta;
         if (final_states && lane < n_lanes) final_states[k * n_lanes + lane] = x;
         cp_async_wait<0>();
         __syncwarp();
@@ -295,11 +353,12 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
     }
     const bool use_packed = packed && scale_bits <= kPackedMaxBits;
     const size_t lut = decode_lut_bytes(scale_bits, use_packed);
-    // warps per CTA: fill the SM (up to 64 warps) given the per-CTA LUT copy
-    int warps = 8;
+    // warps per CTA: small CTAs spread the streams evenly over the SMs; the
+    // per-CTA LUT copy argues for bigger CTAs when the LUT is large
+    int warps = 4;
     const size_t smem_cap = 227 * 1024;
     if (lut > 48 * 1024) warps = 32;
-    else if (lut > 16 * 1024) warps = 16;
+    else if (lut > 8 * 1024) warps = 8;
     while (warps > 1 && lut + size_t(warps) * kWarpSmem > smem_cap) warps >>= 1;
     const size_t smem = lut + size_t(warps) * kWarpSmem;
     int64_t blocks = (n_chunks + warps - 1) / warps;

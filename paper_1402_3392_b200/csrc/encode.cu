@@ -29,26 +29,69 @@ namespace ilans {
 constexpr int kInSeg = 512;            // bytes per cp.async warp-copy
 constexpr int kInRing = 4 * kInSeg;    // 2 KB per warp
 
-__device__ __forceinline__ void issue_msg_segment(uint8_t *ring, const uint8_t *g, int64_t len,
-                                                  int64_t seg, int lane) {
-    const int64_t b0 = seg * kInSeg + lane * 16;
+template <typename Idx>
+__device__ __forceinline__ void issue_msg_segment(uint8_t *ring, const uint8_t *g, Idx len,
+                                                  Idx seg, int lane) {
+    const Idx b0 = seg * kInSeg + lane * 16;
     uint32_t bytes = 0;
     if (seg >= 0 && b0 < len) bytes = (len - b0) >= 16 ? 16u : static_cast<uint32_t>(len - b0);
     const uint8_t *src = bytes ? g + b0 : g;
     cp_async16(ring + (static_cast<uint32_t>(seg) & 3u) * kInSeg + lane * 16, src, bytes);
 }
 
-__global__ void __launch_bounds__(256)
+constexpr int kEncWarps = 4;    // warps per CTA: 7 CTAs/SM hold 4096 streams in one wave
+constexpr int kOutRing = 1024;  // per-warp staging ring for spilled words (2 KB)
+
+// Spilled words are staged in a per-warp shared ring indexed by their final
+// scratch position (w & 1023) and written to HBM as aligned 16-byte blocks:
+// flush() moves the complete 8-word blocks of [top, flushed) and keeps the
+// partial block at the bottom for the next flush; finish() writes the rest.
+template <typename Idx>
+struct SpillStage {
+    uint16_t *ring;   // shared, kOutRing words
+    uint16_t *out;    // chunk's scratch region in HBM
+    Idx flushed;      // words [flushed, len) are in HBM
+
+    __device__ __forceinline__ void put(Idx w, uint32_t v) { ring[w & (kOutRing - 1)] = v; }
+
+    __device__ __forceinline__ void flush(Idx top, int lane) {
+        __syncwarp();
+        Idx hi = flushed;
+        const Idx lo = (top + 7) & ~Idx(7);
+        if (lo >= hi) return;
+        if (hi & 7) {  // unaligned chunk end (last chunk only): scalar words
+            const Idx a = hi & ~Idx(7);
+            const Idx s = a > lo ? a : lo;
+            if (lane < hi - s) out[s + lane] = ring[(s + lane) & (kOutRing - 1)];
+            hi = s;
+        }
+        for (Idx blk = lo + Idx(lane) * 8; blk < hi; blk += 256)
+            *reinterpret_cast<uint4 *>(out + blk) =
+                *reinterpret_cast<const uint4 *>(ring + (blk & (kOutRing - 1)));
+        flushed = lo;
+        __syncwarp();
+    }
+
+    __device__ __forceinline__ void finish(Idx top, int lane) {
+        flush(top, lane);
+        for (Idx w = top + lane; w < flushed; w += 32) out[w] = ring[w & (kOutRing - 1)];
+        flushed = top;
+    }
+};
+
+// Idx: chunk-local index type (int for chunks < 2^30 bytes, the chunked
+// format's case; long long only for huge single-stream calls).
+template <typename Idx>
+__global__ void __launch_bounds__(kEncWarps * 32, 7)
 encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                    uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
                    uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
     __shared__ uint4 enc[kMaxSym];
-    __shared__ __align__(16) uint8_t rings[8][kInRing];
+    __shared__ __align__(16) uint8_t rings[kEncWarps][kInRing];
+    __shared__ __align__(16) uint16_t oring[kEncWarps][kOutRing];
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
     __syncthreads();
-    const int sb = static_cast<int>(tab->scale_bits);
-    const int thr_shift = 32 - sb;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     uint8_t *ring = rings[wib];
@@ -58,10 +101,10 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; k < n_chunks;
          k += warps_total) {
         const int64_t cbase = k * chunk_len;
-        const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+        const Idx len = static_cast<Idx>((n - cbase) < chunk_len ? (n - cbase) : chunk_len);
         const uint8_t *g = msg + cbase;
-        uint16_t *out = scratch + cbase;
-        int64_t cur = (len - 1) >> 9;
+        SpillStage<Idx> st{oring[wib], scratch + cbase, len};
+        Idx cur = (len - 1) >> 9;
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
             issue_msg_segment(ring, g, len, cur - s, lane);
@@ -71,14 +114,17 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         __syncwarp();
 
         uint32_t x = kLow;
-        int64_t top = len;
-        const int64_t groups = (len + n_lanes - 1) / n_lanes;
+        Idx top = len;
+        // N = 32: the 512-byte blocks below `full` run as unrolled batches of
+        // 16 groups after the per-group loop has coded the tail [full*512, len)
+        const Idx full = n_lanes == 32 ? (len >> 9) : 0;
+        const Idx groups = (len + n_lanes - 1) / n_lanes;
         bool bad = false;
-        for (int64_t gi = groups - 1; gi >= 0; --gi) {
-            const int64_t base = gi * n_lanes;
-            const int64_t left = len - base;
+        for (Idx gi = groups - 1; gi >= (full << 4); --gi) {
+            const Idx base = gi * n_lanes;
+            const Idx left = len - base;
             const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
-            const int64_t hi = (base + active - 1) >> 9;
+            const Idx hi = (base + active - 1) >> 9;
             if (hi != cur) {  // segment cur fully consumed: recycle its slot
                 cur = hi;
                 __syncwarp();
@@ -88,9 +134,8 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 __syncwarp();
             }
             const bool on = lane < active;
-            const uint32_t s = on ? ring[(base + lane) & (kInRing - 1)] : 0u;
-            const uint4 e = enc[s];
-            const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.x == 0u);
+            const uint4 e = enc[on ? ring[(base + lane) & (kInRing - 1)] : 0u];
+            const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.y == 0u);
             if (badmask) {
                 if (lane == 0)
                     atomicMax(&status->unenc_index,
@@ -98,20 +143,65 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 bad = true;
                 break;
             }
-            const bool spill = on && (x >> thr_shift) >= e.x;
+            const bool spill = on && x > e.x;
             const uint32_t mk = __ballot_sync(0xffffffffu, spill);
-            const int cnt = __popc(mk);
+            top -= __popc(mk);
             if (spill) {
-                out[top - cnt + __popc(mk & lt)] = static_cast<uint16_t>(x & 0xFFFFu);
+                st.put(top + __popc(mk & lt), x & 0xFFFFu);
                 x >>= 16;
             }
-            top -= cnt;
-            if (on) {
-                const uint32_t q = div_magic(x, e.z, e.w & 0xFFu, (e.w >> 8) & 0xFFu);
-                x = (q << sb) + e.y + (x - q * e.x);
+            if (on) x = enc_push(x, e);
+            if (st.flushed - top >= 256) st.flush(top, lane);
+        }
+        // ---- N = 32 fast path: 512-byte blocks, backwards, 16 groups each ----
+        // Segments cur .. cur-3 are in flight; batch b needs segment b and
+        // keeps three younger ones in flight. Zero-frequency symbols are
+        // detected once per batch (f = 0 only corrupts this chunk's scratch,
+        // which is then discarded).
+        Idx issued_lo = cur - 3;
+        for (Idx b = full - 1; !bad && b >= 0; --b) {
+            if (b - 3 < issued_lo) {
+                __syncwarp();
+                issue_msg_segment(ring, g, len, b - 3, lane);
+                cp_async_commit();
+                issued_lo = b - 3;
             }
+            cp_async_wait<3>();
+            __syncwarp();
+            const uint8_t *blk = ring + (static_cast<uint32_t>(b) & 3u) * kInSeg;
+            uint32_t zero_f = 0;
+#pragma unroll
+            for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
+                const uint4 e = enc[blk[gg * 32 + lane]];
+                zero_f |= e.y == 0u;
+                const bool spill = x > e.x;
+                const uint32_t mk = __ballot_sync(0xffffffffu, spill);
+                top -= __popc(mk);
+                if (spill) {
+                    st.ring[(static_cast<uint32_t>(top) + __popc(mk & lt)) & (kOutRing - 1)] =
+                        x & 0xFFFFu;
+                    x >>= 16;
+                }
+                x = enc_push(x, e);
+            }
+            if (__ballot_sync(0xffffffffu, zero_f)) {  // rare: locate the highest bad index
+                for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
+                    const uint32_t bm =
+                        __ballot_sync(0xffffffffu, enc[blk[gg * 32 + lane]].y == 0u);
+                    if (bm) {
+                        if (lane == 0)
+                            atomicMax(&status->unenc_index,
+                                      static_cast<long long>(cbase) + b * kInSeg + gg * 32 +
+                                          31 - __clz(bm));
+                        break;
+                    }
+                }
+                bad = true;
+            }
+            st.flush(top, lane);
         }
         if (!bad) {
+            st.finish(top, lane);
             if (lane == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
             if (lane < n_lanes) states_out[k * n_lanes + lane] = x;
         }
@@ -165,8 +255,6 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
     const uint8_t *g = msg + cbase;
     uint16_t *out = scratch + cbase;
     uint32_t *ws = ws_all + k * n_lanes;
-    const int sb = static_cast<int>(tab->scale_bits);
-    const int thr_shift = 32 - sb;
     const int per = (n_lanes + blockDim.x - 1) / blockDim.x;
     const int lo = threadIdx.x * per;
     for (int l = lo; l < lo + per && l < n_lanes; ++l) ws[l] = kLow;
@@ -182,9 +270,9 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
         uint32_t cnt = 0;
         long long my_bad = -1;
         for (int l = lo; l < hi; ++l) {
-            const uint32_t f = enc[g[base + l]].x;
-            if (f == 0u) my_bad = base + l;
-            else if ((ws[l] >> thr_shift) >= f) {
+            const uint4 e = enc[g[base + l]];
+            if (e.y == 0u) my_bad = base + l;
+            else if (ws[l] > e.x) {
                 spill |= 1ull << (l - lo);
                 ++cnt;
             }
@@ -206,12 +294,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
             ++r;
         }
         top -= total;
-        for (int l = lo; l < hi; ++l) {
-            const uint4 e = enc[g[base + l]];
-            const uint32_t x = ws[l];
-            const uint32_t q = div_magic(x, e.z, e.w & 0xFFu, (e.w >> 8) & 0xFFu);
-            ws[l] = (q << sb) + e.y + (x - q * e.x);
-        }
+        for (int l = lo; l < hi; ++l) ws[l] = enc_push(ws[l], enc[g[base + l]]);
     }
     if (!bad) {
         if (threadIdx.x == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
@@ -231,13 +314,18 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
             d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states,
             d_status, d_lane_ws);
     } else {
-        constexpr int warps = 8;
-        int64_t blocks = (n_chunks + warps - 1) / warps;
-        const int64_t max_blocks = int64_t(sm_count()) * 32;
+        int64_t blocks = (n_chunks + kEncWarps - 1) / kEncWarps;
+        const int64_t max_blocks = int64_t(sm_count()) * 64;
         if (blocks > max_blocks) blocks = max_blocks;
-        encode_warp_kernel<<<static_cast<unsigned>(blocks), warps * 32, 0, stream>>>(
-            d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_chunk_words,
-            d_states, d_status);
+        if (chunk_len < (int64_t(1) << 30))
+            encode_warp_kernel<int><<<static_cast<unsigned>(blocks), kEncWarps * 32, 0, stream>>>(
+                d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_chunk_words,
+                d_states, d_status);
+        else
+            encode_warp_kernel<long long>
+                <<<static_cast<unsigned>(blocks), kEncWarps * 32, 0, stream>>>(
+                    d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_chunk_words,
+                    d_states, d_status);
     }
     ilans_note_launch();
     return cudaGetLastError();

@@ -170,10 +170,8 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
     const uint32_t m = 1u << scale_bits;
     {
         const uint32_t f = freq[tid];
-        uint32_t magic = 0, sh1 = 0, sh2 = 0;
-        if (f) divmagic(f, &magic, &sh1, &sh2);
         t->freq[tid] = f;
-        t->enc[tid] = make_uint4(f, cum[tid], magic, sh1 | (sh2 << 8));
+        t->enc[tid] = EncSym::make(f, cum[tid], scale_bits);
         t->dec[tid] = make_uint2(f, cum[tid]);
     }
     if (tid == 0) t->cum[kMaxSym] = cum[kMaxSym];
