@@ -31,7 +31,7 @@ struct alignas(16) TableDev {
     uint32_t err_detail[4];
     uint32_t freq[kMaxSym];           // zero-padded past n_sym
     uint32_t cum[kMaxSym + 4];        // cum[0..256]
-    uint4 enc[kMaxSym];               // {f, cum, magic, sh1 | sh2 << 8 | thr_shift << 16}
+    uint2 enc[kMaxSym];               // EncSym records {magic, (m - f) | cum << 16}
     uint2 dec[kMaxSym];               // {f, cum} for the decoder's second lookup
     uint32_t packed[1 << kPackedMaxBits];  // sym | (f-1) << 8 | bias << 20
     uint8_t slot_sym[1 << kMaxScaleBits];
@@ -96,28 +96,42 @@ __device__ __forceinline__ uint32_t div_magic(uint32_t n, uint32_t magic, uint32
     return q;
 }
 
-// Encoder record per symbol (16 bytes, one LDS.128):
-//   .x = spill bound  (f << (32 - sb)) - 1   (x > .x  <=>  x >= f << (32-sb))
-//   .y = magic        (0 marks f == 0: unencodable)
-//   .z = m - f        (push: x' = q*(m - f) + x + cum, since x - q*f + q*m)
-//   .w = cum << 8 | l
+// Encoder record per symbol: 8 bytes, one LDS.64 (the encoder is bound by
+// shared-memory wavefronts on this random-address lookup, so the record is
+// kept small and f / l are re-derived with two ALU ops):
+//   .x = magic                       (0 marks f == 0: unencodable)
+//   .y = (m - f) | cum << 16         (g = m - f in [0, 2^16), cum < 2^16)
+// spill:  x >= f << (32 - sb)  <=>  (x >> (32 - sb)) >= f
+// push:   x' = (x / f) * m + cum + x % f = q * g + x + cum
+// Tables whose f / cum do not fit (f > m or cum >= 2^16 -- never produced by
+// quantize / SymbolTable) are rejected by the host before encoding.
 struct EncSym {
-    __host__ __device__ static uint4 make(uint32_t f, uint32_t cum, int scale_bits) {
-        if (f == 0) return make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+    __host__ __device__ static uint2 make(uint32_t f, uint32_t cum, int scale_bits) {
+        if (f == 0) return make_uint2(0u, 0u);
         uint32_t magic, l;
         divmagic(f, &magic, &l);
-        uint64_t bound = (static_cast<uint64_t>(f) << (32 - scale_bits)) - 1;
-        if (bound > 0xFFFFFFFFull) bound = 0xFFFFFFFFull;  // f > m: never spills
         const uint32_t m = 1u << scale_bits;
-        return make_uint4(static_cast<uint32_t>(bound), magic, m - f, (cum << 8) | l);
+        return make_uint2(magic, ((m - f) & 0xFFFFu) | (cum << 16));
     }
 };
 
-// One rANS push of symbol record e onto state x (after the spill):
-// x' = (x / f) * m + cum + x % f = q*(m - f) + x + cum.
-__device__ __forceinline__ uint32_t enc_push(uint32_t x, const uint4 &e) {
-    const uint32_t q = div_magic(x, e.y, e.w);
-    return q * e.z + x + (e.w >> 8);
+struct EncCtx {
+    uint32_t m;          // 2^sb
+    uint32_t thr_shift;  // 32 - sb
+};
+
+__device__ __forceinline__ uint32_t enc_freq(const EncCtx &c, const uint2 &e) {
+    return c.m - (e.y & 0xFFFFu);
+}
+
+// One rANS push of symbol record e (frequency f) onto state x, after the
+// spill: q = x / f with l = ceil(log2 f) = 32 - clz(f - 1).
+__device__ __forceinline__ uint32_t enc_push(uint32_t x, uint32_t f, const uint2 &e) {
+    uint32_t msb;  // bfind: index of the highest set bit, 0xFFFFFFFF for 0
+    asm("bfind.u32 %0, %1;" : "=r"(msb) : "r"(f - 1u));
+    const uint32_t l = msb + 1u;
+    const uint32_t q = div_magic(x, e.x, l);
+    return q * (e.y & 0xFFFFu) + x + (e.y >> 16);
 }
 
 }  // namespace ilans

@@ -31,11 +31,12 @@
 
 namespace ilans {
 
-constexpr int kSegWords = 512;             // 1 KB per cp.async warp-copy (2 x 16 B / lane)
-constexpr int kRingWords = 4 * kSegWords;  // 4 KB payload ring per warp
-constexpr int kBatch = 16;                 // groups per fast-path batch (N = 32)
-constexpr int kObufBytes = 1024;           // 2 x 512 B output halves per warp
-constexpr int kWarpSmem = kRingWords * 2 + kObufBytes;
+constexpr int kSegWords = 256;             // 512 B per cp.async warp-copy (16 B / lane)
+constexpr int kRingWords = 4 * kSegWords;  // 2 KB payload ring per warp (2 KB aligned)
+constexpr int kRingBytes = kRingWords * 2;
+constexpr int kBatch = 8;                  // groups per fast-path batch (N = 32)
+constexpr int kObufBytes = 512;            // 2 x 256 B output halves per warp
+constexpr int kObufHalf = kObufBytes / 2;
 
 struct SegSrc {
     const uint16_t *g;    // 16-byte aligned base of the chunk's payload
@@ -44,17 +45,23 @@ struct SegSrc {
 
 __device__ __forceinline__ void issue_segment(uint16_t *ring, const SegSrc &src, uint32_t seg,
                                               int lane) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const uint64_t w0 = static_cast<uint64_t>(seg) * kSegWords + h * 256 + lane * 8;
-        uint32_t bytes = 0;
-        if (src.avail > w0) {
-            const uint64_t left = (src.avail - w0) * 2u;
-            bytes = left >= 16u ? 16u : static_cast<uint32_t>(left);
-        }
-        cp_async16(ring + (seg & 3u) * kSegWords + h * 256 + lane * 8, bytes ? src.g + w0 : src.g,
-                   bytes);
+    const uint64_t w0 = static_cast<uint64_t>(seg) * kSegWords + lane * 8;
+    uint32_t bytes = 0;
+    if (src.avail > w0) {
+        const uint64_t left = (src.avail - w0) * 2u;
+        bytes = left >= 16u ? 16u : static_cast<uint32_t>(left);
     }
+    cp_async16(ring + (seg & 3u) * kSegWords + lane * 8, bytes ? src.g + w0 : src.g, bytes);
+}
+
+// Refill read: the ring is kRingBytes-aligned in the shared window, so the
+// address is one LOP3 (base | (byte_cursor & mask)).
+__device__ __forceinline__ uint32_t ring_load(uint32_t ring_addr, uint32_t byte_off) {
+    uint16_t w;
+    asm volatile("ld.shared.u16 %0, [%1];"
+                 : "=h"(w)
+                 : "r"(ring_addr | (byte_off & (kRingBytes - 2))));
+    return w;
 }
 
 template <bool PACKED>
@@ -65,12 +72,13 @@ struct Lut {
     uint32_t mask;
     uint32_t sb;
 
+    // returns the symbol in the low byte (PACKED: the whole entry)
     __device__ __forceinline__ uint32_t pop(uint32_t &x) const {
         const uint32_t slot = x & mask;
         if (PACKED) {
             const uint32_t e = packed[slot];
             x = (((e >> 8) & 0xFFFu) + 1u) * (x >> sb) + (e >> 20);
-            return e & 0xFFu;
+            return e;
         } else {
             const uint32_t s = sym[slot];
             const uint2 d = dec[s];
@@ -80,6 +88,9 @@ struct Lut {
     }
 };
 
+// Shared memory per CTA: [align pad][W rings x 2 KB][W obufs x 512 B][LUT].
+__host__ __device__ constexpr size_t decode_warp_smem() { return kRingBytes + kObufBytes; }
+
 template <bool PACKED>
 __global__ void __launch_bounds__(1024)
 decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
@@ -88,27 +99,29 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                    uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
                    uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
                    int launch_sb) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(16) uint8_t smem_raw[];
     const int sb = static_cast<int>(tab->scale_bits);
     if (sb != launch_sb || (PACKED && !(tab->flags & kTabPacked)) || tab->status != ILANS_OK) {
         if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
         return;
     }
     const uint32_t m = 1u << sb;
+    const int nw = blockDim.x >> 5;
+    const uint32_t raw_addr = smem_addr(smem_raw);
+    uint8_t *smem = smem_raw + (((raw_addr + kRingBytes - 1) & ~uint32_t(kRingBytes - 1)) - raw_addr);
+    uint8_t *lut_base = smem + nw * (kRingBytes + kObufBytes);
 
     // ---- stage the lookup tables in shared memory ------------------------
     Lut<PACKED> lut;
     lut.mask = m - 1u;
     lut.sb = static_cast<uint32_t>(sb);
-    uint32_t lut_bytes;
     if (PACKED) {
-        uint32_t *p = reinterpret_cast<uint32_t *>(smem);
+        uint32_t *p = reinterpret_cast<uint32_t *>(lut_base);
         for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) p[i] = tab->packed[i];
         lut.packed = p;
-        lut_bytes = m * 4u;
     } else {
-        uint2 *d = reinterpret_cast<uint2 *>(smem);
-        uint8_t *s = smem + kMaxSym * sizeof(uint2);
+        uint2 *d = reinterpret_cast<uint2 *>(lut_base);
+        uint8_t *s = lut_base + kMaxSym * sizeof(uint2);
         for (uint32_t i = threadIdx.x; i < kMaxSym; i += blockDim.x) d[i] = tab->dec[i];
         if (m >= 4) {
             const uint32_t *src = reinterpret_cast<const uint32_t *>(tab->slot_sym);
@@ -119,19 +132,18 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         }
         lut.dec = d;
         lut.sym = s;
-        lut_bytes = kMaxSym * sizeof(uint2) + (m < 16 ? 16u : m);
     }
-    lut_bytes = (lut_bytes + 15u) & ~15u;
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    uint16_t *ring = reinterpret_cast<uint16_t *>(smem + lut_bytes + wib * kWarpSmem);
-    uint8_t *obuf = smem + lut_bytes + wib * kWarpSmem + kRingWords * 2;
+    uint16_t *ring = reinterpret_cast<uint16_t *>(smem + wib * kRingBytes);
+    const uint32_t ring_addr = smem_addr(ring);
+    uint8_t *obuf = smem + nw * kRingBytes + wib * kObufBytes;
     const uint32_t lt = lanemask_lt();
-    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nw;
 
-    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; k < n_chunks;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * nw + wib; k < n_chunks;
          k += warps_total) {
         const int64_t cbase = k * chunk_len;
         const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
@@ -154,24 +166,25 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         int64_t base = 0;
 
         if (n_lanes == 32) {
-            // ---------------- fast path: batches of 16 full groups ----------
-            const int64_t full = len >> 9;
-            uint32_t vv = static_cast<uint32_t>(v);  // low 32 bits suffice for ring indexing
+            // ---------------- fast path: batches of 8 full groups -----------
+            const int64_t full = len >> 8;
+            uint32_t vb = static_cast<uint32_t>(v) << 1;  // byte cursor (mod 2^32)
             for (int64_t b = 0; b < full; ++b) {
+                const uint32_t vb0 = vb;
 #pragma unroll
                 for (int g = 0; g < kBatch; ++g) {
                     const uint32_t s = lut.pop(x);
                     const bool need = x < kLow;
                     const uint32_t mk = __ballot_sync(0xffffffffu, need);
-                    if (need) x = (x << 16) | ring[(vv + __popc(mk & lt)) & (kRingWords - 1)];
-                    vv += __popc(mk);
+                    if (need) x = (x << 16) | ring_load(ring_addr, vb + (__popc(mk & lt) << 1));
+                    vb += __popc(mk) << 1;
                     obuf[g * 32 + lane] = static_cast<uint8_t>(s);
                 }
                 __syncwarp();
-                const uint4 o = reinterpret_cast<const uint4 *>(obuf)[lane];
-                reinterpret_cast<uint4 *>(out_k + (b << 9))[lane] = o;
-                // advance the ring: the cursor moved by <= 512 words
-                v += static_cast<uint32_t>(vv - static_cast<uint32_t>(v));
+                const uint2 o = reinterpret_cast<const uint2 *>(obuf)[lane];
+                reinterpret_cast<uint2 *>(out_k + (b << 8))[lane] = o;
+                // advance the ring: the cursor moved by <= 256 words
+                v += (vb - vb0) >> 1;
                 const uint64_t seg = v / kSegWords;
                 if (seg != cur) {
                     cur = seg;
@@ -181,7 +194,7 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                 }
                 __syncwarp();
             }
-            base = full << 9;
+            base = full << 8;
         }
         // ---------------- generic per-group loop (any N <= 32, tails) ------
         bool truncated = (v - delta) > wlen;
@@ -198,15 +211,16 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                 truncated = true;
                 break;
             }
-            if (need) x = (x << 16) | ring[(v + __popc(mk & lt)) & (kRingWords - 1)];
+            if (need)
+                x = (x << 16) | ring_load(ring_addr, static_cast<uint32_t>(v + __popc(mk & lt)) << 1);
             v += cnt;
             if (on) obuf[(base + lane) & (kObufBytes - 1)] = static_cast<uint8_t>(s);
             const int64_t nb = base + active;
-            if ((nb >> 9) != (base >> 9)) {  // a 512-byte half is complete
+            if ((nb >> 8) != (base >> 8)) {  // a 256-byte half is complete
                 __syncwarp();
-                const int64_t blk = base >> 9;
-                const uint4 o = reinterpret_cast<const uint4 *>(obuf + (blk & 1) * 512)[lane];
-                reinterpret_cast<uint4 *>(out_k + (blk << 9))[lane] = o;
+                const int64_t blk = base >> 8;
+                const uint2 o = reinterpret_cast<const uint2 *>(obuf + (blk & 1) * kObufHalf)[lane];
+                reinterpret_cast<uint2 *>(out_k + (blk << 8))[lane] = o;
                 __syncwarp();
             }
             const uint64_t seg = v / kSegWords;
@@ -223,8 +237,8 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
             if (lane == 0) atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
         } else {
             __syncwarp();
-            const int64_t tail0 = (len >> 9) << 9;
-            const uint8_t *half = obuf + ((len >> 9) & 1) * 512;
+            const int64_t tail0 = (len >> 8) << 8;
+            const uint8_t *half = obuf + ((len >> 8) & 1) * kObufHalf;
             for (int64_t i = tail0 + lane; i < len; i += 32) out_k[i] = half[i - tail0];
         }
         if (lane == 0 && consumed) consumed[k] = v - delta;
@@ -353,14 +367,14 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
     }
     const bool use_packed = packed && scale_bits <= kPackedMaxBits;
     const size_t lut = decode_lut_bytes(scale_bits, use_packed);
-    // warps per CTA: small CTAs spread the streams evenly over the SMs; the
-    // per-CTA LUT copy argues for bigger CTAs when the LUT is large
-    int warps = 4;
+    // 4-warp CTAs spread the streams evenly over the SMs (<= 28 per SM for
+    // 4096 chunks); the per-CTA LUT copy argues for bigger CTAs only when the
+    // LUT is large (sb > 14 generic tables).
+    int warps = lut > 24 * 1024 ? 16 : 4;
     const size_t smem_cap = 227 * 1024;
-    if (lut > 48 * 1024) warps = 32;
-    else if (lut > 8 * 1024) warps = 8;
-    while (warps > 1 && lut + size_t(warps) * kWarpSmem > smem_cap) warps >>= 1;
-    const size_t smem = lut + size_t(warps) * kWarpSmem;
+    while (warps > 1 && lut + size_t(warps) * decode_warp_smem() + kRingBytes > smem_cap)
+        warps >>= 1;
+    const size_t smem = lut + size_t(warps) * decode_warp_smem() + kRingBytes;  // + align pad
     int64_t blocks = (n_chunks + warps - 1) / warps;
     const int64_t max_blocks = int64_t(sm_count()) * 64;
     if (blocks > max_blocks) blocks = max_blocks;

@@ -87,11 +87,12 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                    uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
                    uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
-    __shared__ uint4 enc[kMaxSym];
+    __shared__ uint2 enc[kMaxSym];
     __shared__ __align__(16) uint8_t rings[kEncWarps][kInRing];
     __shared__ __align__(16) uint16_t oring[kEncWarps][kOutRing];
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
     __syncthreads();
+    const EncCtx ctx{1u << tab->scale_bits, 32u - tab->scale_bits};
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     uint8_t *ring = rings[wib];
@@ -134,8 +135,8 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 __syncwarp();
             }
             const bool on = lane < active;
-            const uint4 e = enc[on ? ring[(base + lane) & (kInRing - 1)] : 0u];
-            const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.y == 0u);
+            const uint2 e = enc[on ? ring[(base + lane) & (kInRing - 1)] : 0u];
+            const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.x == 0u);
             if (badmask) {
                 if (lane == 0)
                     atomicMax(&status->unenc_index,
@@ -143,14 +144,15 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 bad = true;
                 break;
             }
-            const bool spill = on && x > e.x;
+            const uint32_t f = enc_freq(ctx, e);
+            const bool spill = on && (x >> ctx.thr_shift) >= f;
             const uint32_t mk = __ballot_sync(0xffffffffu, spill);
             top -= __popc(mk);
             if (spill) {
                 st.put(top + __popc(mk & lt), x & 0xFFFFu);
                 x >>= 16;
             }
-            if (on) x = enc_push(x, e);
+            if (on) x = enc_push(x, f, e);
             if (st.flushed - top >= 256) st.flush(top, lane);
         }
         // ---- N = 32 fast path: 512-byte blocks, backwards, 16 groups each ----
@@ -172,9 +174,10 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             uint32_t zero_f = 0;
 #pragma unroll
             for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
-                const uint4 e = enc[blk[gg * 32 + lane]];
-                zero_f |= e.y == 0u;
-                const bool spill = x > e.x;
+                const uint2 e = enc[blk[gg * 32 + lane]];
+                zero_f |= e.x == 0u;
+                const uint32_t f = enc_freq(ctx, e);
+                const bool spill = (x >> ctx.thr_shift) >= f;
                 const uint32_t mk = __ballot_sync(0xffffffffu, spill);
                 top -= __popc(mk);
                 if (spill) {
@@ -182,12 +185,12 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         x & 0xFFFFu;
                     x >>= 16;
                 }
-                x = enc_push(x, e);
+                x = enc_push(x, f, e);
             }
             if (__ballot_sync(0xffffffffu, zero_f)) {  // rare: locate the highest bad index
                 for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
                     const uint32_t bm =
-                        __ballot_sync(0xffffffffu, enc[blk[gg * 32 + lane]].y == 0u);
+                        __ballot_sync(0xffffffffu, enc[blk[gg * 32 + lane]].x == 0u);
                     if (bm) {
                         if (lane == 0)
                             atomicMax(&status->unenc_index,
@@ -246,9 +249,10 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
                     uint32_t *__restrict__ states_out, DStatus *__restrict__ status,
                     uint32_t *__restrict__ ws_all) {
     __shared__ uint32_t scan_sh[32];
-    __shared__ uint4 enc[kMaxSym];
+    __shared__ uint2 enc[kMaxSym];
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
     __syncthreads();
+    const EncCtx ctx{1u << tab->scale_bits, 32u - tab->scale_bits};
     const int64_t k = blockIdx.x;
     const int64_t cbase = k * chunk_len;
     const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
@@ -270,9 +274,9 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
         uint32_t cnt = 0;
         long long my_bad = -1;
         for (int l = lo; l < hi; ++l) {
-            const uint4 e = enc[g[base + l]];
-            if (e.y == 0u) my_bad = base + l;
-            else if (ws[l] > e.x) {
+            const uint2 e = enc[g[base + l]];
+            if (e.x == 0u) my_bad = base + l;
+            else if ((ws[l] >> ctx.thr_shift) >= enc_freq(ctx, e)) {
                 spill |= 1ull << (l - lo);
                 ++cnt;
             }
@@ -294,7 +298,10 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
             ++r;
         }
         top -= total;
-        for (int l = lo; l < hi; ++l) ws[l] = enc_push(ws[l], enc[g[base + l]]);
+        for (int l = lo; l < hi; ++l) {
+            const uint2 e = enc[g[base + l]];
+            ws[l] = enc_push(ws[l], enc_freq(ctx, e), e);
+        }
     }
     if (!bad) {
         if (threadIdx.x == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
@@ -382,10 +389,51 @@ compact_kernel(const uint16_t *__restrict__ scratch, int64_t n, int64_t chunk_le
     const int64_t k = blockIdx.x;
     const int64_t cbase = k * chunk_len;
     const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
-    const uint32_t w = words[k];
-    const uint16_t *src = scratch + cbase + len - w;
-    uint16_t *dst = payload + offsets[k];
-    for (uint32_t i = threadIdx.x; i < w; i += blockDim.x) dst[i] = __ldcs(src + i);
+    uint32_t w = words[k];
+    uint64_t s = static_cast<uint64_t>(cbase + len - w);  // word index in scratch
+    uint64_t d = offsets[k];                               // word index in payload
+    if (w == 0) return;
+    if (d & 1) {  // make the destination 4-byte aligned
+        if (threadIdx.x == 0) payload[d] = scratch[s];
+        ++s, ++d, --w;
+    }
+    uint32_t *dst = reinterpret_cast<uint32_t *>(payload + d);
+    const uint32_t pairs = w >> 1;
+    constexpr int U = 4;  // independent loads in flight per thread
+    const uint32_t step = blockDim.x * U;
+    if (!(s & 1)) {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(scratch + s);
+        for (uint32_t i0 = threadIdx.x; i0 < pairs; i0 += step) {
+            uint32_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + u * blockDim.x;
+                v[u] = i < pairs ? __ldcs(src + i) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + u * blockDim.x;
+                if (i < pairs) dst[i] = v[u];
+            }
+        }
+    } else {  // odd source: each output word is a 16-bit funnel of two inputs
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(scratch + s - 1);
+        for (uint32_t i0 = threadIdx.x; i0 < pairs; i0 += step) {
+            uint32_t a[U], b[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + u * blockDim.x;
+                a[u] = i < pairs ? __ldcs(src + i) : 0u;
+                b[u] = i < pairs ? __ldcs(src + i + 1) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + u * blockDim.x;
+                if (i < pairs) dst[i] = __funnelshift_r(a[u], b[u], 16);
+            }
+        }
+    }
+    if ((w & 1) && threadIdx.x == 0) payload[d + w - 1] = scratch[s + w - 1];
 }
 
 cudaError_t launch_frame(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,

@@ -84,10 +84,18 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
     // rounds: every thread does <= 15 vectors, then the block flushes
     const int64_t per_round = stride * kHistVecPerRound;
     for (int64_t round_base = 0; round_base < nvec; round_base += per_round) {
-#pragma unroll 1
+        // all 15 loads in flight before the first increment (latency hiding:
+        // the increments are a serial shared-memory read-modify-write chain)
+        uint4 v[kHistVecPerRound];
+#pragma unroll
         for (int r = 0; r < kHistVecPerRound; ++r) {
             const int64_t j = i + round_base + static_cast<int64_t>(r) * stride;
-            if (j < nvec) hist_bump16(hist_smem, tid, __ldcs(vec + j));
+            v[r] = j < nvec ? __ldcs(vec + j) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int r = 0; r < kHistVecPerRound; ++r) {
+            const int64_t j = i + round_base + static_cast<int64_t>(r) * stride;
+            if (j < nvec) hist_bump16(hist_smem, tid, v[r]);
         }
         __syncthreads();
         hist_flush(hist_smem, tid, acc);
