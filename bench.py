@@ -251,18 +251,22 @@ def run_b200(a):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    n = a.mib * MIB
+    from paper_1402_3392_b200.dist import allreduce_counts, shard_for
+
     C, N, sb = a.chunk, a.lanes, a.scale_bits
+    # weak scaling: the global message is world x mib MiB; this rank owns a
+    # contiguous chunk-aligned shard of it (dist.shard_for)
+    shard = shard_for(a.mib * MIB * world, rank, world, C)
+    n = shard.n_bytes
     k_chunks = n_chunks_for(n, C)
 
-    d_msg = synth_device(n, a.zipf_s, a.seed, first=rank * n, device=dev)
+    d_msg = synth_device(n, a.zipf_s, a.seed, first=shard.byte_lo, device=dev)
     d_out = torch.empty(n, dtype=torch.uint8, device=dev)
     codec = DeviceCodec(n, C, N, sb, dev)
     stream = torch.cuda.current_stream(dev)
 
     def allreduce(counts):
-        if world > 1:
-            dist.all_reduce(counts)  # int64 sum == u64 sum bit-for-bit
+        allreduce_counts(counts)  # NCCL all-reduce of 256 x u64 (int64 sum == u64 sum)
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
