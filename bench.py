@@ -169,10 +169,11 @@ def _ref_worker(args):
 _REF_STATE = None
 
 
-def cpu_reference(msg: np.ndarray, freqs: list, sb: int, C: int, lanes: int,
-                  per_core_mib: int = 8):
-    """Time the reference CPU path on a bounded sample: all host cores, each
-    core round-trips per_core_mib of the same chunks. Returns dict."""
+def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: int = 8):
+    """Time the reference CPU path on a bounded sample of the same workload:
+    its model build (np.bincount + SymbolTable.from_counts, as
+    cli._build_table does) plus an encode+decode round trip of every sampled
+    chunk, on a fork pool over all host cores (per_core_mib per core)."""
     global _REF_STATE
     import multiprocessing as mp
 
@@ -192,8 +193,23 @@ def cpu_reference(msg: np.ndarray, freqs: list, sb: int, C: int, lanes: int,
     chunks_per_core = max(1, (per_core_mib * MIB) // C)
     total_chunks = len(msg) // C
     n_chunks = min(total_chunks, chunks_per_core * cores)
+    if kind != "reference":
+        n_chunks = min(total_chunks, chunks_per_core)
+    sample_msg = msg[: n_chunks * C]
+    # model build, timed, at the reference's own call site semantics
+    # (cli._build_table: np.bincount(minlength=max+1) -> SymbolTable.from_counts)
+    t0 = time.perf_counter()
+    counts = np.bincount(sample_msg, minlength=int(sample_msg.max()) + 1)
     if kind == "reference":
-        table = RefTable(freqs, sb)
+        table = RefTable.from_counts(counts.tolist(), sb)
+    else:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle
+
+        freqs_s = oracle.quantize(counts, sb)
+        f, cum, slot = oracle.table_views(freqs_s, sb)
+    t_model = time.perf_counter() - t0
+    if kind == "reference":
         _REF_STATE = (msg, table, C, lanes)
         ranges = np.array_split(np.arange(n_chunks), cores)
         jobs = [(int(r[0]), int(r[-1]) + 1) for r in ranges if len(r)]
@@ -206,11 +222,6 @@ def cpu_reference(msg: np.ndarray, freqs: list, sb: int, C: int, lanes: int,
         ok = all(r[1] for r in res)
         workers = len(jobs)
     else:  # oracle port (C restatement), single core
-        sys.path.insert(0, str(ROOT / "oracle"))
-        import oracle
-
-        f, cum, slot = oracle.table_views(freqs, sb)
-        n_chunks = min(total_chunks, chunks_per_core)
         t0 = time.perf_counter()
         ok = True
         for k in range(n_chunks):
@@ -222,14 +233,15 @@ def cpu_reference(msg: np.ndarray, freqs: list, sb: int, C: int, lanes: int,
         workers = 1
     sample = n_chunks * C
     return {
-        "value": sample / busy / 1e9,
+        "value": sample / (t_model + busy) / 1e9,
         "unit": "GB/s",
         "cores": workers,
         "kind": kind,
         "sample": f"{n_chunks} x {C // 1024} KiB chunks ({sample / MIB:.0f} MiB) of the same "
-                  f"workload, encode+decode round trip per chunk, reference ext backend, "
-                  f"fork pool of {workers} workers (slowest worker's time; wall incl. fork "
-                  f"{wall:.2f}s)",
+                  f"workload: model build (np.bincount + SymbolTable.from_counts, "
+                  f"{t_model:.3f}s, 1 thread) then encode+decode round trip per chunk with the "
+                  f"reference ext backend on a fork pool of {workers} workers (slowest "
+                  f"worker {busy:.3f}s; wall incl. fork {wall:.2f}s)",
         "round_trip_ok": ok,
         "wall_s": wall,
     }
@@ -419,7 +431,7 @@ def run_b200(a):
 
     if rank == 0 and world == 1 and not a.no_cpu:
         msg_h = d_msg[:n].cpu().numpy()
-        out["cpu_baseline"] = cpu_reference(msg_h, table.freq, sb, C, N)
+        out["cpu_baseline"] = cpu_reference(msg_h, sb, C, N)
         out["cpu_baseline"].pop("wall_s", None)
 
     if a.sweep and rank == 0:
@@ -477,22 +489,14 @@ def run_reference(a):
         return
     from paper_1402_3392_b200.synth import synth_host
 
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import oracle
-
     n = a.mib * MIB
     cores = len(os.sched_getaffinity(0))
     per_core = 4  # MiB per core per step -> a bounded sample of the workload
     sample = min(n, cores * per_core * MIB)
     msg = synth_host(sample, a.zipf_s, a.seed)
-    # the model is built from the full workload's histogram, as the b200 arm
-    # does; on the sample alone it would differ slightly -- use the sample's
-    # histogram computed by the reference's own call site (np.bincount)
-    counts = np.bincount(msg, minlength=int(msg.max()) + 1)
-    freqs = oracle.quantize(counts, a.scale_bits)
     vals = []
     for i in range(a.warmup + a.steps):
-        r = cpu_reference(msg, freqs, a.scale_bits, a.chunk, a.lanes, per_core_mib=per_core)
+        r = cpu_reference(msg, a.scale_bits, a.chunk, a.lanes, per_core_mib=per_core)
         if i >= a.warmup:
             vals.append(r)
     v = statistics.median([r["value"] for r in vals])
