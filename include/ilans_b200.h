@@ -103,6 +103,21 @@ int ilans_decode_lanes_u16(const uint16_t *payload, int64_t pay_len, const uint3
                            int64_t msg_len, int32_t n_lanes, uint8_t *out,
                            int64_t *consumed, ilans_status *st);
 
+/* Instrumented decode: the device form of interleave.decode_interleaved_steps
+ * (interleave.py:251-268) and lanes.decode_lanes_steps (lanes.py:221-232).
+ * Same arguments as ilans_decode_interleaved_u16 plus, per completed group g
+ * (groups of n_lanes symbols, the last one partial): trace_states[g*N + l] =
+ * lane l's state after the group's refills, trace_pos[g] = words read so
+ * far; *groups_done = completed groups. On ILANS_ERR_TRUNCATED the trace
+ * and the decoded bytes of every completed group are still filled in.
+ * trace_states needs ceil(msg_len/N)*N entries, trace_pos ceil(msg_len/N). */
+int ilans_decode_trace_u16(const uint16_t *payload, int64_t pay_len, const uint32_t *states,
+                           const uint8_t *slot_sym, int64_t n_slots, const uint32_t *freq,
+                           const uint32_t *cum, int32_t n_freq, int32_t scale_bits,
+                           int64_t msg_len, int32_t n_lanes, uint8_t *out,
+                           uint32_t *trace_states, uint64_t *trace_pos, int64_t *groups_done,
+                           int64_t *consumed, ilans_status *st);
+
 /* Replaces rans.quantize(counts, scale_bits) (rans.py:171-211), computed on
  * the device. counts has n <= 256 entries; freq_out receives n entries.
  * Errors (ILANS_ERR_VALUE, with the reference's message): scale_bits not in

@@ -38,7 +38,7 @@ class Status(ctypes.Structure):
 def _load() -> ctypes.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is not built; run `python -m paper_1402_3392_b200.build` "
+            f"{LIB_PATH} is not built; run `python paper_1402_3392_b200/build.py` "
             "(the B200 codec has no CPU fallback)"
         )
     return ctypes.CDLL(str(LIB_PATH))
@@ -64,6 +64,9 @@ PROTOTYPES = [
      [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _st]),
     ("ilans_decode_lanes_u16", ctypes.c_int,
      [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _st]),
+    ("ilans_decode_trace_u16", ctypes.c_int,
+     [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp,
+      _st]),
     ("ilans_quantize", ctypes.c_int, [_vp, _i32, _i32, _vp, _st]),
     ("ilans_histogram_u8", ctypes.c_int, [_vp, _i64, _vp, _vp, _st]),
     ("ilans_table_bytes", ctypes.c_size_t, []),

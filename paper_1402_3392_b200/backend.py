@@ -95,6 +95,41 @@ def decode_lanes_u16(payload, states, slot_sym, freq, cum, scale_bits, msg_len, 
                    n_lanes)
 
 
+def decode_trace_u16(payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):
+    """Instrumented device decode (ilans_decode_trace_u16): returns
+    (msg, trace_states [groups, N], trace_pos [groups], groups_done,
+    consumed, error) where error is the exception the plain decode would
+    raise (TruncatedStreamError) or None; everything up to the failing group
+    is filled in, so step generators can yield before raising."""
+    pay = np.ascontiguousarray(payload, dtype=np.uint16)
+    xs = np.array(states, dtype=np.uint32)
+    slot = np.ascontiguousarray(slot_sym, dtype=np.uint8)
+    f = _u32(freq)
+    c = _u32(cum)
+    groups = -(-msg_len // n_lanes) if msg_len else 0
+    out = np.zeros(max(1, msg_len), dtype=np.uint8)
+    tstates = np.zeros((max(1, groups), n_lanes), dtype=np.uint32)
+    tpos = np.zeros(max(1, groups), dtype=np.uint64)
+    done = ctypes.c_int64(0)
+    consumed = ctypes.c_int64(0)
+    st = _lib.Status()
+    rc = _lib.lib.ilans_decode_trace_u16(
+        _lib.ptr(pay), len(pay), _lib.ptr(xs), _lib.ptr(slot), len(slot), _lib.ptr(f),
+        _lib.ptr(c), len(f), int(scale_bits), int(msg_len), int(n_lanes), _lib.ptr(out),
+        _lib.ptr(tstates), _lib.ptr(tpos), ctypes.byref(done), ctypes.byref(consumed),
+        ctypes.byref(st))
+    err = None
+    if rc == _lib.ERR_TRUNCATED:
+        try:
+            _lib.raise_for(rc, st, "decode")
+        except Exception as exc:  # noqa: BLE001 -- handed back to the generator
+            err = exc
+    else:
+        _lib.raise_for(rc, st, "decode")
+    g = int(done.value)
+    return out[:msg_len], tstates[:g], tpos[:g], g, int(consumed.value), err
+
+
 B200 = Backend("b200", encode_interleaved_u16, decode_interleaved_u16, decode_lanes_u16)
 EXT = B200  # the compiled backend, under the reference's name for it
 PURE = None  # not shipped: the pure-Python kernels are the test oracle

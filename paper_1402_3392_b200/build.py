@@ -1,6 +1,6 @@
 """Build libilans_b200.so (all CUDA kernels + the C ABI) for sm_100a, in-tree.
 
-    python -m paper_1402_3392_b200.build
+    python paper_1402_3392_b200/build.py
 
 nvcc cross-compiles without a GPU; the .so lands next to this file so it
 travels to the GPU box with the repo snapshot.

@@ -134,7 +134,7 @@ struct Ctx {
     bool init = false;
     cudaStream_t stream = nullptr;
     DevBuf msg, scratch, payload, out, states, ws, slot, freq, cum, table, status, counts,
-        offsets, consumed, words;
+        offsets, consumed, words, trace;
 };
 
 Ctx g_ctx[64];
@@ -284,11 +284,17 @@ static bool host_packable(const uint8_t *slot_sym, const uint32_t *f, const uint
     return true;
 }
 
+struct HostTrace {  // host buffers for ilans_decode_trace_u16 (all null = no trace)
+    uint32_t *states;
+    uint64_t *pos;
+    int64_t *groups;
+};
+
 static int decode_common(const uint16_t *payload, int64_t pay_len, const uint32_t *states,
                          const uint8_t *slot_sym, int64_t n_slots, const uint32_t *freq,
                          const uint32_t *cum, int32_t n_freq, int32_t scale_bits,
                          int64_t msg_len, int32_t n_lanes, uint8_t *out, int64_t *consumed,
-                         ilans_status *st) {
+                         ilans_status *st, HostTrace ht = HostTrace{nullptr, nullptr, nullptr}) {
     if (msg_len < 0 || pay_len < 0) return st_fail(st, ILANS_ERR_VALUE, "negative length");
     if (n_lanes < 1 || n_lanes > 0xFFFF)
         return st_fail(st, ILANS_ERR_VALUE, "lane_count must be in [1, 65535]");
@@ -306,9 +312,20 @@ static int decode_common(const uint16_t *payload, int64_t pay_len, const uint32_
     if (msg_len == 0) {
         *consumed = 0;
         st->consumed = 0;
+        if (ht.groups) *ht.groups = 0;
         return ILANS_OK;
     }
     cudaStream_t s = c.stream;
+    const int64_t n_groups = (msg_len + n_lanes - 1) / n_lanes;
+    DecodeTrace dt{nullptr, nullptr, nullptr};
+    if (ht.states) {
+        CK(c.trace.ensure(size_t(n_groups) * n_lanes * 4 + size_t(n_groups) * 8 + 16));
+        dt.states = c.trace.as<uint32_t>();
+        dt.pos = reinterpret_cast<uint64_t *>(
+            c.trace.as<uint8_t>() + ((size_t(n_groups) * n_lanes * 4 + 7) & ~size_t(7)));
+        CK(c.words.ensure(8));
+        dt.groups = reinterpret_cast<uint64_t *>(c.words.p);
+    }
     CK(c.payload.ensure(size_t(pay_len) * 2 + 16));
     CK(c.offsets.ensure(16));
     CK(c.states.ensure(size_t(n_lanes) * 4));
@@ -337,12 +354,26 @@ static int decode_common(const uint16_t *payload, int64_t pay_len, const uint32_
     CK(launch_decode(c.payload.as<uint16_t>(), c.offsets.as<uint64_t>(), c.states.as<uint32_t>(),
                      msg_len, msg_len, n_lanes, c.table.as<TableDev>(), scale_bits, packed,
                      c.out.as<uint8_t>(), c.consumed.as<uint64_t>(), nullptr,
-                     c.status.as<DStatus>(), c.ws.as<uint32_t>(), s));
+                     c.status.as<DStatus>(), c.ws.as<uint32_t>(), s, dt));
     DStatus hs;
     if (int rc = read_dstatus(c.status.as<DStatus>(), s, &hs, st)) return rc;
     uint64_t used = 0;
     CK(cudaMemcpyAsync(&used, c.consumed.p, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (ht.states) {  // trace + decoded bytes of every completed group, even on truncation
+        uint64_t g = 0;
+        CK(cudaMemcpyAsync(&g, dt.groups, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *ht.groups = int64_t(g);
+        if (g) {
+            CK(cudaMemcpyAsync(ht.states, dt.states, size_t(g) * n_lanes * 4,
+                               cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(ht.pos, dt.pos, size_t(g) * 8, cudaMemcpyDeviceToHost, s));
+            const int64_t done = int64_t(g) * n_lanes < msg_len ? int64_t(g) * n_lanes : msg_len;
+            CK(cudaMemcpyAsync(out, c.out.p, size_t(done), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+    }
     if (hs.trunc_stream != ~0ull) {
         st->stream = int64_t(hs.trunc_stream);
         st->consumed = int64_t(used);
@@ -365,6 +396,21 @@ extern "C" int ilans_decode_interleaved_u16(const uint16_t *payload, int64_t pay
     st_clear(st);
     return decode_common(payload, pay_len, states, slot_sym, n_slots, freq, cum, n_freq,
                          scale_bits, msg_len, n_lanes, out, consumed, st);
+}
+
+extern "C" int ilans_decode_trace_u16(const uint16_t *payload, int64_t pay_len,
+                                      const uint32_t *states, const uint8_t *slot_sym,
+                                      int64_t n_slots, const uint32_t *freq, const uint32_t *cum,
+                                      int32_t n_freq, int32_t scale_bits, int64_t msg_len,
+                                      int32_t n_lanes, uint8_t *out, uint32_t *trace_states,
+                                      uint64_t *trace_pos, int64_t *groups_done,
+                                      int64_t *consumed, ilans_status *st) {
+    st_clear(st);
+    if (!trace_states || !trace_pos || !groups_done)
+        return st_fail(st, ILANS_ERR_VALUE, "trace buffers required");
+    return decode_common(payload, pay_len, states, slot_sym, n_slots, freq, cum, n_freq,
+                         scale_bits, msg_len, n_lanes, out, consumed, st,
+                         HostTrace{trace_states, trace_pos, groups_done});
 }
 
 extern "C" int ilans_decode_lanes_u16(const uint16_t *payload, int64_t pay_len,

@@ -37,6 +37,16 @@ struct alignas(16) TableDev {
     uint8_t slot_sym[1 << kMaxScaleBits];
 };
 
+// Optional per-group decode trace (single-stream calls): the lane states and
+// the read position after every group, plus the number of completed groups
+// -- the device form of interleave.decode_interleaved_steps /
+// lanes.decode_lanes_steps (interleave.py:251-268, lanes.py:221-232).
+struct DecodeTrace {
+    uint32_t *states;  // [groups][N]
+    uint64_t *pos;     // [groups]
+    uint64_t *groups;  // [1] completed groups
+};
+
 // Device status blob (first error wins, deterministic by index).
 struct alignas(16) DStatus {
     unsigned long long trunc_stream;  // min failing stream index, ~0 = none

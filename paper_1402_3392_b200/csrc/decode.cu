@@ -98,7 +98,7 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                    uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
                    uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
-                   int launch_sb) {
+                   int launch_sb, DecodeTrace trace) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const int sb = static_cast<int>(tab->scale_bits);
     if (sb != launch_sb || (PACKED && !(tab->flags & kTabPacked)) || tab->status != ILANS_OK) {
@@ -165,7 +165,7 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         uint8_t *out_k = out + cbase;
         int64_t base = 0;
 
-        if (n_lanes == 32) {
+        if (n_lanes == 32 && !trace.states) {
             // ---------------- fast path: batches of 8 full groups -----------
             const int64_t full = len >> 8;
             uint32_t vb = static_cast<uint32_t>(v) << 1;  // byte cursor (mod 2^32)
@@ -214,6 +214,11 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
             if (need)
                 x = (x << 16) | ring_load(ring_addr, static_cast<uint32_t>(v + __popc(mk & lt)) << 1);
             v += cnt;
+            if (trace.states) {
+                const int64_t gi = base / n_lanes;
+                if (lane < n_lanes) trace.states[gi * n_lanes + lane] = x;
+                if (lane == 0) trace.pos[gi] = v - delta;
+            }
             if (on) obuf[(base + lane) & (kObufBytes - 1)] = static_cast<uint8_t>(s);
             const int64_t nb = base + active;
             if ((nb >> 8) != (base >> 8)) {  // a 256-byte half is complete
@@ -233,14 +238,16 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                 __syncwarp();
             }
         }
-        if (truncated) {
-            if (lane == 0) atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
-        } else {
+        if (truncated && lane == 0)
+            atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
+        {   // bytes of the last partial 256-byte block (all groups done so far)
+            const int64_t end = truncated ? base : len;
             __syncwarp();
-            const int64_t tail0 = (len >> 8) << 8;
-            const uint8_t *half = obuf + ((len >> 8) & 1) * kObufHalf;
-            for (int64_t i = tail0 + lane; i < len; i += 32) out_k[i] = half[i - tail0];
+            const int64_t tail0 = (end >> 8) << 8;
+            const uint8_t *half = obuf + ((end >> 8) & 1) * kObufHalf;
+            for (int64_t i = tail0 + lane; i < end; i += 32) out_k[i] = half[i - tail0];
         }
+        if (trace.groups && lane == 0) trace.groups[k] = (base < len ? base : len + n_lanes - 1) / n_lanes;
         if (lane == 0 && consumed) consumed[k] = v - delta;
         if (final_states && lane < n_lanes) final_states[k * n_lanes + lane] = x;
         cp_async_wait<0>();
@@ -285,7 +292,8 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
                     const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
                     int n_lanes, const TableDev *__restrict__ tab, uint8_t *__restrict__ out,
                     uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
-                    DStatus *__restrict__ status, uint32_t *__restrict__ ws_all) {
+                    DStatus *__restrict__ status, uint32_t *__restrict__ ws_all,
+                    DecodeTrace trace) {
     __shared__ uint32_t scan_sh[32];
     const int64_t k = blockIdx.x;
     const int64_t cbase = k * chunk_len;
@@ -301,7 +309,8 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
     for (int l = lo; l < lo + per && l < n_lanes; ++l) ws[l] = states[k * n_lanes + l];
     uint64_t pos = 0;
     bool truncated = false;
-    for (int64_t base = 0; base < len; base += n_lanes) {
+    int64_t base = 0;
+    for (; base < len; base += n_lanes) {
         const int64_t left = len - base;
         const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
         const int hi = lo + per < active ? lo + per : active;
@@ -335,10 +344,17 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
             ++r;
         }
         pos += total;
+        if (trace.states) {
+            const int64_t gi = base / n_lanes;
+            for (int l = lo; l < lo + per && l < n_lanes; ++l)
+                trace.states[gi * n_lanes + l] = ws[l];
+            if (threadIdx.x == 0) trace.pos[gi] = pos;
+        }
     }
     if (threadIdx.x == 0) {
         if (truncated) atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
         if (consumed) consumed[k] = pos;
+        if (trace.groups) trace.groups[k] = (base < len ? base : len + n_lanes - 1) / n_lanes;
     }
     if (final_states)
         for (int l = lo; l < lo + per && l < n_lanes; ++l) final_states[k * n_lanes + l] = ws[l];
@@ -354,14 +370,15 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
                           const uint32_t *d_states, int64_t n, int64_t chunk_len, int n_lanes,
                           const TableDev *d_table, int scale_bits, bool packed,
                           uint8_t *d_out, uint64_t *d_consumed, uint32_t *d_final_states,
-                          DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream) {
+                          DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream,
+                          DecodeTrace trace) {
     if (n <= 0) return cudaSuccess;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
     if (n_lanes > 32) {
         const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
         decode_block_kernel<<<static_cast<unsigned>(n_chunks), threads, 0, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table, d_out,
-            d_consumed, d_final_states, d_status, d_lane_ws);
+            d_consumed, d_final_states, d_status, d_lane_ws, trace);
         ilans_note_launch();
         return cudaGetLastError();
     }
@@ -383,13 +400,13 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         decode_warp_kernel<true><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
-            d_out, d_consumed, d_final_states, d_status, scale_bits);
+            d_out, d_consumed, d_final_states, d_status, scale_bits, trace);
     } else {
         cudaFuncSetAttribute(decode_warp_kernel<false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         decode_warp_kernel<false><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
-            d_out, d_consumed, d_final_states, d_status, scale_bits);
+            d_out, d_consumed, d_final_states, d_status, scale_bits, trace);
     }
     ilans_note_launch();
     return cudaGetLastError();

@@ -35,7 +35,8 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
                           const uint32_t *d_states, int64_t n, int64_t chunk_len, int n_lanes,
                           const TableDev *d_table, int scale_bits, bool packed,
                           uint8_t *d_out, uint64_t *d_consumed, uint32_t *d_final_states,
-                          DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream);
+                          DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream,
+                          DecodeTrace trace = DecodeTrace{nullptr, nullptr, nullptr});
 
 // synth.cu
 cudaError_t launch_synth(uint8_t *d_out, int64_t n, uint64_t seed, int64_t first_index,

@@ -16,12 +16,12 @@ import numpy as np
 
 from . import backend as backend_mod
 from .errors import TrailingGarbageWarning, UnsupportedVariantError
-from .interleave import Container, _as_symbols, encode_interleaved
+from .interleave import Container, _as_symbols, _steps, encode_interleaved
 from .rans import WORD16, SymbolTable
 
 MAX_LANES = 32
 
-__all__ = ["MAX_LANES", "decode_lanes_full", "encode_lanes_full"]
+__all__ = ["MAX_LANES", "decode_lanes_full", "decode_lanes_steps", "encode_lanes_full"]
 
 
 def _check_lane_decodable(container: Container) -> None:
@@ -58,6 +58,14 @@ def decode_lanes_full(container: Container, *, backend=None) -> np.ndarray:
             stacklevel=2,
         )
     return msg
+
+
+def decode_lanes_steps(container: Container):
+    """Instrumented lane decode: yields (symbols, states, digits_read) after
+    every group, in the shape of interleave.decode_interleaved_steps
+    (reference lanes.py:221-232); a device trace of the warp decoder."""
+    _check_lane_decodable(container)
+    yield from _steps(container)
 
 
 def encode_lanes_full(message, table: SymbolTable, lane_count: int) -> Container:

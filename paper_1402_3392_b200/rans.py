@@ -29,6 +29,7 @@ __all__ = [
     "SymbolTable",
     "quantize",
     "encode_threshold",
+    "RenormStats",
     "serialize_table",
     "parse_table",
     "variant_by_tag",
@@ -176,6 +177,37 @@ class SymbolTable:
 
     def __repr__(self):
         return f"SymbolTable(n={self.alphabet_size}, scale_bits={self.scale_bits})"
+
+
+class RenormStats:
+    """Spill / refill counters (reference rans.py:235-263). The B200 path
+    fills them from kernel totals: word16 moves at most one digit per symbol,
+    so symbols, digits and the per-symbol maximum follow from the counts."""
+
+    def __init__(self):
+        self.encode_symbols = 0
+        self.encode_digits = 0
+        self.max_encode_digits = 0
+        self.decode_symbols = 0
+        self.decode_digits = 0
+        self.max_decode_digits = 0
+
+    def note_encode(self, digits: int) -> None:
+        self.encode_symbols += 1
+        self.encode_digits += digits
+        self.max_encode_digits = max(self.max_encode_digits, digits)
+
+    def note_decode(self, digits: int) -> None:
+        self.decode_symbols += 1
+        self.decode_digits += digits
+        self.max_decode_digits = max(self.max_decode_digits, digits)
+
+    def __repr__(self):
+        return (
+            f"RenormStats(enc {self.encode_symbols} syms / {self.encode_digits} digits, "
+            f"max {self.max_encode_digits}; dec {self.decode_symbols} syms / "
+            f"{self.decode_digits} digits, max {self.max_decode_digits})"
+        )
 
 
 def encode_threshold(table: SymbolTable, variant: RenormVariant, symbol: int) -> int:

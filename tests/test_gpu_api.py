@@ -1,0 +1,111 @@
+"""Reference-suite behaviours on the B200 path that go beyond plain
+encode/decode: lockstep step generators (acceptance criterion 2,
+pkg/tests/test_acceptance.py:65-88), the stats= counters (criterion 3,
+test_acceptance.py:91-110; test_interleave.py:128-142) and the
+decoder-returns-to-L property (test_interleave.py:114-121). The expected
+step traces come from the oracle's serial decoder run group by group."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1402_3392_b200 as ilb
+from paper_1402_3392_b200 import _lib
+from paper_1402_3392_b200.errors import TruncatedStreamError, UnsupportedVariantError
+from paper_1402_3392_b200.interleave import Container, decode_interleaved_steps
+from paper_1402_3392_b200.lanes import MAX_LANES, decode_lanes_steps
+from paper_1402_3392_b200.rans import BYTE8, WORD16, RenormStats, SymbolTable
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device: the -m gpu suite must run on a B200")
+
+
+def random_table(rng, max_n=64, max_scale=14):
+    n = int(rng.integers(2, max_n + 1))
+    sb = int(rng.integers(max(1, (n - 1).bit_length()), max_scale + 1))
+    counts = rng.integers(0, 900, size=n)
+    counts[int(rng.integers(0, n))] += 1
+    return SymbolTable(oracle.quantize(counts, sb), sb)
+
+
+def random_message(rng, table, n):
+    return rng.choice(table.alphabet_size, size=n, p=table.freq_u32 / table.total).astype(np.uint8)
+
+
+def oracle_steps(c: Container):
+    """Per-group (symbols, states, read_pos) from the oracle's serial decoder."""
+    t, N, n = c.table, c.lane_count, c.message_length
+    f, cum, slot = t.freq_u32, t.cum_u32, t.slot_u8
+    states = np.asarray(c.final_states, dtype=np.uint32)
+    out = []
+    pos = 0
+    for base in range(0, n, N):
+        active = min(N, n - base)  # one group: symbols base .. base+active-1
+        o, used, states = oracle._decode(oracle.lib().orc_decode_u16, c.payload[pos:], states,
+                                         slot, f, cum, t.scale_bits, active, N)
+        pos += used
+        out.append((tuple(o.tolist()), tuple(int(x) for x in states), pos))
+    return out
+
+
+def test_lockstep_steps_match_serial_decoder():
+    rng = np.random.default_rng(2026)
+    for lanes in (1, 2, 4, 8, 16, 32, 40):
+        for n in (0, 1, max(0, lanes - 1), lanes, lanes + 1, 2 * lanes + 1, 97, 1500):
+            t = random_table(rng)
+            msg = random_message(rng, t, n)
+            c = ilb.encode_interleaved(msg, t, lanes, WORD16)
+            want = oracle_steps(c)
+            got = list(decode_interleaved_steps(c))
+            assert got == want, (lanes, n)
+            if lanes <= MAX_LANES:
+                assert list(decode_lanes_steps(c)) == want
+            if n:
+                assert got[-1][1] == (WORD16.lower_bound,) * lanes  # back to L
+                assert got[-1][2] == len(c.payload)
+            collected = [s for syms, _, _ in got for s in syms]
+            assert collected == msg.tolist()
+
+
+def test_steps_raise_lazily_on_truncation():
+    rng = np.random.default_rng(7)
+    t = random_table(rng)
+    msg = random_message(rng, t, 3000)
+    c = ilb.encode_interleaved(msg, t, 4, WORD16)
+    cut = Container(c.variant, 4, c.message_length, t, c.final_states, c.payload[: len(c.payload) // 2])
+    gen = decode_interleaved_steps(cut)
+    first = next(gen)  # groups before the failure are still produced
+    assert first == oracle_steps(c)[0]
+    with pytest.raises(TruncatedStreamError):
+        for _ in gen:
+            pass
+
+
+def test_steps_reject_unsupported():
+    t = SymbolTable([1, 3], 2)
+    c8 = Container(BYTE8, 2, 3, t, (1 << 23, 1 << 23), np.zeros(0, np.uint8))
+    with pytest.raises(UnsupportedVariantError):
+        next(decode_lanes_steps(c8))
+    c33 = ilb.encode_interleaved([0, 1] * 40, t, MAX_LANES + 1, WORD16)
+    with pytest.raises(UnsupportedVariantError):
+        next(decode_lanes_steps(c33))
+    assert len(list(decode_interleaved_steps(c33))) == 3  # serial steps are fine
+
+
+def test_stats_counters_single_digit_property():
+    rng = np.random.default_rng(3)
+    stats = RenormStats()
+    for _ in range(5):
+        t = random_table(rng)
+        msg = random_message(rng, t, 50_000)
+        c = ilb.encode_interleaved(msg, t, 4, WORD16, stats=stats)
+        assert c.to_bytes() == ilb.encode_interleaved(msg, t, 4, WORD16).to_bytes()
+        assert np.array_equal(ilb.decode_interleaved(c, stats=stats), msg)
+    assert stats.encode_symbols == stats.decode_symbols == 250_000
+    assert stats.encode_digits == stats.decode_digits > 0
+    assert stats.max_encode_digits == stats.max_decode_digits == 1
