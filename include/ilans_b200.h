@@ -168,7 +168,7 @@ int ilans_dstatus_reset_dev(void *d_status, void *stream);
 /* Read a device status blob (synchronizes `stream`). */
 int ilans_dstatus_read_host(const void *d_status, void *stream, ilans_status *st);
 
-/* Chunked encode. d_scratch holds n words (chunk k uses words
+/* Chunked encode. d_scratch holds n + 8 words (chunk k uses words
  * [k*C, k*C + len_k), filled from the end); d_chunk_words[k] receives the
  * payload length of chunk k and d_states[k*N + l] its final lane states.
  * C must be a positive multiple of 16. */

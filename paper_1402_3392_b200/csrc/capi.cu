@@ -233,7 +233,7 @@ extern "C" int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const
     }
     cudaStream_t s = c.stream;
     CK(c.msg.ensure(size_t(n)));
-    CK(c.scratch.ensure(size_t(n) * 2));
+    CK(c.scratch.ensure(size_t(n) * 2 + 16));  // + 8 words of block-store slack
     CK(c.states.ensure(size_t(n_lanes) * 4));
     CK(c.ws.ensure(size_t(n_lanes) * 4));
     CK(c.freq.ensure(kMaxSym * 4));

@@ -110,9 +110,10 @@ __device__ __forceinline__ uint32_t div_magic(uint32_t n, uint32_t magic, uint32
 // shared-memory wavefronts on this random-address lookup, so the record is
 // kept small and f / l are re-derived with two ALU ops):
 //   .x = magic                       (0 marks f == 0: unencodable)
-//   .y = (m - f) | cum << 16         (g = m - f in [0, 2^16), cum < 2^16)
-// spill:  x >= f << (32 - sb)  <=>  (x >> (32 - sb)) >= f
-// push:   x' = (x / f) * m + cum + x % f = q * g + x + cum
+//   .y = (f - 1) | cum << 16         (f - 1 in [0, 2^16), cum < 2^16)
+// spill:  x >= f << (32 - sb)  <=>  (x >> (32 - sb)) > f - 1
+// push:   x' = (x / f) * m + cum + x % f = q * (m - f) + x + cum
+//         with q = x / f via the magic and l = ceil(log2 f) = bfind(f - 1) + 1
 // Tables whose f / cum do not fit (f > m or cum >= 2^16 -- never produced by
 // quantize / SymbolTable) are rejected by the host before encoding.
 struct EncSym {
@@ -120,28 +121,28 @@ struct EncSym {
         if (f == 0) return make_uint2(0u, 0u);
         uint32_t magic, l;
         divmagic(f, &magic, &l);
-        const uint32_t m = 1u << scale_bits;
-        return make_uint2(magic, ((m - f) & 0xFFFFu) | (cum << 16));
+        (void)scale_bits;
+        return make_uint2(magic, ((f - 1u) & 0xFFFFu) | (cum << 16));
     }
 };
 
 struct EncCtx {
-    uint32_t m;          // 2^sb
+    uint32_t mm1;        // 2^sb - 1
     uint32_t thr_shift;  // 32 - sb
+    __device__ explicit EncCtx(uint32_t sb) : mm1((1u << sb) - 1u), thr_shift(32u - sb) {}
 };
 
-__device__ __forceinline__ uint32_t enc_freq(const EncCtx &c, const uint2 &e) {
-    return c.m - (e.y & 0xFFFFu);
+__device__ __forceinline__ bool enc_spill(const EncCtx &c, uint32_t x, const uint2 &e) {
+    return (x >> c.thr_shift) > (e.y & 0xFFFFu);
 }
 
-// One rANS push of symbol record e (frequency f) onto state x, after the
-// spill: q = x / f with l = ceil(log2 f) = 32 - clz(f - 1).
-__device__ __forceinline__ uint32_t enc_push(uint32_t x, uint32_t f, const uint2 &e) {
+// One rANS push of symbol record e onto state x (after the spill).
+__device__ __forceinline__ uint32_t enc_push(const EncCtx &c, uint32_t x, const uint2 &e) {
+    const uint32_t fm1 = e.y & 0xFFFFu;
     uint32_t msb;  // bfind: index of the highest set bit, 0xFFFFFFFF for 0
-    asm("bfind.u32 %0, %1;" : "=r"(msb) : "r"(f - 1u));
-    const uint32_t l = msb + 1u;
-    const uint32_t q = div_magic(x, e.x, l);
-    return q * (e.y & 0xFFFFu) + x + (e.y >> 16);
+    asm("bfind.u32 %0, %1;" : "=r"(msb) : "r"(fm1));
+    const uint32_t q = div_magic(x, e.x, msb + 1u);
+    return q * (c.mm1 - fm1) + x + (e.y >> 16);
 }
 
 }  // namespace ilans

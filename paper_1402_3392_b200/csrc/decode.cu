@@ -176,7 +176,9 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                     const uint32_t s = lut.pop(x);
                     const bool need = x < kLow;
                     const uint32_t mk = __ballot_sync(0xffffffffu, need);
-                    if (need) x = (x << 16) | ring_load(ring_addr, vb + (__popc(mk & lt) << 1));
+                    // every lane loads (one wavefront either way), then selects
+                    const uint32_t w = ring_load(ring_addr, vb + (__popc(mk & lt) << 1));
+                    x = need ? ((x << 16) | w) : x;
                     vb += __popc(mk) << 1;
                     obuf[g * 32 + lane] = static_cast<uint8_t>(s);
                 }

@@ -39,36 +39,39 @@ __device__ __forceinline__ void issue_msg_segment(uint8_t *ring, const uint8_t *
     cp_async16(ring + (static_cast<uint32_t>(seg) & 3u) * kInSeg + lane * 16, src, bytes);
 }
 
-constexpr int kEncWarps = 4;    // warps per CTA: 7 CTAs/SM hold 4096 streams in one wave
-constexpr int kOutRing = 1024;  // per-warp staging ring for spilled words (2 KB)
+constexpr int kEncWarps = 4;     // warps per CTA: 7 CTAs/SM hold 4096 streams in one wave
+constexpr int kOutRing = 1024;   // per-warp staging ring for spilled words (2 KB)
+constexpr uint32_t kOutRingBytes = kOutRing * 2;
 
-// Spilled words are staged in a per-warp shared ring indexed by their final
-// scratch position (w & 1023) and written to HBM as aligned 16-byte blocks:
-// flush() moves the complete 8-word blocks of [top, flushed) and keeps the
-// partial block at the bottom for the next flush; finish() writes the rest.
+__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<uint16_t>(v)));
+}
+
+// Spilled words are staged in a per-warp shared ring (2 KB aligned, so an
+// address is base | (byte_offset & mask)) indexed by their final scratch
+// position w & 1023, and written to HBM as aligned 16-byte blocks. `flushed`
+// starts at len rounded up to 8 words: the padding words past len land in
+// the scratch slack / next chunk's untouched head and are never read.
+// flush() writes the complete blocks of [roundup8(top), flushed); finish()
+// writes the last < 8 words [top, roundup8(top)) one by one.
 template <typename Idx>
 struct SpillStage {
-    uint16_t *ring;   // shared, kOutRing words
-    uint16_t *out;    // chunk's scratch region in HBM
-    Idx flushed;      // words [flushed, len) are in HBM
+    uint16_t *ring;      // generic pointer to the ring
+    uint32_t ring_addr;  // shared-window address of the ring (2 KB aligned)
+    uint16_t *out;       // chunk's scratch region in HBM
+    Idx flushed;         // words [flushed, len) are in HBM (flushed % 8 == 0)
 
-    __device__ __forceinline__ void put(Idx w, uint32_t v) { ring[w & (kOutRing - 1)] = v; }
+    __device__ __forceinline__ void put(Idx w, uint32_t v) {
+        sts16(ring_addr | ((static_cast<uint32_t>(w) << 1) & (kOutRingBytes - 2)), v);
+    }
 
     __device__ __forceinline__ void flush(Idx top, int lane) {
         __syncwarp();
-        Idx hi = flushed;
         const Idx lo = (top + 7) & ~Idx(7);
-        if (lo >= hi) return;
-        if (hi & 7) {  // unaligned chunk end (last chunk only): scalar words
-            const Idx a = hi & ~Idx(7);
-            const Idx s = a > lo ? a : lo;
-            if (lane < hi - s) out[s + lane] = ring[(s + lane) & (kOutRing - 1)];
-            hi = s;
-        }
-        for (Idx blk = lo + Idx(lane) * 8; blk < hi; blk += 256)
+        for (Idx blk = lo + Idx(lane) * 8; blk < flushed; blk += 256)
             *reinterpret_cast<uint4 *>(out + blk) =
                 *reinterpret_cast<const uint4 *>(ring + (blk & (kOutRing - 1)));
-        flushed = lo;
+        if (lo < flushed) flushed = lo;
         __syncwarp();
     }
 
@@ -89,13 +92,17 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                    uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
     __shared__ uint2 enc[kMaxSym];
     __shared__ __align__(16) uint8_t rings[kEncWarps][kInRing];
-    __shared__ __align__(16) uint16_t oring[kEncWarps][kOutRing];
+    __shared__ __align__(16) uint16_t oring_raw[kEncWarps * kOutRing + kOutRing];
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
     __syncthreads();
-    const EncCtx ctx{1u << tab->scale_bits, 32u - tab->scale_bits};
+    const EncCtx ctx(tab->scale_bits);
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     uint8_t *ring = rings[wib];
+    const uint32_t oraw = smem_addr(oring_raw);
+    const uint32_t oalign = ((oraw + kOutRingBytes - 1) & ~(kOutRingBytes - 1)) - oraw;
+    uint16_t *oring = oring_raw + oalign / 2 + wib * kOutRing;
+    const uint32_t oring_addr = smem_addr(oring);
     const uint32_t lt = lanemask_lt();
     const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
 
@@ -104,7 +111,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         const int64_t cbase = k * chunk_len;
         const Idx len = static_cast<Idx>((n - cbase) < chunk_len ? (n - cbase) : chunk_len);
         const uint8_t *g = msg + cbase;
-        SpillStage<Idx> st{oring[wib], scratch + cbase, len};
+        SpillStage<Idx> st{oring, oring_addr, scratch + cbase, (len + 7) & ~Idx(7)};
         Idx cur = (len - 1) >> 9;
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
@@ -144,15 +151,14 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 bad = true;
                 break;
             }
-            const uint32_t f = enc_freq(ctx, e);
-            const bool spill = on && (x >> ctx.thr_shift) >= f;
+            const bool spill = on && enc_spill(ctx, x, e);
             const uint32_t mk = __ballot_sync(0xffffffffu, spill);
             top -= __popc(mk);
             if (spill) {
                 st.put(top + __popc(mk & lt), x & 0xFFFFu);
                 x >>= 16;
             }
-            if (on) x = enc_push(x, f, e);
+            if (on) x = enc_push(ctx, x, e);
             if (st.flushed - top >= 256) st.flush(top, lane);
         }
         // ---- N = 32 fast path: 512-byte blocks, backwards, 16 groups each ----
@@ -172,21 +178,22 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             __syncwarp();
             const uint8_t *blk = ring + (static_cast<uint32_t>(b) & 3u) * kInSeg;
             uint32_t zero_f = 0;
+            uint32_t topb = static_cast<uint32_t>(top) << 1;  // ring byte cursor
+            const uint32_t topb0 = topb;
 #pragma unroll
             for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
                 const uint2 e = enc[blk[gg * 32 + lane]];
                 zero_f |= e.x == 0u;
-                const uint32_t f = enc_freq(ctx, e);
-                const bool spill = (x >> ctx.thr_shift) >= f;
+                const bool spill = enc_spill(ctx, x, e);
                 const uint32_t mk = __ballot_sync(0xffffffffu, spill);
-                top -= __popc(mk);
-                if (spill) {
-                    st.ring[(static_cast<uint32_t>(top) + __popc(mk & lt)) & (kOutRing - 1)] =
-                        x & 0xFFFFu;
-                    x >>= 16;
-                }
-                x = enc_push(x, f, e);
+                topb -= __popc(mk) << 1;
+                if (spill)
+                    sts16(oring_addr | ((topb + (__popc(mk & lt) << 1)) & (kOutRingBytes - 2)),
+                          x);
+                x = spill ? x >> 16 : x;
+                x = enc_push(ctx, x, e);
             }
+            top -= static_cast<Idx>((topb0 - topb) >> 1);
             if (__ballot_sync(0xffffffffu, zero_f)) {  // rare: locate the highest bad index
                 for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
                     const uint32_t bm =
@@ -252,7 +259,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
     __shared__ uint2 enc[kMaxSym];
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
     __syncthreads();
-    const EncCtx ctx{1u << tab->scale_bits, 32u - tab->scale_bits};
+    const EncCtx ctx(tab->scale_bits);
     const int64_t k = blockIdx.x;
     const int64_t cbase = k * chunk_len;
     const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
@@ -276,7 +283,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
         for (int l = lo; l < hi; ++l) {
             const uint2 e = enc[g[base + l]];
             if (e.x == 0u) my_bad = base + l;
-            else if ((ws[l] >> ctx.thr_shift) >= enc_freq(ctx, e)) {
+            else if (enc_spill(ctx, ws[l], e)) {
                 spill |= 1ull << (l - lo);
                 ++cnt;
             }
@@ -300,7 +307,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
         top -= total;
         for (int l = lo; l < hi; ++l) {
             const uint2 e = enc[g[base + l]];
-            ws[l] = enc_push(ws[l], enc_freq(ctx, e), e);
+            ws[l] = enc_push(ctx, ws[l], e);
         }
     }
     if (!bad) {
