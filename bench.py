@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="config 4: entropy x precision sweep")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     return ap.parse_args()
 
 
@@ -73,7 +74,8 @@ def config_of(a, world):
         "seed": a.seed,
         "parallelism": f"chunk-sharded x{world} (weak), histogram all-reduce" if world > 1
         else "single GPU",
-        "l2": "inputs (256 MiB) larger than the 126 MB L2; no flush",
+        "l2": f"inputs ({a.mib} MiB/GPU) vs the 126 MB L2: "
+              + ("larger, no flush needed" if a.mib * MIB > 126e6 else "SMALLER: L2-resident"),
     }
 
 
@@ -259,10 +261,16 @@ def run_b200(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; --dist-backend gloo (+ wrap-around device index)
+    # only exists to smoke-test the multi-rank logic on a single-GPU box
+    local = local % max(1, torch.cuda.device_count()) if a.dist_backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     from paper_1402_3392_b200.dist import allreduce_counts, shard_for
 
     C, N, sb = a.chunk, a.lanes, a.scale_bits
@@ -290,9 +298,7 @@ def run_b200(a):
         if marks: marks[1].record(stream)
         codec.encode(d_msg, n, frame=False)
         if marks: marks[2].record(stream)
-        _lib.check_dev(_lib.lib.ilans_frame_chunks_dev(
-            codec.scratch.data_ptr(), n, C, codec.chunk_words.data_ptr(),
-            codec.offsets.data_ptr(), codec.payload.data_ptr(), stream.cuda_stream), "frame")
+        codec.frame_range(n, 0, k_chunks, codec.payload.data_ptr())
         if marks: marks[3].record(stream)
         codec.decode(d_out, n)
         if marks: marks[4].record(stream)
@@ -356,8 +362,10 @@ def run_b200(a):
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback 6.65 TB/s"
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text())
+    if tf.exists():  # dram bytes per launch from the committed ncu --set full capture
+        t = json.loads(tf.read_text())
+        if t.get("config") == f"mib={a.mib},chunk={C},lanes={N},sb={sb}":
+            traffic = t
     dom = "decode" if dec_ms >= enc_ms else "encode"
     dom_ms = max(dec_ms, enc_ms)
     dom_bytes = dec_bytes if dom == "decode" else enc_bytes

@@ -178,10 +178,13 @@ int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
                             void *stream);
 /* Framing: d_word_offsets[0..n_chunks] = exclusive prefix sum of chunk
  * words, and the chunk payloads packed back to back into d_payload
- * (capacity n words). */
+ * (capacity n words) at those offsets. carry_in != 0 continues a previous
+ * batch: d_word_offsets[0] is read as the starting offset instead of being
+ * set to 0 (so batches of chunks pack into one stream). d_payload may be a
+ * mapped pinned host pointer (the packing then streams over PCIe). */
 int ilans_frame_chunks_dev(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
                            const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
-                           uint16_t *d_payload, void *stream);
+                           uint16_t *d_payload, int32_t carry_in, void *stream);
 /* Chunked decode of a framed stream: d_out receives n bytes, d_consumed[k]
  * the words chunk k consumed (== its payload length on valid input), and
  * d_final_states (optional, n_chunks*N) the lane states after decoding.

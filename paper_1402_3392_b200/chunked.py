@@ -229,17 +229,58 @@ class DeviceCodec:
     def encode(self, d_msg, n: int, frame: bool = True):
         """Encode n bytes at d_msg with the current table: one launch for all
         chunks, then (frame=True) the offset scan + payload compaction."""
+        k = n_chunks_for(n, self.chunk_len)
+        self.encode_range(self._p(d_msg), n, 0, k)
+        if frame:
+            self.frame_range(n, 0, k, self._p(self.payload))
+
+    # chunk-range pieces (for batched / pipelined use; pointers are ints)
+    def _range(self, n: int, k0: int, k1: int):
         if n > self.capacity:
             raise ValueError("message larger than codec capacity")
-        s = self._s()
+        lo = k0 * self.chunk_len
+        return lo, min(n, k1 * self.chunk_len) - lo
+
+    def encode_range(self, msg_ptr: int, n: int, k0: int, k1: int):
+        """Encode chunks [k0, k1) of the n-byte message starting at msg_ptr."""
+        lo, nb = self._range(n, k0, k1)
+        if nb <= 0:
+            return
         _lib.check_dev(_lib.lib.ilans_encode_chunks_dev(
-            self._p(d_msg), int(n), self.chunk_len, self.lane_count, self._p(self.table),
-            self._p(self.scratch), self._p(self.chunk_words), self._p(self.states),
-            self._p(self.status), s), "encode")
-        if frame:
-            _lib.check_dev(_lib.lib.ilans_frame_chunks_dev(
-                self._p(self.scratch), int(n), self.chunk_len, self._p(self.chunk_words),
-                self._p(self.offsets), self._p(self.payload), s), "frame")
+            msg_ptr + lo, nb, self.chunk_len, self.lane_count, self._p(self.table),
+            self._p(self.scratch) + 2 * lo, self._p(self.chunk_words) + 4 * k0,
+            self._p(self.states) + 4 * k0 * self.lane_count, self._p(self.status), self._s()),
+            "encode")
+
+    def frame_range(self, n: int, k0: int, k1: int, payload_ptr: int, stream: int | None = None):
+        """Offsets for chunks [k0, k1) (continuing from offsets[k0] when
+        k0 > 0) and their payloads packed at payload_ptr + 2*offset. The
+        destination may be mapped pinned host memory (packing over PCIe)."""
+        lo, nb = self._range(n, k0, k1)
+        if nb <= 0:
+            if k0 == 0:
+                self.offsets[:1].zero_()
+            return
+        _lib.check_dev(_lib.lib.ilans_frame_chunks_dev(
+            self._p(self.scratch) + 2 * lo, nb, self.chunk_len,
+            self._p(self.chunk_words) + 4 * k0, self._p(self.offsets) + 8 * k0, payload_ptr,
+            1 if k0 > 0 else 0, self._s() if stream is None else stream), "frame")
+
+    def decode_range(self, out_ptr: int, n: int, k0: int, k1: int, payload_ptr: int,
+                     offsets_ptr: int, states_ptr: int, final_states: bool = False,
+                     stream: int | None = None):
+        """Decode chunks [k0, k1) into out_ptr + k0*C. offsets_ptr/states_ptr
+        point at the whole message's directory (global word offsets into
+        payload_ptr)."""
+        lo, nb = self._range(n, k0, k1)
+        if nb <= 0:
+            return
+        N = self.lane_count
+        _lib.check_dev(_lib.lib.ilans_decode_chunks_dev(
+            payload_ptr, offsets_ptr + 8 * k0, states_ptr + 4 * k0 * N, nb, self.chunk_len, N,
+            self._p(self.table), self.scale_bits, out_ptr + lo, self._p(self.consumed) + 8 * k0,
+            (self._p(self.final_states) + 4 * k0 * N) if final_states else None,
+            self._p(self.status), self._s() if stream is None else stream), "decode")
 
     def decode(self, d_out, n: int, payload=None, offsets=None, states=None,
                final_states: bool = False):
@@ -337,16 +378,30 @@ def decode_chunked(cc: ChunkedContainer) -> np.ndarray:
 
 class HostCodec:
     """End-to-end chunked codec over pinned host buffers: the public call a
-    user makes with data in host memory. encode(): H2D message -> device
-    model build -> encode -> framing -> D2H (offsets, states, payload).
-    decode(): H2D (payload, offsets, states) -> decode -> D2H message.
+    user makes with data in host memory. Work is split into chunk-aligned
+    batches on three streams so PCIe traffic overlaps the kernels:
+
+    encode(): H2D batch b (copy stream) || histogram of batch b (compute
+      stream) -> [NCCL all-reduce] -> quantize + tables -> encode batch b
+      (compute) || pack batch b straight into the pinned host payload over
+      PCIe (output stream: the framing kernel writes mapped host memory, so
+      compaction and D2H are one pass) -> offsets + states D2H.
+    decode(): directory H2D -> per batch: payload H2D (copy) || decode
+      (compute) || decoded bytes D2H (output stream).
     Buffers (device and pinned host) are allocated once for ``capacity``."""
 
     def __init__(self, capacity: int, chunk_len: int = DEFAULT_CHUNK, lane_count: int = 32,
-                 scale_bits: int = 14, device=None, counts_allreduce=None):
+                 scale_bits: int = 14, device=None, counts_allreduce=None,
+                 batch_bytes: int = 32 << 20):
         torch = _torch()
-        self.codec = DeviceCodec(capacity, chunk_len, lane_count, scale_bits, device)
-        dev = self.codec.device
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.s_in = torch.cuda.Stream(dev)
+        self.s_comp = torch.cuda.Stream(dev)
+        self.s_out = torch.cuda.Stream(dev)
+        self.s_dec = [torch.cuda.Stream(dev) for _ in range(4)]
+        self.codec = DeviceCodec(capacity, chunk_len, lane_count, scale_bits, dev,
+                                 stream=self.s_comp)
         self.d_msg = torch.empty(max(16, capacity), dtype=torch.uint8, device=dev)
         self.d_out = torch.empty(max(16, capacity), dtype=torch.uint8, device=dev)
         k = max(1, n_chunks_for(capacity, chunk_len))
@@ -355,41 +410,111 @@ class HostCodec:
         self.h_states = pin(k * lane_count, torch.int32)
         self.h_payload = pin(max(1, capacity) + 8, torch.int16)
         self.counts_allreduce = counts_allreduce
+        self.batch_chunks = max(1, batch_bytes // chunk_len)
         self.h2d_bytes = 0
         self.d2h_bytes = 0
+
+    def _batches(self, k: int):
+        return [(a, min(k, a + self.batch_chunks)) for a in range(0, k, self.batch_chunks)]
+
+    def _event(self, stream):
+        e = _torch().cuda.Event()
+        e.record(stream)
+        return e
 
     def encode(self, h_msg, n: int):
         """h_msg: pinned uint8 tensor. Returns (payload, offsets, states) as
         views of the pinned host buffers (valid until the next encode)."""
+        torch = _torch()
         c = self.codec
-        k = n_chunks_for(n, c.chunk_len)
-        self.d_msg[:n].copy_(h_msg[:n], non_blocking=True)
-        c.histogram(self.d_msg, n)
+        C, N = c.chunk_len, c.lane_count
+        k = n_chunks_for(n, C)
+        batches = self._batches(k)
+        cur = torch.cuda.current_stream(c.device)
+        for s in (self.s_in, self.s_comp, self.s_out):
+            s.wait_stream(cur)
+        p_msg = self.d_msg.data_ptr()
+        c.reset_status()
+        # phase 1: H2D per batch, histogram as each batch lands
+        _lib.check_dev(_lib.lib.ilans_counts_zero_dev(c.counts.data_ptr(), c._s()), "counts")
+        for k0, k1 in batches:
+            lo, hi = k0 * C, min(n, k1 * C)
+            with torch.cuda.stream(self.s_in):
+                self.d_msg[lo:hi].copy_(h_msg[lo:hi], non_blocking=True)
+            self.s_comp.wait_event(self._event(self.s_in))
+            _lib.check_dev(_lib.lib.ilans_histogram_u8_dev(p_msg + lo, hi - lo,
+                                                           c.counts.data_ptr(), c._s()), "hist")
         if self.counts_allreduce is not None:
-            self.counts_allreduce(c.counts)
+            with torch.cuda.stream(self.s_comp):
+                self.counts_allreduce(c.counts)
         c.build_table_from_counts()
-        c.encode(self.d_msg, n)
-        self.h_offsets[: k + 1].copy_(c.offsets[: k + 1], non_blocking=True)
-        self.h_states[: k * c.lane_count].copy_(c.states[: k * c.lane_count], non_blocking=True)
-        _torch().cuda.current_stream(c.device).synchronize()
+        # phase 2: one encode launch over all chunks (a chunk is one warp's
+        # sequential work, so splitting it would only serialise), then per
+        # batch: pack into HBM + copy its word offsets out; as soon as a
+        # batch's offsets are on the host its payload D2H is issued.
+        c.encode_range(p_msg, n, 0, k)
+        if k == 0:
+            c.frame_range(n, 0, 0, c.payload.data_ptr())
+        ev_off = []
+        for k0, k1 in batches:
+            c.frame_range(n, k0, k1, c.payload.data_ptr())
+            self.s_out.wait_event(self._event(self.s_comp))
+            with torch.cuda.stream(self.s_out):
+                self.h_offsets[k0 + 1: k1 + 1].copy_(c.offsets[k0 + 1: k1 + 1], non_blocking=True)
+            ev_off.append(self._event(self.s_out))
+        self.h_offsets[:1].zero_()
+        for (k0, k1), ev in zip(batches, ev_off):
+            ev.synchronize()
+            a, b = int(self.h_offsets[k0]), int(self.h_offsets[k1])
+            with torch.cuda.stream(self.s_out):
+                self.h_payload[a:b].copy_(c.payload[a:b], non_blocking=True)
+        with torch.cuda.stream(self.s_out):
+            self.h_states[: k * N].copy_(c.states[: k * N], non_blocking=True)
+        self.s_out.synchronize()
+        c.check_status()
         words = int(self.h_offsets[k]) if k else 0
-        self.h_payload[:words].copy_(c.payload[:words], non_blocking=True)
-        _torch().cuda.current_stream(c.device).synchronize()
         self.h2d_bytes = n
-        self.d2h_bytes = 8 * (k + 1) + 4 * k * c.lane_count + 2 * words
-        return self.h_payload[:words], self.h_offsets[: k + 1], self.h_states[: k * c.lane_count]
+        self.d2h_bytes = 8 * (k + 1) + 4 * k * N + 2 * words
+        return self.h_payload[:words], self.h_offsets[: k + 1], self.h_states[: k * N]
 
     def decode(self, h_payload, h_offsets, h_states, n: int, h_out):
         """Decode into pinned uint8 tensor h_out (device table = last model)."""
+        torch = _torch()
         c = self.codec
-        k = n_chunks_for(n, c.chunk_len)
-        words = h_payload.numel()
-        c.payload[:words].copy_(h_payload, non_blocking=True)
-        c.offsets[: k + 1].copy_(h_offsets, non_blocking=True)
-        c.states[: k * c.lane_count].copy_(h_states, non_blocking=True)
-        c.decode(self.d_out, n)
-        h_out[:n].copy_(self.d_out[:n], non_blocking=True)
-        _torch().cuda.current_stream(c.device).synchronize()
-        self.h2d_bytes = 2 * words + 8 * (k + 1) + 4 * k * c.lane_count
+        C, N = c.chunk_len, c.lane_count
+        k = n_chunks_for(n, C)
+        offs = h_offsets.numpy()
+        words = int(offs[k]) if k else 0
+        cur = torch.cuda.current_stream(c.device)
+        for s in (self.s_in, self.s_comp, self.s_out):
+            s.wait_stream(cur)
+        c.reset_status()
+        for s in self.s_dec:  # table + status reset happen on the compute stream
+            s.wait_stream(self.s_comp)
+        with torch.cuda.stream(self.s_in):
+            c.offsets[: k + 1].copy_(h_offsets, non_blocking=True)
+            c.states[: k * N].copy_(h_states, non_blocking=True)
+        p_pay, p_off = c.payload.data_ptr(), c.offsets.data_ptr()
+        p_st, p_out = c.states.data_ptr(), self.d_out.data_ptr()
+        # batches decode concurrently on their own streams as their payload
+        # lands (one batch alone cannot fill the GPU: a chunk is one warp)
+        ev_dir = self._event(self.s_in)
+        for i, (k0, k1) in enumerate(self._batches(k)):
+            a, b = int(offs[k0]), int(offs[k1])
+            with torch.cuda.stream(self.s_in):
+                c.payload[a:b].copy_(h_payload[a:b], non_blocking=True)
+            s_dec = self.s_dec[i % len(self.s_dec)]
+            s_dec.wait_event(self._event(self.s_in))
+            s_dec.wait_event(ev_dir)
+            c.decode_range(p_out, n, k0, k1, p_pay, p_off, p_st, stream=s_dec.cuda_stream)
+            self.s_out.wait_event(self._event(s_dec))
+            lo, hi = k0 * C, min(n, k1 * C)
+            with torch.cuda.stream(self.s_out):
+                h_out[lo:hi].copy_(self.d_out[lo:hi], non_blocking=True)
+        self.s_out.synchronize()
+        for s in self.s_dec:
+            self.s_comp.wait_stream(s)
+        c.check_status()
+        self.h2d_bytes = 2 * words + 8 * (k + 1) + 4 * k * N
         self.d2h_bytes = n
         return h_out[:n]

@@ -596,10 +596,10 @@ extern "C" int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t 
 
 extern "C" int ilans_frame_chunks_dev(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
                                       const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
-                                      uint16_t *d_payload, void *stream) {
+                                      uint16_t *d_payload, int32_t carry_in, void *stream) {
     if (chunk_len <= 0) return ILANS_ERR_VALUE;
     return launch_frame(d_scratch, n, chunk_len, d_chunk_words, d_word_offsets, d_payload,
-                        ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+                        carry_in, ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
 }
 
 extern "C" int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t *d_word_offsets,

@@ -351,11 +351,11 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
 // Single CTA exclusive scan of n_chunks word counts -> offsets[n_chunks + 1].
 __global__ void __launch_bounds__(1024)
 chunk_offsets_kernel(const uint32_t *__restrict__ words, int64_t n_chunks,
-                     uint64_t *__restrict__ offsets) {
+                     uint64_t *__restrict__ offsets, int carry_in) {
     __shared__ unsigned long long wsum[32];
     __shared__ unsigned long long carry;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) carry = 0;
+    if (threadIdx.x == 0) carry = carry_in ? offsets[0] : 0ull;  // batch continuation
     __syncthreads();
     for (int64_t base = 0; base < n_chunks; base += blockDim.x) {
         const int64_t i = base + threadIdx.x;
@@ -445,9 +445,10 @@ compact_kernel(const uint16_t *__restrict__ scratch, int64_t n, int64_t chunk_le
 
 cudaError_t launch_frame(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
                          const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
-                         uint16_t *d_payload, cudaStream_t stream) {
+                         uint16_t *d_payload, int carry_in, cudaStream_t stream) {
     const int64_t n_chunks = n <= 0 ? 0 : (n + chunk_len - 1) / chunk_len;
-    chunk_offsets_kernel<<<1, 1024, 0, stream>>>(d_chunk_words, n_chunks, d_word_offsets);
+    chunk_offsets_kernel<<<1, 1024, 0, stream>>>(d_chunk_words, n_chunks, d_word_offsets,
+                                                  carry_in);
     ilans_note_launch();
     if (n_chunks > 0) {
         compact_kernel<<<static_cast<unsigned>(n_chunks), 256, 0, stream>>>(

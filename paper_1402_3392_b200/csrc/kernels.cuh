@@ -28,7 +28,7 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
                           uint32_t *d_lane_ws, cudaStream_t stream);
 cudaError_t launch_frame(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
                          const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
-                         uint16_t *d_payload, cudaStream_t stream);
+                         uint16_t *d_payload, int carry_in, cudaStream_t stream);
 
 // decode.cu
 cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offsets,

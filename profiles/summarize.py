@@ -46,7 +46,7 @@ def to_bytes(v: str, unit: str) -> float:
     return float(v) * scale
 
 
-def main(rep: str, launches: str, tag: str) -> None:
+def main(rep: str, launches: str, tag: str, config: str = "mib=256,chunk=65536,lanes=32,sb=12") -> None:
     hdr, units, rows = load_raw(rep)
     col = {h: i for i, h in enumerate(hdr)}
     lines = [f"# ncu summary `{tag}`", "", f"source: `{rep}` (ncu --set full, --clock-control none)",
@@ -81,6 +81,7 @@ def main(rep: str, launches: str, tag: str) -> None:
             if key in short:
                 traffic[key] = rd + wr
     (HERE / f"{tag}_kernels.md").write_text("\n".join(lines) + "\n")
+    traffic["config"] = config  # bench.py uses these bytes only for the same workload
     (HERE / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
     # launch list: name, duration
     out = [["id", "kernel", "duration_ns"]]
@@ -99,4 +100,4 @@ def main(rep: str, launches: str, tag: str) -> None:
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])

@@ -97,6 +97,31 @@ def test_steps_reject_unsupported():
     assert len(list(decode_interleaved_steps(c33))) == 3  # serial steps are fine
 
 
+def test_host_codec_batched_pipeline_matches_oracle():
+    """HostCodec (pinned host buffers, 3 streams, batches packed straight into
+    host memory over PCIe) == the oracle's chunk framing, and round-trips."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import HostCodec
+    from paper_1402_3392_b200.synth import synth_host
+
+    for n, C, batch in ((5_000_003, 65536, 1 << 20), (300_000, 16384, 64 << 10), (100, 1024, 4096)):
+        msg = synth_host(n, 1.3, seed=n)
+        hc = HostCodec(n, C, 32, 12, batch_bytes=batch)
+        h_msg = torch.from_numpy(msg).pin_memory()
+        pay, offs, states = hc.encode(h_msg, n)
+        counts, alpha = oracle.histogram(msg)
+        freqs = oracle.quantize(counts[:alpha], 12)
+        f, cum, _ = oracle.table_views(freqs, 12)
+        ref_p, ref_o, ref_s = oracle.encode_chunks_u16(msg, C, f, cum, 12, 32)
+        assert np.array_equal(pay.numpy().view(np.uint16), ref_p)
+        assert np.array_equal(offs.numpy().view(np.uint64), ref_o)
+        assert np.array_equal(states.numpy().view(np.uint32).reshape(-1, 32), ref_s)
+        h_out = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        hc.decode(pay.clone(), offs.clone(), states.clone(), n, h_out)
+        assert np.array_equal(h_out.numpy(), msg)
+
+
 def test_stats_counters_single_digit_property():
     rng = np.random.default_rng(3)
     stats = RenormStats()
