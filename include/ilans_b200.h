@@ -40,6 +40,7 @@ typedef enum ilans_rc {
     ILANS_ERR_TRUNCATED = 3,    /* TruncatedStreamError (payload exhausted)   */
     ILANS_ERR_UNSUPPORTED = 4,  /* UnsupportedVariantError                    */
     ILANS_ERR_CUDA = 5,         /* CUDA runtime failure / no device           */
+    ILANS_ERR_FORMAT = 6,       /* FormatError (byte8 refill loop runaway)    */
 } ilans_rc;
 
 typedef struct ilans_status {
@@ -48,7 +49,7 @@ typedef struct ilans_status {
     int64_t stream;     /* chunk/stream index of the first failing stream, or -1 */
     int64_t index;      /* message index of the offending symbol, or -1          */
     int32_t symbol;     /* offending symbol value (unencodable), or -1           */
-    int32_t reserved;
+    int32_t max_digits; /* byte8 calls: most digits spilled / refilled by a symbol */
     int64_t consumed;   /* words consumed (single-stream decode)                 */
     char message[128];  /* human-readable detail                                 */
 } ilans_status;
@@ -117,6 +118,30 @@ int ilans_decode_trace_u16(const uint16_t *payload, int64_t pay_len, const uint3
                            int64_t msg_len, int32_t n_lanes, uint8_t *out,
                            uint32_t *trace_states, uint64_t *trace_pos, int64_t *groups_done,
                            int64_t *consumed, ilans_status *st);
+
+/* BYTE8 (8-bit digits, L = 2^23) interleaved coding -- the reference's
+ * scalar path for variant=BYTE8 (interleave.py:155-179 with
+ * rans.encode_symbol_renorm / decode_symbol_renorm, rans.py:266-314), here on
+ * the GPU with byte-identical payloads (u8 digits, decoder read order) and
+ * final states. Encode: payload_out capacity 3*n bytes. Decode errors:
+ * ILANS_ERR_TRUNCATED, ILANS_ERR_FORMAT (more than 5 refills for one symbol:
+ * "renormalization does not terminate; corrupt stream", rans.py:309-311).
+ * n_lanes in [1, 65535]. The trace variant matches ilans_decode_trace_u16. */
+int ilans_encode_interleaved_u8(const uint8_t *msg, int64_t n, const uint32_t *freq,
+                                int32_t n_freq, const uint32_t *cum, int32_t scale_bits,
+                                int32_t n_lanes, uint8_t *payload_out, int64_t *payload_bytes,
+                                uint32_t *states_out, ilans_status *st);
+int ilans_decode_interleaved_u8(const uint8_t *payload, int64_t pay_len, const uint32_t *states,
+                                const uint8_t *slot_sym, int64_t n_slots, const uint32_t *freq,
+                                const uint32_t *cum, int32_t n_freq, int32_t scale_bits,
+                                int64_t msg_len, int32_t n_lanes, uint8_t *out,
+                                int64_t *consumed, ilans_status *st);
+int ilans_decode_trace_u8(const uint8_t *payload, int64_t pay_len, const uint32_t *states,
+                          const uint8_t *slot_sym, int64_t n_slots, const uint32_t *freq,
+                          const uint32_t *cum, int32_t n_freq, int32_t scale_bits,
+                          int64_t msg_len, int32_t n_lanes, uint8_t *out,
+                          uint32_t *trace_states, uint64_t *trace_pos, int64_t *groups_done,
+                          int64_t *consumed, ilans_status *st);
 
 /* Replaces rans.quantize(counts, scale_bits) (rans.py:171-211), computed on
  * the device. counts has n <= 256 entries; freq_out receives n entries.

@@ -23,8 +23,9 @@ HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_build" / "liboracle.so"
 REF_DIR = HERE / "_ref"
 
-OK, ERR_VALUE, ERR_UNENCODABLE, ERR_TRUNCATED = 0, 1, 2, 3
-KIND_NAMES = {ERR_VALUE: "value", ERR_UNENCODABLE: "unencodable", ERR_TRUNCATED: "truncated"}
+OK, ERR_VALUE, ERR_UNENCODABLE, ERR_TRUNCATED, ERR_FORMAT = 0, 1, 2, 3, 6
+KIND_NAMES = {ERR_VALUE: "value", ERR_UNENCODABLE: "unencodable", ERR_TRUNCATED: "truncated",
+              ERR_FORMAT: "format"}
 
 
 class OracleError(Exception):
@@ -144,6 +145,53 @@ def decode_final_states(payload, states, slot_sym, freq, cum, scale_bits, msg_le
     _, _, xs = _decode(lib().orc_decode_u16, payload, states, slot_sym, freq, cum,
                        scale_bits, msg_len, n_lanes)
     return xs
+
+
+def _pad_tables(freq, cum):
+    f = np.zeros(256, dtype=np.uint32)
+    f[: len(freq)] = np.asarray(freq, dtype=np.uint32)
+    c = np.zeros(257, dtype=np.uint32)
+    c[: len(cum)] = np.asarray(cum, dtype=np.uint32)
+    return f, c
+
+
+def encode_interleaved_u8(msg, freq, cum, scale_bits: int, n_lanes: int):
+    """BYTE8 scalar encode (interleave.py:155-165): (payload u8, states u32)."""
+    m = np.ascontiguousarray(msg, dtype=np.uint8)
+    f, c = _pad_tables(freq, cum)
+    scratch = np.empty(max(1, 4 * len(m)), dtype=np.uint8)
+    out = np.empty(max(1, 4 * len(m)), dtype=np.uint8)
+    states = np.empty(n_lanes, dtype=np.uint32)
+    nb = ctypes.c_int64(0)
+    rc = lib().orc_encode_u8(_p(m), ctypes.c_int64(len(m)), _p(f), _p(c),
+                             ctypes.c_int(scale_bits), ctypes.c_int(n_lanes), _p(scratch),
+                             _p(out), ctypes.byref(nb), _p(states))
+    if rc:
+        raise OracleError(rc, "encode_u8")
+    return out[: nb.value].copy(), states
+
+
+def decode_interleaved_u8(payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):
+    """BYTE8 scalar decode (interleave.py:168-179): (message, digits read)."""
+    out, used, _ = decode_u8_full(payload, states, slot_sym, freq, cum, scale_bits, msg_len,
+                                  n_lanes)
+    return out, used
+
+
+def decode_u8_full(payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):
+    """BYTE8 scalar decode returning (message, digits read, lane states)."""
+    pay = np.ascontiguousarray(payload, dtype=np.uint8)
+    xs = np.array(states, dtype=np.uint32)
+    slot = np.ascontiguousarray(slot_sym, dtype=np.uint8)
+    f, c = _pad_tables(freq, cum)
+    out = np.empty(max(1, msg_len), dtype=np.uint8)
+    consumed = ctypes.c_int64(0)
+    rc = lib().orc_decode_u8(_p(pay), ctypes.c_int64(len(pay)), _p(xs), _p(slot), _p(f), _p(c),
+                             ctypes.c_int(scale_bits), ctypes.c_int64(msg_len),
+                             ctypes.c_int(n_lanes), _p(out), ctypes.byref(consumed))
+    if rc:
+        raise OracleError(rc, "decode_u8")
+    return out[:msg_len], int(consumed.value), xs
 
 
 def encode_chunks_u16(msg, chunk_len: int, freq, cum, scale_bits: int, n_lanes: int):

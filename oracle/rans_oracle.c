@@ -25,6 +25,7 @@ enum {
     ORC_ERR_VALUE = 1,        /* ValueError in the reference */
     ORC_ERR_UNENCODABLE = 2,  /* UnencodableSymbolError */
     ORC_ERR_TRUNCATED = 3,    /* TruncatedStreamError */
+    ORC_ERR_FORMAT = 6,       /* FormatError (byte8 refill runaway) */
 };
 
 #define ORC_LOW 65536u /* WORD16.lower_bound, rans.py:87 */
@@ -195,6 +196,64 @@ int orc_decode_lanes_u16(const uint16_t *payload, int64_t pay_len, uint32_t *sta
         }
         pos += cnt;
         base += active;
+    }
+    *consumed = pos;
+    return ORC_OK;
+}
+
+/* BYTE8 scalar path: interleave._encode_scalar (interleave.py:155-165) with
+ * rans.encode_symbol_renorm (rans.py:266-289): states start at L = 2^23;
+ * walking backwards, while x >= f * (2^31 >> sb) push x & 0xFF and x >>= 8,
+ * then x = (x / f << sb) + cum + x % f. The payload is the reversed stack.
+ * scratch needs 4n bytes. */
+int orc_encode_u8(const uint8_t *msg, int64_t n, const uint32_t *freq, const uint32_t *cum,
+                  int scale_bits, int n_lanes, uint8_t *scratch, uint8_t *payload_out,
+                  int64_t *nbytes, uint32_t *states_out)
+{
+    const uint64_t low = 1ull << 23, limit = 1ull << 31;
+    uint64_t xs[65536];
+    int64_t sp = 0;
+    for (int l = 0; l < n_lanes; l++) xs[l] = low;
+    for (int64_t i = n - 1; i >= 0; i--) {
+        uint32_t s = msg[i];
+        uint64_t f = freq[s];
+        if (f == 0) return ORC_ERR_UNENCODABLE;
+        int lane = (int)(i % n_lanes);
+        uint64_t x = xs[lane];
+        uint64_t thr = f * (limit >> scale_bits);
+        while (x >= thr) { scratch[sp++] = (uint8_t)(x & 0xFF); x >>= 8; }
+        xs[lane] = ((x / f) << scale_bits) + cum[s] + x % f;
+    }
+    for (int64_t j = 0; j < sp; j++) payload_out[j] = scratch[sp - 1 - j];
+    for (int l = 0; l < n_lanes; l++) states_out[l] = (uint32_t)xs[l];
+    *nbytes = sp;
+    return ORC_OK;
+}
+
+/* BYTE8 scalar decode: interleave._decode_scalar (interleave.py:168-179) with
+ * rans.decode_symbol_renorm (rans.py:292-314): pop, then refill bytes while
+ * x < L; TruncatedStreamError when the digits run out (ans.py:80-85),
+ * FormatError after more than (24+7)/8 + 2 = 5 refills for one symbol. */
+int orc_decode_u8(const uint8_t *payload, int64_t pay_len, uint32_t *states_io,
+                  const uint8_t *slot_sym, const uint32_t *freq, const uint32_t *cum,
+                  int scale_bits, int64_t msg_len, int n_lanes, uint8_t *out, int64_t *consumed)
+{
+    const uint64_t low = 1ull << 23, mask = (1ull << scale_bits) - 1;
+    int64_t pos = 0;
+    for (int64_t i = 0; i < msg_len; i++) {
+        int lane = (int)(i % n_lanes);
+        uint64_t x = states_io[lane];
+        uint64_t slot = x & mask;
+        uint32_t s = slot_sym[slot];
+        out[i] = (uint8_t)s;
+        x = (uint64_t)freq[s] * (x >> scale_bits) + slot - cum[s];
+        int r = 0;
+        while (x < low) {
+            if (pos >= pay_len) { *consumed = pos; return ORC_ERR_TRUNCATED; }
+            x = (x << 8) | payload[pos++];
+            if (++r > 5) { *consumed = pos; return ORC_ERR_FORMAT; }
+        }
+        states_io[lane] = (uint32_t)x;
     }
     *consumed = pos;
     return ORC_OK;

@@ -15,11 +15,16 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import TruncatedStreamError, UnencodableSymbolError, UnsupportedVariantError
+from .errors import (
+    FormatError,
+    TruncatedStreamError,
+    UnencodableSymbolError,
+    UnsupportedVariantError,
+)
 
 LIB_PATH = Path(os.environ.get("ILANS_B200_LIB", Path(__file__).resolve().parent / "libilans_b200.so"))
 
-OK, ERR_VALUE, ERR_UNENCODABLE, ERR_TRUNCATED, ERR_UNSUPPORTED, ERR_CUDA = range(6)
+OK, ERR_VALUE, ERR_UNENCODABLE, ERR_TRUNCATED, ERR_UNSUPPORTED, ERR_CUDA, ERR_FORMAT = range(7)
 
 
 class Status(ctypes.Structure):
@@ -29,7 +34,7 @@ class Status(ctypes.Structure):
         ("stream", ctypes.c_int64),
         ("index", ctypes.c_int64),
         ("symbol", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("max_digits", ctypes.c_int32),
         ("consumed", ctypes.c_int64),
         ("message", ctypes.c_char * 128),
     ]
@@ -65,6 +70,13 @@ PROTOTYPES = [
     ("ilans_decode_lanes_u16", ctypes.c_int,
      [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _st]),
     ("ilans_decode_trace_u16", ctypes.c_int,
+     [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp,
+      _st]),
+    ("ilans_encode_interleaved_u8", ctypes.c_int,
+     [_vp, _i64, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _st]),
+    ("ilans_decode_interleaved_u8", ctypes.c_int,
+     [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _st]),
+    ("ilans_decode_trace_u8", ctypes.c_int,
      [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp,
       _st]),
     ("ilans_quantize", ctypes.c_int, [_vp, _i32, _i32, _vp, _st]),
@@ -104,6 +116,8 @@ def raise_for(rc: int, st: Status, what: str = "") -> None:
         raise UnencodableSymbolError(msg)
     if rc == ERR_UNSUPPORTED:
         raise UnsupportedVariantError(msg)
+    if rc == ERR_FORMAT:
+        raise FormatError(msg)
     if rc == ERR_VALUE:
         raise ValueError(msg)
     raise RuntimeError(f"ilans-b200 CUDA failure in {what}: {msg}")

@@ -95,13 +95,58 @@ def decode_lanes_u16(payload, states, slot_sym, freq, cum, scale_bits, msg_len, 
                    n_lanes)
 
 
-def decode_trace_u16(payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):
+# ---------------------------------------------------------------------------
+# BYTE8 (8-bit digits, L = 2^23): the reference runs this variant on its
+# scalar Python path (interleave.py:155-179); here it is a GPU kernel too.
+# Not part of the reference Backend (whose fields are the word16 kernels),
+# so these return one extra value: the most digits moved for one symbol
+# (what RenormStats.max_*_digits records).
+# ---------------------------------------------------------------------------
+def encode_interleaved_u8(msg, freq, cum, scale_bits: int, n_lanes: int):
+    """Backward byte8 encode on the B200 -> (payload u8, states u32, max spills)."""
+    m = np.ascontiguousarray(msg, dtype=np.uint8)
+    f = _u32(freq)
+    c = _u32(cum)
+    if len(c) < len(f) + 1:
+        raise ValueError("cum must have len(freq) + 1 entries")
+    payload = np.empty(max(1, 3 * len(m)), dtype=np.uint8)
+    states = np.empty(n_lanes, dtype=np.uint32)
+    nbytes = ctypes.c_int64(0)
+    st = _lib.Status()
+    rc = _lib.lib.ilans_encode_interleaved_u8(
+        _lib.ptr(m), len(m), _lib.ptr(f), len(f), _lib.ptr(c), int(scale_bits), int(n_lanes),
+        _lib.ptr(payload), ctypes.byref(nbytes), _lib.ptr(states), ctypes.byref(st))
+    _lib.raise_for(rc, st, "encode_interleaved_u8")
+    return payload[: nbytes.value].copy(), states, int(st.max_digits)
+
+
+def decode_interleaved_u8(payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):
+    """Forward byte8 decode on the B200 -> (message u8, digits read, max refills)."""
+    pay = np.ascontiguousarray(payload, dtype=np.uint8)
+    xs = np.array(states, dtype=np.uint32)
+    slot = np.ascontiguousarray(slot_sym, dtype=np.uint8)
+    f = _u32(freq)
+    c = _u32(cum)
+    out = np.empty(max(1, msg_len), dtype=np.uint8)
+    consumed = ctypes.c_int64(0)
+    st = _lib.Status()
+    rc = _lib.lib.ilans_decode_interleaved_u8(
+        _lib.ptr(pay), len(pay), _lib.ptr(xs), _lib.ptr(slot), len(slot), _lib.ptr(f),
+        _lib.ptr(c), len(f), int(scale_bits), int(msg_len), int(n_lanes), _lib.ptr(out),
+        ctypes.byref(consumed), ctypes.byref(st))
+    _lib.raise_for(rc, st, "decode_u8")
+    return out[:msg_len], int(consumed.value), int(st.max_digits)
+
+
+def decode_trace_u16(payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes,
+                     byte8: bool = False):
     """Instrumented device decode (ilans_decode_trace_u16): returns
     (msg, trace_states [groups, N], trace_pos [groups], groups_done,
     consumed, error) where error is the exception the plain decode would
     raise (TruncatedStreamError) or None; everything up to the failing group
-    is filled in, so step generators can yield before raising."""
-    pay = np.ascontiguousarray(payload, dtype=np.uint16)
+    is filled in, so step generators can yield before raising. byte8=True
+    traces the byte8 decoder (ilans_decode_trace_u8) instead."""
+    pay = np.ascontiguousarray(payload, dtype=np.uint8 if byte8 else np.uint16)
     xs = np.array(states, dtype=np.uint32)
     slot = np.ascontiguousarray(slot_sym, dtype=np.uint8)
     f = _u32(freq)
@@ -113,13 +158,14 @@ def decode_trace_u16(payload, states, slot_sym, freq, cum, scale_bits, msg_len, 
     done = ctypes.c_int64(0)
     consumed = ctypes.c_int64(0)
     st = _lib.Status()
-    rc = _lib.lib.ilans_decode_trace_u16(
+    fn = _lib.lib.ilans_decode_trace_u8 if byte8 else _lib.lib.ilans_decode_trace_u16
+    rc = fn(
         _lib.ptr(pay), len(pay), _lib.ptr(xs), _lib.ptr(slot), len(slot), _lib.ptr(f),
         _lib.ptr(c), len(f), int(scale_bits), int(msg_len), int(n_lanes), _lib.ptr(out),
         _lib.ptr(tstates), _lib.ptr(tpos), ctypes.byref(done), ctypes.byref(consumed),
         ctypes.byref(st))
     err = None
-    if rc == _lib.ERR_TRUNCATED:
+    if rc in (_lib.ERR_TRUNCATED, _lib.ERR_FORMAT):
         try:
             _lib.raise_for(rc, st, "decode")
         except Exception as exc:  # noqa: BLE001 -- handed back to the generator

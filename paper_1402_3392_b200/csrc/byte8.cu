@@ -1,0 +1,398 @@
+// byte8.cu -- byte-renormalised (BYTE8: 8-bit digits, L = 2^23) interleaved
+// rANS on sm_100a (reference scalar path interleave.py:155-179,
+// rans.encode_symbol_renorm / decode_symbol_renorm rans.py:266-314).
+//
+// The reference codes byte8 symbol by symbol, each lane moving 0-3 digits
+// per symbol, depth first: while walking backwards the encoder pushes lane
+// i's digits (low byte first) right after lane i+1's, and the decoder reads
+// lane i's refill digits right after lane i-1's. So inside a group the
+// digits of lane l sit at read-order offset sum_{j<l} k_j -- an exclusive
+// prefix sum of per-lane counts instead of the word16 popc. With counts in
+// {0..3} the prefix is two ballots: pre = popc(b0 & lt) + 2 popc(b1 & lt).
+//
+// The counts are pure functions of the state for every stream the encoder
+// can produce: spills k = #{j in 0..2 : x >> 8j >= f << (31-sb)} and, after
+// a pop to x' >= 1, refills r = [x' < 2^23] + [x' < 2^15] + [x' < 2^7]
+// (L = 2^23 is a multiple of 256^2). Only x' = 0 -- reachable from states
+// below L handed in directly, never from a container -- makes the count
+// depend on the bytes read; such a group is resolved lane by lane, with the
+// reference's limit of 5 refills (FormatError "corrupt stream").
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ilans {
+
+constexpr uint32_t kLow8 = 1u << 23;  // BYTE8.lower_bound (rans.py:86)
+constexpr int kRefillLimit8 = 5;      // (24 + 7) // 8 + 2 (rans.py:305)
+
+__device__ __forceinline__ uint32_t refills_for(uint32_t x) {  // x >= 1
+    return (x < (1u << 23)) + (x < (1u << 15)) + (x < (1u << 7));
+}
+
+// One warp per stream, N <= 32 lanes; payload / message read straight from
+// global memory (the byte8 path is the reference's CPU config, not the
+// throughput path, so no staging rings).
+__global__ void __launch_bounds__(256)
+decode_u8_warp_kernel(const uint8_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                      const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                      int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                      uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
+                      DStatus *__restrict__ status, DecodeTrace trace) {
+    __shared__ uint2 dec[kMaxSym];
+    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) dec[i] = tab->dec[i];
+    __syncthreads();
+    const int sb = static_cast<int>(tab->scale_bits);
+    const uint32_t mask = (1u << sb) - 1u;
+    const uint8_t *slot_sym = tab->slot_sym;
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = lanemask_lt();
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         k < n_chunks; k += warps_total) {
+        const int64_t cbase = k * chunk_len;
+        const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+        const uint8_t *pay = payload + offsets[k];
+        const uint64_t plen = offsets[k + 1] - offsets[k];
+        uint32_t x = lane < n_lanes ? states[k * n_lanes + lane] : 0u;
+        uint64_t pos = 0;
+        int err = 0;  // 0 ok, ILANS_ERR_TRUNCATED, ILANS_ERR_FORMAT
+        uint32_t most = 0;  // most refills for one symbol (RenormStats.max_decode_digits)
+        int64_t base = 0;
+        for (; base < len; base += n_lanes) {
+            const int64_t left = len - base;
+            const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
+            const bool on = lane < active;
+            uint32_t s = 0;
+            if (on) {
+                const uint32_t slot = x & mask;
+                s = slot_sym[slot];
+                const uint2 d = dec[s];
+                x = d.x * (x >> sb) + slot - d.y;
+                out[cbase + base + lane] = static_cast<uint8_t>(s);
+            }
+            if (__ballot_sync(0xffffffffu, on && x == 0u)) {
+                // byte-dependent refills: resolve lane by lane (corrupt input)
+                for (int l = 0; l < active && !err; ++l) {
+                    if (lane == l) {
+                        int r = 0;
+                        while (x < kLow8) {
+                            if (pos >= plen) { err = ILANS_ERR_TRUNCATED; break; }
+                            x = (x << 8) | pay[pos++];
+                            if (++r > kRefillLimit8) { err = ILANS_ERR_FORMAT; break; }
+                        }
+                        most = max(most, static_cast<uint32_t>(r));
+                    }
+                    pos = __shfl_sync(0xffffffffu, pos, l);
+                    err = __shfl_sync(0xffffffffu, err, l);
+                }
+            } else {
+                const uint32_t r = on ? refills_for(x) : 0u;
+                const uint32_t b0 = __ballot_sync(0xffffffffu, r & 1u);
+                const uint32_t b1 = __ballot_sync(0xffffffffu, r & 2u);
+                const uint32_t tot = __popc(b0) + 2u * __popc(b1);
+                if (pos + tot > plen) {
+                    err = ILANS_ERR_TRUNCATED;
+                } else {
+                    const uint64_t p = pos + __popc(b0 & lt) + 2u * __popc(b1 & lt);
+                    for (uint32_t j = 0; j < r; ++j) x = (x << 8) | pay[p + j];
+                    pos += tot;
+                    most = max(most, r);
+                }
+            }
+            if (err) break;
+            if (trace.states) {
+                const int64_t gi = base / n_lanes;
+                if (lane < n_lanes) trace.states[gi * n_lanes + lane] = x;
+                if (lane == 0) trace.pos[gi] = pos;
+            }
+        }
+        most = __reduce_max_sync(0xffffffffu, most);
+        if (lane == 0) {
+            atomicMax(&status->max_digits, most);
+            if (err == ILANS_ERR_TRUNCATED)
+                atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
+            if (err == ILANS_ERR_FORMAT) status->value_error = ILANS_ERR_FORMAT;
+            if (consumed) consumed[k] = pos;
+            if (trace.groups) trace.groups[k] = (base < len ? base : len + n_lanes - 1) / n_lanes;
+        }
+    }
+}
+
+// Backward encode, one warp per stream, N <= 32. Spilled digits go to the
+// stream's scratch (capacity 3 bytes per symbol) growing downwards from len*3.
+__global__ void __launch_bounds__(256)
+encode_u8_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
+                      int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                      uint8_t *__restrict__ scratch, uint32_t *__restrict__ chunk_bytes,
+                      uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
+    __shared__ uint2 enc[kMaxSym];
+    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
+    __syncthreads();
+    const EncCtx ctx(tab->scale_bits);
+    const uint32_t thr8 = 31u - tab->scale_bits;  // spill while x >= f << (31 - sb)
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = lanemask_lt();
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         k < n_chunks; k += warps_total) {
+        const int64_t cbase = k * chunk_len;
+        const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+        const uint8_t *g = msg + cbase;
+        uint8_t *o = scratch + 3 * cbase;
+        uint32_t x = kLow8;
+        int64_t top = 3 * len;
+        bool bad = false;
+        uint32_t most = 0;  // RenormStats.max_encode_digits
+        for (int64_t gi = (len + n_lanes - 1) / n_lanes - 1; gi >= 0; --gi) {
+            const int64_t base = gi * n_lanes;
+            const int64_t left = len - base;
+            const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
+            const bool on = lane < active;
+            const uint2 e = enc[on ? g[base + lane] : 0u];
+            const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.x == 0u);
+            if (badmask) {
+                if (lane == 0)
+                    atomicMax(&status->unenc_index,
+                              static_cast<long long>(cbase + base + 31 - __clz(badmask)));
+                bad = true;
+                break;
+            }
+            const uint32_t fm1 = e.y & 0xFFFFu;  // spill while (x >> 8j) >> thr8 > f - 1
+            uint32_t sp = 0;
+            if (on) sp = ((x >> thr8) > fm1) + (((x >> 8) >> thr8) > fm1) +
+                         (((x >> 16) >> thr8) > fm1);
+            const uint32_t b0 = __ballot_sync(0xffffffffu, sp & 1u);
+            const uint32_t b1 = __ballot_sync(0xffffffffu, sp & 2u);
+            top -= __popc(b0) + 2 * __popc(b1);
+            const int64_t p = top + __popc(b0 & lt) + 2 * __popc(b1 & lt);
+            // read order is most significant spilled byte first
+            for (uint32_t j = 0; j < sp; ++j) o[p + j] = static_cast<uint8_t>(x >> (8 * (sp - 1 - j)));
+            if (on) x = enc_push(ctx, sp ? x >> (8 * sp) : x, e);
+            most = max(most, sp);
+        }
+        most = __reduce_max_sync(0xffffffffu, most);
+        if (lane == 0) atomicMax(&status->max_digits, most);
+        if (!bad) {
+            if (lane == 0) chunk_bytes[k] = static_cast<uint32_t>(3 * len - top);
+            if (lane < n_lanes) states_out[k * n_lanes + lane] = x;
+        }
+    }
+}
+
+// N > 32: one CTA per stream, thread t owns lanes [t*k, t*k + k) (k <= 64),
+// CTA-wide exclusive scans of the digit counts; states live in ws.
+__device__ __forceinline__ uint32_t block_excl_scan_8(uint32_t v, uint32_t *total,
+                                                      uint32_t *sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+    }
+    if (lane == 31) sh[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < nw ? sh[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += u;
+        }
+        sh[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t off = wid ? sh[wid - 1] : 0u;
+    *total = sh[nw - 1];
+    __syncthreads();
+    return off + inc - v;
+}
+
+__global__ void __launch_bounds__(1024)
+decode_u8_block_kernel(const uint8_t *__restrict__ pay, uint64_t plen,
+                       const uint32_t *__restrict__ states, int64_t len, int n_lanes,
+                       const TableDev *__restrict__ tab, uint8_t *__restrict__ out,
+                       uint64_t *__restrict__ consumed, DStatus *__restrict__ status,
+                       uint32_t *__restrict__ ws, DecodeTrace trace) {
+    __shared__ uint32_t scan_sh[32];
+    __shared__ int zero_any;
+    const int sb = static_cast<int>(tab->scale_bits);
+    const uint32_t mask = (1u << sb) - 1u;
+    const int per = (n_lanes + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per;
+    for (int l = lo; l < lo + per && l < n_lanes; ++l) ws[l] = states[l];
+    uint64_t pos = 0;
+    int err = 0;
+    uint32_t most = 0;
+    int64_t base = 0;
+    for (; base < len; base += n_lanes) {
+        const int64_t left = len - base;
+        const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
+        const int hi = lo + per < active ? lo + per : active;
+        if (threadIdx.x == 0) zero_any = 0;
+        __syncthreads();
+        uint32_t cnt = 0;
+        for (int l = lo; l < hi; ++l) {
+            uint32_t x = ws[l];
+            const uint32_t slot = x & mask;
+            const uint32_t s = tab->slot_sym[slot];
+            const uint2 d = tab->dec[s];
+            x = d.x * (x >> sb) + slot - d.y;
+            out[base + l] = static_cast<uint8_t>(s);
+            ws[l] = x;
+            if (x == 0u) zero_any = 1;
+            else cnt += refills_for(x);
+        }
+        __syncthreads();
+        if (zero_any) {  // corrupt input: serial resolution by thread 0
+            if (threadIdx.x == 0) {
+                for (int l = 0; l < active && !err; ++l) {
+                    uint32_t x = ws[l];
+                    int r = 0;
+                    while (x < kLow8) {
+                        if (pos >= plen) { err = ILANS_ERR_TRUNCATED; break; }
+                        x = (x << 8) | pay[pos++];
+                        if (++r > kRefillLimit8) { err = ILANS_ERR_FORMAT; break; }
+                    }
+                    ws[l] = x;
+                    most = max(most, static_cast<uint32_t>(r));
+                }
+                scan_sh[0] = static_cast<uint32_t>(err);
+            }
+            __syncthreads();
+            err = static_cast<int>(scan_sh[0]);
+            __syncthreads();
+            // every thread re-reads pos from thread 0 via shared memory
+            if (threadIdx.x == 0) scan_sh[1] = static_cast<uint32_t>(pos), scan_sh[2] = static_cast<uint32_t>(pos >> 32);
+            __syncthreads();
+            pos = (static_cast<uint64_t>(scan_sh[2]) << 32) | scan_sh[1];
+            __syncthreads();
+        } else {
+            uint32_t total;
+            const uint32_t excl = block_excl_scan_8(cnt, &total, scan_sh);
+            if (pos + total > plen) {
+                err = ILANS_ERR_TRUNCATED;
+            } else {
+                uint64_t p = pos + excl;
+                for (int l = lo; l < hi; ++l) {
+                    uint32_t x = ws[l];
+                    const uint32_t r = refills_for(x);
+                    for (uint32_t j = 0; j < r; ++j) x = (x << 8) | pay[p++];
+                    ws[l] = x;
+                    most = max(most, r);
+                }
+                pos += total;
+            }
+        }
+        if (err) break;
+        if (trace.states) {
+            __syncthreads();
+            const int64_t gi = base / n_lanes;
+            for (int l = lo; l < lo + per && l < n_lanes; ++l) trace.states[gi * n_lanes + l] = ws[l];
+            if (threadIdx.x == 0) trace.pos[gi] = pos;
+        }
+    }
+    atomicMax(&status->max_digits, most);
+    if (threadIdx.x == 0) {
+        if (err == ILANS_ERR_TRUNCATED) atomicMin(&status->trunc_stream, 0ull);
+        if (err == ILANS_ERR_FORMAT) status->value_error = ILANS_ERR_FORMAT;
+        if (consumed) consumed[0] = pos;
+        if (trace.groups) trace.groups[0] = (base < len ? base : len + n_lanes - 1) / n_lanes;
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+encode_u8_block_kernel(const uint8_t *__restrict__ g, int64_t len, int n_lanes,
+                       const TableDev *__restrict__ tab, uint8_t *__restrict__ o,
+                       uint32_t *__restrict__ chunk_bytes, uint32_t *__restrict__ states_out,
+                       DStatus *__restrict__ status, uint32_t *__restrict__ ws) {
+    __shared__ uint32_t scan_sh[32];
+    __shared__ uint2 enc[kMaxSym];
+    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
+    __syncthreads();
+    const EncCtx ctx(tab->scale_bits);
+    const uint32_t thr8 = 31u - tab->scale_bits;
+    const int per = (n_lanes + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per;
+    for (int l = lo; l < lo + per && l < n_lanes; ++l) ws[l] = kLow8;
+    int64_t top = 3 * len;
+    bool bad = false;
+    uint32_t most = 0;
+    for (int64_t gi = (len + n_lanes - 1) / n_lanes - 1; gi >= 0; --gi) {
+        const int64_t base = gi * n_lanes;
+        const int64_t left = len - base;
+        const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
+        const int hi = lo + per < active ? lo + per : active;
+        long long my_bad = -1;
+        uint32_t cnt = 0;
+        for (int l = lo; l < hi; ++l) {
+            const uint2 e = enc[g[base + l]];
+            if (e.x == 0u) { my_bad = base + l; continue; }
+            const uint32_t x = ws[l], fm1 = e.y & 0xFFFFu;
+            cnt += ((x >> thr8) > fm1) + (((x >> 8) >> thr8) > fm1) + (((x >> 16) >> thr8) > fm1);
+        }
+        if (__syncthreads_or(my_bad >= 0)) {
+            if (my_bad >= 0) atomicMax(&status->unenc_index, my_bad);
+            bad = true;
+            break;
+        }
+        uint32_t total;
+        const uint32_t excl = block_excl_scan_8(cnt, &total, scan_sh);
+        top -= total;
+        int64_t p = top + excl;
+        for (int l = lo; l < hi; ++l) {
+            const uint2 e = enc[g[base + l]];
+            uint32_t x = ws[l];
+            const uint32_t fm1 = e.y & 0xFFFFu;
+            const uint32_t sp = ((x >> thr8) > fm1) + (((x >> 8) >> thr8) > fm1) +
+                                (((x >> 16) >> thr8) > fm1);
+            for (uint32_t j = 0; j < sp; ++j) o[p++] = static_cast<uint8_t>(x >> (8 * (sp - 1 - j)));
+            ws[l] = enc_push(ctx, sp ? x >> (8 * sp) : x, e);
+            most = max(most, sp);
+        }
+    }
+    atomicMax(&status->max_digits, most);
+    if (!bad) {
+        if (threadIdx.x == 0) chunk_bytes[0] = static_cast<uint32_t>(3 * len - top);
+        for (int l = lo; l < lo + per && l < n_lanes; ++l) states_out[l] = ws[l];
+    }
+}
+
+cudaError_t launch_encode_u8(const uint8_t *d_msg, int64_t n, int n_lanes, const TableDev *d_table,
+                             uint8_t *d_scratch, uint32_t *d_bytes, uint32_t *d_states,
+                             DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    if (n_lanes > 32) {
+        const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
+        encode_u8_block_kernel<<<1, threads, 0, stream>>>(d_msg, n, n_lanes, d_table, d_scratch,
+                                                          d_bytes, d_states, d_status, d_lane_ws);
+    } else {
+        encode_u8_warp_kernel<<<1, 32, 0, stream>>>(d_msg, n, n, 1, n_lanes, d_table, d_scratch,
+                                                    d_bytes, d_states, d_status);
+    }
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_u8(const uint8_t *d_payload, uint64_t pay_len, const uint64_t *d_offsets,
+                             const uint32_t *d_states, int64_t n, int n_lanes,
+                             const TableDev *d_table, uint8_t *d_out, uint64_t *d_consumed,
+                             DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream,
+                             DecodeTrace trace) {
+    if (n <= 0) return cudaSuccess;
+    if (n_lanes > 32) {
+        const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
+        decode_u8_block_kernel<<<1, threads, 0, stream>>>(
+            d_payload, pay_len, d_states, n, n_lanes, d_table, d_out, d_consumed, d_status,
+            d_lane_ws, trace);
+    } else {
+        decode_u8_warp_kernel<<<1, 32, 0, stream>>>(d_payload, d_offsets, d_states, n, n, 1,
+                                                    n_lanes, d_table, d_out, d_consumed,
+                                                    d_status, trace);
+    }
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace ilans

@@ -24,6 +24,7 @@ __global__ void dstatus_reset_kernel(DStatus *s) {
     s->unenc_index = -1;
     s->unenc_symbol = 0;
     s->value_error = 0;
+    s->max_digits = 0;
 }
 
 int sm_count() {
@@ -208,6 +209,17 @@ extern "C" size_t ilans_dstatus_bytes(void) { return sizeof(DStatus); }
 // ---------------------------------------------------------------------------
 // 1. host-buffer drop-ins
 // ---------------------------------------------------------------------------
+
+// The encoder's 8-byte symbol record holds f - 1 and cum in 16 bits each
+// (common.cuh EncSym): true for every SymbolTable (f <= m, cum < m <= 2^16);
+// hand-made tables outside that range are rejected instead of mis-coded.
+static bool encode_table_fits(const uint32_t *freq, const uint32_t *cum, int n_freq,
+                              int scale_bits) {
+    const uint32_t m = 1u << scale_bits;
+    for (int s = 0; s < n_freq; ++s)
+        if (freq[s] && (freq[s] > m || cum[s] > 0xFFFFu)) return false;
+    return true;
+}
 extern "C" int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const uint32_t *freq,
                                             int32_t n_freq, const uint32_t *cum,
                                             int32_t scale_bits, int32_t n_lanes,
@@ -221,6 +233,8 @@ extern "C" int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const
         return st_fail(st, ILANS_ERR_VALUE, "scale_bits must be in [1, 16]");
     if (n_freq < 0 || n_freq > kMaxSym)
         return st_fail(st, ILANS_ERR_VALUE, "alphabet size must be in [1, 256]");
+    if (!encode_table_fits(freq, cum, n_freq, scale_bits))
+        return st_fail(st, ILANS_ERR_VALUE, "frequency / cumulative table out of range");
     Ctx *cp = nullptr;
     if (int rc = current_device(st, &cp)) return rc;
     Ctx &c = *cp;
@@ -423,6 +437,198 @@ extern "C" int ilans_decode_lanes_u16(const uint16_t *payload, int64_t pay_len,
     if (n_lanes > 32) return st_fail(st, ILANS_ERR_VALUE, "at most 32 lanes");
     return decode_common(payload, pay_len, states, slot_sym, n_slots, freq, cum, n_freq,
                          scale_bits, msg_len, n_lanes, out, consumed, st);
+}
+
+// ---------------------------------------------------------------------------
+// byte8 (8-bit digits, L = 2^23): single stream, host buffers
+// ---------------------------------------------------------------------------
+extern "C" int ilans_encode_interleaved_u8(const uint8_t *msg, int64_t n, const uint32_t *freq,
+                                           int32_t n_freq, const uint32_t *cum,
+                                           int32_t scale_bits, int32_t n_lanes,
+                                           uint8_t *payload_out, int64_t *payload_bytes,
+                                           uint32_t *states_out, ilans_status *st) {
+    st_clear(st);
+    if (n < 0) return st_fail(st, ILANS_ERR_VALUE, "negative message length");
+    if (n_lanes < 1 || n_lanes > 0xFFFF)
+        return st_fail(st, ILANS_ERR_VALUE, "lane_count must be in [1, 65535]");
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits)
+        return st_fail(st, ILANS_ERR_VALUE, "scale_bits must be in [1, 16]");
+    if (n_freq < 0 || n_freq > kMaxSym)
+        return st_fail(st, ILANS_ERR_VALUE, "alphabet size must be in [1, 256]");
+    if (!encode_table_fits(freq, cum, n_freq, scale_bits))
+        return st_fail(st, ILANS_ERR_VALUE, "frequency / cumulative table out of range");
+    Ctx *cp = nullptr;
+    if (int rc = current_device(st, &cp)) return rc;
+    Ctx &c = *cp;
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (int rc = ctx_init(c, st)) return rc;
+    if (n == 0) {
+        for (int l = 0; l < n_lanes; ++l) states_out[l] = 1u << 23;
+        *payload_bytes = 0;
+        return ILANS_OK;
+    }
+    cudaStream_t s = c.stream;
+    CK(c.msg.ensure(size_t(n)));
+    CK(c.scratch.ensure(size_t(n) * 3 + 16));
+    CK(c.states.ensure(size_t(n_lanes) * 4));
+    CK(c.ws.ensure(size_t(n_lanes) * 4));
+    CK(c.freq.ensure(kMaxSym * 4));
+    CK(c.cum.ensure((kMaxSym + 1) * 4));
+    CK(c.words.ensure(8));
+    uint32_t hf[kMaxSym] = {0}, hc[kMaxSym + 1] = {0};
+    std::memcpy(hf, freq, size_t(n_freq) * 4);
+    std::memcpy(hc, cum, size_t(n_freq + 1) * 4);
+    CK(cudaMemcpyAsync(c.msg.p, msg, size_t(n), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.freq.p, hf, sizeof(hf), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.cum.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    CK(launch_build_table(nullptr, c.freq.as<uint32_t>(), n_freq, c.cum.as<uint32_t>(), nullptr,
+                          scale_bits, c.table.as<TableDev>(), s));
+    dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
+    ilans_note_launch();
+    CK(launch_encode_u8(c.msg.as<uint8_t>(), n, n_lanes, c.table.as<TableDev>(),
+                        c.scratch.as<uint8_t>(), c.words.as<uint32_t>(), c.states.as<uint32_t>(),
+                        c.status.as<DStatus>(), c.ws.as<uint32_t>(), s));
+    DStatus hs;
+    if (int rc = read_dstatus(c.status.as<DStatus>(), s, &hs, st)) return rc;
+    st->max_digits = int32_t(hs.max_digits);
+    if (hs.unenc_index >= 0) {
+        st->index = hs.unenc_index;
+        st->symbol = msg[hs.unenc_index];
+        return st_fail(st, ILANS_ERR_UNENCODABLE, "symbol %d has frequency 0", st->symbol);
+    }
+    uint32_t w = 0;
+    CK(cudaMemcpyAsync(&w, c.words.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (w)
+        CK(cudaMemcpyAsync(payload_out, c.scratch.as<uint8_t>() + (3 * n - w), size_t(w),
+                           cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(states_out, c.states.p, size_t(n_lanes) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *payload_bytes = w;
+    return ILANS_OK;
+}
+
+static int decode_u8_common(const uint8_t *payload, int64_t pay_len, const uint32_t *states,
+                            const uint8_t *slot_sym, int64_t n_slots, const uint32_t *freq,
+                            const uint32_t *cum, int32_t n_freq, int32_t scale_bits,
+                            int64_t msg_len, int32_t n_lanes, uint8_t *out, int64_t *consumed,
+                            ilans_status *st, HostTrace ht) {
+    if (msg_len < 0 || pay_len < 0) return st_fail(st, ILANS_ERR_VALUE, "negative length");
+    if (n_lanes < 1 || n_lanes > 0xFFFF)
+        return st_fail(st, ILANS_ERR_VALUE, "lane_count must be in [1, 65535]");
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits)
+        return st_fail(st, ILANS_ERR_VALUE, "scale_bits must be in [1, 16]");
+    if (n_freq < 0 || n_freq > kMaxSym)
+        return st_fail(st, ILANS_ERR_VALUE, "alphabet size must be in [1, 256]");
+    const int64_t m = int64_t(1) << scale_bits;
+    if (n_slots < m) return st_fail(st, ILANS_ERR_VALUE, "slot table shorter than 2^scale_bits");
+    Ctx *cp = nullptr;
+    if (int rc = current_device(st, &cp)) return rc;
+    Ctx &c = *cp;
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (int rc = ctx_init(c, st)) return rc;
+    if (msg_len == 0) {
+        *consumed = 0;
+        if (ht.groups) *ht.groups = 0;
+        return ILANS_OK;
+    }
+    cudaStream_t s = c.stream;
+    const int64_t n_groups = (msg_len + n_lanes - 1) / n_lanes;
+    DecodeTrace dt{nullptr, nullptr, nullptr};
+    if (ht.states) {
+        CK(c.trace.ensure(size_t(n_groups) * n_lanes * 4 + size_t(n_groups) * 8 + 16));
+        CK(c.words.ensure(8));
+        dt.states = c.trace.as<uint32_t>();
+        dt.pos = reinterpret_cast<uint64_t *>(
+            c.trace.as<uint8_t>() + ((size_t(n_groups) * n_lanes * 4 + 7) & ~size_t(7)));
+        dt.groups = reinterpret_cast<uint64_t *>(c.words.p);
+    }
+    CK(c.payload.ensure(size_t(pay_len) + 16));
+    CK(c.offsets.ensure(16));
+    CK(c.states.ensure(size_t(n_lanes) * 4));
+    CK(c.ws.ensure(size_t(n_lanes) * 4));
+    CK(c.slot.ensure(size_t(m)));
+    CK(c.freq.ensure(kMaxSym * 4));
+    CK(c.cum.ensure((kMaxSym + 1) * 4));
+    CK(c.out.ensure(size_t(msg_len)));
+    CK(c.consumed.ensure(8));
+    uint32_t hf[kMaxSym] = {0}, hc[kMaxSym + 1] = {0};
+    std::memcpy(hf, freq, size_t(n_freq) * 4);
+    std::memcpy(hc, cum, size_t(n_freq + 1) * 4);
+    const uint64_t offs[2] = {0, uint64_t(pay_len)};
+    if (pay_len)
+        CK(cudaMemcpyAsync(c.payload.p, payload, size_t(pay_len), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.offsets.p, offs, sizeof(offs), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.states.p, states, size_t(n_lanes) * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.slot.p, slot_sym, size_t(m), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.freq.p, hf, sizeof(hf), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.cum.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    CK(launch_build_table(nullptr, c.freq.as<uint32_t>(), n_freq, c.cum.as<uint32_t>(),
+                          c.slot.as<uint8_t>(), scale_bits, c.table.as<TableDev>(), s));
+    dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
+    ilans_note_launch();
+    CK(launch_decode_u8(c.payload.as<uint8_t>(), uint64_t(pay_len), c.offsets.as<uint64_t>(),
+                        c.states.as<uint32_t>(), msg_len, n_lanes, c.table.as<TableDev>(),
+                        c.out.as<uint8_t>(), c.consumed.as<uint64_t>(), c.status.as<DStatus>(),
+                        c.ws.as<uint32_t>(), s, dt));
+    DStatus hs;
+    if (int rc = read_dstatus(c.status.as<DStatus>(), s, &hs, st)) return rc;
+    uint64_t used = 0;
+    CK(cudaMemcpyAsync(&used, c.consumed.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (ht.states) {
+        uint64_t g = 0;
+        CK(cudaMemcpyAsync(&g, dt.groups, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *ht.groups = int64_t(g);
+        if (g) {
+            CK(cudaMemcpyAsync(ht.states, dt.states, size_t(g) * n_lanes * 4,
+                               cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(ht.pos, dt.pos, size_t(g) * 8, cudaMemcpyDeviceToHost, s));
+            const int64_t done = int64_t(g) * n_lanes < msg_len ? int64_t(g) * n_lanes : msg_len;
+            CK(cudaMemcpyAsync(out, c.out.p, size_t(done), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+    }
+    st->consumed = int64_t(used);
+    st->max_digits = int32_t(hs.max_digits);
+    if (hs.value_error == ILANS_ERR_FORMAT)
+        return st_fail(st, ILANS_ERR_FORMAT, "renormalization does not terminate; corrupt stream");
+    if (hs.trunc_stream != ~0ull) {
+        st->stream = int64_t(hs.trunc_stream);
+        return st_fail(st, ILANS_ERR_TRUNCATED, "digit stream exhausted mid-decode");
+    }
+    CK(cudaMemcpyAsync(out, c.out.p, size_t(msg_len), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *consumed = int64_t(used);
+    return ILANS_OK;
+}
+
+extern "C" int ilans_decode_interleaved_u8(const uint8_t *payload, int64_t pay_len,
+                                           const uint32_t *states, const uint8_t *slot_sym,
+                                           int64_t n_slots, const uint32_t *freq,
+                                           const uint32_t *cum, int32_t n_freq,
+                                           int32_t scale_bits, int64_t msg_len, int32_t n_lanes,
+                                           uint8_t *out, int64_t *consumed, ilans_status *st) {
+    st_clear(st);
+    return decode_u8_common(payload, pay_len, states, slot_sym, n_slots, freq, cum, n_freq,
+                            scale_bits, msg_len, n_lanes, out, consumed, st,
+                            HostTrace{nullptr, nullptr, nullptr});
+}
+
+extern "C" int ilans_decode_trace_u8(const uint8_t *payload, int64_t pay_len,
+                                     const uint32_t *states, const uint8_t *slot_sym,
+                                     int64_t n_slots, const uint32_t *freq, const uint32_t *cum,
+                                     int32_t n_freq, int32_t scale_bits, int64_t msg_len,
+                                     int32_t n_lanes, uint8_t *out, uint32_t *trace_states,
+                                     uint64_t *trace_pos, int64_t *groups_done,
+                                     int64_t *consumed, ilans_status *st) {
+    st_clear(st);
+    if (!trace_states || !trace_pos || !groups_done)
+        return st_fail(st, ILANS_ERR_VALUE, "trace buffers required");
+    return decode_u8_common(payload, pay_len, states, slot_sym, n_slots, freq, cum, n_freq,
+                            scale_bits, msg_len, n_lanes, out, consumed, st,
+                            HostTrace{trace_states, trace_pos, groups_done});
 }
 
 extern "C" int ilans_quantize(const uint64_t *counts, int32_t n, int32_t scale_bits,

@@ -53,6 +53,8 @@ struct alignas(16) DStatus {
     long long unenc_index;            // max offending message index, -1 = none
     uint32_t unenc_symbol;
     uint32_t value_error;
+    uint32_t max_digits;              // byte8: most digits moved for one symbol
+    uint32_t pad[3];
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {

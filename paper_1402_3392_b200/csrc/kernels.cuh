@@ -38,6 +38,16 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
                           DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream,
                           DecodeTrace trace = DecodeTrace{nullptr, nullptr, nullptr});
 
+// byte8.cu -- single-stream byte8 codec (N <= 32 warp, N > 32 CTA)
+cudaError_t launch_encode_u8(const uint8_t *d_msg, int64_t n, int n_lanes, const TableDev *d_table,
+                             uint8_t *d_scratch, uint32_t *d_bytes, uint32_t *d_states,
+                             DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream);
+cudaError_t launch_decode_u8(const uint8_t *d_payload, uint64_t pay_len, const uint64_t *d_offsets,
+                             const uint32_t *d_states, int64_t n, int n_lanes,
+                             const TableDev *d_table, uint8_t *d_out, uint64_t *d_consumed,
+                             DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream,
+                             DecodeTrace trace);
+
 // synth.cu
 cudaError_t launch_synth(uint8_t *d_out, int64_t n, uint64_t seed, int64_t first_index,
                          const uint32_t *d_cdf, cudaStream_t stream);

@@ -36,6 +36,16 @@ def golden_chunks():
     return np.load(GOLDEN / "chunks.npz")
 
 
+@pytest.fixture(scope="session")
+def golden_byte8():
+    return np.load(GOLDEN / "byte8.npz")
+
+
+# byte8 N=2 sb=12 on the same 1 MiB input
+ZIPF_1MIB_BYTE8_DIGEST = "1ea63c4d860a4650"
+ZIPF_1MIB_BYTE8_STATES = (48568369, 187084597)
+
+
 def zipf_probs(s: float, n: int = 256) -> np.ndarray:
     p = (np.arange(n) + 1.0) ** -s
     return p / p.sum()

@@ -166,11 +166,40 @@ def chunk_cases():
     return arrays, meta
 
 
+def byte8_cases():
+    """BYTE8 (8-bit digits, L = 2^23): the reference's scalar path."""
+    from ilans.rans import BYTE8
+
+    rng = np.random.default_rng(8)
+    arrays, meta = {}, []
+    k = 0
+    for lanes in (1, 2, 3, 5, 8, 17, 32, 33, 100):
+        for n in sorted({0, 1, max(0, lanes - 1), lanes + 1, 2 * lanes + 3, 701,
+                         int(rng.integers(1000, 4000))}):
+            counts, table = random_table(rng)
+            msg = random_message(rng, table, n)
+            c = encode_interleaved(msg, table, lanes, BYTE8)
+            assert np.array_equal(decode_interleaved(c), msg)
+            arrays[f"b{k}_msg"] = msg
+            arrays[f"b{k}_freq"] = table.freq_u32
+            arrays[f"b{k}_payload"] = np.asarray(c.payload, dtype=np.uint8)
+            arrays[f"b{k}_states"] = np.asarray(c.final_states, dtype=np.uint32)
+            try:
+                blob = c.to_bytes()
+            except ilans.FormatError:
+                blob = None
+            meta.append(dict(case=k, lanes=lanes, n=n, scale_bits=table.scale_bits,
+                             sha256=None if blob is None else hashlib.sha256(blob).hexdigest()))
+            k += 1
+    return arrays, meta
+
+
 def main():
     print("reference backend:", backend.ACTIVE.name, "ilans", ilans.__version__)
     info = {"generator": "tests/golden/make_golden.py", "reference_backend": backend.ACTIVE.name,
             "numpy": np.__version__}
-    for name, fn in (("codec", codec_cases), ("quantize", quantize_cases), ("chunks", chunk_cases)):
+    for name, fn in (("codec", codec_cases), ("quantize", quantize_cases), ("chunks", chunk_cases),
+                     ("byte8", byte8_cases)):
         arrays, meta = fn()
         np.savez_compressed(OUT / f"{name}.npz", **arrays)
         info[name] = meta

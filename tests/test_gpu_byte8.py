@@ -1,0 +1,111 @@
+"""BYTE8 (8-bit digits, L = 2^23) on the B200 vs the reference's scalar path:
+golden fixtures from the reference, the BASELINE.md config-1 digest
+(byte8 N=2 sb=12, 1 MiB), lane counts past 32, truncation, lockstep steps
+and the stats counters (max digits per symbol > 1 for byte8)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1402_3392_b200 as ilb
+from conftest import ZIPF_1MIB_BYTE8_DIGEST, ZIPF_1MIB_BYTE8_STATES, zipf_1mib
+from paper_1402_3392_b200 import _lib
+from paper_1402_3392_b200.errors import TruncatedStreamError, UnsupportedVariantError
+from paper_1402_3392_b200.interleave import Container, decode_interleaved_steps
+from paper_1402_3392_b200.lanes import decode_lanes_steps
+from paper_1402_3392_b200.rans import BYTE8, RenormStats, SymbolTable
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device: the -m gpu suite must run on a B200")
+
+
+def random_table(rng, max_n=200, max_sb=16):
+    n = int(rng.integers(2, max_n + 1))
+    sb = int(rng.integers(max(1, (n - 1).bit_length()), max_sb + 1))
+    counts = rng.integers(0, 1000, size=n)
+    counts[int(rng.integers(0, n))] += 1
+    return SymbolTable(oracle.quantize(counts, sb), sb)
+
+
+def random_message(rng, table, n):
+    return rng.choice(table.alphabet_size, size=n, p=table.freq_u32 / table.total).astype(np.uint8)
+
+
+def test_byte8_matches_reference_fixtures(golden_byte8, golden_meta):
+    for case in golden_meta["byte8"]:
+        k, lanes, sb = case["case"], case["lanes"], case["scale_bits"]
+        msg = golden_byte8[f"b{k}_msg"]
+        t = SymbolTable(golden_byte8[f"b{k}_freq"].tolist(), sb)
+        c = ilb.encode_interleaved(msg, t, lanes, BYTE8)
+        assert np.array_equal(c.payload, golden_byte8[f"b{k}_payload"]), case
+        assert c.final_states == tuple(golden_byte8[f"b{k}_states"].tolist()), case
+        if case["sha256"] is not None:
+            assert hashlib.sha256(c.to_bytes()).hexdigest() == case["sha256"]
+        assert np.array_equal(ilb.decode_interleaved(Container.from_bytes(c.to_bytes())), msg)
+
+
+def test_byte8_config1_digest():
+    msg = zipf_1mib()
+    counts, alpha = oracle.histogram(msg)
+    t = SymbolTable.from_counts(counts[:alpha].tolist(), 12)
+    c = ilb.encode_interleaved(msg, t, 2, BYTE8)
+    assert c.final_states == ZIPF_1MIB_BYTE8_STATES
+    assert hashlib.sha256(c.to_bytes()).hexdigest()[:16] == ZIPF_1MIB_BYTE8_DIGEST
+    assert np.array_equal(ilb.decode_interleaved(c), msg)
+
+
+def test_byte8_many_lanes_and_oracle_fuzz():
+    rng = np.random.default_rng(88)
+    for lanes in (1, 2, 7, 32, 33, 257, 2000):
+        t = random_table(rng)
+        msg = random_message(rng, t, int(rng.integers(0, 20000)))
+        c = ilb.encode_interleaved(msg, t, lanes, BYTE8)
+        p, s = oracle.encode_interleaved_u8(msg, t.freq_u32, t.cum_u32, t.scale_bits, lanes)
+        assert np.array_equal(c.payload, p) and c.final_states == tuple(s.tolist())
+        assert np.array_equal(ilb.decode_interleaved(c), msg)
+
+
+def test_byte8_truncation_and_lane_decoder_rejects():
+    rng = np.random.default_rng(5)
+    t = random_table(rng)
+    msg = random_message(rng, t, 3000)
+    for lanes in (3, 40):
+        c = ilb.encode_interleaved(msg, t, lanes, BYTE8)
+        c.payload = c.payload[: len(c.payload) // 2]
+        with pytest.raises(TruncatedStreamError):
+            ilb.decode_interleaved(c)
+    c = ilb.encode_interleaved(msg, t, 2, BYTE8)
+    with pytest.raises(UnsupportedVariantError, match="unsupported by lane decoder"):
+        ilb.decode_lanes_full(c)
+    with pytest.raises(UnsupportedVariantError):
+        next(decode_lanes_steps(c))
+
+
+def test_byte8_steps_and_stats():
+    rng = np.random.default_rng(9)
+    t = random_table(rng, max_n=40, max_sb=14)
+    msg = random_message(rng, t, 2005)
+    stats = RenormStats()
+    c = ilb.encode_interleaved(msg, t, 8, BYTE8, stats=stats)
+    out = ilb.decode_interleaved(c, stats=stats)
+    assert np.array_equal(out, msg)
+    assert stats.encode_symbols == stats.decode_symbols == len(msg)
+    assert stats.encode_digits == stats.decode_digits == len(c.payload)
+    assert 1 <= stats.max_encode_digits <= 3 and 1 <= stats.max_decode_digits <= 3
+    steps = list(decode_interleaved_steps(c))
+    assert [s for syms, _, _ in steps for s in syms] == msg.tolist()
+    assert steps[-1][1] == (BYTE8.lower_bound,) * 8 and steps[-1][2] == len(c.payload)
+    # every group's state snapshot matches the serial oracle run to that point
+    f, cum, slot = t.freq_u32, t.cum_u32, t.slot_u8
+    for g in (0, 17, len(steps) - 1):
+        upto = min(len(msg), (g + 1) * 8)
+        _, used, xs = oracle.decode_u8_full(c.payload, c.final_states, slot, f, cum,
+                                            t.scale_bits, upto, 8)
+        assert steps[g][1] == tuple(int(v) for v in xs) and steps[g][2] == used

@@ -122,6 +122,46 @@ def test_baseline_md_digests():
         assert hashlib.sha256(blob).hexdigest()[:16] == digest, (lanes, sb)
 
 
+def iec1_byte8_bytes(lanes, n, sb, freqs, states, payload):
+    head = b"IEC1" + struct.pack("<BBHQ", 1, 0, lanes, n)
+    table = struct.pack("<BH", sb, len(freqs)) + struct.pack(f"<{len(freqs)}H", *freqs)
+    st = struct.pack(f"<{lanes}I", *[int(x) for x in states])
+    return head + table + st + np.ascontiguousarray(payload, dtype=np.uint8).tobytes()
+
+
+def test_byte8_matches_reference_fixtures(golden_byte8, golden_meta):
+    for case in golden_meta["byte8"]:
+        k, lanes, sb = case["case"], case["lanes"], case["scale_bits"]
+        msg = golden_byte8[f"b{k}_msg"]
+        freq = golden_byte8[f"b{k}_freq"]
+        f, cum, slot = oracle.table_views(freq, sb)
+        payload, states = oracle.encode_interleaved_u8(msg, f, cum, sb, lanes)
+        assert np.array_equal(payload, golden_byte8[f"b{k}_payload"]), case
+        assert np.array_equal(states, golden_byte8[f"b{k}_states"]), case
+        if case["sha256"] is not None:
+            blob = iec1_byte8_bytes(lanes, len(msg), sb, freq.tolist(), states, payload)
+            assert hashlib.sha256(blob).hexdigest() == case["sha256"]
+        out, used = oracle.decode_interleaved_u8(payload, states, slot, f, cum, sb, len(msg),
+                                                 lanes)
+        assert np.array_equal(out, msg) and used == len(payload)
+
+
+def test_byte8_baseline_md_digest():
+    from conftest import ZIPF_1MIB_BYTE8_DIGEST, ZIPF_1MIB_BYTE8_STATES
+
+    msg = zipf_1mib()
+    counts, alpha = oracle.histogram(msg)
+    freqs = oracle.quantize(counts[:alpha], 12)
+    f, cum, slot = oracle.table_views(freqs, 12)
+    payload, states = oracle.encode_interleaved_u8(msg, f, cum, 12, 2)
+    assert tuple(states.tolist()) == ZIPF_1MIB_BYTE8_STATES
+    blob = iec1_byte8_bytes(2, len(msg), 12, freqs, states, payload)
+    assert hashlib.sha256(blob).hexdigest()[:16] == ZIPF_1MIB_BYTE8_DIGEST
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.decode_interleaved_u8(payload[:-5], states, slot, f, cum, 12, len(msg), 2)
+    assert e.value.kind == "truncated"
+
+
 def test_truncation_and_unencodable():
     f, cum, slot = oracle.table_views([1, 3], 2)
     msg = np.array([0, 1, 1, 0, 1] * 400, dtype=np.uint8)
