@@ -249,6 +249,47 @@ def test_chunked_matches_reference_per_chunk(golden_chunks, golden_meta):
             assert np.array_equal(ilb.decode_interleaved(one), msg[j * C:(j + 1) * C])
 
 
+@pytest.mark.parametrize("sb", [12, 15])
+def test_full_size_config2_properties(sb):
+    """BASELINE config 2 at full size (256 MiB, 4096 x 64 KiB chunks, N=32):
+    size-independent properties -- exact round trip, every chunk consumes its
+    whole payload and returns all lanes to L, the device model equals
+    bincount + quantize, and sampled chunks equal the oracle's encode."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import DeviceCodec, n_chunks_for
+    from paper_1402_3392_b200.synth import synth_device
+
+    n, C = 256 << 20, 65536
+    k = n_chunks_for(n, C)
+    d_msg = synth_device(n, 1.1, 77)
+    d_out = torch.empty(n, dtype=torch.uint8, device=d_msg.device)
+    codec = DeviceCodec(n, C, 32, sb)
+    codec.reset_status()
+    codec.histogram(d_msg, n)
+    codec.build_table_from_counts()
+    codec.encode(d_msg, n)
+    codec.decode(d_out, n, final_states=True)
+    codec.check_status()
+    torch.cuda.synchronize()
+    assert torch.equal(d_out, d_msg[:n])
+    offs = codec.offsets[: k + 1].cpu().numpy().view(np.uint64)
+    assert np.array_equal(codec.consumed[:k].cpu().numpy().view(np.uint64), np.diff(offs))
+    assert (codec.final_states[: k * 32].cpu().numpy().view(np.uint32) == 1 << 16).all()
+    msg = d_msg[:n].cpu().numpy()
+    counts, alpha = oracle.histogram(msg)
+    assert np.array_equal(codec.counts.cpu().numpy().view(np.uint64), counts)
+    table = codec.read_table()
+    assert table.freq == oracle.quantize(counts[:alpha], sb)
+    payload = codec.payload[: int(offs[-1])].cpu().numpy().view(np.uint16)
+    states = codec.states[: k * 32].cpu().numpy().view(np.uint32).reshape(k, 32)
+    for j in (0, 1, 2047, k - 1):
+        chunk = msg[j * C:(j + 1) * C]
+        p, s = oracle.encode_interleaved_u16(chunk, table.freq_u32, table.cum_u32, sb, 32)
+        assert np.array_equal(payload[int(offs[j]):int(offs[j + 1])], p)
+        assert np.array_equal(states[j], s)
+
+
 def test_chunked_edge_shapes():
     from paper_1402_3392_b200.chunked import ChunkedContainer, decode_chunked, encode_chunked
 
