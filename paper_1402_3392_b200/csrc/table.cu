@@ -1,6 +1,8 @@
 // table.cu -- model builder on the device: byte histogram, bit-exact
 // quantize (rans.quantize, rans.py:171-211) and the lookup tables the coders
 // use (SymbolTable, rans.py:99-146).
+#include <climits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -170,6 +172,27 @@ __device__ __forceinline__ uint32_t floor_cm_over_t(unsigned long long c, uint32
     return lo;
 }
 
+// Same for T < 2^47 (every realistic message): a double estimate is within
+// one of the exact quotient; fix it with exact 64-bit products
+// (q <= 2^16, T < 2^47: q*T < 2^63).
+__device__ __forceinline__ uint32_t floor_cm_over_t64(unsigned long long cm,
+                                                      unsigned long long total) {
+    unsigned long long q = static_cast<unsigned long long>(
+        static_cast<double>(cm) / static_cast<double>(total));
+    while (q > 0 && q * total > cm) --q;
+    while ((q + 1) * total <= cm) ++q;
+    return static_cast<uint32_t>(q);
+}
+
+// Number of keys strictly greater than `my` among keys[0..256) (64-bit keys
+// made unique by the symbol index in the low byte; absent = INT64_MIN).
+__device__ __forceinline__ int rank_of(const long long *keys, long long my) {
+    int rank = 0;
+#pragma unroll 16
+    for (int j = 0; j < kMaxSym; ++j) rank += keys[j] > my;
+    return rank;
+}
+
 // Writes freq/cum/enc/dec/slot/packed for the table described by t->freq,
 // t->cum (already in shared `freq`, `cum`). Runs on the whole CTA.
 __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *cum,
@@ -184,19 +207,28 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
     }
     if (tid == 0) t->cum[kMaxSym] = cum[kMaxSym];
     t->cum[tid] = cum[tid];
-    // slot -> symbol; consistent (packable) check for the sb <= 12 LUT
+    // slot -> symbol; consistent (packable) check for the sb <= 12 LUT.
+    // Thread t owns the contiguous slots [t*per, (t+1)*per): one binary
+    // search for the first, then a forward walk over cum.
     int ok = scale_bits <= kPackedMaxBits ? 1 : 0;
-    for (uint32_t j = tid; j < m; j += kMaxSym) {
+    const uint32_t per = (m + kMaxSym - 1) / kMaxSym;
+    const uint32_t j0 = tid * per, j1 = min(m, j0 + per);
+    int s_cur = 0;
+    if (!slot_in && j0 < j1) {  // largest s with cum[s] <= j0 (zero-f symbols skip)
+        int lo = 0, hi = kMaxSym - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cum[mid] <= j0) lo = mid; else hi = mid - 1;
+        }
+        s_cur = lo;
+    }
+    for (uint32_t j = j0; j < j1; ++j) {
         uint32_t s;
         if (slot_in) {
             s = slot_in[j];
-        } else {  // largest s with cum[s] <= j and f[s] > 0
-            int lo = 0, hi = kMaxSym - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (cum[mid] <= j) lo = mid; else hi = mid - 1;
-            }
-            s = static_cast<uint32_t>(lo);
+        } else {
+            while (s_cur < kMaxSym - 1 && cum[s_cur + 1] <= j) ++s_cur;
+            s = static_cast<uint32_t>(s_cur);
         }
         t->slot_sym[j] = static_cast<uint8_t>(s);
         if (scale_bits <= kPackedMaxBits) {
@@ -220,6 +252,7 @@ build_table_kernel(const unsigned long long *__restrict__ counts, const uint32_t
     __shared__ uint32_t freq[kMaxSym];
     __shared__ uint32_t cum[kMaxSym + 1];
     __shared__ I128 keys[kMaxSym];
+    __shared__ long long keys64[kMaxSym];
     __shared__ unsigned long long red64[8];
     __shared__ int red[8];
     __shared__ int status_sh;
@@ -260,15 +293,52 @@ build_table_kernel(const unsigned long long *__restrict__ counts, const uint32_t
             }
             return;
         }
+        // T < 2^47 (all realistic inputs): every product and key fits 64 bits
+        // and a key * 256 + (255 - i) orders exactly like (key, -i)
+        const bool fast = total < ((u128)1 << 47);
         uint32_t f = 0;
         if (c) {
-            f = floor_cm_over_t(c, m, total);
+            f = fast ? floor_cm_over_t64(c * m, static_cast<unsigned long long>(total))
+                     : floor_cm_over_t(c, m, total);
             if (f < 1) f = 1;
         }
         const long long diff =
             static_cast<long long>(m) - block_sum_256<long long>(static_cast<long long>(f), reinterpret_cast<long long *>(red64));
         const u128 cm = (u128)c * m;
-        if (diff > 0) {
+        if (fast && diff > 0) {
+            const long long key = static_cast<long long>(c * m) -
+                                  static_cast<long long>(f * static_cast<unsigned long long>(total));
+            keys64[tid] = c ? key * 256 + (255 - tid) : LLONG_MIN;
+            __syncthreads();
+            if (c && rank_of(keys64, keys64[tid]) < diff) f += 1;
+            __syncthreads();
+        } else if (fast && diff < 0) {
+            const long long need = -diff;
+            const long long P1 = block_sum_256<long long>((c && f > 1) ? 1 : 0,
+                                                          reinterpret_cast<long long *>(red64));
+            uint32_t R = 0;
+            if (need >= P1) {  // more than one round: binary search R in [1, max f]
+                uint32_t lo = 1, hi = static_cast<uint32_t>(block_max_256(c ? static_cast<int>(f) : 0, red));
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi + 1) >> 1;
+                    const long long take = (c && f > 1) ? static_cast<long long>(min(mid, f - 1)) : 0;
+                    const long long P = block_sum_256<long long>(take, reinterpret_cast<long long *>(red64));
+                    if (P <= need) lo = mid; else hi = mid - 1;
+                }
+                R = lo;
+            }
+            const long long took = (c && f > 1) ? static_cast<long long>(min(R, f - 1)) : 0;
+            const long long rem = need - block_sum_256<long long>(took, reinterpret_cast<long long *>(red64));
+            const long long key = static_cast<long long>(f * static_cast<unsigned long long>(total)) -
+                                  static_cast<long long>(c * m);
+            const bool eligible = c && f >= R + 2;
+            keys64[tid] = eligible ? key * 256 + (255 - tid) : LLONG_MIN;
+            __syncthreads();
+            uint32_t dec = static_cast<uint32_t>(took);
+            if (eligible && rank_of(keys64, keys64[tid]) < rem) dec += 1;
+            __syncthreads();
+            f -= dec;
+        } else if (diff > 0) {
             // picks are the top-`diff` present symbols by (c*m - f*T, -i):
             // with diff > 0 every key is < T and >= diff+1 keys are > 0, so
             // no symbol is picked twice.
