@@ -15,11 +15,13 @@ namespace ilans {
 // counters (256 bins x 256 threads = 64 KB of shared memory), laid out so a
 // warp's 32 increments always hit 32 distinct banks whatever the byte values
 // (bank = lane): byte (bin, w, l) lives at bin*256 + ((w>>2)*32 + l)*4 + (w&3).
-// No atomics, so a 1-bit-entropy source (80% of bytes in one bin) costs the
-// same as a uniform one. Counters flush every 240 bytes per thread (before an
-// 8-bit counter can wrap): thread t sums bin t's 256 counters with
-// dp4a, reading the 64 words in a per-thread staggered order (conflict-free),
-// and zeroes them.
+// A warp's 32 increments never collide, so a 1-bit-entropy source (80% of
+// bytes in one bin) costs the same as a uniform one. Each increment is one
+// fire-and-forget shared add (red.shared) on the 32-bit word that holds the
+// counter (no per-thread read-modify-write chain). Counters flush every 240
+// bytes per thread (before an 8-bit counter could carry into its
+// neighbour): thread t sums bin t's 256 counters with dp4a, reading the 64
+// words in a per-thread staggered order (conflict-free), and zeroes them.
 // ---------------------------------------------------------------------------
 constexpr int kHistThreads = 256;
 constexpr int kHistVecPerRound = 15;  // 15 x 16 B = 240 bytes < 256 per counter
@@ -34,12 +36,22 @@ __device__ __forceinline__ void hist_bump(uint8_t *h, uint32_t tid, uint32_t b) 
     *p = static_cast<uint8_t>(*p + 1);
 }
 
-__device__ __forceinline__ void hist_bump16(uint8_t *h, uint32_t tid, uint4 v) {
+// The word holding this thread's byte counter also holds three other warps'
+// counters for the same bin and lane; a fire-and-forget shared add of
+// 1 << 8*(w & 3) bumps only ours as long as no counter passes 255 (flush
+// every 240 bytes), with no read-modify-write chain in the thread.
+__device__ __forceinline__ void hist_red(uint32_t base_addr, uint32_t tid, uint32_t b) {
+    const uint32_t off = hist_byte_offset(b, tid);
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base_addr + (off & ~3u)),
+                 "r"(1u << ((off & 3u) * 8)) : "memory");
+}
+
+__device__ __forceinline__ void hist_bump16(uint32_t base_addr, uint32_t tid, uint4 v) {
     const uint32_t words[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) hist_bump(h, tid, (words[q] >> (8 * j)) & 0xFFu);
+        for (int j = 0; j < 4; ++j) hist_red(base_addr, tid, (words[q] >> (8 * j)) & 0xFFu);
     }
 }
 
@@ -61,6 +73,7 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
                     unsigned long long *__restrict__ counts) {
     extern __shared__ __align__(16) uint8_t hist_smem[];
     const uint32_t tid = threadIdx.x;
+    const uint32_t base_addr = smem_addr(hist_smem);
     uint32_t *z = reinterpret_cast<uint32_t *>(hist_smem);
     for (uint32_t i = tid; i < 256u * 256u / 4u; i += kHistThreads) z[i] = 0;
     __syncthreads();
@@ -82,13 +95,11 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
 
     const uint4 *vec = reinterpret_cast<const uint4 *>(msg + head);
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kHistThreads;
-    int64_t i = static_cast<int64_t>(blockIdx.x) * kHistThreads + tid;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kHistThreads + tid;
     // rounds: every thread does <= 15 vectors, then the block flushes
     const int64_t per_round = stride * kHistVecPerRound;
     for (int64_t round_base = 0; round_base < nvec; round_base += per_round) {
-        // all 15 loads in flight before the first increment (latency hiding:
-        // the increments are a serial shared-memory read-modify-write chain)
-        uint4 v[kHistVecPerRound];
+        uint4 v[kHistVecPerRound];  // all loads in flight before the increments
 #pragma unroll
         for (int r = 0; r < kHistVecPerRound; ++r) {
             const int64_t j = i + round_base + static_cast<int64_t>(r) * stride;
@@ -97,7 +108,7 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
 #pragma unroll
         for (int r = 0; r < kHistVecPerRound; ++r) {
             const int64_t j = i + round_base + static_cast<int64_t>(r) * stride;
-            if (j < nvec) hist_bump16(hist_smem, tid, v[r]);
+            if (j < nvec) hist_bump16(base_addr, tid, v[r]);
         }
         __syncthreads();
         hist_flush(hist_smem, tid, acc);
