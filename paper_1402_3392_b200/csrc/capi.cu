@@ -52,11 +52,11 @@ cudaError_t launch_histogram(const uint8_t *d_msg, int64_t n, unsigned long long
                              smem);
         attr_set[dev & 63] = true;
     }
-    // 3 CTAs x 64 KB per SM; a block needs >= 15 x 4 KB of input per round
+    // 3 CTAs x 64 KB per SM (128 threads each); small inputs get fewer CTAs
     int64_t blocks = int64_t(sm_count()) * 3;
-    const int64_t want = (n + 256 * 16 * 15 - 1) / (256 * 16 * 15);
+    const int64_t want = (n + 128 * 16 * 8 - 1) / (128 * 16 * 8);
     if (blocks > want) blocks = want < 1 ? 1 : want;
-    histogram_u8_kernel<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(d_msg, n, d_counts);
+    histogram_u8_kernel<<<static_cast<unsigned>(blocks), 128, smem, stream>>>(d_msg, n, d_counts);
     ilans_note_launch();
     return cudaGetLastError();
 }

@@ -11,71 +11,71 @@ namespace ilans {
 // ---------------------------------------------------------------------------
 // Histogram (np.bincount at cli.py:31-37 / bench.py:47-51)
 //
-// HBM-bound streaming read. Every thread owns a private column of 8-bit
-// counters (256 bins x 256 threads = 64 KB of shared memory), laid out so a
+// HBM-bound streaming read. Every thread owns a private column of 16-bit
+// counters (256 bins x 128 threads = 64 KB of shared memory): the 32-bit
+// word (bin, w >> 1, lane) holds warp w's and warp w^1's counters, so a
 // warp's 32 increments always hit 32 distinct banks whatever the byte values
-// (bank = lane): byte (bin, w, l) lives at bin*256 + ((w>>2)*32 + l)*4 + (w&3).
-// A warp's 32 increments never collide, so a 1-bit-entropy source (80% of
-// bytes in one bin) costs the same as a uniform one. Each increment is one
-// fire-and-forget shared add (red.shared) on the 32-bit word that holds the
-// counter (no per-thread read-modify-write chain). Counters flush every 240
-// bytes per thread (before an 8-bit counter could carry into its
-// neighbour): thread t sums bin t's 256 counters with dp4a, reading the 64
-// words in a per-thread staggered order (conflict-free), and zeroes them.
+// (bank = lane) and a 1-bit-entropy source (80% of bytes in one bin) costs
+// the same as a uniform one. Each increment is one fire-and-forget shared
+// add (red.shared of 1 << 16*(w & 1)) -- no per-thread read-modify-write
+// chain, one shared-memory wavefront per 32 bytes. A counter can only carry
+// into its neighbour after 65536 bytes of one thread, so the block flushes
+// every 4095 vectors per thread (once per launch at every realistic size):
+// thread t sums bins t and t+128 over all 128 columns and zeroes them.
 // ---------------------------------------------------------------------------
-constexpr int kHistThreads = 256;
-constexpr int kHistVecPerRound = 15;  // 15 x 16 B = 240 bytes < 256 per counter
+constexpr int kHistThreads = 128;
+constexpr int kHistBatch = 8;                 // 16-byte loads in flight per thread
+constexpr int64_t kHistVecPerRound = 4088;    // <= 65535 / 16 vectors between flushes
 
-__device__ __forceinline__ uint32_t hist_byte_offset(uint32_t bin, uint32_t tid) {
-    const uint32_t w = tid >> 5, l = tid & 31;
-    return bin * 256u + (((w >> 2) * 32u + l) << 2) + (w & 3u);
+__device__ __forceinline__ uint32_t hist_word(uint32_t bin, uint32_t tid) {
+    return bin * 64u + ((tid >> 6) << 5) + (tid & 31u);  // 64 words per bin
 }
 
-__device__ __forceinline__ void hist_bump(uint8_t *h, uint32_t tid, uint32_t b) {
-    uint8_t *p = h + hist_byte_offset(b, tid);
-    *p = static_cast<uint8_t>(*p + 1);
-}
-
-// The word holding this thread's byte counter also holds three other warps'
-// counters for the same bin and lane; a fire-and-forget shared add of
-// 1 << 8*(w & 3) bumps only ours as long as no counter passes 255 (flush
-// every 240 bytes), with no read-modify-write chain in the thread.
 __device__ __forceinline__ void hist_red(uint32_t base_addr, uint32_t tid, uint32_t b) {
-    const uint32_t off = hist_byte_offset(b, tid);
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base_addr + (off & ~3u)),
-                 "r"(1u << ((off & 3u) * 8)) : "memory");
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base_addr + 4u * hist_word(b, tid)),
+                 "r"(1u << (((tid >> 5) & 1u) * 16)) : "memory");
 }
 
-__device__ __forceinline__ void hist_bump16(uint32_t base_addr, uint32_t tid, uint4 v) {
+// 16 bytes: per byte one PRMT (byte j -> bits 15..8, i.e. bin * 256 = the
+// bin's row offset), one add of the thread's column address, one RED.
+__device__ __forceinline__ void hist_bump16(uint32_t col_addr, uint32_t inc, uint4 v) {
     const uint32_t words[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) hist_red(base_addr, tid, (words[q] >> (8 * j)) & 0xFFu);
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t row = __byte_perm(words[q], 0u, 0x4404u | (j << 4));
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(col_addr + row), "r"(inc)
+                         : "memory");
+        }
     }
 }
 
-// thread t: add the 256 counters of bin t into acc and zero them.
-__device__ __forceinline__ void hist_flush(uint8_t *h, uint32_t tid, unsigned long long &acc) {
-    uint32_t *row = reinterpret_cast<uint32_t *>(h + tid * 256u);
-    uint32_t sum = 0;
+// thread t: add every column's counters of bins t and t + 128 into acc[0/1]
+// and zero them (staggered word order: conflict-free).
+__device__ __forceinline__ void hist_flush(uint32_t *h, uint32_t tid, unsigned long long *acc) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        uint32_t *row = h + (tid + 128u * half) * 64u;
+        uint32_t sum = 0;
 #pragma unroll 8
-    for (int k = 0; k < 64; ++k) {
-        const int idx = (k + static_cast<int>(tid)) & 63;
-        sum = __dp4a(row[idx], 0x01010101u, sum);
-        row[idx] = 0;
+        for (int k = 0; k < 64; ++k) {
+            const int idx = (k + static_cast<int>(tid)) & 63;
+            const uint32_t w = row[idx];
+            sum += (w & 0xFFFFu) + (w >> 16);
+            row[idx] = 0;
+        }
+        acc[half] += sum;
     }
-    acc += sum;
 }
 
 __global__ void __launch_bounds__(kHistThreads)
 histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
                     unsigned long long *__restrict__ counts) {
-    extern __shared__ __align__(16) uint8_t hist_smem[];
+    extern __shared__ __align__(16) uint32_t hist_smem[];
     const uint32_t tid = threadIdx.x;
     const uint32_t base_addr = smem_addr(hist_smem);
-    uint32_t *z = reinterpret_cast<uint32_t *>(hist_smem);
-    for (uint32_t i = tid; i < 256u * 256u / 4u; i += kHistThreads) z[i] = 0;
+    for (uint32_t i = tid; i < 256u * 64u; i += kHistThreads) hist_smem[i] = 0;
     __syncthreads();
 
     // unaligned head / tail bytes: block 0, thread 0 (its own counters)
@@ -84,37 +84,41 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
     if (head > n) head = n;
     const int64_t nvec = (n - head) >> 4;
     const int64_t tail_start = head + (nvec << 4);
-    unsigned long long acc = 0;
     if (blockIdx.x == 0 && tid == 0) {
-        for (int64_t i = 0; i < head; ++i) hist_bump(hist_smem, 0, msg[i]);
-        for (int64_t i = tail_start; i < n; ++i) hist_bump(hist_smem, 0, msg[i]);
+        for (int64_t i = 0; i < head; ++i) hist_red(base_addr, 0, msg[i]);
+        for (int64_t i = tail_start; i < n; ++i) hist_red(base_addr, 0, msg[i]);
     }
-    __syncthreads();
-    hist_flush(hist_smem, tid, acc);
-    __syncthreads();
 
+    unsigned long long acc[2] = {0, 0};
+    const uint32_t col_addr = base_addr + 4u * hist_word(0, tid);
+    const uint32_t inc = 1u << (((tid >> 5) & 1u) * 16);
     const uint4 *vec = reinterpret_cast<const uint4 *>(msg + head);
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kHistThreads;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * kHistThreads + tid;
-    // rounds: every thread does <= 15 vectors, then the block flushes
+    const int64_t first = static_cast<int64_t>(blockIdx.x) * kHistThreads + tid;
     const int64_t per_round = stride * kHistVecPerRound;
     for (int64_t round_base = 0; round_base < nvec; round_base += per_round) {
-        uint4 v[kHistVecPerRound];  // all loads in flight before the increments
+        const int64_t round_end = min(nvec, round_base + per_round);
+        for (int64_t j0 = round_base + first; j0 < round_end; j0 += stride * kHistBatch) {
+            uint4 v[kHistBatch];
 #pragma unroll
-        for (int r = 0; r < kHistVecPerRound; ++r) {
-            const int64_t j = i + round_base + static_cast<int64_t>(r) * stride;
-            v[r] = j < nvec ? __ldcs(vec + j) : make_uint4(0, 0, 0, 0);
-        }
+            for (int r = 0; r < kHistBatch; ++r) {
+                const int64_t j = j0 + r * stride;
+                v[r] = j < round_end ? __ldcs(vec + j) : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-        for (int r = 0; r < kHistVecPerRound; ++r) {
-            const int64_t j = i + round_base + static_cast<int64_t>(r) * stride;
-            if (j < nvec) hist_bump16(base_addr, tid, v[r]);
+            for (int r = 0; r < kHistBatch; ++r)
+                if (j0 + r * stride < round_end) hist_bump16(col_addr, inc, v[r]);
         }
         __syncthreads();
         hist_flush(hist_smem, tid, acc);
         __syncthreads();
     }
-    if (acc) atomicAdd(counts + tid, acc);
+    if (nvec == 0) {  // head / tail only
+        __syncthreads();
+        hist_flush(hist_smem, tid, acc);
+    }
+    if (acc[0]) atomicAdd(counts + tid, acc[0]);
+    if (acc[1]) atomicAdd(counts + tid + 128, acc[1]);
 }
 
 // ---------------------------------------------------------------------------
