@@ -406,7 +406,7 @@ compact_kernel(const uint16_t *__restrict__ scratch, int64_t n, int64_t chunk_le
     }
     uint32_t *dst = reinterpret_cast<uint32_t *>(payload + d);
     const uint32_t pairs = w >> 1;
-    constexpr int U = 4;  // independent loads in flight per thread
+    constexpr int U = 8;  // independent loads in flight per thread (latency-bound copy)
     const uint32_t step = blockDim.x * U;
     if (!(s & 1)) {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(scratch + s);

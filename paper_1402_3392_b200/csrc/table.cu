@@ -24,7 +24,7 @@ namespace ilans {
 // thread t sums bins t and t+128 over all 128 columns and zeroes them.
 // ---------------------------------------------------------------------------
 constexpr int kHistThreads = 128;
-constexpr int kHistBatch = 8;                 // 16-byte loads in flight per thread
+constexpr int kHistBatch = 12;                // 16-byte loads in flight per thread
 constexpr int64_t kHistVecPerRound = 4088;    // <= 65535 / 16 vectors between flushes
 
 __device__ __forceinline__ uint32_t hist_word(uint32_t bin, uint32_t tid) {
