@@ -286,14 +286,14 @@ extern "C" int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const
 }
 
 // sb <= 12 packed LUT is valid only for self-consistent tables (every slot's
-// symbol s has 1 <= f[s] <= 4096 and 0 <= slot - cum[s] < 4096).
+// symbol s has 1 <= f[s] <= 4095 and 0 <= slot - cum[s] < 4096).
 static bool host_packable(const uint8_t *slot_sym, const uint32_t *f, const uint32_t *cum,
                           int scale_bits) {
     if (scale_bits > kPackedMaxBits) return false;
     const uint32_t m = 1u << scale_bits;
     for (uint32_t j = 0; j < m; ++j) {
         const uint32_t s = slot_sym[j];
-        if (f[s] < 1 || f[s] > 4096 || j - cum[s] >= 4096u) return false;
+        if (f[s] < 1 || f[s] > 4095 || j - cum[s] >= 4096u) return false;
     }
     return true;
 }
@@ -817,10 +817,9 @@ extern "C" int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t
     if (scale_bits < 1 || scale_bits > kMaxScaleBits) return ILANS_ERR_VALUE;
     if ((reinterpret_cast<uintptr_t>(d_payload) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
         return ILANS_ERR_VALUE;
-    // tables built by the model builder are self-consistent, so the packed
-    // LUT applies whenever scale_bits <= 12; the kernel re-checks the table
-    // header on the device (scale_bits match, packed flag) and records a
-    // value error instead of decoding with a mismatched layout.
+    // scale_bits <= 12: the kernel reads the device table's packed flag and
+    // takes the packed or the two-lookup LUT; it re-checks scale_bits against
+    // the launch and records a value error instead of decoding a mismatch.
     const bool packed = scale_bits <= kPackedMaxBits;
     return launch_decode(d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes,
                          static_cast<const TableDev *>(d_table), scale_bits, packed, d_out,

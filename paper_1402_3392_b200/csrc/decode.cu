@@ -12,15 +12,15 @@
 //                                                      (lanes.packed_load)
 //   pos += popc(mask)
 // The payload is staged into a per-warp shared-memory ring by cp.async
-// (4 segments x 512 words; two segments = ~88 groups ahead of the reader),
+// (4 segments x 256 words; two segments = ~44 groups ahead of the reader),
 // so the refill read is a conflict-free LDS, never an HBM round trip.
 //
-// N = 32 fast path: 16 groups (512 symbols) per batch, fully unrolled; the
-// ring is advanced and the 512 decoded bytes are written (one 16-byte
+// N = 32 fast path: 8 groups (256 symbols) per batch, fully unrolled; the
+// ring is advanced and the 256 decoded bytes are written (one 8-byte
 // vector store per lane) once per batch, and truncation is checked once per
 // batch (pos is monotone, so "some group overran" == "pos > len at the end
 // of the batch"; reads past the payload hit zero-filled ring words and are
-// never used). Other N and the < 512-symbol tail run the per-group loop.
+// never used). Other N and the < 256-symbol tail run the per-group loop.
 //
 // Block kernel (N > 32, up to 65535 lanes): one CTA per stream, contiguous
 // lane ranges per thread and a CTA-wide exclusive scan of refill counts in
@@ -66,19 +66,21 @@ __device__ __forceinline__ uint32_t ring_load(uint32_t ring_addr, uint32_t byte_
 
 template <bool PACKED>
 struct Lut {
-    const uint32_t *packed;  // PACKED: sym | (f-1) << 8 | bias << 20
+    const uint32_t *packed;  // PACKED: bias | sym << 12 | f << 20
     const uint8_t *sym;      // else: slot -> symbol
     const uint2 *dec;        //       symbol -> {f, cum}
     uint32_t mask;
     uint32_t sb;
 
-    // returns the symbol in the low byte (PACKED: the whole entry)
+    // returns the symbol in the low byte
     __device__ __forceinline__ uint32_t pop(uint32_t &x) const {
         const uint32_t slot = x & mask;
         if (PACKED) {
             const uint32_t e = packed[slot];
-            x = (((e >> 8) & 0xFFFu) + 1u) * (x >> sb) + (e >> 20);
-            return e;
+            // f * (x >> sb) + bias: the two field extracts run in parallel,
+            // so the dependent chain after the load is extract + IMAD
+            x = (e >> 20) * (x >> sb) + (e & 0xFFFu);
+            return e >> 12;  // symbol in the low byte
         } else {
             const uint32_t s = sym[slot];
             const uint2 d = dec[s];
@@ -91,24 +93,19 @@ struct Lut {
 // Shared memory per CTA: [align pad][W rings x 2 KB][W obufs x 512 B][LUT].
 __host__ __device__ constexpr size_t decode_warp_smem() { return kRingBytes + kObufBytes; }
 
+// Not inlined: with both LUT forms inlined into one kernel the packed
+// path's schedule degrades (~8% slower decode, measured); as a call each
+// body keeps its own register allocation.
 template <bool PACKED>
-__global__ void __launch_bounds__(1024)
-decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
-                   const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
-                   int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
-                   uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
-                   uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
-                   int launch_sb, DecodeTrace trace) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    const int sb = static_cast<int>(tab->scale_bits);
-    if (sb != launch_sb || (PACKED && !(tab->flags & kTabPacked)) || tab->status != ILANS_OK) {
-        if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
-        return;
-    }
+__device__ __noinline__ void
+decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                 const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                 int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                 uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
+                 uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
+                 DecodeTrace trace, uint8_t *smem, int sb) {
     const uint32_t m = 1u << sb;
     const int nw = blockDim.x >> 5;
-    const uint32_t raw_addr = smem_addr(smem_raw);
-    uint8_t *smem = smem_raw + (((raw_addr + kRingBytes - 1) & ~uint32_t(kRingBytes - 1)) - raw_addr);
     uint8_t *lut_base = smem + nw * (kRingBytes + kObufBytes);
 
     // ---- stage the lookup tables in shared memory ------------------------
@@ -257,6 +254,33 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
     }
 }
 
+// ALLOW_PACKED: sb <= 12 launch whose smem fits either LUT; the device
+// table's flag picks the packed entry or the two-lookup form (a
+// single-symbol sb=12 table has f = 4096, which the 12-bit field cannot hold).
+template <bool ALLOW_PACKED>
+__global__ void __launch_bounds__(1024)
+decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                   const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                   int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                   uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
+                   uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
+                   int launch_sb, DecodeTrace trace) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const int sb = static_cast<int>(tab->scale_bits);
+    if (sb != launch_sb || tab->status != ILANS_OK) {
+        if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
+        return;
+    }
+    const uint32_t raw_addr = smem_addr(smem_raw);
+    uint8_t *smem = smem_raw + (((raw_addr + kRingBytes - 1) & ~uint32_t(kRingBytes - 1)) - raw_addr);
+    if (ALLOW_PACKED && (tab->flags & kTabPacked))
+        decode_warp_body<true>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes, tab,
+                               out, consumed, final_states, status, trace, smem, sb);
+    else
+        decode_warp_body<false>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes, tab,
+                                out, consumed, final_states, status, trace, smem, sb);
+}
+
 // ---------------------------------------------------------------------------
 // CTA-wide exclusive scan (blockDim multiple of 32, <= 1024)
 // ---------------------------------------------------------------------------
@@ -385,7 +409,8 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
         return cudaGetLastError();
     }
     const bool use_packed = packed && scale_bits <= kPackedMaxBits;
-    const size_t lut = decode_lut_bytes(scale_bits, use_packed);
+    size_t lut = decode_lut_bytes(scale_bits, false);
+    if (use_packed && decode_lut_bytes(scale_bits, true) > lut) lut = decode_lut_bytes(scale_bits, true);
     // 4-warp CTAs spread the streams evenly over the SMs (<= 28 per SM for
     // 4096 chunks); the per-CTA LUT copy argues for bigger CTAs only when the
     // LUT is large (sb > 14 generic tables).

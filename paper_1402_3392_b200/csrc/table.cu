@@ -249,8 +249,10 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         if (scale_bits <= kPackedMaxBits) {
             const uint32_t f = freq[s];
             const uint32_t bias = j - cum[s];
-            if (f < 1 || f > 4096 || bias >= 4096) ok = 0;
-            t->packed[j] = s | ((f - 1u) & 0xFFFu) << 8 | (bias & 0xFFFu) << 20;
+            // f == 4096 (a single-symbol sb=12 table) does not fit 12 bits:
+            // such tables take the two-lookup path
+            if (f < 1 || f > 4095 || bias >= 4096) ok = 0;
+            t->packed[j] = (bias & 0xFFFu) | s << 12 | (f & 0xFFFu) << 20;
         }
     }
     __syncthreads();

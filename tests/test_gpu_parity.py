@@ -304,3 +304,24 @@ def test_chunked_edge_shapes():
         assert np.array_equal(cc.payload, ref_p) and np.array_equal(cc.states, ref_s)
         back = ChunkedContainer.from_bytes(cc.to_bytes())
         assert np.array_equal(decode_chunked(back), msg)
+
+
+@pytest.mark.parametrize("sb", [11, 12, 13])
+def test_chunked_skewed_tables_both_lut_forms(sb):
+    """The packed decode entry holds f in 12 bits: a single-symbol source at
+    sb=12 (f = 4096) must take the two-lookup form, f = 4095 and sb = 11
+    the packed one; all decode through the device-built model."""
+    from paper_1402_3392_b200.chunked import decode_chunked, encode_chunked
+
+    rng = np.random.default_rng(sb)
+    single = np.full(70_000, 9, dtype=np.uint8)
+    skew = np.zeros(70_000, dtype=np.uint8)
+    skew[rng.integers(0, len(skew), 3)] = 1   # -> f = {m - 1, 1}
+    for msg in (single, skew):
+        cc = encode_chunked(msg, None, 32, 4096, sb)
+        t = cc.table
+        ref_p, _, ref_s = oracle.encode_chunks_u16(msg, 4096, t.freq_u32, t.cum_u32, sb, 32)
+        assert np.array_equal(cc.payload, ref_p) and np.array_equal(cc.states, ref_s)
+        assert np.array_equal(decode_chunked(cc), msg)
+        c = ilb.encode_interleaved(msg, t, 32, WORD16)
+        assert np.array_equal(ilb.decode_interleaved(c), msg)
