@@ -15,12 +15,12 @@
 // (4 segments x 256 words; two segments = ~44 groups ahead of the reader),
 // so the refill read is a conflict-free LDS, never an HBM round trip.
 //
-// N = 32 fast path: 8 groups (256 symbols) per batch, fully unrolled; the
-// ring is advanced and the 256 decoded bytes are written (one 8-byte
+// N = 32 fast path: 16 groups (512 symbols) per batch, fully unrolled; the
+// ring is advanced and the 512 decoded bytes are written (one 16-byte
 // vector store per lane) once per batch, and truncation is checked once per
 // batch (pos is monotone, so "some group overran" == "pos > len at the end
 // of the batch"; reads past the payload hit zero-filled ring words and are
-// never used). Other N and the < 256-symbol tail run the per-group loop.
+// never used). Other N and the < 512-symbol tail run the per-group loop.
 //
 // Block kernel (N > 32, up to 65535 lanes): one CTA per stream, contiguous
 // lane ranges per thread and a CTA-wide exclusive scan of refill counts in
@@ -34,7 +34,7 @@ namespace ilans {
 constexpr int kSegWords = 256;             // 512 B per cp.async warp-copy (16 B / lane)
 constexpr int kRingWords = 4 * kSegWords;  // 2 KB payload ring per warp (2 KB aligned)
 constexpr int kRingBytes = kRingWords * 2;
-constexpr int kBatch = 8;                  // groups per fast-path batch (N = 32)
+constexpr int kBatch = 16;                 // groups per fast-path batch (N = 32)
 constexpr int kObufBytes = 512;            // 2 x 256 B output halves per warp
 constexpr int kObufHalf = kObufBytes / 2;
 
@@ -163,9 +163,16 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
         int64_t base = 0;
 
         if (n_lanes == 32 && !trace.states) {
-            // ---------------- fast path: batches of 8 full groups -----------
-            const int64_t full = len >> 8;
+            // ---------------- fast path: batches of kBatch full groups ------
+            // A batch reads <= 512 words, i.e. up to two segments past the
+            // one holding the cursor, so the ring runs one segment deeper
+            // here (wait<1>: everything but the newest segment has landed).
+            const int64_t full = len / (32 * kBatch);
             uint32_t vb = static_cast<uint32_t>(v) << 1;  // byte cursor (mod 2^32)
+            uint32_t seg_cur = 0;                          // vb >> 9 of the cursor
+            uint32_t next_seg = 4;                         // next segment to issue
+            cp_async_wait<1>();
+            __syncwarp();
             for (int64_t b = 0; b < full; ++b) {
                 const uint32_t vb0 = vb;
 #pragma unroll
@@ -177,23 +184,28 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                     const uint32_t w = ring_load(ring_addr, vb + (__popc(mk & lt) << 1));
                     x = need ? ((x << 16) | w) : x;
                     vb += __popc(mk) << 1;
+                    // keep the byte cursor itself as the induction variable
+                    // (address = one LEA + one LOP3 per group)
+                    asm volatile("" : "+r"(vb));
                     obuf[g * 32 + lane] = static_cast<uint8_t>(s);
                 }
                 __syncwarp();
-                const uint2 o = reinterpret_cast<const uint2 *>(obuf)[lane];
-                reinterpret_cast<uint2 *>(out_k + (b << 8))[lane] = o;
-                // advance the ring: the cursor moved by <= 256 words
+                const uint4 o = reinterpret_cast<const uint4 *>(obuf)[lane];
+                reinterpret_cast<uint4 *>(out_k + b * (32 * kBatch))[lane] = o;
                 v += (vb - vb0) >> 1;
-                const uint64_t seg = v / kSegWords;
-                if (seg != cur) {
-                    cur = seg;
-                    issue_segment(ring, src, static_cast<uint32_t>(cur + 3), lane);
-                    cp_async_commit();
-                    cp_async_wait<2>();
+                const uint32_t seg = (vb >> 9) & 0x7FFFFFu;
+                if (seg != seg_cur) {  // one or two segments were finished
+                    do {
+                        seg_cur = (seg_cur + 1) & 0x7FFFFFu;
+                        issue_segment(ring, src, next_seg++, lane);
+                        cp_async_commit();
+                    } while (seg_cur != seg);
+                    cp_async_wait<1>();
                 }
                 __syncwarp();
             }
-            base = full << 8;
+            cur = next_seg - 4;  // == v / kSegWords; cur + 1.. cur + 3 issued
+            base = full * (32 * kBatch);
         }
         // ---------------- generic per-group loop (any N <= 32, tails) ------
         bool truncated = (v - delta) > wlen;
