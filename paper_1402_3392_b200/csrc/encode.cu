@@ -75,6 +75,19 @@ struct SpillStage {
         __syncwarp();
     }
 
+    // Fast-path drain: whole 256-word blocks [flushed - 256, flushed), one
+    // 16-byte store per lane, while at least 256 final words are pending
+    // (keeps pending < 256, so a 512-symbol batch cannot wrap the ring).
+    __device__ __forceinline__ void drain(Idx top, int lane) {
+        while (flushed - top >= 256) {
+            __syncwarp();
+            const Idx blk = flushed - 256 + Idx(lane) * 8;
+            *reinterpret_cast<uint4 *>(out + blk) =
+                *reinterpret_cast<const uint4 *>(ring + (blk & (kOutRing - 1)));
+            flushed -= 256;
+        }
+    }
+
     __device__ __forceinline__ void finish(Idx top, int lane) {
         flush(top, lane);
         for (Idx w = top + lane; w < flushed; w += 32) out[w] = ring[w & (kOutRing - 1)];
@@ -168,11 +181,14 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         // which is then discarded).
         Idx issued_lo = cur - 3;
         for (Idx b = full - 1; !bad && b >= 0; --b) {
-            if (b - 3 < issued_lo) {
+            if (b - 3 < issued_lo) {  // segments below `full` are whole 512-byte blocks
                 __syncwarp();
-                issue_msg_segment(ring, g, len, b - 3, lane);
+                const Idx sg = b - 3;
+                if (sg >= 0)
+                    cp_async16(ring + (static_cast<uint32_t>(sg) & 3u) * kInSeg + lane * 16,
+                               g + sg * kInSeg + lane * 16, 16u);
                 cp_async_commit();
-                issued_lo = b - 3;
+                issued_lo = sg;
             }
             cp_async_wait<3>();
             __syncwarp();
@@ -208,7 +224,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 }
                 bad = true;
             }
-            st.flush(top, lane);
+            st.drain(top, lane);
         }
         if (!bad) {
             st.finish(top, lane);
