@@ -33,7 +33,7 @@ struct alignas(16) TableDev {
     uint32_t cum[kMaxSym + 4];        // cum[0..256]
     uint2 enc[kMaxSym];               // EncSym records {magic, (m - f) | cum << 16}
     uint2 dec[kMaxSym];               // {f, cum} for the decoder's second lookup
-    uint32_t packed[1 << kPackedMaxBits];  // bias | sym << 12 | f << 20 (f < 4096)
+    uint32_t packed[1 << kPackedMaxBits];  // sym | bias << 8 | f << 20 (f < 4096)
     uint8_t slot_sym[1 << kMaxScaleBits];
 };
 

@@ -14,6 +14,9 @@
 // The payload is staged into a per-warp shared-memory ring by cp.async
 // (4 segments x 256 words; two segments = ~44 groups ahead of the reader),
 // so the refill read is a conflict-free LDS, never an HBM round trip.
+// Slots 0 and 1 are mirrored past the end of the ring (1536 words), so a
+// 512-word batch read starting anywhere in the ring never wraps: inside a
+// batch the read address is the batch base plus a running byte offset.
 //
 // N = 32 fast path: 16 groups (512 symbols) per batch, fully unrolled; the
 // ring is advanced and the 512 decoded bytes are written (one 16-byte
@@ -32,8 +35,9 @@
 namespace ilans {
 
 constexpr int kSegWords = 256;             // 512 B per cp.async warp-copy (16 B / lane)
-constexpr int kRingWords = 4 * kSegWords;  // 2 KB payload ring per warp (2 KB aligned)
+constexpr int kRingWords = 4 * kSegWords;  // 2 KB payload ring per warp
 constexpr int kRingBytes = kRingWords * 2;
+constexpr int kRingAllocBytes = kRingBytes + 2 * kSegWords * 2;  // + mirror of slots 0, 1
 constexpr int kBatch = 16;                 // groups per fast-path batch (N = 32)
 constexpr int kObufBytes = 512;            // 2 x 256 B output halves per warp
 constexpr int kObufHalf = kObufBytes / 2;
@@ -51,36 +55,51 @@ __device__ __forceinline__ void issue_segment(uint16_t *ring, const SegSrc &src,
         const uint64_t left = (src.avail - w0) * 2u;
         bytes = left >= 16u ? 16u : static_cast<uint32_t>(left);
     }
-    cp_async16(ring + (seg & 3u) * kSegWords + lane * 8, bytes ? src.g + w0 : src.g, bytes);
+    const uint16_t *g = bytes ? src.g + w0 : src.g;
+    cp_async16(ring + (seg & 3u) * kSegWords + lane * 8, g, bytes);
+    if ((seg & 3u) < 2u)  // mirror (warp-uniform branch)
+        cp_async16(ring + (4u + (seg & 3u)) * kSegWords + lane * 8, g, bytes);
 }
 
-// Refill read: the ring is kRingBytes-aligned in the shared window, so the
-// address is one LOP3 (base | (byte_cursor & mask)).
-__device__ __forceinline__ uint32_t ring_load(uint32_t ring_addr, uint32_t byte_off) {
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     uint16_t w;
-    asm volatile("ld.shared.u16 %0, [%1];"
-                 : "=h"(w)
-                 : "r"(ring_addr | (byte_off & (kRingBytes - 2))));
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(w) : "r"(addr));
     return w;
+}
+
+// Per-group refill read (generic loop): ring base + cursor modulo the ring.
+__device__ __forceinline__ uint32_t ring_load(uint32_t ring_addr, uint32_t byte_off) {
+    return lds_u16(ring_addr + (byte_off & (kRingBytes - 2)));
 }
 
 template <bool PACKED>
 struct Lut {
-    const uint32_t *packed;  // PACKED: bias | sym << 12 | f << 20
+    const uint32_t *packed;  // PACKED: sym | bias << 8 | f << 20
     const uint8_t *sym;      // else: slot -> symbol
     const uint2 *dec;        //       symbol -> {f, cum}
     uint32_t mask;
     uint32_t sb;
+    uint32_t hmul;           // 2^(32 - sb): x >> sb as a multiply-high (FMA pipe)
+    uint64_t hbias64;        // -4096 << 32
 
     // returns the symbol in the low byte
     __device__ __forceinline__ uint32_t pop(uint32_t &x) const {
         const uint32_t slot = x & mask;
         if (PACKED) {
+            // h = (x >> sb) - 4096 in one IMAD.HI; e >> 8 = bias + f * 4096,
+            // so f * h + (e >> 8) = f * (x >> sb) + bias with no field mask,
+            // and the symbol is e's low byte (stored as is). The integer ALU
+            // pipe is the decoder's busiest; this moves work to the FMA pipe.
+            const uint32_t h = (x >> sb) - 4096u;
             const uint32_t e = packed[slot];
-            // f * (x >> sb) + bias: the two field extracts run in parallel,
-            // so the dependent chain after the load is extract + IMAD
-            x = (e >> 20) * (x >> sb) + (e & 0xFFFu);
-            return e >> 12;  // symbol in the low byte
+            x = (e >> 20) * h + (e >> 8);
+            return e;
         } else {
             const uint32_t s = sym[slot];
             const uint2 d = dec[s];
@@ -91,7 +110,7 @@ struct Lut {
 };
 
 // Shared memory per CTA: [align pad][W rings x 2 KB][W obufs x 512 B][LUT].
-__host__ __device__ constexpr size_t decode_warp_smem() { return kRingBytes + kObufBytes; }
+__host__ __device__ constexpr size_t decode_warp_smem() { return kRingAllocBytes + kObufBytes; }
 
 // Not inlined: with both LUT forms inlined into one kernel the packed
 // path's schedule degrades (~8% slower decode, measured); as a call each
@@ -106,12 +125,14 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                  DecodeTrace trace, uint8_t *smem, int sb) {
     const uint32_t m = 1u << sb;
     const int nw = blockDim.x >> 5;
-    uint8_t *lut_base = smem + nw * (kRingBytes + kObufBytes);
+    uint8_t *lut_base = smem + nw * (kRingAllocBytes + kObufBytes);
 
     // ---- stage the lookup tables in shared memory ------------------------
     Lut<PACKED> lut;
     lut.mask = m - 1u;
     lut.sb = static_cast<uint32_t>(sb);
+    lut.hmul = 1u << (32 - sb);
+    lut.hbias64 = static_cast<uint64_t>(0u - 4096u) << 32;
     if (PACKED) {
         uint32_t *p = reinterpret_cast<uint32_t *>(lut_base);
         for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) p[i] = tab->packed[i];
@@ -134,10 +155,16 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
 
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    uint16_t *ring = reinterpret_cast<uint16_t *>(smem + wib * kRingBytes);
+    uint16_t *ring = reinterpret_cast<uint16_t *>(smem + wib * kRingAllocBytes);
     const uint32_t ring_addr = smem_addr(ring);
-    uint8_t *obuf = smem + nw * kRingBytes + wib * kObufBytes;
+    uint8_t *obuf = smem + nw * kRingAllocBytes + wib * kObufBytes;
     const uint32_t lt = lanemask_lt();
+    // popc(mk & lanemask_lt) == popc(mk << (32 - lane)): a multiply (FMA
+    // pipe) instead of a LOP3 (ALU pipe); lane 0 multiplies by 0
+    const uint32_t lt_mul = lane ? 1u << (32 - lane) : 0u;
+    // 2 as an opaque register: keeps the cursor updates as IMADs (FMA pipe)
+    uint32_t two;
+    asm volatile("mov.u32 %0, 2;" : "=r"(two));
     const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nw;
 
     for (int64_t k = static_cast<int64_t>(blockIdx.x) * nw + wib; k < n_chunks;
@@ -175,20 +202,22 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
             __syncwarp();
             for (int64_t b = 0; b < full; ++b) {
                 const uint32_t vb0 = vb;
+                // shared address of the cursor; the batch reads < 512 words
+                // past it, which the mirrored slots keep contiguous
+                const uint32_t a0 = ring_addr + (vb & (kRingBytes - 2));
+                uint32_t a = a0;
 #pragma unroll
                 for (int g = 0; g < kBatch; ++g) {
                     const uint32_t s = lut.pop(x);
                     const bool need = x < kLow;
                     const uint32_t mk = __ballot_sync(0xffffffffu, need);
                     // every lane loads (one wavefront either way), then selects
-                    const uint32_t w = ring_load(ring_addr, vb + (__popc(mk & lt) << 1));
-                    x = need ? ((x << 16) | w) : x;
-                    vb += __popc(mk) << 1;
-                    // keep the byte cursor itself as the induction variable
-                    // (address = one LEA + one LOP3 per group)
-                    asm volatile("" : "+r"(vb));
+                    const uint32_t w = lds_u16(mad_lo(__popc(mk * lt_mul), two, a));
+                    x = need ? x * 65536u + w : x;
+                    a = mad_lo(__popc(mk), two, a);
                     obuf[g * 32 + lane] = static_cast<uint8_t>(s);
                 }
+                vb = vb0 + (a - a0);
                 __syncwarp();
                 const uint4 o = reinterpret_cast<const uint4 *>(obuf)[lane];
                 reinterpret_cast<uint4 *>(out_k + b * (32 * kBatch))[lane] = o;
@@ -277,14 +306,12 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                    uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
                    uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
                    int launch_sb, DecodeTrace trace) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
+    extern __shared__ __align__(16) uint8_t smem[];
     const int sb = static_cast<int>(tab->scale_bits);
     if (sb != launch_sb || tab->status != ILANS_OK) {
         if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
         return;
     }
-    const uint32_t raw_addr = smem_addr(smem_raw);
-    uint8_t *smem = smem_raw + (((raw_addr + kRingBytes - 1) & ~uint32_t(kRingBytes - 1)) - raw_addr);
     if (ALLOW_PACKED && (tab->flags & kTabPacked))
         decode_warp_body<true>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes, tab,
                                out, consumed, final_states, status, trace, smem, sb);
@@ -428,9 +455,9 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
     // LUT is large (sb > 14 generic tables).
     int warps = lut > 24 * 1024 ? 16 : 4;
     const size_t smem_cap = 227 * 1024;
-    while (warps > 1 && lut + size_t(warps) * decode_warp_smem() + kRingBytes > smem_cap)
+    while (warps > 1 && lut + size_t(warps) * decode_warp_smem() > smem_cap)
         warps >>= 1;
-    const size_t smem = lut + size_t(warps) * decode_warp_smem() + kRingBytes;  // + align pad
+    const size_t smem = lut + size_t(warps) * decode_warp_smem();
     int64_t blocks = (n_chunks + warps - 1) / warps;
     const int64_t max_blocks = int64_t(sm_count()) * 64;
     if (blocks > max_blocks) blocks = max_blocks;

@@ -252,7 +252,7 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
             // f == 4096 (a single-symbol sb=12 table) does not fit 12 bits:
             // such tables take the two-lookup path
             if (f < 1 || f > 4095 || bias >= 4096) ok = 0;
-            t->packed[j] = (bias & 0xFFFu) | s << 12 | (f & 0xFFFu) << 20;
+            t->packed[j] = s | (bias & 0xFFFu) << 8 | (f & 0xFFFu) << 20;
         }
     }
     __syncthreads();
