@@ -20,6 +20,8 @@ constexpr int kPackedMaxBits = 12;           // packed 32-bit slot entry: sym|f-
 
 // Table flags
 constexpr uint32_t kTabPacked = 1u;          // packed[] valid (sb <= 12, consistent)
+constexpr uint32_t kTabEncFast = 2u;         // encf/encz valid (sb <= 12, every f <= m/2)
+constexpr int kEncFastMaxBits = 12;
 
 // Device-resident model: everything a kernel needs, in one blob so a single
 // pointer travels through the C ABI. Layout is 16-byte aligned throughout.
@@ -33,6 +35,8 @@ struct alignas(16) TableDev {
     uint32_t cum[kMaxSym + 4];        // cum[0..256]
     uint2 enc[kMaxSym];               // EncSym records {magic, (m - f) | cum << 16}
     uint2 dec[kMaxSym];               // {f, cum} for the decoder's second lookup
+    uint2 encf[kMaxSym];              // EncFast records {M, f << (32 - sb) | (m - f)}
+    uint2 encz[kMaxSym];              // {s | bias << 19, 0} (kept at the records' stride)
     uint32_t packed[1 << kPackedMaxBits];  // sym | bias << 8 | f << 20 (f < 4096)
     uint8_t slot_sym[1 << kMaxScaleBits];
 };
@@ -125,6 +129,45 @@ struct EncSym {
         divmagic(f, &magic, &l);
         (void)scale_bits;
         return make_uint2(magic, ((f - 1u) & 0xFFFFu) | (cum << 16));
+    }
+};
+
+// Fast encoder record (tables with sb <= 12 whose every f <= m / 2, flag
+// kTabEncFast): three words so that every field is used with at most one op.
+//   A.x = M = ceil(2^(31+c) / f), c = ceil(log2 f), s = c - 1
+//         (f = 1: M = 2^32 - 1, s = 0, i.e. q = x - 1, compensated in bias)
+//   A.y = Y = f << t | (m - f),  t = 32 - sb          (m - f < 2^t)
+//   Z   = s | bias << 19,  bias = cum (+ m - 1 when f = 1)  (< 2^13)
+// spill:  x >= f << t  <=>  (x | (2^t - 1)) >= Y     (the low t bits of Y
+//         hold m - f < 2^t, so they never decide the comparison)
+// push:   q = umulhi(x, M) >> s   (shf.r.wrap reads s from Z's low 5 bits)
+//         x' = x + bias + q * (m - f)   (= (x / f) * m + x % f + cum)
+// Exactness of q = floor(x / f) for every post-spill x < f * 2^t: with
+// e = M f - 2^(31+c) in [0, f), x e < f^2 2^t <= 2^(31+c) iff
+// f <= 2^(sb-1), so the rounding error x e / (f 2^(31+c)) < 1 / f never
+// crosses an integer (tests/test_host.py checks every f for sb <= 12).
+// M = 0 marks f = 0 (unencodable).
+struct EncFast {
+    __host__ __device__ static void make(uint32_t f, uint32_t cum, int sb, uint2 *a, uint32_t *z) {
+        const uint32_t m = 1u << sb, t = 32u - static_cast<uint32_t>(sb);
+        if (f == 0 || f > m / 2) {
+            *a = make_uint2(0u, 0u);
+            *z = 0u;
+            return;
+        }
+        uint32_t M, sh, bias = cum;
+        if (f == 1) {
+            M = 0xFFFFFFFFu;
+            sh = 0u;
+            bias = cum + m - 1u;
+        } else {
+            uint32_t c = 0;
+            while ((1u << c) < f) ++c;
+            M = static_cast<uint32_t>(((1ull << (31 + c)) + f - 1) / f);
+            sh = c - 1u;
+        }
+        *a = make_uint2(M, (f << t) | (m - f));
+        *z = sh | bias << 19;
     }
 };
 

@@ -104,12 +104,23 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                    uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
                    uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
     __shared__ uint2 enc[kMaxSym];
+    __shared__ uint2 encf[2 * kMaxSym];  // EncFast records, then {Z, 0} at +2 KB
     __shared__ __align__(16) uint8_t rings[kEncWarps][kInRing];
     __shared__ __align__(16) uint16_t oring_raw[kEncWarps * kOutRing + kOutRing];
-    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
+    const bool fast = (tab->flags & kTabEncFast) != 0u;
+    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) {
+        enc[i] = tab->enc[i];
+        encf[i] = tab->encf[i];
+        encf[kMaxSym + i] = tab->encz[i];
+    }
     __syncthreads();
     const EncCtx ctx(tab->scale_bits);
+    const uint32_t lowm = ~0u >> tab->scale_bits;  // 2^(32 - sb) - 1
     const int lane = threadIdx.x & 31;
+    // popc(mk & lanemask_lt) == popc(mk * 2^(32 - lane)) (FMA pipe, not ALU)
+    const uint32_t lt_mul = lane ? 1u << (32 - lane) : 0u;
+    uint32_t two;  // opaque 2: keeps the cursor arithmetic as IMADs
+    asm volatile("mov.u32 %0, 2;" : "=r"(two));
     const int wib = threadIdx.x >> 5;
     uint8_t *ring = rings[wib];
     const uint32_t oraw = smem_addr(oring_raw);
@@ -196,6 +207,27 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             uint32_t zero_f = 0;
             uint32_t topb = static_cast<uint32_t>(top) << 1;  // ring byte cursor
             const uint32_t topb0 = topb;
+            if (fast) {
+                uint32_t macc = ~0u;  // AND of the records' M: bit 31 clears on f = 0
+#pragma unroll
+                for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
+                    const uint32_t sym = blk[gg * 32 + lane];
+                    const uint2 a = encf[sym];
+                    const uint32_t z = encf[kMaxSym + sym].x;
+                    macc &= a.x;
+                    const bool spill = (x | lowm) >= a.y;
+                    const uint32_t mk = __ballot_sync(0xffffffffu, spill);
+                    topb -= two * __popc(mk);
+                    if (spill)
+                        sts16(oring_addr | ((topb + two * __popc(mk * lt_mul)) & (kOutRingBytes - 2)),
+                              x);
+                    x = spill ? x >> 16 : x;
+                    uint32_t q = __umulhi(x, a.x);
+                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
+                    x = q * (a.y & lowm) + (x + (z >> 19));
+                }
+                zero_f = macc >> 31 ^ 1u;
+            } else {
 #pragma unroll
             for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
                 const uint2 e = enc[blk[gg * 32 + lane]];
@@ -208,6 +240,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                           x);
                 x = spill ? x >> 16 : x;
                 x = enc_push(ctx, x, e);
+            }
             }
             top -= static_cast<Idx>((topb0 - topb) >> 1);
             if (__ballot_sync(0xffffffffu, zero_f)) {  // rare: locate the highest bad index

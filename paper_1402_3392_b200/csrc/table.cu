@@ -219,7 +219,14 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         t->freq[tid] = f;
         t->enc[tid] = EncSym::make(f, cum[tid], scale_bits);
         t->dec[tid] = make_uint2(f, cum[tid]);
+        uint2 a;
+        uint32_t z;
+        EncFast::make(f, cum[tid], scale_bits, &a, &z);
+        t->encf[tid] = a;
+        t->encz[tid] = make_uint2(z, 0u);
     }
+    // fast encoder records: sb <= 12 and no symbol above half the range
+    const int fast_ok = scale_bits <= kEncFastMaxBits && freq[tid] <= (m >> 1) ? 1 : 0;
     if (tid == 0) t->cum[kMaxSym] = cum[kMaxSym];
     t->cum[tid] = cum[tid];
     // slot -> symbol; consistent (packable) check for the sb <= 12 LUT.
@@ -257,7 +264,8 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
     }
     __syncthreads();
     const int all_ok = -block_max_256(-ok, red);  // min over threads
-    if (tid == 0) t->flags = all_ok ? kTabPacked : 0u;
+    const int all_fast = -block_max_256(-fast_ok, red);
+    if (tid == 0) t->flags = (all_ok ? kTabPacked : 0u) | (all_fast ? kTabEncFast : 0u);
 }
 
 // mode: counts != nullptr -> quantize(counts) first (alphabet = max+1).

@@ -194,6 +194,48 @@ def test_unencodable_symbol():
         B.encode_interleaved_u16(np.array([0, 1], np.uint8), [4, 0], [0, 4, 4], 2, 1)
 
 
+@pytest.mark.parametrize("sb", [2, 8, 12])
+def test_fast_encoder_record_edges(sb):
+    """Tables at the edge of the fast encoder record (common.cuh EncFast:
+    sb <= 12, every f <= m/2): f = m/2 exactly and f = 1 symbols take it,
+    f = m/2 + 1 falls back to the 33-bit magic; both match the oracle on
+    N = 32 streams long enough for the unrolled batches."""
+    from paper_1402_3392_b200.chunked import decode_chunked, encode_chunked
+
+    m = 1 << sb
+    rng = np.random.default_rng(100 + sb)
+    tables = [[m // 2, m // 2], [m // 2 + 1, m // 2 - 1] if m > 2 else [1, 1]]
+    if m >= 8:
+        k = min(m // 2 - 1, 200)                           # many f = 1 symbols
+        tables.append([1] * k + [m // 2, m // 2 - k])
+        tables.append([1] * k + [m - k])
+    for freq in tables:
+        t = SymbolTable(freq, sb)
+        msg = random_message(rng, t, 70_001)
+        payload, states = B.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, 32)
+        ref_p, ref_s = oracle.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, 32)
+        assert np.array_equal(payload, ref_p) and np.array_equal(states, ref_s), freq
+        cc = encode_chunked(msg, t, 32, 4096)
+        ref_p, _, ref_s = oracle.encode_chunks_u16(msg, 4096, t.freq_u32, t.cum_u32, sb, 32)
+        assert np.array_equal(cc.payload, ref_p) and np.array_equal(cc.states, ref_s), freq
+        assert np.array_equal(decode_chunked(cc), msg)
+
+
+def test_unencodable_symbol_in_fast_batches():
+    """Zero-frequency symbols deep inside the unrolled fast path: the error
+    names the symbol at the highest offending index (the reference's
+    backward walk meets it first, _core.pyx:33-34)."""
+    t = SymbolTable([2048, 2047, 0, 0, 1], 12)
+    msg = np.zeros(70_000, dtype=np.uint8)
+    msg[100], msg[60_000] = 2, 3
+    with pytest.raises(UnencodableSymbolError, match="symbol 3"):
+        ilb.encode_interleaved(msg, t, 32, WORD16)
+    msg[60_000] = 1
+    msg[40_000] = 2
+    with pytest.raises(UnencodableSymbolError, match="symbol 2"):
+        ilb.encode_interleaved(msg, t, 32, WORD16)
+
+
 def test_trailing_garbage_warns():
     t = SymbolTable([1, 3], 2)
     c = ilb.encode_interleaved([1, 0, 1, 1, 0] * 20, t, 1, WORD16)

@@ -192,6 +192,46 @@ def test_division_magic_exhaustive_divisors():
         assert np.array_equal(q, n // d)
 
 
+def _encfast(f, cum, sb):
+    """common.cuh EncFast::make, restated."""
+    m = 1 << sb
+    if f == 1:
+        return (1 << 32) - 1, 0, cum + m - 1
+    c = (f - 1).bit_length()
+    return -(-(1 << (31 + c)) // f), c - 1, cum
+
+
+def test_fast_encoder_record_exact():
+    """The fast encoder record (common.cuh EncFast, tables with sb <= 12 and
+    every f <= m/2): q = umulhi(x, M) >> s equals x // f (x - 1 for f = 1)
+    on every post-spill numerator x < f << (32 - sb) -- edges, the top of
+    the range, multiples - 1 and random x, for every f and sb -- and the
+    push x + bias + q (m - f) and the spill test (x | (2^t - 1)) >= Y agree
+    with the reference formulas (_core.pyx:36-41)."""
+    rng = np.random.default_rng(1)
+    u = np.uint64
+    for sb in range(1, 13):
+        m, t = 1 << sb, 32 - sb
+        for f in range(1, max(1, m // 2) + 1):
+            cum = (m - f) // 2  # any cum in [0, m - f]
+            M, s, bias = _encfast(f, cum, sb)
+            assert (1 << 31) <= M < (1 << 32) and 0 <= s < 32 and bias < (1 << 13)
+            X = f << t
+            k = np.arange(1, 400, dtype=np.uint64) * u(f) - u(1)
+            xs = np.concatenate([np.arange(max(1, X - 600), X, dtype=np.uint64), k[k < u(X)],
+                                 rng.integers(1, X, 600, dtype=np.uint64),
+                                 np.array([1, 65536], dtype=np.uint64)])
+            xs = xs[(xs >= u(1)) & (xs < u(X))]
+            q = ((xs * u(M)) >> u(32)) >> u(s)
+            assert np.array_equal(q, xs - u(1) if f == 1 else xs // u(f)), (sb, f)
+            x2 = (xs + u(bias) + q * u(m - f)) & u(0xFFFFFFFF)
+            assert np.array_equal(x2, (xs // u(f)) * u(m) + xs % u(f) + u(cum)), (sb, f)
+            Y = (f << t) | (m - f)
+            xx = np.concatenate([np.arange(max(0, X - 3000), min(1 << 32, X + 3000), dtype=np.uint64),
+                                 rng.integers(0, 1 << 32, 300, dtype=np.uint64)])
+            assert np.array_equal((xx | u((1 << t) - 1)) >= u(Y), xx >= u(X)), (sb, f)
+
+
 def test_synth_host_deterministic_and_zipf():
     a = synth.synth_host(1 << 16, 1.1, seed=7)
     b = synth.synth_host(1 << 16, 1.1, seed=7)
