@@ -104,14 +104,15 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                    uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
                    uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
     __shared__ uint2 enc[kMaxSym];
-    __shared__ uint2 encf[2 * kMaxSym];  // EncFast records, then {Z, 0} at +2 KB
+    __shared__ uint2 encf[kMaxSym];      // EncFast records {M, Y}
+    __shared__ uint32_t encz[kMaxSym];   // EncFast Z words (stride 4: fewer bank conflicts)
     __shared__ __align__(16) uint8_t rings[kEncWarps][kInRing];
     __shared__ __align__(16) uint16_t oring_raw[kEncWarps * kOutRing + kOutRing];
     const bool fast = (tab->flags & kTabEncFast) != 0u;
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) {
         enc[i] = tab->enc[i];
         encf[i] = tab->encf[i];
-        encf[kMaxSym + i] = tab->encz[i];
+        encz[i] = tab->encz[i].x;
     }
     __syncthreads();
     const EncCtx ctx(tab->scale_bits);
@@ -209,11 +210,22 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             const uint32_t topb0 = topb;
             if (fast) {
                 uint32_t macc = ~0u;  // AND of the records' M: bit 31 clears on f = 0
+                // Records are loaded one group ahead of their use: the spill
+                // stores go to shared memory too, so the compiler cannot
+                // hoist a later group's loads above them by itself.
+                uint32_t sym_n = blk[(kInSeg / 32 - 1) * 32 + lane];
+                uint2 a_n = encf[sym_n];
+                uint32_t z_n = encz[sym_n];
+                sym_n = blk[(kInSeg / 32 - 2) * 32 + lane];
 #pragma unroll
                 for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
-                    const uint32_t sym = blk[gg * 32 + lane];
-                    const uint2 a = encf[sym];
-                    const uint32_t z = encf[kMaxSym + sym].x;
+                    const uint2 a = a_n;
+                    const uint32_t z = z_n;
+                    if (gg > 0) {
+                        a_n = encf[sym_n];
+                        z_n = encz[sym_n];
+                        if (gg > 1) sym_n = blk[(gg - 2) * 32 + lane];
+                    }
                     macc &= a.x;
                     const bool spill = (x | lowm) >= a.y;
                     const uint32_t mk = __ballot_sync(0xffffffffu, spill);
