@@ -192,6 +192,9 @@ int ilans_table_read_host(const void *d_table, int32_t *alphabet, int32_t *scale
 int ilans_dstatus_reset_dev(void *d_status, void *stream);
 /* Read a device status blob (synchronizes `stream`). */
 int ilans_dstatus_read_host(const void *d_status, void *stream, ilans_status *st);
+/* Interpret a status blob already copied to host memory (e.g. by a
+ * stream-ordered copy into pinned memory): same result as read_host. */
+int ilans_dstatus_parse(const void *h_status, ilans_status *st);
 
 /* Chunked encode. d_scratch holds n + 8 words (chunk k uses words
  * [k*C, k*C + len_k), filled from the end); d_chunk_words[k] receives the

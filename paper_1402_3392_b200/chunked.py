@@ -160,6 +160,10 @@ class DeviceCodec:
         e = lambda n, dt: torch.empty(n, dtype=dt, device=dev)  # noqa: E731
         self.table = e(int(_lib.lib.ilans_table_bytes()), torch.uint8)
         self.status = e(int(_lib.lib.ilans_dstatus_bytes()), torch.uint8)
+        # pinned landing buffer for stream-ordered status reads (a pageable
+        # read would queue behind every copy already on the copy engine)
+        self.status_host = torch.empty(int(_lib.lib.ilans_dstatus_bytes()), dtype=torch.uint8,
+                                       pin_memory=True)
         self.counts = torch.zeros(256, dtype=torch.int64, device=dev)
         self.scratch = e(max(1, self.capacity) + 8, torch.int16)
         self.payload = e(max(1, self.capacity) + 8, torch.int16)
@@ -224,6 +228,17 @@ class DeviceCodec:
     def check_status(self):
         st = _lib.Status()
         rc = _lib.lib.ilans_dstatus_read_host(self._p(self.status), self._s(), ctypes.byref(st))
+        _lib.raise_for(rc, st, "device status")
+
+    def copy_status(self, stream):
+        """Queue a copy of the device status into status_host on ``stream``."""
+        with _torch().cuda.stream(stream):
+            self.status_host.copy_(self.status, non_blocking=True)
+
+    def check_status_host(self):
+        """Raise for the status last landed by copy_status (caller synced)."""
+        st = _lib.Status()
+        rc = _lib.lib.ilans_dstatus_parse(self._p(self.status_host), ctypes.byref(st))
         _lib.raise_for(rc, st, "device status")
 
     def encode(self, d_msg, n: int, frame: bool = True):
@@ -376,26 +391,11 @@ def decode_chunked(cc: ChunkedContainer) -> np.ndarray:
     return out.cpu().numpy()
 
 
-class HostCodec:
-    """End-to-end chunked codec over pinned host buffers: the public call a
-    user makes with data in host memory. Work is split into chunk-aligned
-    batches on three streams so PCIe traffic overlaps the kernels:
+class _Slot:
+    """One in-flight round trip: device buffers, pinned host buffers and the
+    streams of one HostCodec slot."""
 
-    encode(): H2D batch b (copy stream) || histogram of batch b (compute
-      stream) -> [NCCL all-reduce] -> quantize + tables -> encode batch b
-      (compute) || pack batch b straight into the pinned host payload over
-      PCIe (output stream: the framing kernel writes mapped host memory, so
-      compaction and D2H are one pass) -> offsets + states D2H.
-    decode(): directory H2D -> per batch: payload H2D (copy) || decode
-      (compute) || decoded bytes D2H (output stream).
-    Buffers (device and pinned host) are allocated once for ``capacity``."""
-
-    def __init__(self, capacity: int, chunk_len: int = DEFAULT_CHUNK, lane_count: int = 32,
-                 scale_bits: int = 14, device=None, counts_allreduce=None,
-                 batch_bytes: int = 32 << 20):
-        torch = _torch()
-        dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
-            else torch.device(device)
+    def __init__(self, torch, dev, capacity, chunk_len, lane_count, scale_bits):
         self.s_in = torch.cuda.Stream(dev)
         self.s_comp = torch.cuda.Stream(dev)
         self.s_out = torch.cuda.Stream(dev)
@@ -409,112 +409,270 @@ class HostCodec:
         self.h_offsets = pin(k + 1, torch.int64)
         self.h_states = pin(k * lane_count, torch.int32)
         self.h_payload = pin(max(1, capacity) + 8, torch.int16)
+        self.free = None  # event: the slot's last round trip has finished on the device
+
+    def streams(self):
+        return (self.s_in, self.s_comp, self.s_out, *self.s_dec)
+
+
+class EncodeJob:
+    """An ``HostCodec.encode_async`` in flight. Its payload / offsets /
+    states are views of the slot's pinned buffers; the word offsets are
+    already on the host when the job is returned, the payload and states land
+    when ``wait()`` returns (or when a decode queued after it reads them)."""
+
+    def __init__(self, slot, n, k, words, batches, ev_states, ev_pay, ev_done, h2d, d2h):
+        self.slot, self.n, self.k, self.words = slot, n, k, words
+        self.batches, self.ev_states, self.ev_pay = batches, ev_states, ev_pay
+        self.ev_done = ev_done
+        self.h2d_bytes, self.d2h_bytes = h2d, d2h
+        N = slot.codec.lane_count
+        self.payload = slot.h_payload[:words]
+        self.offsets = slot.h_offsets[: k + 1]
+        self.states = slot.h_states[: k * N]
+
+    def wait(self):
+        """Payload and states are on the host (device errors were raised by
+        encode_async itself)."""
+        self.ev_done.synchronize()
+        return self.payload, self.offsets, self.states
+
+
+class DecodeJob:
+    def __init__(self, slot, out, ev_done, h2d, d2h):
+        self.slot, self.out, self.ev_done = slot, out, ev_done
+        self.h2d_bytes, self.d2h_bytes = h2d, d2h
+        self._checked = False
+
+    def wait(self):
+        self.ev_done.synchronize()
+        if not self._checked:
+            self.slot.codec.check_status_host()
+            self._checked = True
+        return self.out
+
+
+class HostCodec:
+    """End-to-end chunked codec over pinned host buffers: the public call a
+    user makes with data in host memory. Work is split into chunk-aligned
+    batches on per-slot streams so PCIe traffic overlaps the kernels:
+
+    encode(): H2D batch b (copy stream) || histogram of batch b (compute
+      stream) -> [NCCL all-reduce] -> quantize + tables -> one encode launch
+      -> per batch: framing (offsets + packing) -> offsets D2H; the payload
+      of batch b goes D2H as soon as its size is known on the host.
+    decode(): directory H2D -> per batch: payload H2D (copy) || decode
+      (one of four streams: a batch alone cannot fill the GPU, a chunk is one
+      warp) || decoded bytes D2H (output stream).
+
+    ``slots`` (default 2) independent buffer sets let consecutive calls
+    overlap: ``encode_async`` / ``decode_async`` return jobs, and the upload
+    of the next message runs while the previous round trip's results are
+    still coming down (PCIe is full duplex; a lone call leaves one direction
+    idle while the whole message is uploaded for the histogram). Job
+    results are views of the slot's pinned buffers, valid until the slot is
+    reused ``slots`` calls later. ``encode`` / ``decode`` are the blocking
+    forms. Buffers (device and pinned host) are allocated once for
+    ``capacity`` bytes per slot."""
+
+    def __init__(self, capacity: int, chunk_len: int = DEFAULT_CHUNK, lane_count: int = 32,
+                 scale_bits: int = 14, device=None, counts_allreduce=None,
+                 batch_bytes: int = 32 << 20, slots: int = 2):
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        _check_chunking(chunk_len, lane_count)
+        self.device = dev
+        self.capacity = int(capacity)
+        self.chunk_len, self.lane_count = int(chunk_len), int(lane_count)
+        self.slots = [_Slot(torch, dev, self.capacity, chunk_len, lane_count, scale_bits)
+                      for _ in range(max(1, int(slots)))]
+        self._next = 0
+        self._last = None  # slot of the most recent encode (its device table)
         self.counts_allreduce = counts_allreduce
         self.batch_chunks = max(1, batch_bytes // chunk_len)
         self.h2d_bytes = 0
         self.d2h_bytes = 0
+        self.trace = None
+        self._h2d_tail = None
+
+    # back-compat views of the first slot
+    @property
+    def codec(self):
+        return self.slots[0].codec
 
     def _batches(self, k: int):
         return [(a, min(k, a + self.batch_chunks)) for a in range(0, k, self.batch_chunks)]
 
-    def _event(self, stream):
+    @staticmethod
+    def _event(stream):
         e = _torch().cuda.Event()
         e.record(stream)
         return e
 
-    def encode(self, h_msg, n: int):
-        """h_msg: pinned uint8 tensor. Returns (payload, offsets, states) as
-        views of the pinned host buffers (valid until the next encode)."""
+    def _mark(self, name, stream):
+        """Timeline probe: with ``self.trace`` a list, record a timing event."""
+        if self.trace is not None:
+            e = _torch().cuda.Event(enable_timing=True)
+            e.record(stream)
+            self.trace.append((name, e))
+
+    def _take_slot(self):
         torch = _torch()
-        c = self.codec
+        slot = self.slots[self._next]
+        self._next = (self._next + 1) % len(self.slots)
+        cur = torch.cuda.current_stream(self.device)
+        for s in slot.streams():
+            s.wait_stream(cur)
+            if slot.free is not None:
+                s.wait_event(slot.free)
+        return slot
+
+    def encode_async(self, h_msg, n: int) -> EncodeJob:
+        """Queue the encode of pinned uint8 h_msg[:n]. Blocks the host only
+        until the word offsets are known (to size the payload copies)."""
+        torch = _torch()
+        if n > self.capacity:
+            raise ValueError("message larger than codec capacity")
+        slot = self._take_slot()
+        c = slot.codec
         C, N = c.chunk_len, c.lane_count
         k = n_chunks_for(n, C)
         batches = self._batches(k)
-        cur = torch.cuda.current_stream(c.device)
-        for s in (self.s_in, self.s_comp, self.s_out):
-            s.wait_stream(cur)
-        p_msg = self.d_msg.data_ptr()
+        p_msg = slot.d_msg.data_ptr()
         c.reset_status()
         # phase 1: H2D per batch, histogram as each batch lands
         _lib.check_dev(_lib.lib.ilans_counts_zero_dev(c.counts.data_ptr(), c._s()), "counts")
+        if self._h2d_tail is not None:
+            # uploads are issued in order: this message follows the previous
+            # round trip's payload upload instead of sharing the link with it
+            # (that upload is on the previous decode's critical path)
+            slot.s_in.wait_event(self._h2d_tail)
+        self._mark("enc.h2d.start", slot.s_in)
         for k0, k1 in batches:
             lo, hi = k0 * C, min(n, k1 * C)
-            with torch.cuda.stream(self.s_in):
-                self.d_msg[lo:hi].copy_(h_msg[lo:hi], non_blocking=True)
-            self.s_comp.wait_event(self._event(self.s_in))
+            with torch.cuda.stream(slot.s_in):
+                slot.d_msg[lo:hi].copy_(h_msg[lo:hi], non_blocking=True)
+            slot.s_comp.wait_event(self._event(slot.s_in))
             _lib.check_dev(_lib.lib.ilans_histogram_u8_dev(p_msg + lo, hi - lo,
                                                            c.counts.data_ptr(), c._s()), "hist")
         if self.counts_allreduce is not None:
-            with torch.cuda.stream(self.s_comp):
+            with torch.cuda.stream(slot.s_comp):
                 self.counts_allreduce(c.counts)
+        self._mark("enc.h2d.end", slot.s_in)
         c.build_table_from_counts()
+        self._mark("enc.kernel.start", slot.s_comp)
         # phase 2: one encode launch over all chunks (a chunk is one warp's
         # sequential work, so splitting it would only serialise), then per
         # batch: pack into HBM + copy its word offsets out; as soon as a
         # batch's offsets are on the host its payload D2H is issued.
         c.encode_range(p_msg, n, 0, k)
+        self._mark("enc.kernel.end", slot.s_comp)
         if k == 0:
             c.frame_range(n, 0, 0, c.payload.data_ptr())
         ev_off = []
         for k0, k1 in batches:
             c.frame_range(n, k0, k1, c.payload.data_ptr())
-            self.s_out.wait_event(self._event(self.s_comp))
-            with torch.cuda.stream(self.s_out):
-                self.h_offsets[k0 + 1: k1 + 1].copy_(c.offsets[k0 + 1: k1 + 1], non_blocking=True)
-            ev_off.append(self._event(self.s_out))
-        self.h_offsets[:1].zero_()
-        for (k0, k1), ev in zip(batches, ev_off):
+            slot.s_out.wait_event(self._event(slot.s_comp))
+            with torch.cuda.stream(slot.s_out):
+                slot.h_offsets[k0 + 1: k1 + 1].copy_(c.offsets[k0 + 1: k1 + 1],
+                                                     non_blocking=True)
+            ev_off.append(self._event(slot.s_out))
+        slot.h_offsets[:1].zero_()
+        c.copy_status(slot.s_out)  # after the last frame, so after the encode kernel
+        ev_status = self._event(slot.s_out)
+        with torch.cuda.stream(slot.s_out):
+            slot.h_states[: k * N].copy_(c.states[: k * N], non_blocking=True)
+        ev_states = self._event(slot.s_out)
+        ev_pay = []
+        for i, ((k0, k1), ev) in enumerate(zip(batches, ev_off)):
             ev.synchronize()
-            a, b = int(self.h_offsets[k0]), int(self.h_offsets[k1])
-            with torch.cuda.stream(self.s_out):
-                self.h_payload[a:b].copy_(c.payload[a:b], non_blocking=True)
-        with torch.cuda.stream(self.s_out):
-            self.h_states[: k * N].copy_(c.states[: k * N], non_blocking=True)
-        self.s_out.synchronize()
-        c.check_status()
-        words = int(self.h_offsets[k]) if k else 0
-        self.h2d_bytes = n
-        self.d2h_bytes = 8 * (k + 1) + 4 * k * N + 2 * words
-        return self.h_payload[:words], self.h_offsets[: k + 1], self.h_states[: k * N]
+            if i == len(batches) - 1:  # the encode kernel is done: report its errors now
+                ev_status.synchronize()
+                c.check_status_host()
+            a, b = int(slot.h_offsets[k0]), int(slot.h_offsets[k1])
+            with torch.cuda.stream(slot.s_out):
+                slot.h_payload[a:b].copy_(c.payload[a:b], non_blocking=True)
+            ev_pay.append(self._event(slot.s_out))
+        self._mark("enc.d2h.end", slot.s_out)
+        ev_done = self._event(slot.s_out)
+        words = int(slot.h_offsets[k]) if k else 0
+        self._last = slot
+        h2d, d2h = n, 8 * (k + 1) + 4 * k * N + 2 * words
+        self.h2d_bytes, self.d2h_bytes = h2d, d2h
+        return EncodeJob(slot, n, k, words, batches, ev_states, ev_pay, ev_done, h2d, d2h)
 
-    def decode(self, h_payload, h_offsets, h_states, n: int, h_out):
-        """Decode into pinned uint8 tensor h_out (device table = last model)."""
+    def encode(self, h_msg, n: int):
+        """h_msg: pinned uint8 tensor. Returns (payload, offsets, states) as
+        views of the pinned host buffers (valid until the slot is reused)."""
+        return self.encode_async(h_msg, n).wait()
+
+    def decode_async(self, src, h_out, n: int | None = None, h_offsets=None, h_states=None):
+        """Queue the decode into pinned uint8 h_out. ``src`` is an EncodeJob
+        of this codec (its device model; payload batches are uploaded as
+        soon as their download finished) or a pinned int16 payload with
+        ``h_offsets``, ``h_states`` and ``n`` (decoded with the model of the
+        most recent encode)."""
         torch = _torch()
-        c = self.codec
+        if isinstance(src, EncodeJob):
+            slot, job = src.slot, src
+            n, h_payload, h_offsets, h_states = src.n, src.payload, src.offsets, src.states
+            cur = torch.cuda.current_stream(self.device)
+            for s in slot.streams():
+                s.wait_stream(cur)
+        else:
+            if self._last is None:
+                raise RuntimeError("decode needs a device model: encode first")
+            slot, job, h_payload = self._last, None, src
+            cur = torch.cuda.current_stream(self.device)
+            for s in slot.streams():
+                s.wait_stream(cur)
+        c = slot.codec
         C, N = c.chunk_len, c.lane_count
         k = n_chunks_for(n, C)
         offs = h_offsets.numpy()
         words = int(offs[k]) if k else 0
-        cur = torch.cuda.current_stream(c.device)
-        for s in (self.s_in, self.s_comp, self.s_out):
-            s.wait_stream(cur)
         c.reset_status()
-        for s in self.s_dec:  # table + status reset happen on the compute stream
-            s.wait_stream(self.s_comp)
-        with torch.cuda.stream(self.s_in):
+        for s in slot.s_dec:  # table + status reset happen on the compute stream
+            s.wait_stream(slot.s_comp)
+        with torch.cuda.stream(slot.s_in):
+            if job is not None:  # the offsets are on the host already; states may not be
+                slot.s_in.wait_event(job.ev_states)
             c.offsets[: k + 1].copy_(h_offsets, non_blocking=True)
             c.states[: k * N].copy_(h_states, non_blocking=True)
         p_pay, p_off = c.payload.data_ptr(), c.offsets.data_ptr()
-        p_st, p_out = c.states.data_ptr(), self.d_out.data_ptr()
-        # batches decode concurrently on their own streams as their payload
-        # lands (one batch alone cannot fill the GPU: a chunk is one warp)
-        ev_dir = self._event(self.s_in)
-        for i, (k0, k1) in enumerate(self._batches(k)):
+        p_st, p_out = c.states.data_ptr(), slot.d_out.data_ptr()
+        ev_dir = self._event(slot.s_in)
+        self._mark("dec.h2d.start", slot.s_in)
+        batches = self._batches(k)
+        for i, (k0, k1) in enumerate(batches):
             a, b = int(offs[k0]), int(offs[k1])
-            with torch.cuda.stream(self.s_in):
+            with torch.cuda.stream(slot.s_in):
+                if job is not None:
+                    slot.s_in.wait_event(job.ev_pay[i])
                 c.payload[a:b].copy_(h_payload[a:b], non_blocking=True)
-            s_dec = self.s_dec[i % len(self.s_dec)]
-            s_dec.wait_event(self._event(self.s_in))
+            s_dec = slot.s_dec[i % len(slot.s_dec)]
+            s_dec.wait_event(self._event(slot.s_in))
             s_dec.wait_event(ev_dir)
             c.decode_range(p_out, n, k0, k1, p_pay, p_off, p_st, stream=s_dec.cuda_stream)
-            self.s_out.wait_event(self._event(s_dec))
+            slot.s_out.wait_event(self._event(s_dec))
             lo, hi = k0 * C, min(n, k1 * C)
-            with torch.cuda.stream(self.s_out):
-                h_out[lo:hi].copy_(self.d_out[lo:hi], non_blocking=True)
-        self.s_out.synchronize()
-        for s in self.s_dec:
-            self.s_comp.wait_stream(s)
-        c.check_status()
-        self.h2d_bytes = 2 * words + 8 * (k + 1) + 4 * k * N
-        self.d2h_bytes = n
-        return h_out[:n]
+            with torch.cuda.stream(slot.s_out):
+                h_out[lo:hi].copy_(slot.d_out[lo:hi], non_blocking=True)
+        self._mark("dec.h2d.end", slot.s_in)
+        self._h2d_tail = self._event(slot.s_in)
+        for s in (slot.s_in, *slot.s_dec):
+            slot.s_out.wait_stream(s)
+        self._mark("dec.d2h.end", slot.s_out)
+        c.copy_status(slot.s_out)
+        ev_done = self._event(slot.s_out)
+        slot.s_comp.wait_event(ev_done)
+        slot.free = ev_done
+        h2d, d2h = 2 * words + 8 * (k + 1) + 4 * k * N, n
+        self.h2d_bytes, self.d2h_bytes = h2d, d2h
+        return DecodeJob(slot, h_out[:n], ev_done, h2d, d2h)
+
+    def decode(self, h_payload, h_offsets, h_states, n: int, h_out):
+        """Decode into pinned uint8 tensor h_out (device model = the most
+        recent encode's)."""
+        return self.decode_async(h_payload, h_out, n, h_offsets, h_states).wait()

@@ -773,6 +773,13 @@ extern "C" int ilans_dstatus_read_host(const void *d_status, void *stream, ilans
     cudaError_t e = cudaMemcpyAsync(&h, d_status, sizeof(h), cudaMemcpyDeviceToHost, ST(stream));
     if (e == cudaSuccess) e = cudaStreamSynchronize(ST(stream));
     if (e != cudaSuccess) return st_cuda(st, e, "status readback");
+    return ilans_dstatus_parse(&h, st);
+}
+
+extern "C" int ilans_dstatus_parse(const void *h_status, ilans_status *st) {
+    st_clear(st);
+    DStatus h;
+    std::memcpy(&h, h_status, sizeof(h));
     if (h.trunc_stream != ~0ull) {
         st->stream = int64_t(h.trunc_stream);
         return st_fail(st, ILANS_ERR_TRUNCATED, "payload exhausted mid-decode (chunk %lld)",

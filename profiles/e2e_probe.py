@@ -1,5 +1,10 @@
-"""Break down the HostCodec end-to-end round trip (encode / decode wall time
-per call, batch sizes) to see where PCIe and the kernels overlap."""
+"""Timeline of the HostCodec end-to-end round trips (pipelined two deep, as
+bench.py's e2e runs them): per step, device timestamps of the message
+upload, the encode kernel, the payload download, the payload upload and the
+decoded-bytes download, relative to the first step's start.
+
+    python profiles/e2e_probe.py [batch_MiB]
+"""
 
 import json
 import sys
@@ -15,30 +20,36 @@ from paper_1402_3392_b200.synth import synth_device  # noqa: E402
 
 def main():
     n = 256 << 20
+    batch = (int(sys.argv[1]) if len(sys.argv) > 1 else 32) << 20
     dev = torch.device("cuda", 0)
     d = synth_device(n, 1.1, 1234, device=dev)
     h_msg = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     h_msg.copy_(d[:n])
-    h_out = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    res = {}
-    for batch in (8 << 20, 32 << 20, 64 << 20, 256 << 20):
-        hc = HostCodec(n, 65536, 32, 12, dev, batch_bytes=batch)
-        p, o, s = hc.encode(h_msg, n)
-        hc.decode(p, o, s, n, h_out)
-        assert torch.equal(h_out, h_msg)
-        enc, dec = [], []
-        for _ in range(3):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            p, o, s = hc.encode(h_msg, n)
-            t1 = time.perf_counter()
-            hc.decode(p, o, s, n, h_out)
-            t2 = time.perf_counter()
-            enc.append(t1 - t0)
-            dec.append(t2 - t1)
-        res[f"batch_{batch >> 20}MiB"] = {"encode_ms": 1e3 * min(enc), "decode_ms": 1e3 * min(dec),
-                                          "round_trip_GBps": n / (min(enc) + min(dec)) / 1e9}
-    print(json.dumps(res, indent=1))
+    outs = [torch.empty(n, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    hc = HostCodec(n, 65536, 32, 12, dev, batch_bytes=batch, slots=2)
+    for i in range(2):
+        hc.decode_async(hc.encode_async(h_msg, n), outs[i]).wait()
+    torch.cuda.synchronize()
+    hc.trace = []
+    t0 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    w0 = time.perf_counter()
+    pend = []
+    steps = 6
+    for i in range(steps):
+        hc._mark(f"step{i}", torch.cuda.current_stream())
+        pend.append(hc.decode_async(hc.encode_async(h_msg, n), outs[i % 2]))
+        if len(pend) == 2:
+            pend.pop(0).wait()
+    for p in pend:
+        p.wait()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    rows = [(name, round(t0.elapsed_time(e), 3)) for name, e in hc.trace]
+    print(json.dumps({"batch_MiB": batch >> 20, "GBps": n * steps / wall / 1e9,
+                      "ms_per_step": 1e3 * wall / steps}))
+    for name, t in rows:
+        print(f"{t:9.3f}  {name}")
 
 
 if __name__ == "__main__":

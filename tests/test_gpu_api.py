@@ -122,6 +122,45 @@ def test_host_codec_batched_pipeline_matches_oracle():
         assert np.array_equal(h_out.numpy(), msg)
 
 
+def test_host_codec_async_round_trips_overlap():
+    """encode_async / decode_async with two slots and three different
+    messages in flight the way bench.py pipelines them: every payload equals
+    the oracle's chunk framing under that message's own model, every decode
+    returns its own message, and slot reuse waits for the earlier round trip."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import HostCodec
+    from paper_1402_3392_b200.synth import synth_host
+
+    n, C = 3_000_017, 65536
+    hc = HostCodec(n, C, 32, 12, batch_bytes=1 << 20, slots=2)
+    msgs = [synth_host(n - 7 * i, s, seed=i) for i, s in enumerate((1.1, 1.6, 0.7))]
+    outs = [torch.zeros(n, dtype=torch.uint8, pin_memory=True) for _ in msgs]
+    pins = [torch.from_numpy(m).pin_memory() for m in msgs]
+
+    def check(i, ej):
+        pay, offs, states = ej.wait()
+        counts, alpha = oracle.histogram(msgs[i])
+        f, cum, _ = oracle.table_views(oracle.quantize(counts[:alpha], 12), 12)
+        ref_p, ref_o, ref_s = oracle.encode_chunks_u16(msgs[i], C, f, cum, 12, 32)
+        assert np.array_equal(pay.numpy().view(np.uint16), ref_p)
+        assert np.array_equal(offs.numpy().view(np.uint64), ref_o)
+        assert np.array_equal(states.numpy().view(np.uint32).reshape(-1, 32), ref_s)
+
+    jobs = []
+    for i in range(2):
+        ej = hc.encode_async(pins[i], len(msgs[i]))
+        jobs.append((ej, hc.decode_async(ej, outs[i])))
+    check(0, jobs[0][0])
+    jobs[0][1].wait()
+    ej = hc.encode_async(pins[2], len(msgs[2]))  # reuses slot 0
+    jobs.append((ej, hc.decode_async(ej, outs[2])))
+    check(1, jobs[1][0])
+    check(2, jobs[2][0])
+    for i, (_, dj) in enumerate(jobs):
+        assert np.array_equal(dj.wait().numpy(), msgs[i])
+
+
 def test_stats_counters_single_digit_property():
     rng = np.random.default_rng(3)
     stats = RenormStats()
