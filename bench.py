@@ -56,26 +56,38 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="config 4: entropy x precision sweep")
+    ap.add_argument("--stress", action="store_true",
+                    help="config 5: small chunks x many streams (framing / tail overhead)")
+    ap.add_argument("--global-mib", type=int, default=0,
+                    help="config 3: fixed global size split over the ranks (strong scaling)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     return ap.parse_args()
 
 
 def config_of(a, world):
+    if a.global_mib:
+        per = a.global_mib * MIB / world
+        name = (f"config3: {a.global_mib} MiB global synthetic Zipf(s={a.zipf_s}) bytes split "
+                f"over {world} GPU(s) (strong scaling)")
+        glob = a.global_mib * MIB
+    else:
+        per = a.mib * MIB
+        name = f"config2: {a.mib} MiB/GPU synthetic Zipf(s={a.zipf_s}) bytes"
+        glob = a.mib * MIB * world
     return {
-        "workload": f"config2: {a.mib} MiB/GPU synthetic Zipf(s={a.zipf_s}) bytes, "
-                    f"N={a.lanes} lanes word16, {a.chunk // 1024} KiB chunks, sb={a.scale_bits}, "
-                    "round trip (model build + encode + framing + decode)",
-        "bytes_per_gpu": a.mib * MIB,
-        "global_bytes": a.mib * MIB * world,
+        "workload": f"{name}, N={a.lanes} lanes word16, {a.chunk // 1024} KiB chunks, "
+                    f"sb={a.scale_bits}, round trip (model build + encode + framing + decode)",
+        "bytes_per_gpu": int(per),
+        "global_bytes": glob,
         "chunk_len": a.chunk,
         "lanes": a.lanes,
         "scale_bits": a.scale_bits,
         "zipf_s": a.zipf_s,
         "seed": a.seed,
-        "parallelism": f"chunk-sharded x{world} (weak), histogram all-reduce" if world > 1
-        else "single GPU",
-        "l2": f"inputs ({a.mib} MiB/GPU) vs the 126 MB L2: "
-              + ("larger, no flush needed" if a.mib * MIB > 126e6 else "SMALLER: L2-resident"),
+        "parallelism": f"chunk-sharded x{world} ({'strong' if a.global_mib else 'weak'}), "
+                       "histogram all-reduce" if world > 1 else "single GPU",
+        "l2": f"inputs ({per / MIB:.0f} MiB/GPU) vs the 126 MB L2: "
+              + ("larger, no flush needed" if per > 126e6 else "SMALLER: L2-resident"),
     }
 
 
@@ -250,7 +262,7 @@ def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: in
 
 
 # ---------------------------------------------------------------- b200 ---
-def e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world):
+def e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes):
     """The same round trip through the public host API (chunked.HostCodec)
     from pinned host memory: every step uploads its message, builds the
     model, encodes, downloads the framed payload, uploads it again, decodes
@@ -289,7 +301,7 @@ def e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world):
         el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        return n * world * steps / float(el.item()) / 1e9, h2d // steps, d2h // steps
+        return global_bytes * steps / float(el.item()) / 1e9, h2d // steps, d2h // steps
 
     def pipelined():
         h2d = d2h = 0
@@ -351,7 +363,9 @@ def run_b200(a):
     C, N, sb = a.chunk, a.lanes, a.scale_bits
     # weak scaling: the global message is world x mib MiB; this rank owns a
     # contiguous chunk-aligned shard of it (dist.shard_for)
-    shard = shard_for(a.mib * MIB * world, rank, world, C)
+    # (--global-mib: strong scaling, the global message is fixed, config 3)
+    global_bytes = a.global_mib * MIB if a.global_mib else a.mib * MIB * world
+    shard = shard_for(global_bytes, rank, world, C)
     n = shard.n_bytes
     k_chunks = n_chunks_for(n, C)
 
@@ -439,7 +453,7 @@ def run_b200(a):
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():  # dram bytes per launch from the committed ncu --set full capture
         t = json.loads(tf.read_text())
-        if t.get("config") == f"mib={a.mib},chunk={C},lanes={N},sb={sb}":
+        if t.get("config") == f"mib={n / MIB:g},chunk={C},lanes={N},sb={sb}":
             traffic = t
     dom = "decode" if dec_ms >= enc_ms else "encode"
     dom_ms = max(dec_ms, enc_ms)
@@ -448,14 +462,14 @@ def run_b200(a):
 
     out = {
         "metric": METRIC,
-        "value": gbs(n * world, ms_step),
+        "value": gbs(global_bytes, ms_step),
         "unit": "GB/s",
         "n_gpus": world,
         "steps": a.steps,
         "warmup": a.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if a.global_mib else "weak",
         "vs_baseline": None,
         "dtype": "u8 symbols / u32 states / u16 digits (integer)",
         "data": "synthetic (counter-based splitmix64 Zipf sampler, csrc/synth.cu)",
@@ -479,7 +493,7 @@ def run_b200(a):
     }
 
     if not a.no_e2e:
-        out["e2e"] = e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world)
+        out["e2e"] = e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes)
 
     if rank == 0 and world == 1 and not a.no_cpu:
         msg_h = d_msg[:n].cpu().numpy()
@@ -488,6 +502,8 @@ def run_b200(a):
 
     if a.sweep and rank == 0:
         out["sweep"] = sweep(a, dev)
+    if a.stress and rank == 0:
+        out["stress"] = stress(a, dev)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
@@ -534,6 +550,55 @@ def sweep(a, dev):
     return rows
 
 
+def stress(a, dev):
+    """Config 5: small-chunk stress -- chunk sizes 64 KiB down to 4 KiB over
+    the same 256 MiB (4 K .. 64 K streams) and 1 GiB of 64 KiB chunks (16 K
+    streams, several waves): encode (kernel + framing) and decode GB/s, and
+    the framing overhead (framed ICH1 bits/byte vs one stream's payload)."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import DeviceCodec, n_chunks_for
+    from paper_1402_3392_b200.synth import entropy_bits, synth_device
+
+    rows = []
+    for mib, C in ((256, 65536), (256, 16384), (256, 4096), (1024, 65536)):
+        n = mib * MIB
+        d_msg = synth_device(n, a.zipf_s, a.seed, device=dev)
+        d_out = torch.empty(n, dtype=torch.uint8, device=dev)
+        codec = DeviceCodec(n, C, a.lanes, a.scale_bits, dev)
+        codec.histogram(d_msg, n)
+        codec.build_table_from_counts()
+        codec.reset_status()
+        codec.encode(d_msg, n)
+        codec.decode(d_out, n)
+        codec.check_status()
+        assert torch.equal(d_out, d_msg[:n])
+        reps = 5
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        for _ in range(reps):
+            codec.encode(d_msg, n)
+        ev[1].record()
+        for _ in range(reps):
+            codec.decode(d_out, n)
+        ev[2].record()
+        torch.cuda.synchronize(dev)
+        k = n_chunks_for(n, C)
+        words = int(codec.offsets[k])
+        alpha = codec.read_table().alphabet_size
+        framed = 24 + 3 + 2 * alpha + 4 * k + 4 * k * a.lanes + 2 * words
+        counts = codec.counts.cpu().numpy().astype(np.float64)
+        rows.append({"bytes": n, "chunk_len": C, "streams": k,
+                     "encode_GBps": n * reps / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9,
+                     "decode_GBps": n * reps / (ev[1].elapsed_time(ev[2]) * 1e-3) / 1e9,
+                     "framed_bits_per_byte": 8 * framed / n,
+                     "entropy_bpb": entropy_bits(counts / counts.sum()),
+                     "framing_overhead_bytes_per_chunk": (framed - 2 * words) / k})
+        del codec, d_msg, d_out
+        torch.cuda.empty_cache()
+    return rows
+
+
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -541,7 +606,7 @@ def run_reference(a):
         return
     from paper_1402_3392_b200.synth import synth_host
 
-    n = a.mib * MIB
+    n = a.global_mib * MIB // world if a.global_mib else a.mib * MIB
     cores = len(os.sched_getaffinity(0))
     per_core = 4  # MiB per core per step -> a bounded sample of the workload
     sample = min(n, cores * per_core * MIB)
