@@ -36,16 +36,19 @@ __device__ __forceinline__ void hist_red(uint32_t base_addr, uint32_t tid, uint3
                  "r"(1u << (((tid >> 5) & 1u) * 16)) : "memory");
 }
 
-// 16 bytes: per byte one PRMT (byte j -> bits 15..8, i.e. bin * 256 = the
-// bin's row offset), one add of the thread's column address, one RED.
-__device__ __forceinline__ void hist_bump16(uint32_t col_addr, uint32_t inc, uint4 v) {
+// 16 bytes: per byte one PRMT and one RED. The thread's column offset
+// (col < 256) and the bin's row offset (bin * 256) occupy different bytes of
+// the address, so one PRMT assembles col | byte_j << 8; the CTA-uniform
+// shared base is added by the RED's [R + UR] addressing.
+__device__ __forceinline__ void hist_bump16(uint32_t base_addr, uint32_t col, uint32_t inc,
+                                           uint4 v) {
     const uint32_t words[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const uint32_t row = __byte_perm(words[q], 0u, 0x4404u | (j << 4));
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(col_addr + row), "r"(inc)
+            const uint32_t off = __byte_perm(words[q], col, 0x7604u | (j << 4));
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base_addr + off), "r"(inc)
                          : "memory");
         }
     }
@@ -90,7 +93,7 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
     }
 
     unsigned long long acc[2] = {0, 0};
-    const uint32_t col_addr = base_addr + 4u * hist_word(0, tid);
+    const uint32_t col = 4u * hist_word(0, tid);  // < 256: byte 0 of the offset
     const uint32_t inc = 1u << (((tid >> 5) & 1u) * 16);
     const uint4 *vec = reinterpret_cast<const uint4 *>(msg + head);
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kHistThreads;
@@ -107,7 +110,7 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
             }
 #pragma unroll
             for (int r = 0; r < kHistBatch; ++r)
-                if (j0 + r * stride < round_end) hist_bump16(col_addr, inc, v[r]);
+                if (j0 + r * stride < round_end) hist_bump16(base_addr, col, inc, v[r]);
         }
         __syncthreads();
         hist_flush(hist_smem, tid, acc);
