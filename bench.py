@@ -486,11 +486,23 @@ def run_b200(a):
                   "framed_bytes": framed, "payload_words": total_words},
         "roofline": {"bound": "hbm", "kernel": f"{dom}_warp_kernel", "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": (traffic or {}).get(dom), "algorithmic_bytes": dom_bytes,
-                     "peak_source": peak_src},
+                     "traffic": ((traffic or {}).get("dram_bytes") or {}).get(dom),
+                     "algorithmic_bytes": dom_bytes, "peak_source": peak_src},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    # the bound that actually binds the coders: shared-memory wavefronts (the
+    # random-address table lookups) -- ncu's per-launch wavefront count over
+    # this run's kernel time, against one wavefront per SM per clock
+    wf = ((traffic or {}).get("smem_wavefronts") or {}).get(dom)
+    sm_mhz = out["clocks"].get("sm_mhz") or 1965.0
+    if wf:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        per_clk = wf / (sms * dom_ms * 1e-3 * sm_mhz * 1e6)
+        out["roofline"]["smem"] = {"wavefronts_per_launch": wf, "achieved_per_sm_clk": per_clk,
+                                   "peak_per_sm_clk": 1.0, "frac": per_clk,
+                                   "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum "
+                                             "(profiles/ncu_traffic.json) / live kernel time"}
 
     if not a.no_e2e:
         out["e2e"] = e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes)

@@ -28,6 +28,11 @@ KEYS = [
     ("smsp__inst_executed.sum", "warp instructions"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem ld bank conflicts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed",
+     "smem pipe % of peak"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe %"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
@@ -77,9 +82,11 @@ def main(rep: str, launches: str, tag: str, config: str = "mib=256,chunk=65536,l
         lines.append("")
         rd = to_bytes(r[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
         wr = to_bytes(r[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
+        wf = float(r[col["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]])
         for key in ("decode", "encode", "histogram", "compact"):
             if key in short:
-                traffic[key] = rd + wr
+                traffic.setdefault("dram_bytes", {})[key] = rd + wr
+                traffic.setdefault("smem_wavefronts", {})[key] = wf
     (HERE / f"{tag}_kernels.md").write_text("\n".join(lines) + "\n")
     traffic["config"] = config  # bench.py uses these bytes only for the same workload
     (HERE / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
