@@ -228,6 +228,22 @@ int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t *d_word_of
                             uint64_t *d_consumed, uint32_t *d_final_states, void *d_status,
                             void *stream);
 
+/* Decode fused with a consumer: the same chunked decode,
+ * but the decoded bytes are consumed in registers instead of written to
+ * HBM -- here by a zlib-compatible Adler-32 per chunk, d_adler[k] =
+ * adler32(chunk k) (after the whole chunk, or after its decoded prefix when
+ * the chunk is truncated, which is also recorded in the status). */
+int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload, const uint64_t *d_word_offsets,
+                                    const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                    int32_t n_lanes, const void *d_table, int32_t scale_bits,
+                                    uint32_t *d_adler, uint64_t *d_consumed, void *d_status,
+                                    void *stream);
+
+/* Per-chunk Adler-32 of bytes already on the device (the unfused
+ * consumer, and a device-side integrity check of raw data). */
+int ilans_adler32_chunks_dev(const uint8_t *d_data, int64_t n, int64_t chunk_len,
+                             uint32_t *d_adler, void *stream);
+
 /* Deterministic synthetic source used by the benches: byte i is
  * the inverse-CDF of a counter-based hash, u = splitmix64(seed ^ i) >> 32,
  * against d_cdf[256] (u32, non-decreasing, last entry is treated as 2^32).

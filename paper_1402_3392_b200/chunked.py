@@ -310,6 +310,33 @@ class DeviceCodec:
             self._p(self.consumed), self._p(self.final_states) if final_states else None,
             self._p(self.status), self._s()), "decode")
 
+    def decode_adler32(self, n: int, adler=None, payload=None, offsets=None, states=None):
+        """Decode fused with its consumer: the zlib Adler-32
+        of every decoded chunk (uint32 per chunk, as int32 tensor), computed
+        in registers -- the decoded bytes never reach HBM."""
+        torch = _torch()
+        k = n_chunks_for(n, self.chunk_len)
+        if adler is None:
+            adler = torch.empty(max(1, k), dtype=torch.int32, device=self.device)
+        payload = self.payload if payload is None else payload
+        offsets = self.offsets if offsets is None else offsets
+        states = self.states if states is None else states
+        _lib.check_dev(_lib.lib.ilans_decode_chunks_adler32_dev(
+            self._p(payload), self._p(offsets), self._p(states), int(n), self.chunk_len,
+            self.lane_count, self._p(self.table), self.scale_bits, self._p(adler),
+            self._p(self.consumed), self._p(self.status), self._s()), "decode_adler32")
+        return adler[:k]
+
+    def adler32(self, d_data, n: int, adler=None):
+        """Per-chunk Adler-32 of n bytes already on the device (unfused)."""
+        torch = _torch()
+        k = n_chunks_for(n, self.chunk_len)
+        if adler is None:
+            adler = torch.empty(max(1, k), dtype=torch.int32, device=self.device)
+        _lib.check_dev(_lib.lib.ilans_adler32_chunks_dev(
+            self._p(d_data), int(n), self.chunk_len, self._p(adler), self._s()), "adler32")
+        return adler[:k]
+
     # -- read-back --------------------------------------------------------
     def encoded_host(self, n: int, table: SymbolTable) -> ChunkedContainer:
         torch = _torch()

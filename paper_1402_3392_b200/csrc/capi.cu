@@ -834,6 +834,33 @@ extern "C" int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t
                          ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
 }
 
+extern "C" int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload,
+                                               const uint64_t *d_word_offsets,
+                                               const uint32_t *d_states, int64_t n,
+                                               int64_t chunk_len, int32_t n_lanes,
+                                               const void *d_table, int32_t scale_bits,
+                                               uint32_t *d_adler, uint64_t *d_consumed,
+                                               void *d_status, void *stream) {
+    if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits) return ILANS_ERR_VALUE;
+    if (reinterpret_cast<uintptr_t>(d_payload) & 15) return ILANS_ERR_VALUE;
+    return launch_decode_adler32(d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes,
+                                 static_cast<const TableDev *>(d_table), scale_bits, d_adler,
+                                 d_consumed, static_cast<DStatus *>(d_status), ST(stream)) ==
+                   cudaSuccess
+               ? ILANS_OK
+               : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_adler32_chunks_dev(const uint8_t *d_data, int64_t n, int64_t chunk_len,
+                                        uint32_t *d_adler, void *stream) {
+    if (chunk_len <= 0 || (chunk_len & 15) || (reinterpret_cast<uintptr_t>(d_data) & 15))
+        return ILANS_ERR_VALUE;
+    return launch_adler32_chunks(d_data, n, chunk_len, d_adler, ST(stream)) == cudaSuccess
+               ? ILANS_OK
+               : ILANS_ERR_CUDA;
+}
+
 extern "C" int ilans_synth_bytes_dev(uint8_t *d_out, int64_t n, uint64_t seed,
                                      int64_t first_index, const uint32_t *d_cdf, void *stream) {
     if (reinterpret_cast<uintptr_t>(d_out) & 15) return ILANS_ERR_VALUE;

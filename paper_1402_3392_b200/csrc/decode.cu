@@ -109,18 +109,98 @@ struct Lut {
     }
 };
 
+// ---------------------------------------------------------------------------
+// Sinks: what happens to the decoded bytes (decode fused into
+// its consumer). The decoder stages each 32-symbol group in a per-warp
+// shared buffer and hands complete blocks to the sink -- 512 bytes per
+// fast-path batch, 256-byte halves and a final partial block on the generic
+// path -- always at chunk positions that are multiples of the block size.
+// StoreSink writes them to HBM (the plain decoder); any other sink consumes
+// them in registers and the decoded bytes never reach HBM.
+// ---------------------------------------------------------------------------
+struct StoreSink {
+    uint8_t *out;
+    uint8_t *out_k;
+    __device__ __forceinline__ void begin(int64_t, int64_t cbase, int) { out_k = out + cbase; }
+    __device__ __forceinline__ void block512(const uint8_t *buf, int64_t pos, int lane) {
+        reinterpret_cast<uint4 *>(out_k + pos)[lane] = reinterpret_cast<const uint4 *>(buf)[lane];
+    }
+    __device__ __forceinline__ void block256(const uint8_t *buf, int64_t pos, int lane) {
+        reinterpret_cast<uint2 *>(out_k + pos)[lane] = reinterpret_cast<const uint2 *>(buf)[lane];
+    }
+    __device__ __forceinline__ void tail(const uint8_t *buf, int64_t pos, int64_t end, int lane) {
+        for (int64_t i = pos + lane; i < end; i += 32) out_k[i] = buf[i - pos];
+    }
+    __device__ __forceinline__ void end(int64_t, int64_t, int) {}
+};
+
+// zlib-compatible Adler-32 of every decoded chunk (one u32 per chunk), e.g.
+// to verify a stream on the device without materialising it. With bytes
+// b_0..b_{n-1}: A = 1 + S, B = n + n S - sum(i b_i) (mod 65521), S = sum(b_i);
+// each lane sums its bytes and their positions (dp4a: 4 bytes per op), the
+// warp reduces once per chunk.
+struct Adler32Sink {
+    uint32_t *adler;
+    unsigned long long s1, si;  // per-lane partial sums (exact: < 2^40 per chunk)
+    __device__ __forceinline__ void begin(int64_t, int64_t, int) { s1 = si = 0; }
+    __device__ __forceinline__ void words(const uint32_t *w, int nw, int64_t pos0) {
+        uint32_t t1 = 0, tj = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (q < nw) {
+                const uint32_t b = static_cast<uint32_t>(__dp4a(w[q], 0x01010101u, 0u));
+                t1 += b;
+                tj += static_cast<uint32_t>(__dp4a(w[q], 0x03020100u, 0u)) + 4u * q * b;
+            }
+        }
+        s1 += t1;
+        si += static_cast<unsigned long long>(pos0) * t1 + tj;
+    }
+    __device__ __forceinline__ void block512(const uint8_t *buf, int64_t pos, int lane) {
+        const uint4 o = reinterpret_cast<const uint4 *>(buf)[lane];
+        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+        words(w, 4, pos + 16 * lane);
+    }
+    __device__ __forceinline__ void block256(const uint8_t *buf, int64_t pos, int lane) {
+        const uint2 o = reinterpret_cast<const uint2 *>(buf)[lane];
+        const uint32_t w[4] = {o.x, o.y, 0u, 0u};
+        words(w, 2, pos + 8 * lane);
+    }
+    __device__ __forceinline__ void tail(const uint8_t *buf, int64_t pos, int64_t end, int lane) {
+        for (int64_t i = pos + lane; i < end; i += 32) {
+            const uint32_t b = buf[i - pos];
+            s1 += b;
+            si += static_cast<unsigned long long>(i) * b;
+        }
+    }
+    __device__ __forceinline__ void end(int64_t k, int64_t len, int lane) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            si += __shfl_xor_sync(0xffffffffu, si, o);
+        }
+        if (lane == 0) {
+            constexpr unsigned long long P = 65521ull;
+            const unsigned long long n = static_cast<unsigned long long>(len);
+            const unsigned long long a = (1ull + s1) % P;
+            const unsigned long long b = ((n % P) * a + P - si % P) % P;  // n(1+S) - SI
+            adler[k] = static_cast<uint32_t>(b << 16 | a);
+        }
+    }
+};
+
 // Shared memory per CTA: [align pad][W rings x 2 KB][W obufs x 512 B][LUT].
 __host__ __device__ constexpr size_t decode_warp_smem() { return kRingAllocBytes + kObufBytes; }
 
 // Not inlined: with both LUT forms inlined into one kernel the packed
 // path's schedule degrades (~8% slower decode, measured); as a call each
 // body keeps its own register allocation.
-template <bool PACKED>
+template <bool PACKED, class Sink>
 __device__ __noinline__ void
 decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                  const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
                  int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
-                 uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
+                 Sink sink, uint64_t *__restrict__ consumed,
                  uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
                  DecodeTrace trace, uint8_t *smem, int sb) {
     const uint32_t m = 1u << sb;
@@ -186,7 +266,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
         uint64_t cur = 0;            // ring segment holding the read cursor
         uint64_t v = delta;          // read cursor in words from src.g
         uint32_t x = lane < n_lanes ? states[k * n_lanes + lane] : 0u;
-        uint8_t *out_k = out + cbase;
+        sink.begin(k, cbase, lane);
         int64_t base = 0;
 
         if (n_lanes == 32 && !trace.states) {
@@ -219,8 +299,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                 }
                 vb = vb0 + (a - a0);
                 __syncwarp();
-                const uint4 o = reinterpret_cast<const uint4 *>(obuf)[lane];
-                reinterpret_cast<uint4 *>(out_k + b * (32 * kBatch))[lane] = o;
+                sink.block512(obuf, b * (32 * kBatch), lane);
                 v += (vb - vb0) >> 1;
                 const uint32_t seg = (vb >> 9) & 0x7FFFFFu;
                 if (seg != seg_cur) {  // one or two segments were finished
@@ -264,8 +343,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
             if ((nb >> 8) != (base >> 8)) {  // a 256-byte half is complete
                 __syncwarp();
                 const int64_t blk = base >> 8;
-                const uint2 o = reinterpret_cast<const uint2 *>(obuf + (blk & 1) * kObufHalf)[lane];
-                reinterpret_cast<uint2 *>(out_k + (blk << 8))[lane] = o;
+                sink.block256(obuf + (blk & 1) * kObufHalf, blk << 8, lane);
                 __syncwarp();
             }
             const uint64_t seg = v / kSegWords;
@@ -285,7 +363,8 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
             __syncwarp();
             const int64_t tail0 = (end >> 8) << 8;
             const uint8_t *half = obuf + ((end >> 8) & 1) * kObufHalf;
-            for (int64_t i = tail0 + lane; i < end; i += 32) out_k[i] = half[i - tail0];
+            sink.tail(half, tail0, end, lane);
+            sink.end(k, end, lane);
         }
         if (trace.groups && lane == 0) trace.groups[k] = (base < len ? base : len + n_lanes - 1) / n_lanes;
         if (lane == 0 && consumed) consumed[k] = v - delta;
@@ -298,12 +377,12 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
 // ALLOW_PACKED: sb <= 12 launch whose smem fits either LUT; the device
 // table's flag picks the packed entry or the two-lookup form (a
 // single-symbol sb=12 table has f = 4096, which the 12-bit field cannot hold).
-template <bool ALLOW_PACKED>
+template <bool ALLOW_PACKED, class Sink>
 __global__ void __launch_bounds__(1024)
 decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                    const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
-                   uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
+                   Sink out, uint64_t *__restrict__ consumed,
                    uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
                    int launch_sb, DecodeTrace trace) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -313,11 +392,11 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         return;
     }
     if (ALLOW_PACKED && (tab->flags & kTabPacked))
-        decode_warp_body<true>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes, tab,
-                               out, consumed, final_states, status, trace, smem, sb);
+        decode_warp_body<true, Sink>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes,
+                                     tab, out, consumed, final_states, status, trace, smem, sb);
     else
-        decode_warp_body<false>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes, tab,
-                                out, consumed, final_states, status, trace, smem, sb);
+        decode_warp_body<false, Sink>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes,
+                                      tab, out, consumed, final_states, status, trace, smem, sb);
 }
 
 // ---------------------------------------------------------------------------
@@ -431,6 +510,66 @@ static size_t decode_lut_bytes(int scale_bits, bool packed) {
     return (b + 15) & ~size_t(15);
 }
 
+// Per-chunk Adler-32 of bytes already in HBM (the unfused consumer: decode
+// to HBM, then read the bytes back). One warp per chunk, 16 bytes per lane
+// per step, the same sums as Adler32Sink.
+__global__ void __launch_bounds__(256)
+adler32_chunks_kernel(const uint8_t *__restrict__ data, int64_t n, int64_t chunk_len,
+                      int64_t n_chunks, uint32_t *__restrict__ adler) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         k < n_chunks; k += warps_total) {
+        const int64_t cbase = k * chunk_len;
+        const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+        Adler32Sink sink{adler, 0ull, 0ull};
+        const int64_t full = len >> 9;
+        for (int64_t b = 0; b < full; ++b)
+            sink.block512(data + cbase + (b << 9), b << 9, lane);  // 16-byte aligned chunks
+        sink.tail(data + cbase + (full << 9), full << 9, len, lane);
+        sink.end(k, len, lane);
+    }
+}
+
+template <class Sink>
+static cudaError_t launch_decode_warp(const uint16_t *d_payload, const uint64_t *d_word_offsets,
+                                     const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                     int n_lanes, const TableDev *d_table, int scale_bits,
+                                     bool packed, Sink sink, uint64_t *d_consumed,
+                                     uint32_t *d_final_states, DStatus *d_status,
+                                     cudaStream_t stream, DecodeTrace trace) {
+    const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
+    const bool use_packed = packed && scale_bits <= kPackedMaxBits;
+    size_t lut = decode_lut_bytes(scale_bits, false);
+    if (use_packed && decode_lut_bytes(scale_bits, true) > lut) lut = decode_lut_bytes(scale_bits, true);
+    // 4-warp CTAs spread the streams evenly over the SMs (<= 28 per SM for
+    // 4096 chunks); the per-CTA LUT copy argues for bigger CTAs only when the
+    // LUT is large (sb > 14 generic tables).
+    int warps = lut > 24 * 1024 ? 16 : 4;
+    const size_t smem_cap = 227 * 1024;
+    while (warps > 1 && lut + size_t(warps) * decode_warp_smem() > smem_cap)
+        warps >>= 1;
+    const size_t smem = lut + size_t(warps) * decode_warp_smem();
+    int64_t blocks = (n_chunks + warps - 1) / warps;
+    const int64_t max_blocks = int64_t(sm_count()) * 64;
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (use_packed) {
+        cudaFuncSetAttribute(decode_warp_kernel<true, Sink>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        decode_warp_kernel<true, Sink><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
+            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
+            sink, d_consumed, d_final_states, d_status, scale_bits, trace);
+    } else {
+        cudaFuncSetAttribute(decode_warp_kernel<false, Sink>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        decode_warp_kernel<false, Sink><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
+            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
+            sink, d_consumed, d_final_states, d_status, scale_bits, trace);
+    }
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offsets,
                           const uint32_t *d_states, int64_t n, int64_t chunk_len, int n_lanes,
                           const TableDev *d_table, int scale_bits, bool packed,
@@ -447,35 +586,35 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
         ilans_note_launch();
         return cudaGetLastError();
     }
-    const bool use_packed = packed && scale_bits <= kPackedMaxBits;
-    size_t lut = decode_lut_bytes(scale_bits, false);
-    if (use_packed && decode_lut_bytes(scale_bits, true) > lut) lut = decode_lut_bytes(scale_bits, true);
-    // 4-warp CTAs spread the streams evenly over the SMs (<= 28 per SM for
-    // 4096 chunks); the per-CTA LUT copy argues for bigger CTAs only when the
-    // LUT is large (sb > 14 generic tables).
-    int warps = lut > 24 * 1024 ? 16 : 4;
-    const size_t smem_cap = 227 * 1024;
-    while (warps > 1 && lut + size_t(warps) * decode_warp_smem() > smem_cap)
-        warps >>= 1;
-    const size_t smem = lut + size_t(warps) * decode_warp_smem();
-    int64_t blocks = (n_chunks + warps - 1) / warps;
-    const int64_t max_blocks = int64_t(sm_count()) * 64;
+    return launch_decode_warp(d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table,
+                              scale_bits, packed, StoreSink{d_out, nullptr}, d_consumed,
+                              d_final_states, d_status, stream, trace);
+}
+
+cudaError_t launch_adler32_chunks(const uint8_t *d_data, int64_t n, int64_t chunk_len,
+                                  uint32_t *d_adler, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
+    int64_t blocks = (n_chunks + 7) / 8;
+    const int64_t max_blocks = int64_t(sm_count()) * 16;
     if (blocks > max_blocks) blocks = max_blocks;
-    if (use_packed) {
-        cudaFuncSetAttribute(decode_warp_kernel<true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        decode_warp_kernel<true><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
-            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
-            d_out, d_consumed, d_final_states, d_status, scale_bits, trace);
-    } else {
-        cudaFuncSetAttribute(decode_warp_kernel<false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        decode_warp_kernel<false><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
-            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
-            d_out, d_consumed, d_final_states, d_status, scale_bits, trace);
-    }
+    adler32_chunks_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(d_data, n, chunk_len,
+                                                                              n_chunks, d_adler);
     ilans_note_launch();
     return cudaGetLastError();
+}
+
+cudaError_t launch_decode_adler32(const uint16_t *d_payload, const uint64_t *d_word_offsets,
+                                  const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                  int n_lanes, const TableDev *d_table, int scale_bits,
+                                  uint32_t *d_adler, uint64_t *d_consumed, DStatus *d_status,
+                                  cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    if (n_lanes > 32) return cudaErrorInvalidValue;
+    return launch_decode_warp(d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table,
+                              scale_bits, scale_bits <= kPackedMaxBits,
+                              Adler32Sink{d_adler, 0ull, 0ull}, d_consumed, nullptr, d_status,
+                              stream, DecodeTrace{nullptr, nullptr, nullptr});
 }
 
 }  // namespace ilans

@@ -367,3 +367,38 @@ def test_chunked_skewed_tables_both_lut_forms(sb):
         assert np.array_equal(decode_chunked(cc), msg)
         c = ilb.encode_interleaved(msg, t, 32, WORD16)
         assert np.array_equal(ilb.decode_interleaved(c), msg)
+
+
+@pytest.mark.parametrize("n, C, lanes, sb, zipf", [
+    (3_000_017, 65536, 32, 12, 1.1),    # packed LUT, fast batches, partial last chunk
+    (1_000_003, 16384, 7, 12, 1.4),     # generic per-group loop (N < 32)
+    (700_001, 4096, 32, 14, 0.8),       # two-lookup LUT (sb > 12)
+    (300, 1024, 32, 11, 1.1),           # one partial chunk: tail only
+])
+def test_decode_fused_adler32_matches_zlib(n, C, lanes, sb, zipf):
+    """Decode fused with its consumer: the per-chunk Adler-32
+    computed in registers by the decoder equals zlib.adler32 of each chunk
+    of the original message, and the stream is consumed exactly."""
+    import zlib
+
+    import torch
+
+    from paper_1402_3392_b200.chunked import DeviceCodec, n_chunks_for
+    from paper_1402_3392_b200.synth import synth_host
+
+    msg = synth_host(n, zipf, seed=n)
+    dev = torch.device("cuda", 0)
+    codec = DeviceCodec(n, C, lanes, sb, dev)
+    d_msg = torch.from_numpy(msg).to(dev)
+    codec.histogram(d_msg, n)
+    codec.build_table_from_counts()
+    codec.reset_status()
+    codec.encode(d_msg, n)
+    adler = codec.decode_adler32(n).cpu().numpy().view(np.uint32)
+    codec.check_status()
+    k = n_chunks_for(n, C)
+    want = [zlib.adler32(msg[i * C:(i + 1) * C].tobytes()) for i in range(k)]
+    assert adler.tolist() == want
+    assert codec.adler32(d_msg, n).cpu().numpy().view(np.uint32).tolist() == want
+    offs = codec.offsets[: k + 1].cpu().numpy()
+    assert np.array_equal(codec.consumed[:k].cpu().numpy(), offs[1:] - offs[:-1])
