@@ -123,10 +123,14 @@ struct StoreSink {
     uint8_t *out_k;
     __device__ __forceinline__ void begin(int64_t, int64_t cbase, int) { out_k = out + cbase; }
     __device__ __forceinline__ void block512(const uint8_t *buf, int64_t pos, int lane) {
-        reinterpret_cast<uint4 *>(out_k + pos)[lane] = reinterpret_cast<const uint4 *>(buf)[lane];
+        const uint4 o = reinterpret_cast<const uint4 *>(buf)[lane];
+        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(out_k + pos + 16 * lane),
+                     "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w) : "memory");
     }
     __device__ __forceinline__ void block256(const uint8_t *buf, int64_t pos, int lane) {
-        reinterpret_cast<uint2 *>(out_k + pos)[lane] = reinterpret_cast<const uint2 *>(buf)[lane];
+        const uint2 o = reinterpret_cast<const uint2 *>(buf)[lane];
+        asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(out_k + pos + 8 * lane), "r"(o.x),
+                     "r"(o.y) : "memory");
     }
     __device__ __forceinline__ void tail(const uint8_t *buf, int64_t pos, int64_t end, int lane) {
         for (int64_t i = pos + lane; i < end; i += 32) out_k[i] = buf[i - pos];
@@ -278,6 +282,10 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
             uint32_t vb = static_cast<uint32_t>(v) << 1;  // byte cursor (mod 2^32)
             uint32_t seg_cur = 0;                          // vb >> 9 of the cursor
             uint32_t next_seg = 4;                         // next segment to issue
+            // segments wholly inside the payload are issued without bounds
+            // arithmetic from a running source pointer (the common case)
+            const uint64_t segs_whole = src.avail / kSegWords;
+            const uint16_t *seg_g = src.g + 4 * kSegWords + lane * 8;
             cp_async_wait<1>();
             __syncwarp();
             for (int64_t b = 0; b < full; ++b) {
@@ -305,7 +313,15 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                 if (seg != seg_cur) {  // one or two segments were finished
                     do {
                         seg_cur = (seg_cur + 1) & 0x7FFFFFu;
-                        issue_segment(ring, src, next_seg++, lane);
+                        if (next_seg < segs_whole) {
+                            uint16_t *dst = ring + (next_seg & 3u) * kSegWords + lane * 8;
+                            cp_async16(dst, seg_g, 16u);
+                            if ((next_seg & 3u) < 2u) cp_async16(dst + kRingWords, seg_g, 16u);
+                        } else {
+                            issue_segment(ring, src, next_seg, lane);
+                        }
+                        ++next_seg;
+                        seg_g += kSegWords;
                         cp_async_commit();
                     } while (seg_cur != seg);
                     cp_async_wait<1>();
