@@ -20,7 +20,7 @@ constexpr int kPackedMaxBits = 12;           // packed 32-bit slot entry: sym|f-
 
 // Table flags
 constexpr uint32_t kTabPacked = 1u;          // packed[] valid (sb <= 12, consistent)
-constexpr uint32_t kTabEncFast = 2u;         // encf/encz valid (sb <= 12, every f <= m/2)
+constexpr uint32_t kTabEncFast = 2u;         // encf valid (sb <= 12, every f <= m/2)
 constexpr int kEncFastMaxBits = 12;
 
 // Device-resident model: everything a kernel needs, in one blob so a single
@@ -35,8 +35,7 @@ struct alignas(16) TableDev {
     uint32_t cum[kMaxSym + 4];        // cum[0..256]
     uint2 enc[kMaxSym];               // EncSym records {magic, (m - f) | cum << 16}
     uint2 dec[kMaxSym];               // {f, cum} for the decoder's second lookup
-    uint2 encf[kMaxSym];              // EncFast records {M, f << (32 - sb) | (m - f)}
-    uint2 encz[kMaxSym];              // {s | bias << 19, 0} (kept at the records' stride)
+    uint2 encf[kMaxSym];              // EncFast records {M, (m - f) << t | bias << 5 | s}
     uint32_t packed[1 << kPackedMaxBits];  // sym | bias << 8 | f << 20 (f < 4096)
     uint8_t slot_sym[1 << kMaxScaleBits];
 };
@@ -133,28 +132,28 @@ struct EncSym {
 };
 
 // Fast encoder record (tables with sb <= 12 whose every f <= m / 2, flag
-// kTabEncFast): three words so that every field is used with at most one op.
-//   A.x = M = ceil(2^(31+c) / f), c = ceil(log2 f), s = c - 1
-//         (f = 1: M = 2^32 - 1, s = 0, i.e. q = x - 1, compensated in bias)
-//   A.y = Y = f << t | (m - f),  t = 32 - sb          (m - f < 2^t)
-//   Z   = s | bias << 19,  bias = cum (+ m - 1 when f = 1)  (< 2^13)
-// spill:  x >= f << t  <=>  (x | (2^t - 1)) >= Y     (the low t bits of Y
-//         hold m - f < 2^t, so they never decide the comparison)
-// push:   q = umulhi(x, M) >> s   (shf.r.wrap reads s from Z's low 5 bits)
-//         x' = x + bias + q * (m - f)   (= (x / f) * m + x % f + cum)
+// kTabEncFast): 8 bytes, one LDS.64, every field used with at most one op.
+//   .x = M = ceil(2^(31+c) / f), c = ceil(log2 f), s = c - 1
+//        (f = 1: M = 2^32 - 1, s = 0, i.e. q = x - 1, compensated in bias)
+//   .y = Z = (m - f) << t | bias << 5 | s,  t = 32 - sb,
+//        bias = cum (+ m - 1 when f = 1) < 2^13 in bits [5, t)
+// spill:  x >= f << t  <=>  (x & ~(2^t - 1)) + Z carries out of 32 bits
+//         (the bits below t never decide it; the compiler turns it into
+//         one LOP3 + one compare against Z)
+// push:   q = umulhi(x, M) >> s     (shf.r.wrap reads s from Z's low 5 bits)
+//         x' = x + bias + q (m - f)
+//            = (x + (Z >> 5)) + (m - f) (q - 2^(t-5))
+//         since Z >> 5 = (m - f) 2^(t-5) + bias: one LEA.HI, one add to q,
+//         one shift for m - f = Z >> t, one IMAD
 // Exactness of q = floor(x / f) for every post-spill x < f * 2^t: with
 // e = M f - 2^(31+c) in [0, f), x e < f^2 2^t <= 2^(31+c) iff
 // f <= 2^(sb-1), so the rounding error x e / (f 2^(31+c)) < 1 / f never
 // crosses an integer (tests/test_host.py checks every f for sb <= 12).
 // M = 0 marks f = 0 (unencodable).
 struct EncFast {
-    __host__ __device__ static void make(uint32_t f, uint32_t cum, int sb, uint2 *a, uint32_t *z) {
+    __host__ __device__ static uint2 make(uint32_t f, uint32_t cum, int sb) {
         const uint32_t m = 1u << sb, t = 32u - static_cast<uint32_t>(sb);
-        if (f == 0 || f > m / 2) {
-            *a = make_uint2(0u, 0u);
-            *z = 0u;
-            return;
-        }
+        if (f == 0 || f > m / 2) return make_uint2(0u, 0u);
         uint32_t M, sh, bias = cum;
         if (f == 1) {
             M = 0xFFFFFFFFu;
@@ -166,8 +165,7 @@ struct EncFast {
             M = static_cast<uint32_t>(((1ull << (31 + c)) + f - 1) / f);
             sh = c - 1u;
         }
-        *a = make_uint2(M, (f << t) | (m - f));
-        *z = sh | bias << 19;
+        return make_uint2(M, (m - f) << t | bias << 5 | sh);
     }
 };
 

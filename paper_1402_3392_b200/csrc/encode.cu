@@ -104,19 +104,19 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                    uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
                    uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
     __shared__ uint2 enc[kMaxSym];
-    __shared__ uint2 encf[kMaxSym];      // EncFast records {M, Y}
-    __shared__ uint32_t encz[kMaxSym];   // EncFast Z words (stride 4: fewer bank conflicts)
+    __shared__ uint2 encf[kMaxSym];      // EncFast records {M, Z}
     __shared__ __align__(16) uint8_t rings[kEncWarps][kInRing];
     __shared__ __align__(16) uint16_t oring_raw[kEncWarps * kOutRing + kOutRing];
     const bool fast = (tab->flags & kTabEncFast) != 0u;
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) {
         enc[i] = tab->enc[i];
         encf[i] = tab->encf[i];
-        encz[i] = tab->encz[i].x;
     }
     __syncthreads();
     const EncCtx ctx(tab->scale_bits);
-    const uint32_t lowm = ~0u >> tab->scale_bits;  // 2^(32 - sb) - 1
+    const uint32_t lowm = ~0u >> tab->scale_bits;  // 2^t - 1, t = 32 - sb
+    const uint32_t t_shift = 32u - tab->scale_bits;
+    const uint32_t qoff = 1u << (27u - tab->scale_bits);  // 2^(t-5) (fast record)
     const int lane = threadIdx.x & 31;
     // popc(mk & lanemask_lt) == popc(mk * 2^(32 - lane)) (FMA pipe, not ALU)
     const uint32_t lt_mul = lane ? 1u << (32 - lane) : 0u;
@@ -215,19 +215,17 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 // hoist a later group's loads above them by itself.
                 uint32_t sym_n = blk[(kInSeg / 32 - 1) * 32 + lane];
                 uint2 a_n = encf[sym_n];
-                uint32_t z_n = encz[sym_n];
                 sym_n = blk[(kInSeg / 32 - 2) * 32 + lane];
 #pragma unroll
                 for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
-                    const uint2 a = a_n;
-                    const uint32_t z = z_n;
+                    const uint2 a = a_n;  // {M, Z}
                     if (gg > 0) {
                         a_n = encf[sym_n];
-                        z_n = encz[sym_n];
                         if (gg > 1) sym_n = blk[(gg - 2) * 32 + lane];
                     }
                     macc &= a.x;
-                    const bool spill = (x | lowm) >= a.y;
+                    const uint32_t xm = x & ~lowm;
+                    const bool spill = xm + a.y < xm;  // carry out of (x & ~(2^t-1)) + Z
                     const uint32_t mk = __ballot_sync(0xffffffffu, spill);
                     topb -= two * __popc(mk);
                     if (spill)
@@ -235,8 +233,8 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                               x);
                     x = spill ? x >> 16 : x;
                     uint32_t q = __umulhi(x, a.x);
-                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
-                    x = q * (a.y & lowm) + (x + (z >> 19));
+                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
+                    x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
                 }
                 zero_f = macc >> 31 ^ 1u;
             } else {

@@ -222,11 +222,7 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         t->freq[tid] = f;
         t->enc[tid] = EncSym::make(f, cum[tid], scale_bits);
         t->dec[tid] = make_uint2(f, cum[tid]);
-        uint2 a;
-        uint32_t z;
-        EncFast::make(f, cum[tid], scale_bits, &a, &z);
-        t->encf[tid] = a;
-        t->encz[tid] = make_uint2(z, 0u);
+        t->encf[tid] = EncFast::make(f, cum[tid], scale_bits);
     }
     // fast encoder records: sb <= 12 and no symbol above half the range
     const int fast_ok = scale_bits <= kEncFastMaxBits && freq[tid] <= (m >> 1) ? 1 : 0;

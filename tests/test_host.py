@@ -206,8 +206,9 @@ def test_fast_encoder_record_exact():
     every f <= m/2): q = umulhi(x, M) >> s equals x // f (x - 1 for f = 1)
     on every post-spill numerator x < f << (32 - sb) -- edges, the top of
     the range, multiples - 1 and random x, for every f and sb -- and the
-    push x + bias + q (m - f) and the spill test (x | (2^t - 1)) >= Y agree
-    with the reference formulas (_core.pyx:36-41)."""
+    push x + bias + q (m - f) -- and its in-kernel form through the record
+    word Z -- and the carry-out spill test agree with the reference formulas
+    (_core.pyx:36-41)."""
     rng = np.random.default_rng(1)
     u = np.uint64
     for sb in range(1, 13):
@@ -226,10 +227,17 @@ def test_fast_encoder_record_exact():
             assert np.array_equal(q, xs - u(1) if f == 1 else xs // u(f)), (sb, f)
             x2 = (xs + u(bias) + q * u(m - f)) & u(0xFFFFFFFF)
             assert np.array_equal(x2, (xs // u(f)) * u(m) + xs % u(f) + u(cum)), (sb, f)
-            Y = (f << t) | (m - f)
+            # the record word Z = (m - f) << t | bias << 5 | s and the kernel's
+            # forms of the push and of the spill test (encode.cu fast loop)
+            Z = (m - f) << t | bias << 5 | s
+            assert Z < (1 << 32) and (Z & 31) == s
+            x3 = (xs + u(Z >> 5) + u(m - f) * ((q - u(1 << (t - 5))) & u(0xFFFFFFFF))) \
+                & u(0xFFFFFFFF)
+            assert np.array_equal(x3, x2), (sb, f)
             xx = np.concatenate([np.arange(max(0, X - 3000), min(1 << 32, X + 3000), dtype=np.uint64),
                                  rng.integers(0, 1 << 32, 300, dtype=np.uint64)])
-            assert np.array_equal((xx | u((1 << t) - 1)) >= u(Y), xx >= u(X)), (sb, f)
+            xm = xx & u(((1 << 32) - 1) ^ ((1 << t) - 1))
+            assert np.array_equal(xm + u(Z) >= u(1 << 32), xx >= u(X)), (sb, f)
 
 
 def test_synth_host_deterministic_and_zipf():
