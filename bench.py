@@ -523,15 +523,24 @@ def run_b200(a):
     # the bound that actually binds the coders: shared-memory wavefronts (the
     # random-address table lookups) -- ncu's per-launch wavefront count over
     # this run's kernel time, against one wavefront per SM per clock
+    # and the instruction-issue bound (one warp instruction per SMSP-clock)
     wf = ((traffic or {}).get("smem_wavefronts") or {}).get(dom)
+    wi = ((traffic or {}).get("warp_instructions") or {}).get(dom)
     sm_mhz = out["clocks"].get("sm_mhz") or 1965.0
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clks = dom_ms * 1e-3 * sm_mhz * 1e6
     if wf:
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        per_clk = wf / (sms * dom_ms * 1e-3 * sm_mhz * 1e6)
+        per_clk = wf / (sms * clks)
         out["roofline"]["smem"] = {"wavefronts_per_launch": wf, "achieved_per_sm_clk": per_clk,
                                    "peak_per_sm_clk": 1.0, "frac": per_clk,
                                    "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum "
                                              "(profiles/ncu_traffic.json) / live kernel time"}
+    if wi:
+        per_clk = wi / (4 * sms * clks)
+        out["roofline"]["issue"] = {"warp_instructions_per_launch": wi,
+                                    "achieved_per_smsp_clk": per_clk, "peak_per_smsp_clk": 1.0,
+                                    "frac": per_clk,
+                                    "source": "ncu smsp__inst_executed.sum / live kernel time"}
 
     out["fused_consumer"] = fused_consumer(codec, d_out, n, dev)
 

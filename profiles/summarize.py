@@ -83,10 +83,12 @@ def main(rep: str, launches: str, tag: str, config: str = "mib=256,chunk=65536,l
         rd = to_bytes(r[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
         wr = to_bytes(r[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
         wf = float(r[col["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]])
+        inst = float(r[col["smsp__inst_executed.sum"]])
         for key in ("decode", "encode", "histogram", "compact"):
             if key in short:
                 traffic.setdefault("dram_bytes", {})[key] = rd + wr
                 traffic.setdefault("smem_wavefronts", {})[key] = wf
+                traffic.setdefault("warp_instructions", {})[key] = inst
     (HERE / f"{tag}_kernels.md").write_text("\n".join(lines) + "\n")
     traffic["config"] = config  # bench.py uses these bytes only for the same workload
     (HERE / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
