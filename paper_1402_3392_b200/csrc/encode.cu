@@ -75,16 +75,19 @@ struct SpillStage {
         __syncwarp();
     }
 
-    // Fast-path drain: whole 256-word blocks [flushed - 256, flushed), one
-    // 16-byte store per lane, while at least 256 final words are pending
-    // (keeps pending < 256, so a 512-symbol batch cannot wrap the ring).
+    // Fast-path drain: whole 512-word blocks [flushed - 512, flushed), two
+    // 16-byte stores per lane, while at least 512 final words are pending
+    // (keeps pending < 512, so a 512-symbol batch -- at most 512 spills --
+    // cannot wrap the 1024-word ring).
     __device__ __forceinline__ void drain(Idx top, int lane) {
-        while (flushed - top >= 256) {
+        while (flushed - top >= 512) {
             __syncwarp();
-            const Idx blk = flushed - 256 + Idx(lane) * 8;
-            *reinterpret_cast<uint4 *>(out + blk) =
-                *reinterpret_cast<const uint4 *>(ring + (blk & (kOutRing - 1)));
-            flushed -= 256;
+            const Idx blk = flushed - 512 + Idx(lane) * 8;
+            const uint4 lo = *reinterpret_cast<const uint4 *>(ring + (blk & (kOutRing - 1)));
+            const uint4 hi = *reinterpret_cast<const uint4 *>(ring + ((blk + 256) & (kOutRing - 1)));
+            *reinterpret_cast<uint4 *>(out + blk) = lo;
+            *reinterpret_cast<uint4 *>(out + blk + 256) = hi;
+            flushed -= 512;
         }
     }
 
@@ -189,9 +192,13 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         // ---- N = 32 fast path: 512-byte blocks, backwards, 16 groups each ----
         // Segments cur .. cur-3 are in flight; batch b needs segment b and
         // keeps three younger ones in flight. Zero-frequency symbols are
-        // detected once per batch (f = 0 only corrupts this chunk's scratch,
-        // which is then discarded).
+        // detected once per batch (generic records) or once per chunk (fast
+        // records); f = 0 only corrupts this chunk's scratch, which is then
+        // discarded.
         Idx issued_lo = cur - 3;
+        // fast records: AND of every record's M over the whole fast region;
+        // bit 31 clears iff some symbol had f = 0 (checked once, after it)
+        uint32_t macc = ~0u;
         for (Idx b = full - 1; !bad && b >= 0; --b) {
             if (b - 3 < issued_lo) {  // segments below `full` are whole 512-byte blocks
                 __syncwarp();
@@ -209,7 +216,6 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             uint32_t topb = static_cast<uint32_t>(top) << 1;  // ring byte cursor
             const uint32_t topb0 = topb;
             if (fast) {
-                uint32_t macc = ~0u;  // AND of the records' M: bit 31 clears on f = 0
                 // Records are loaded one group ahead of their use: the spill
                 // stores go to shared memory too, so the compiler cannot
                 // hoist a later group's loads above them by itself.
@@ -236,7 +242,6 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                     asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
                     x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
                 }
-                zero_f = macc >> 31 ^ 1u;
             } else {
 #pragma unroll
             for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
@@ -253,7 +258,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             }
             }
             top -= static_cast<Idx>((topb0 - topb) >> 1);
-            if (__ballot_sync(0xffffffffu, zero_f)) {  // rare: locate the highest bad index
+            if (!fast && __ballot_sync(0xffffffffu, zero_f)) {  // rare: the highest bad index
                 for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
                     const uint32_t bm =
                         __ballot_sync(0xffffffffu, enc[blk[gg * 32 + lane]].x == 0u);
@@ -268,6 +273,22 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 bad = true;
             }
             st.drain(top, lane);
+        }
+        if (fast && !bad && __ballot_sync(0xffffffffu, (macc >> 31) == 0u)) {
+            // rare: some symbol of the fast region has f = 0 (its scratch is
+            // garbage but stayed inside the chunk: at most 32 spills per
+            // group). The highest offending index, as the reference's
+            // backward walk meets it first (_core.pyx:33-34):
+            for (Idx i0 = (full << 9) - 32; i0 >= 0; i0 -= 32) {
+                const uint32_t bm = __ballot_sync(0xffffffffu, enc[g[i0 + lane]].x == 0u);
+                if (bm) {
+                    if (lane == 0)
+                        atomicMax(&status->unenc_index,
+                                  static_cast<long long>(cbase + i0) + 31 - __clz(bm));
+                    break;
+                }
+            }
+            bad = true;
         }
         if (!bad) {
             st.finish(top, lane);
