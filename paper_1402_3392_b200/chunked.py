@@ -570,14 +570,17 @@ class HostCodec:
         c.reset_status()
         # phase 1: H2D per batch, histogram as each batch lands
         _lib.check_dev(_lib.lib.ilans_counts_zero_dev(c.counts.data_ptr(), c._s()), "counts")
-        if self._h2d_tail is not None:
-            # uploads are issued in order: this message follows the previous
-            # round trip's payload upload instead of sharing the link with it
-            # (that upload is on the previous decode's critical path)
-            slot.s_in.wait_event(self._h2d_tail)
         self._mark("enc.h2d.start", slot.s_in)
-        for k0, k1 in batches:
+        for i, (k0, k1) in enumerate(batches):
             lo, hi = k0 * C, min(n, k1 * C)
+            if i == 1 and self._h2d_tail is not None:
+                # uploads are ordered: after its first batch (which fills the
+                # link while the previous encode's first payload batch is
+                # still coming down) this message waits for the previous
+                # round trip's payload upload instead of sharing the link
+                # with it (that upload is on the previous decode's critical
+                # path)
+                slot.s_in.wait_event(self._h2d_tail)
             with torch.cuda.stream(slot.s_in):
                 slot.d_msg[lo:hi].copy_(h_msg[lo:hi], non_blocking=True)
             slot.s_comp.wait_event(self._event(slot.s_in))
