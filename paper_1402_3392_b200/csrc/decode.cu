@@ -558,16 +558,20 @@ static cudaError_t launch_decode_warp(const uint16_t *d_payload, const uint64_t 
     const bool use_packed = packed && scale_bits <= kPackedMaxBits;
     size_t lut = decode_lut_bytes(scale_bits, false);
     if (use_packed && decode_lut_bytes(scale_bits, true) > lut) lut = decode_lut_bytes(scale_bits, true);
-    // 4-warp CTAs spread the streams evenly over the SMs (<= 28 per SM for
-    // 4096 chunks); the per-CTA LUT copy argues for bigger CTAs only when the
-    // LUT is large (sb > 14 generic tables).
-    int warps = lut > 24 * 1024 ? 16 : 4;
+    // One CTA per SM with that SM's share of the streams (up to 28 warps;
+    // 4096 chunks = one wave on 148 SMs): the warp scheduler is not fair
+    // across CTAs, and co-resident CTAs finish far apart (encode.cu,
+    // kEncMaxWarps); as one CTA the SM's warps finish together.
+    const int64_t sms = sm_count();
+    int warps = static_cast<int>((n_chunks + sms - 1) / sms);
+    if (warps > 28) warps = 28;
+    if (warps < 1) warps = 1;
     const size_t smem_cap = 227 * 1024;
-    while (warps > 1 && lut + size_t(warps) * decode_warp_smem() > smem_cap)
-        warps >>= 1;
+    while (warps > 1 && lut + size_t(warps) * decode_warp_smem() > smem_cap) --warps;
     const size_t smem = lut + size_t(warps) * decode_warp_smem();
     int64_t blocks = (n_chunks + warps - 1) / warps;
-    const int64_t max_blocks = int64_t(sm_count()) * 64;
+    const int64_t per_sm = static_cast<int64_t>(smem_cap / (smem + 1024));
+    const int64_t max_blocks = sms * (per_sm < 1 ? 1 : per_sm);
     if (blocks > max_blocks) blocks = max_blocks;
     if (use_packed) {
         cudaFuncSetAttribute(decode_warp_kernel<true, Sink>,

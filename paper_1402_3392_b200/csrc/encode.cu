@@ -26,6 +26,7 @@
 
 namespace ilans {
 
+
 constexpr int kInSeg = 512;            // bytes per cp.async warp-copy
 constexpr int kInRing = 4 * kInSeg;    // 2 KB per warp
 
@@ -39,9 +40,22 @@ __device__ __forceinline__ void issue_msg_segment(uint8_t *ring, const uint8_t *
     cp_async16(ring + (static_cast<uint32_t>(seg) & 3u) * kInSeg + lane * 16, src, bytes);
 }
 
-constexpr int kEncWarps = 4;     // warps per CTA: 7 CTAs/SM hold 4096 streams in one wave
+// One CTA per SM holding all of that SM's streams (up to 28 warps: 4096
+// streams in one wave on 148 SMs). The warp scheduler is not fair across
+// CTAs: with 7 CTAs of 4 warps per SM the first warps finished at 56% of the
+// kernel time and the last at 100% (%globaltimer per warp), so each SM ran
+// its last ~40% with ever fewer warps to hide latency; as one CTA per SM the
+// same 28 warps finish together (320 -> 269 us at config 2; 2 CTAs of 14
+// warps per SM are worse than either, 365 us).
+constexpr int kEncMaxWarps = 28;
 constexpr int kOutRing = 1024;   // per-warp staging ring for spilled words (2 KB)
 constexpr uint32_t kOutRingBytes = kOutRing * 2;
+
+// dynamic shared memory: enc[256] | encf[256] | W message rings | pad | W spill rings
+__host__ __device__ constexpr size_t encode_smem_bytes(int warps) {
+    return 2 * kMaxSym * sizeof(uint2) + size_t(warps) * kInRing + kOutRingBytes +
+           size_t(warps) * kOutRingBytes;
+}
 
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<uint16_t>(v)));
@@ -101,15 +115,17 @@ struct SpillStage {
 // Idx: chunk-local index type (int for chunks < 2^30 bytes, the chunked
 // format's case; long long only for huge single-stream calls).
 template <typename Idx>
-__global__ void __launch_bounds__(kEncWarps * 32, 7)
+__global__ void __launch_bounds__(kEncMaxWarps * 32, 1)
 encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                    uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
                    uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
-    __shared__ uint2 enc[kMaxSym];
-    __shared__ uint2 encf[kMaxSym];      // EncFast records {M, Z}
-    __shared__ __align__(16) uint8_t rings[kEncWarps][kInRing];
-    __shared__ __align__(16) uint16_t oring_raw[kEncWarps * kOutRing + kOutRing];
+    extern __shared__ __align__(16) uint8_t esmem[];
+    const int nw = blockDim.x >> 5;
+    uint2 *enc = reinterpret_cast<uint2 *>(esmem);
+    uint2 *encf = enc + kMaxSym;  // EncFast records {M, Z}
+    uint8_t *rings = esmem + 2 * kMaxSym * sizeof(uint2);
+    uint16_t *oring_raw = reinterpret_cast<uint16_t *>(rings + nw * kInRing);
     const bool fast = (tab->flags & kTabEncFast) != 0u;
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) {
         enc[i] = tab->enc[i];
@@ -126,15 +142,16 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     uint32_t two;  // opaque 2: keeps the cursor arithmetic as IMADs
     asm volatile("mov.u32 %0, 2;" : "=r"(two));
     const int wib = threadIdx.x >> 5;
-    uint8_t *ring = rings[wib];
+    uint8_t *ring = rings + wib * kInRing;
     const uint32_t oraw = smem_addr(oring_raw);
     const uint32_t oalign = ((oraw + kOutRingBytes - 1) & ~(kOutRingBytes - 1)) - oraw;
     uint16_t *oring = oring_raw + oalign / 2 + wib * kOutRing;
     const uint32_t oring_addr = smem_addr(oring);
     const uint32_t lt = lanemask_lt();
-    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
 
-    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; k < n_chunks;
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nw;
+
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * nw + wib; k < n_chunks;
          k += warps_total) {
         const int64_t cbase = k * chunk_len;
         const Idx len = static_cast<Idx>((n - cbase) < chunk_len ? (n - cbase) : chunk_len);
@@ -408,18 +425,32 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
             d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states,
             d_status, d_lane_ws);
     } else {
-        int64_t blocks = (n_chunks + kEncWarps - 1) / kEncWarps;
-        const int64_t max_blocks = int64_t(sm_count()) * 64;
+        // one CTA per SM with the SM's share of the streams (<= 28 warps);
+        // more streams than 28 per SM: grid-stride over CTA-sized groups
+        const int64_t sms = sm_count();
+        int warps = static_cast<int>((n_chunks + sms - 1) / sms);
+        if (warps > kEncMaxWarps) warps = kEncMaxWarps;
+        if (warps < 1) warps = 1;
+        int64_t blocks = (n_chunks + warps - 1) / warps;
+        const int64_t per_sm = static_cast<int64_t>(
+            (227 * 1024) / (encode_smem_bytes(warps) + 1024));
+        const int64_t max_blocks = sms * (per_sm < 1 ? 1 : per_sm);
         if (blocks > max_blocks) blocks = max_blocks;
-        if (chunk_len < (int64_t(1) << 30))
-            encode_warp_kernel<int><<<static_cast<unsigned>(blocks), kEncWarps * 32, 0, stream>>>(
+        const size_t smem = encode_smem_bytes(warps);
+        if (chunk_len < (int64_t(1) << 30)) {
+            cudaFuncSetAttribute(encode_warp_kernel<int>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            encode_warp_kernel<int><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
                 d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_chunk_words,
                 d_states, d_status);
-        else
+        } else {
+            cudaFuncSetAttribute(encode_warp_kernel<long long>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             encode_warp_kernel<long long>
-                <<<static_cast<unsigned>(blocks), kEncWarps * 32, 0, stream>>>(
+                <<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
                     d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_chunk_words,
                     d_states, d_status);
+        }
     }
     ilans_note_launch();
     return cudaGetLastError();
