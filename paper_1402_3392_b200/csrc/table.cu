@@ -23,7 +23,11 @@ namespace ilans {
 // every 4095 vectors per thread (once per launch at every realistic size):
 // thread t sums bins t and t+128 over all 128 columns and zeroes them.
 // ---------------------------------------------------------------------------
-constexpr int kHistThreads = 128;
+// Three independent 128-thread counter blocks (64 KB each) per CTA, one CTA
+// per SM: the sub-block index sits in byte 2 of each thread's column
+// offset, so the PRMT that assembles the address still does all of it.
+constexpr int kHistGroups = 3;
+constexpr int kHistThreads = 128 * kHistGroups;
 constexpr int kHistBatch = 12;                // 16-byte loads in flight per thread
 constexpr int64_t kHistVecPerRound = 4088;    // <= 65535 / 16 vectors between flushes
 
@@ -72,13 +76,15 @@ __device__ __forceinline__ void hist_flush(uint32_t *h, uint32_t tid, unsigned l
     }
 }
 
-__global__ void __launch_bounds__(kHistThreads)
+__global__ void __launch_bounds__(kHistThreads, 1)
 histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
                     unsigned long long *__restrict__ counts) {
     extern __shared__ __align__(16) uint32_t hist_smem[];
-    const uint32_t tid = threadIdx.x;
+    const uint32_t gtid = threadIdx.x;
+    const uint32_t sub = gtid >> 7;   // counter block of this thread
+    const uint32_t tid = gtid & 127u;  // column within the block
     const uint32_t base_addr = smem_addr(hist_smem);
-    for (uint32_t i = tid; i < 256u * 64u; i += kHistThreads) hist_smem[i] = 0;
+    for (uint32_t i = gtid; i < 256u * 64u * kHistGroups; i += kHistThreads) hist_smem[i] = 0;
     __syncthreads();
 
     // unaligned head / tail bytes: block 0, thread 0 (its own counters)
@@ -87,17 +93,18 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
     if (head > n) head = n;
     const int64_t nvec = (n - head) >> 4;
     const int64_t tail_start = head + (nvec << 4);
-    if (blockIdx.x == 0 && tid == 0) {
+    if (blockIdx.x == 0 && gtid == 0) {
         for (int64_t i = 0; i < head; ++i) hist_red(base_addr, 0, msg[i]);
         for (int64_t i = tail_start; i < n; ++i) hist_red(base_addr, 0, msg[i]);
     }
 
     unsigned long long acc[2] = {0, 0};
-    const uint32_t col = 4u * hist_word(0, tid);  // < 256: byte 0 of the offset
+    // byte 0: column (< 256), byte 1: bin (PRMT), byte 2: counter block
+    const uint32_t col = 4u * hist_word(0, tid) | sub << 16;
     const uint32_t inc = 1u << (((tid >> 5) & 1u) * 16);
     const uint4 *vec = reinterpret_cast<const uint4 *>(msg + head);
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kHistThreads;
-    const int64_t first = static_cast<int64_t>(blockIdx.x) * kHistThreads + tid;
+    const int64_t first = static_cast<int64_t>(blockIdx.x) * kHistThreads + gtid;
     const int64_t per_round = stride * kHistVecPerRound;
     for (int64_t round_base = 0; round_base < nvec; round_base += per_round) {
         const int64_t round_end = min(nvec, round_base + per_round);
@@ -113,12 +120,12 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
                 if (j0 + r * stride < round_end) hist_bump16(base_addr, col, inc, v[r]);
         }
         __syncthreads();
-        hist_flush(hist_smem, tid, acc);
+        hist_flush(hist_smem + sub * (256u * 64u), tid, acc);
         __syncthreads();
     }
     if (nvec == 0) {  // head / tail only
         __syncthreads();
-        hist_flush(hist_smem, tid, acc);
+        hist_flush(hist_smem + sub * (256u * 64u), tid, acc);
     }
     if (acc[0]) atomicAdd(counts + tid, acc[0]);
     if (acc[1]) atomicAdd(counts + tid + 128, acc[1]);
