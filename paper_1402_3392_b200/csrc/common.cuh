@@ -20,8 +20,8 @@ constexpr int kPackedMaxBits = 12;           // packed 32-bit slot entry: sym|f-
 
 // Table flags
 constexpr uint32_t kTabPacked = 1u;          // packed[] valid (sb <= 12, consistent)
-constexpr uint32_t kTabEncFast = 2u;         // encf valid (sb <= 12, every f <= m/2)
-constexpr int kEncFastMaxBits = 12;
+constexpr uint32_t kTabEncFast = 2u;         // encf valid (sb <= 13, every f <= m/2)
+constexpr int kEncFastMaxBits = 13;             // bias < 2^(sb+1) fits Z's bits [5, 32-sb)
 
 // Device-resident model: everything a kernel needs, in one blob so a single
 // pointer travels through the C ABI. Layout is 16-byte aligned throughout.
@@ -131,12 +131,12 @@ struct EncSym {
     }
 };
 
-// Fast encoder record (tables with sb <= 12 whose every f <= m / 2, flag
+// Fast encoder record (tables with sb <= 13 whose every f <= m / 2, flag
 // kTabEncFast): 8 bytes, one LDS.64, every field used with at most one op.
 //   .x = M = ceil(2^(31+c) / f), c = ceil(log2 f), s = c - 1
 //        (f = 1: M = 2^32 - 1, s = 0, i.e. q = x - 1, compensated in bias)
 //   .y = Z = (m - f) << t | bias << 5 | s,  t = 32 - sb,
-//        bias = cum (+ m - 1 when f = 1) < 2^13 in bits [5, t)
+//        bias = cum (+ m - 1 when f = 1) < 2^(sb+1) in bits [5, t)
 // spill:  x >= f << t  <=>  (x & ~(2^t - 1)) + Z carries out of 32 bits
 //         (the bits below t never decide it; the compiler turns it into
 //         one LOP3 + one compare against Z)
@@ -148,7 +148,7 @@ struct EncSym {
 // Exactness of q = floor(x / f) for every post-spill x < f * 2^t: with
 // e = M f - 2^(31+c) in [0, f), x e < f^2 2^t <= 2^(31+c) iff
 // f <= 2^(sb-1), so the rounding error x e / (f 2^(31+c)) < 1 / f never
-// crosses an integer (tests/test_host.py checks every f for sb <= 12).
+// crosses an integer (tests/test_host.py checks every f for sb <= 13).
 // M = 0 marks f = 0 (unencodable).
 struct EncFast {
     __host__ __device__ static uint2 make(uint32_t f, uint32_t cum, int sb) {

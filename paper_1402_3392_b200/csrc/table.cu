@@ -231,7 +231,7 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         t->dec[tid] = make_uint2(f, cum[tid]);
         t->encf[tid] = EncFast::make(f, cum[tid], scale_bits);
     }
-    // fast encoder records: sb <= 12 and no symbol above half the range
+    // fast encoder records: sb <= 13 and no symbol above half the range
     const int fast_ok = scale_bits <= kEncFastMaxBits && freq[tid] <= (m >> 1) ? 1 : 0;
     if (tid == 0) t->cum[kMaxSym] = cum[kMaxSym];
     t->cum[tid] = cum[tid];

@@ -202,7 +202,7 @@ def _encfast(f, cum, sb):
 
 
 def test_fast_encoder_record_exact():
-    """The fast encoder record (common.cuh EncFast, tables with sb <= 12 and
+    """The fast encoder record (common.cuh EncFast, tables with sb <= 13 and
     every f <= m/2): q = umulhi(x, M) >> s equals x // f (x - 1 for f = 1)
     on every post-spill numerator x < f << (32 - sb) -- edges, the top of
     the range, multiples - 1 and random x, for every f and sb -- and the
@@ -211,12 +211,12 @@ def test_fast_encoder_record_exact():
     (_core.pyx:36-41)."""
     rng = np.random.default_rng(1)
     u = np.uint64
-    for sb in range(1, 13):
+    for sb in range(1, 14):
         m, t = 1 << sb, 32 - sb
         for f in range(1, max(1, m // 2) + 1):
             cum = (m - f) // 2  # any cum in [0, m - f]
             M, s, bias = _encfast(f, cum, sb)
-            assert (1 << 31) <= M < (1 << 32) and 0 <= s < 32 and bias < (1 << 13)
+            assert (1 << 31) <= M < (1 << 32) and 0 <= s < 32 and bias < (1 << (sb + 1))
             X = f << t
             k = np.arange(1, 400, dtype=np.uint64) * u(f) - u(1)
             xs = np.concatenate([np.arange(max(1, X - 600), X, dtype=np.uint64), k[k < u(X)],
