@@ -21,6 +21,9 @@ constexpr int kPackedMaxBits = 12;           // packed 32-bit slot entry: sym|f-
 // Table flags
 constexpr uint32_t kTabPacked = 1u;          // packed[] valid (sb <= 12, consistent)
 constexpr uint32_t kTabEncFast = 2u;         // encf valid (sb <= 13, every f <= m/2)
+constexpr uint32_t kTabPacked64 = 4u;        // packed64[] valid (13 <= sb <= 14)
+constexpr int kPacked64MinBits = 13;
+constexpr int kPacked64MaxBits = 14;
 constexpr int kEncFastMaxBits = 13;             // bias < 2^(sb+1) fits Z's bits [5, 32-sb)
 
 // Device-resident model: everything a kernel needs, in one blob so a single
@@ -38,6 +41,7 @@ struct alignas(16) TableDev {
     uint2 encf[kMaxSym];              // EncFast records {M, (m - f) << t | bias << 5 | s}
     uint32_t packed[1 << kPackedMaxBits];  // sym | bias << 8 | f << 20 (f < 4096)
     uint8_t slot_sym[1 << kMaxScaleBits];
+    uint2 packed64[1 << 14];          // 13 <= sb <= 14: {sym | bias << 8, f}
 };
 
 // Optional per-group decode trace (single-stream calls): the lane states and

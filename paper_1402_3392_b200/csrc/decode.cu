@@ -78,28 +78,36 @@ __device__ __forceinline__ uint32_t ring_load(uint32_t ring_addr, uint32_t byte_
     return lds_u16(ring_addr + (byte_off & (kRingBytes - 2)));
 }
 
-template <bool PACKED>
+// LUT forms: packed 32-bit entries (sb <= 12), packed 64-bit entries
+// (13 <= sb <= 14: one LDS.64 per lane instead of two dependent lookups),
+// and the two-lookup form slot -> symbol -> {f, cum} (any sb).
+enum : int { kLutGeneric = 0, kLutPacked32 = 1, kLutPacked64 = 2 };
+
+template <int KIND>
 struct Lut {
-    const uint32_t *packed;  // PACKED: sym | bias << 8 | f << 20
-    const uint8_t *sym;      // else: slot -> symbol
-    const uint2 *dec;        //       symbol -> {f, cum}
+    const uint32_t *packed;  // kLutPacked32: sym | bias << 8 | f << 20
+    const uint2 *packed64;   // kLutPacked64: {sym | bias << 8, f}
+    const uint8_t *sym;      // kLutGeneric: slot -> symbol
+    const uint2 *dec;        //              symbol -> {f, cum}
     uint32_t mask;
     uint32_t sb;
-    uint32_t hmul;           // 2^(32 - sb): x >> sb as a multiply-high (FMA pipe)
-    uint64_t hbias64;        // -4096 << 32
 
     // returns the symbol in the low byte
     __device__ __forceinline__ uint32_t pop(uint32_t &x) const {
         const uint32_t slot = x & mask;
-        if (PACKED) {
-            // h = (x >> sb) - 4096 in one IMAD.HI; e >> 8 = bias + f * 4096,
-            // so f * h + (e >> 8) = f * (x >> sb) + bias with no field mask,
+        if (KIND == kLutPacked32) {
+            // h = (x >> sb) - 4096; e >> 8 = bias + f * 4096, so
+            // f * h + (e >> 8) = f * (x >> sb) + bias with no field mask,
             // and the symbol is e's low byte (stored as is). The integer ALU
-            // pipe is the decoder's busiest; this moves work to the FMA pipe.
+            // pipe is the decoder's busiest; this keeps work off it.
             const uint32_t h = (x >> sb) - 4096u;
             const uint32_t e = packed[slot];
             x = (e >> 20) * h + (e >> 8);
             return e;
+        } else if (KIND == kLutPacked64) {
+            const uint2 e = packed64[slot];
+            x = e.y * (x >> sb) + (e.x >> 8);
+            return e.x;
         } else {
             const uint32_t s = sym[slot];
             const uint2 d = dec[s];
@@ -199,7 +207,7 @@ __host__ __device__ constexpr size_t decode_warp_smem() { return kRingAllocBytes
 // Not inlined: with both LUT forms inlined into one kernel the packed
 // path's schedule degrades (~8% slower decode, measured); as a call each
 // body keeps its own register allocation.
-template <bool PACKED, class Sink>
+template <int KIND, class Sink>
 __device__ __noinline__ void
 decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                  const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -212,15 +220,18 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
     uint8_t *lut_base = smem + nw * (kRingAllocBytes + kObufBytes);
 
     // ---- stage the lookup tables in shared memory ------------------------
-    Lut<PACKED> lut;
+    Lut<KIND> lut;
     lut.mask = m - 1u;
     lut.sb = static_cast<uint32_t>(sb);
-    lut.hmul = 1u << (32 - sb);
-    lut.hbias64 = static_cast<uint64_t>(0u - 4096u) << 32;
-    if (PACKED) {
+    if (KIND == kLutPacked32) {
         uint32_t *p = reinterpret_cast<uint32_t *>(lut_base);
         for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) p[i] = tab->packed[i];
         lut.packed = p;
+    } else if (KIND == kLutPacked64) {
+        uint4 *p = reinterpret_cast<uint4 *>(lut_base);
+        const uint4 *src = reinterpret_cast<const uint4 *>(tab->packed64);
+        for (uint32_t i = threadIdx.x; i < m / 2; i += blockDim.x) p[i] = src[i];
+        lut.packed64 = reinterpret_cast<const uint2 *>(lut_base);
     } else {
         uint2 *d = reinterpret_cast<uint2 *>(lut_base);
         uint8_t *s = lut_base + kMaxSym * sizeof(uint2);
@@ -390,10 +401,11 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
     }
 }
 
-// ALLOW_PACKED: sb <= 12 launch whose smem fits either LUT; the device
-// table's flag picks the packed entry or the two-lookup form (a
-// single-symbol sb=12 table has f = 4096, which the 12-bit field cannot hold).
-template <bool ALLOW_PACKED, class Sink>
+// MAXKIND: the packed form this launch's shared memory was sized for (it
+// also fits the two-lookup form); the device table's flags pick which one
+// runs (a single-symbol sb=12 table has f = 4096, which the 12-bit field of
+// the 32-bit entry cannot hold).
+template <int MAXKIND, class Sink>
 __global__ void __launch_bounds__(1024)
 decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                    const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -407,12 +419,18 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
         return;
     }
-    if (ALLOW_PACKED && (tab->flags & kTabPacked))
-        decode_warp_body<true, Sink>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes,
-                                     tab, out, consumed, final_states, status, trace, smem, sb);
+    if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
+        decode_warp_body<kLutPacked32, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
+                                             n_lanes, tab, out, consumed, final_states, status,
+                                             trace, smem, sb);
+    else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
+        decode_warp_body<kLutPacked64, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
+                                             n_lanes, tab, out, consumed, final_states, status,
+                                             trace, smem, sb);
     else
-        decode_warp_body<false, Sink>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes,
-                                      tab, out, consumed, final_states, status, trace, smem, sb);
+        decode_warp_body<kLutGeneric, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
+                                            n_lanes, tab, out, consumed, final_states, status,
+                                            trace, smem, sb);
 }
 
 // ---------------------------------------------------------------------------
@@ -520,9 +538,11 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
         for (int l = lo; l < lo + per && l < n_lanes; ++l) final_states[k * n_lanes + l] = ws[l];
 }
 
-static size_t decode_lut_bytes(int scale_bits, bool packed) {
+static size_t decode_lut_bytes(int scale_bits, int kind) {
     const size_t m = size_t(1) << scale_bits;
-    size_t b = packed ? m * 4 : kMaxSym * sizeof(uint2) + (m < 16 ? 16 : m);
+    size_t b = kind == kLutPacked32 ? m * 4
+             : kind == kLutPacked64 ? m * 8
+                                    : kMaxSym * sizeof(uint2) + (m < 16 ? 16 : m);
     return (b + 15) & ~size_t(15);
 }
 
@@ -555,9 +575,13 @@ static cudaError_t launch_decode_warp(const uint16_t *d_payload, const uint64_t 
                                      uint32_t *d_final_states, DStatus *d_status,
                                      cudaStream_t stream, DecodeTrace trace) {
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
-    const bool use_packed = packed && scale_bits <= kPackedMaxBits;
-    size_t lut = decode_lut_bytes(scale_bits, false);
-    if (use_packed && decode_lut_bytes(scale_bits, true) > lut) lut = decode_lut_bytes(scale_bits, true);
+    // the packed form this launch allows (the device table's flags decide
+    // whether it runs; its shared memory always fits the two-lookup form too)
+    const int maxkind = (packed && scale_bits <= kPackedMaxBits) ? kLutPacked32
+                      : (scale_bits >= kPacked64MinBits && scale_bits <= kPacked64MaxBits)
+                          ? kLutPacked64 : kLutGeneric;
+    size_t lut = decode_lut_bytes(scale_bits, kLutGeneric);
+    if (decode_lut_bytes(scale_bits, maxkind) > lut) lut = decode_lut_bytes(scale_bits, maxkind);
     // One CTA per SM with that SM's share of the streams (up to 28 warps;
     // 4096 chunks = one wave on 148 SMs): the warp scheduler is not fair
     // across CTAs, and co-resident CTAs finish far apart (encode.cu,
@@ -573,16 +597,23 @@ static cudaError_t launch_decode_warp(const uint16_t *d_payload, const uint64_t 
     const int64_t per_sm = static_cast<int64_t>(smem_cap / (smem + 1024));
     const int64_t max_blocks = sms * (per_sm < 1 ? 1 : per_sm);
     if (blocks > max_blocks) blocks = max_blocks;
-    if (use_packed) {
-        cudaFuncSetAttribute(decode_warp_kernel<true, Sink>,
+    const unsigned g = static_cast<unsigned>(blocks);
+    if (maxkind == kLutPacked32) {
+        cudaFuncSetAttribute(decode_warp_kernel<kLutPacked32, Sink>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        decode_warp_kernel<true, Sink><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
+        decode_warp_kernel<kLutPacked32, Sink><<<g, warps * 32, smem, stream>>>(
+            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
+            sink, d_consumed, d_final_states, d_status, scale_bits, trace);
+    } else if (maxkind == kLutPacked64) {
+        cudaFuncSetAttribute(decode_warp_kernel<kLutPacked64, Sink>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        decode_warp_kernel<kLutPacked64, Sink><<<g, warps * 32, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
             sink, d_consumed, d_final_states, d_status, scale_bits, trace);
     } else {
-        cudaFuncSetAttribute(decode_warp_kernel<false, Sink>,
+        cudaFuncSetAttribute(decode_warp_kernel<kLutGeneric, Sink>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        decode_warp_kernel<false, Sink><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
+        decode_warp_kernel<kLutGeneric, Sink><<<g, warps * 32, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
             sink, d_consumed, d_final_states, d_status, scale_bits, trace);
     }

@@ -239,6 +239,7 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
     // Thread t owns the contiguous slots [t*per, (t+1)*per): one binary
     // search for the first, then a forward walk over cum.
     int ok = scale_bits <= kPackedMaxBits ? 1 : 0;
+    int ok64 = scale_bits >= kPacked64MinBits && scale_bits <= kPacked64MaxBits ? 1 : 0;
     const uint32_t per = (m + kMaxSym - 1) / kMaxSym;
     const uint32_t j0 = tid * per, j1 = min(m, j0 + per);
     int s_cur = 0;
@@ -267,11 +268,19 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
             if (f < 1 || f > 4095 || bias >= 4096) ok = 0;
             t->packed[j] = s | (bias & 0xFFFu) << 8 | (f & 0xFFFu) << 20;
         }
+        if (scale_bits >= kPacked64MinBits && scale_bits <= kPacked64MaxBits) {
+            const uint32_t bias = j - cum[s];  // < 2^24 for every consistent table
+            if (bias >= (1u << 24)) ok64 = 0;
+            t->packed64[j] = make_uint2(s | bias << 8, freq[s]);
+        }
     }
     __syncthreads();
     const int all_ok = -block_max_256(-ok, red);  // min over threads
     const int all_fast = -block_max_256(-fast_ok, red);
-    if (tid == 0) t->flags = (all_ok ? kTabPacked : 0u) | (all_fast ? kTabEncFast : 0u);
+    const bool p64 = -block_max_256(-ok64, red) != 0;
+    if (tid == 0)
+        t->flags = (all_ok ? kTabPacked : 0u) | (all_fast ? kTabEncFast : 0u) |
+                   (p64 ? kTabPacked64 : 0u);
 }
 
 // mode: counts != nullptr -> quantize(counts) first (alphabet = max+1).
