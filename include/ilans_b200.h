@@ -201,9 +201,9 @@ int ilans_dstatus_parse(const void *h_status, ilans_status *st);
  * payload length of chunk k and d_states[k*N + l] its final lane states.
  * C must be a positive multiple of 16. */
 int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
-                            int32_t n_lanes, const void *d_table, uint16_t *d_scratch,
-                            uint32_t *d_chunk_words, uint32_t *d_states, void *d_status,
-                            void *stream);
+                            int32_t n_lanes, const void *d_table, int32_t scale_bits,
+                            uint16_t *d_scratch, uint32_t *d_chunk_words, uint32_t *d_states,
+                            void *d_status, void *stream);
 /* Framing: d_word_offsets[0..n_chunks] = exclusive prefix sum of chunk
  * words, and the chunk payloads packed back to back into d_payload
  * (capacity n words) at those offsets. carry_in != 0 continues a previous

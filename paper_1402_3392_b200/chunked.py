@@ -263,7 +263,7 @@ class DeviceCodec:
             return
         _lib.check_dev(_lib.lib.ilans_encode_chunks_dev(
             msg_ptr + lo, nb, self.chunk_len, self.lane_count, self._p(self.table),
-            self._p(self.scratch) + 2 * lo, self._p(self.chunk_words) + 4 * k0,
+            self.scale_bits, self._p(self.scratch) + 2 * lo, self._p(self.chunk_words) + 4 * k0,
             self._p(self.states) + 4 * k0 * self.lane_count, self._p(self.status), self._s()),
             "encode")
 

@@ -264,7 +264,7 @@ extern "C" int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const
                           scale_bits, c.table.as<TableDev>(), s));
     dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
     ilans_note_launch();
-    CK(launch_encode(c.msg.as<uint8_t>(), n, n, n_lanes, c.table.as<TableDev>(),
+    CK(launch_encode(c.msg.as<uint8_t>(), n, n, n_lanes, c.table.as<TableDev>(), scale_bits,
                      c.scratch.as<uint16_t>(), c.words.as<uint32_t>(), c.states.as<uint32_t>(),
                      c.status.as<DStatus>(), c.ws.as<uint32_t>(), s));
     DStatus hs;
@@ -798,14 +798,17 @@ extern "C" int ilans_dstatus_parse(const void *h_status, ilans_status *st) {
 }
 
 extern "C" int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
-                                       int32_t n_lanes, const void *d_table,
+                                       int32_t n_lanes, const void *d_table, int32_t scale_bits,
                                        uint16_t *d_scratch, uint32_t *d_chunk_words,
                                        uint32_t *d_states, void *d_status, void *stream) {
     if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits) return ILANS_ERR_VALUE;
     if (reinterpret_cast<uintptr_t>(d_msg) & 15) return ILANS_ERR_VALUE;
     return launch_encode(d_msg, n, chunk_len, n_lanes, static_cast<const TableDev *>(d_table),
-                         d_scratch, d_chunk_words, d_states, static_cast<DStatus *>(d_status),
-                         nullptr, ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+                         scale_bits, d_scratch, d_chunk_words, d_states,
+                         static_cast<DStatus *>(d_status), nullptr, ST(stream)) == cudaSuccess
+               ? ILANS_OK
+               : ILANS_ERR_CUDA;
 }
 
 extern "C" int ilans_frame_chunks_dev(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,

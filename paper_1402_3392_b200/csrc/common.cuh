@@ -22,6 +22,7 @@ constexpr int kPackedMaxBits = 12;           // packed 32-bit slot entry: sym|f-
 constexpr uint32_t kTabPacked = 1u;          // packed[] valid (sb <= 12, consistent)
 constexpr uint32_t kTabEncFast = 2u;         // encf valid (sb <= 13, every f <= m/2)
 constexpr uint32_t kTabPacked64 = 4u;        // packed64[] valid (13 <= sb <= 14)
+constexpr uint32_t kTabEncFast12 = 8u;       // encf = {M, Y} + encz valid (sb = 14, f <= m/2)
 constexpr int kPacked64MinBits = 13;
 constexpr int kPacked64MaxBits = 14;
 constexpr int kEncFastMaxBits = 13;             // bias < 2^(sb+1) fits Z's bits [5, 32-sb)
@@ -39,6 +40,8 @@ struct alignas(16) TableDev {
     uint2 enc[kMaxSym];               // EncSym records {magic, (m - f) | cum << 16}
     uint2 dec[kMaxSym];               // {f, cum} for the decoder's second lookup
     uint2 encf[kMaxSym];              // EncFast records {M, (m - f) << t | bias << 5 | s}
+                                      // (sb = 14: EncFast12 {M, f << t | (m - f)})
+    uint32_t encz[kMaxSym];           // EncFast12: s | bias << 17
     uint32_t packed[1 << kPackedMaxBits];  // sym | bias << 8 | f << 20 (f < 4096)
     uint8_t slot_sym[1 << kMaxScaleBits];
     uint2 packed64[1 << 14];          // 13 <= sb <= 14: {sym | bias << 8, f}
@@ -170,6 +173,37 @@ struct EncFast {
             sh = c - 1u;
         }
         return make_uint2(M, (m - f) << t | bias << 5 | sh);
+    }
+};
+
+// sb = 14 (every f <= m / 2): bias < 2^15 no longer fits beside m - f and s
+// in one word, so the record takes 12 bytes:
+//   .x = M (as EncFast),  .y = Y = f << t | (m - f)   (m - f < 2^t)
+//   Z  = s | bias << 17   (a separate 4-byte array)
+// spill: (x | (2^t - 1)) >= Y;  q = umulhi(x, M) >> s (s = Z & 31);
+// x' = q (Y & (2^t - 1)) + x + (Z >> 17).
+struct EncFast12 {
+    __host__ __device__ static void make(uint32_t f, uint32_t cum, int sb, uint2 *a,
+                                         uint32_t *z) {
+        const uint32_t m = 1u << sb, t = 32u - static_cast<uint32_t>(sb);
+        if (f == 0 || f > m / 2) {
+            *a = make_uint2(0u, 0u);
+            *z = 0u;
+            return;
+        }
+        uint32_t M, sh, bias = cum;
+        if (f == 1) {
+            M = 0xFFFFFFFFu;
+            sh = 0u;
+            bias = cum + m - 1u;
+        } else {
+            uint32_t c = 0;
+            while ((1u << c) < f) ++c;
+            M = static_cast<uint32_t>(((1ull << (31 + c)) + f - 1) / f);
+            sh = c - 1u;
+        }
+        *a = make_uint2(M, f << t | (m - f));
+        *z = sh | bias << 17;
     }
 };
 

@@ -51,10 +51,11 @@ constexpr int kEncMaxWarps = 28;
 constexpr int kOutRing = 1024;   // per-warp staging ring for spilled words (2 KB)
 constexpr uint32_t kOutRingBytes = kOutRing * 2;
 
-// dynamic shared memory: enc[256] | encf[256] | W message rings | pad | W spill rings
+// dynamic shared memory: enc[256] | encf[256] | encz[256] | W message rings |
+// pad | W spill rings
 __host__ __device__ constexpr size_t encode_smem_bytes(int warps) {
-    return 2 * kMaxSym * sizeof(uint2) + size_t(warps) * kInRing + kOutRingBytes +
-           size_t(warps) * kOutRingBytes;
+    return 2 * kMaxSym * sizeof(uint2) + kMaxSym * sizeof(uint32_t) + size_t(warps) * kInRing +
+           kOutRingBytes + size_t(warps) * kOutRingBytes;
 }
 
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
@@ -114,7 +115,9 @@ struct SpillStage {
 
 // Idx: chunk-local index type (int for chunks < 2^30 bytes, the chunked
 // format's case; long long only for huge single-stream calls).
-template <typename Idx>
+// F12: the sb = 14 instantiation (12-byte fast records); the other one
+// carries the 8-byte fast loop, so neither pays for the other's registers.
+template <typename Idx, bool F12>
 __global__ void __launch_bounds__(kEncMaxWarps * 32, 1)
 encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
@@ -123,13 +126,16 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     extern __shared__ __align__(16) uint8_t esmem[];
     const int nw = blockDim.x >> 5;
     uint2 *enc = reinterpret_cast<uint2 *>(esmem);
-    uint2 *encf = enc + kMaxSym;  // EncFast records {M, Z}
-    uint8_t *rings = esmem + 2 * kMaxSym * sizeof(uint2);
+    uint2 *encf = enc + kMaxSym;  // EncFast {M, Z} / EncFast12 {M, Y}
+    uint32_t *encz = reinterpret_cast<uint32_t *>(encf + kMaxSym);  // EncFast12 Z
+    uint8_t *rings = reinterpret_cast<uint8_t *>(encz + kMaxSym);
     uint16_t *oring_raw = reinterpret_cast<uint16_t *>(rings + nw * kInRing);
-    const bool fast = (tab->flags & kTabEncFast) != 0u;
+    const bool fast = !F12 && (tab->flags & kTabEncFast) != 0u;
+    const bool fast12 = F12 && (tab->flags & kTabEncFast12) != 0u;
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) {
         enc[i] = tab->enc[i];
         encf[i] = tab->encf[i];
+        encz[i] = tab->encz[i];
     }
     __syncthreads();
     const EncCtx ctx(tab->scale_bits);
@@ -259,6 +265,32 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                     asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
                     x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
                 }
+            } else if (fast12) {
+                uint32_t sym_n = blk[(kInSeg / 32 - 1) * 32 + lane];
+                uint2 a_n = encf[sym_n];
+                uint32_t z_n = encz[sym_n];
+                sym_n = blk[(kInSeg / 32 - 2) * 32 + lane];
+#pragma unroll
+                for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
+                    const uint2 a = a_n;  // {M, Y}
+                    const uint32_t z = z_n;
+                    if (gg > 0) {
+                        a_n = encf[sym_n];
+                        z_n = encz[sym_n];
+                        if (gg > 1) sym_n = blk[(gg - 2) * 32 + lane];
+                    }
+                    macc &= a.x;
+                    const bool spill = (x | lowm) >= a.y;
+                    const uint32_t mk = __ballot_sync(0xffffffffu, spill);
+                    topb -= two * __popc(mk);
+                    if (spill)
+                        sts16(oring_addr | ((topb + two * __popc(mk * lt_mul)) & (kOutRingBytes - 2)),
+                              x);
+                    x = spill ? x >> 16 : x;
+                    uint32_t q = __umulhi(x, a.x);
+                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
+                    x = q * (a.y & lowm) + (x + (z >> 17));
+                }
             } else {
 #pragma unroll
             for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
@@ -275,7 +307,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             }
             }
             top -= static_cast<Idx>((topb0 - topb) >> 1);
-            if (!fast && __ballot_sync(0xffffffffu, zero_f)) {  // rare: the highest bad index
+            if (!fast && !fast12 && __ballot_sync(0xffffffffu, zero_f)) {  // rare: highest bad index
                 for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
                     const uint32_t bm =
                         __ballot_sync(0xffffffffu, enc[blk[gg * 32 + lane]].x == 0u);
@@ -291,7 +323,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             }
             st.drain(top, lane);
         }
-        if (fast && !bad && __ballot_sync(0xffffffffu, (macc >> 31) == 0u)) {
+        if ((fast || fast12) && !bad && __ballot_sync(0xffffffffu, (macc >> 31) == 0u)) {
             // rare: some symbol of the fast region has f = 0 (its scratch is
             // garbage but stayed inside the chunk: at most 32 spills per
             // group). The highest offending index, as the reference's
@@ -414,7 +446,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
 }
 
 cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, int n_lanes,
-                          const TableDev *d_table, uint16_t *d_scratch,
+                          const TableDev *d_table, int scale_bits, uint16_t *d_scratch,
                           uint32_t *d_chunk_words, uint32_t *d_states, DStatus *d_status,
                           uint32_t *d_lane_ws, cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
@@ -437,19 +469,22 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
         const int64_t max_blocks = sms * (per_sm < 1 ? 1 : per_sm);
         if (blocks > max_blocks) blocks = max_blocks;
         const size_t smem = encode_smem_bytes(warps);
+        const unsigned g = static_cast<unsigned>(blocks);
+        auto go = [&](auto kernel) {
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            kernel<<<g, warps * 32, smem, stream>>>(d_msg, n, chunk_len, n_chunks, n_lanes,
+                                                    d_table, d_scratch, d_chunk_words, d_states,
+                                                    d_status);
+        };
+        // the table's scale_bits is on the device; the sb = 14 instantiation
+        // is picked by the caller's scale_bits and re-checks the flag itself
+        const bool sb14 = scale_bits == 14;
         if (chunk_len < (int64_t(1) << 30)) {
-            cudaFuncSetAttribute(encode_warp_kernel<int>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            encode_warp_kernel<int><<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
-                d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_chunk_words,
-                d_states, d_status);
+            if (sb14) go(encode_warp_kernel<int, true>);
+            else go(encode_warp_kernel<int, false>);
         } else {
-            cudaFuncSetAttribute(encode_warp_kernel<long long>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            encode_warp_kernel<long long>
-                <<<static_cast<unsigned>(blocks), warps * 32, smem, stream>>>(
-                    d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_chunk_words,
-                    d_states, d_status);
+            if (sb14) go(encode_warp_kernel<long long, true>);
+            else go(encode_warp_kernel<long long, false>);
         }
     }
     ilans_note_launch();

@@ -23,7 +23,7 @@ cudaError_t launch_build_table(const unsigned long long *d_counts, const uint32_
 // encode.cu -- chunked encode (N <= 32: one warp per chunk; N > 32: one CTA
 // per stream), then framing (scan + compaction).
 cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, int n_lanes,
-                          const TableDev *d_table, uint16_t *d_scratch,
+                          const TableDev *d_table, int scale_bits, uint16_t *d_scratch,
                           uint32_t *d_chunk_words, uint32_t *d_states, DStatus *d_status,
                           uint32_t *d_lane_ws, cudaStream_t stream);
 cudaError_t launch_frame(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,

@@ -229,10 +229,20 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         t->freq[tid] = f;
         t->enc[tid] = EncSym::make(f, cum[tid], scale_bits);
         t->dec[tid] = make_uint2(f, cum[tid]);
-        t->encf[tid] = EncFast::make(f, cum[tid], scale_bits);
+        if (scale_bits == 14) {
+            uint2 a;
+            uint32_t z;
+            EncFast12::make(f, cum[tid], scale_bits, &a, &z);
+            t->encf[tid] = a;
+            t->encz[tid] = z;
+        } else {
+            t->encf[tid] = EncFast::make(f, cum[tid], scale_bits);
+            t->encz[tid] = 0u;
+        }
     }
     // fast encoder records: sb <= 13 and no symbol above half the range
-    const int fast_ok = scale_bits <= kEncFastMaxBits && freq[tid] <= (m >> 1) ? 1 : 0;
+    const int fast_ok = (scale_bits <= kEncFastMaxBits || scale_bits == 14) &&
+                        freq[tid] <= (m >> 1) ? 1 : 0;
     if (tid == 0) t->cum[kMaxSym] = cum[kMaxSym];
     t->cum[tid] = cum[tid];
     // slot -> symbol; consistent (packable) check for the sb <= 12 LUT.
@@ -279,7 +289,8 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
     const int all_fast = -block_max_256(-fast_ok, red);
     const bool p64 = -block_max_256(-ok64, red) != 0;
     if (tid == 0)
-        t->flags = (all_ok ? kTabPacked : 0u) | (all_fast ? kTabEncFast : 0u) |
+        t->flags = (all_ok ? kTabPacked : 0u) |
+                   (all_fast ? (scale_bits == 14 ? kTabEncFast12 : kTabEncFast) : 0u) |
                    (p64 ? kTabPacked64 : 0u);
 }
 

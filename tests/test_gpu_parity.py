@@ -194,7 +194,7 @@ def test_unencodable_symbol():
         B.encode_interleaved_u16(np.array([0, 1], np.uint8), [4, 0], [0, 4, 4], 2, 1)
 
 
-@pytest.mark.parametrize("sb", [2, 8, 12, 13])
+@pytest.mark.parametrize("sb", [2, 8, 12, 13, 14])
 def test_fast_encoder_record_edges(sb):
     """Tables at the edge of the fast encoder record (common.cuh EncFast:
     sb <= 12, every f <= m/2): f = m/2 exactly and f = 1 symbols take it,
