@@ -437,30 +437,64 @@ class _Slot:
         self.h_states = pin(k * lane_count, torch.int32)
         self.h_payload = pin(max(1, capacity) + 8, torch.int16)
         self.free = None  # event: the slot's last round trip has finished on the device
+        self.pending = None  # an EncodeJob whose payload downloads are not issued yet
 
     def streams(self):
         return (self.s_in, self.s_comp, self.s_out, *self.s_dec)
 
 
 class EncodeJob:
-    """An ``HostCodec.encode_async`` in flight. Its payload / offsets /
-    states are views of the slot's pinned buffers; the word offsets are
-    already on the host when the job is returned, the payload and states land
-    when ``wait()`` returns (or when a decode queued after it reads them)."""
+    """An ``HostCodec.encode_async`` in flight. ``encode_async`` returns as
+    soon as the work is queued; the payload downloads need the word offsets
+    on the host, so they are issued by ``materialize()`` -- called by
+    ``wait()`` and by a ``decode_async`` of this job -- which blocks only
+    until the offsets have landed (and raises the encode's device errors).
+    payload / offsets / states are views of the slot's pinned buffers."""
 
-    def __init__(self, slot, n, k, words, batches, ev_states, ev_pay, ev_done, h2d, d2h):
-        self.slot, self.n, self.k, self.words = slot, n, k, words
-        self.batches, self.ev_states, self.ev_pay = batches, ev_states, ev_pay
-        self.ev_done = ev_done
-        self.h2d_bytes, self.d2h_bytes = h2d, d2h
-        N = slot.codec.lane_count
-        self.payload = slot.h_payload[:words]
+    def __init__(self, codec, slot, n, k, batches, ev_off, ev_status, ev_states, h2d):
+        self.codec, self.slot, self.n, self.k = codec, slot, n, k
+        self.batches, self.ev_off, self.ev_status = batches, ev_off, ev_status
+        self.ev_states = ev_states
+        self.ev_pay = None
+        self.ev_done = None
+        self.h2d_bytes = h2d
+        self.d2h_bytes = None
+        self.words = None
+
+    def materialize(self):
+        """Issue the payload downloads (once): per batch, as soon as its word
+        offsets are on the host."""
+        if self.ev_pay is not None:
+            return self
+        if self.slot.pending is self:
+            self.slot.pending = None
+        torch = _torch()
+        slot, c = self.slot, self.slot.codec
+        N = c.lane_count
+        ev_pay = []
+        for i, ((k0, k1), ev) in enumerate(zip(self.batches, self.ev_off)):
+            ev.synchronize()
+            if i == len(self.batches) - 1:  # the encode kernel is done: report its errors
+                self.ev_status.synchronize()
+                c.check_status_host()
+            a, b = int(slot.h_offsets[k0]), int(slot.h_offsets[k1])
+            with torch.cuda.stream(slot.s_out):
+                slot.h_payload[a:b].copy_(c.payload[a:b], non_blocking=True)
+            ev_pay.append(HostCodec._event(slot.s_out))
+        self.codec._mark("enc.d2h.end", slot.s_out)
+        self.ev_done = HostCodec._event(slot.s_out)
+        self.ev_pay = ev_pay
+        k = self.k
+        self.words = int(slot.h_offsets[k]) if k else 0
+        self.d2h_bytes = 8 * (k + 1) + 4 * k * N + 2 * self.words
+        self.payload = slot.h_payload[: self.words]
         self.offsets = slot.h_offsets[: k + 1]
         self.states = slot.h_states[: k * N]
+        return self
 
     def wait(self):
-        """Payload and states are on the host (device errors were raised by
-        encode_async itself)."""
+        """Payload, offsets and states on the host."""
+        self.materialize()
         self.ev_done.synchronize()
         return self.payload, self.offsets, self.states
 
@@ -548,6 +582,9 @@ class HostCodec:
         torch = _torch()
         slot = self.slots[self._next]
         self._next = (self._next + 1) % len(self.slots)
+        if slot.pending is not None:  # its offsets / payload buffers are about to be reused
+            slot.pending.materialize()
+            slot.pending = None
         cur = torch.cuda.current_stream(self.device)
         for s in slot.streams():
             s.wait_stream(cur)
@@ -556,8 +593,8 @@ class HostCodec:
         return slot
 
     def encode_async(self, h_msg, n: int) -> EncodeJob:
-        """Queue the encode of pinned uint8 h_msg[:n]. Blocks the host only
-        until the word offsets are known (to size the payload copies)."""
+        """Queue the encode of pinned uint8 h_msg[:n] (never blocks the host;
+        the payload downloads are issued by the job's materialize())."""
         torch = _torch()
         if n > self.capacity:
             raise ValueError("message larger than codec capacity")
@@ -614,28 +651,18 @@ class HostCodec:
         with torch.cuda.stream(slot.s_out):
             slot.h_states[: k * N].copy_(c.states[: k * N], non_blocking=True)
         ev_states = self._event(slot.s_out)
-        ev_pay = []
-        for i, ((k0, k1), ev) in enumerate(zip(batches, ev_off)):
-            ev.synchronize()
-            if i == len(batches) - 1:  # the encode kernel is done: report its errors now
-                ev_status.synchronize()
-                c.check_status_host()
-            a, b = int(slot.h_offsets[k0]), int(slot.h_offsets[k1])
-            with torch.cuda.stream(slot.s_out):
-                slot.h_payload[a:b].copy_(c.payload[a:b], non_blocking=True)
-            ev_pay.append(self._event(slot.s_out))
-        self._mark("enc.d2h.end", slot.s_out)
-        ev_done = self._event(slot.s_out)
-        words = int(slot.h_offsets[k]) if k else 0
         self._last = slot
-        h2d, d2h = n, 8 * (k + 1) + 4 * k * N + 2 * words
-        self.h2d_bytes, self.d2h_bytes = h2d, d2h
-        return EncodeJob(slot, n, k, words, batches, ev_states, ev_pay, ev_done, h2d, d2h)
+        self.h2d_bytes = n
+        slot.pending = EncodeJob(self, slot, n, k, batches, ev_off, ev_status, ev_states, n)
+        return slot.pending
 
     def encode(self, h_msg, n: int):
         """h_msg: pinned uint8 tensor. Returns (payload, offsets, states) as
         views of the pinned host buffers (valid until the slot is reused)."""
-        return self.encode_async(h_msg, n).wait()
+        job = self.encode_async(h_msg, n)
+        out = job.wait()
+        self.d2h_bytes = job.d2h_bytes
+        return out
 
     def decode_async(self, src, h_out, n: int | None = None, h_offsets=None, h_states=None):
         """Queue the decode into pinned uint8 h_out. ``src`` is an EncodeJob
@@ -645,7 +672,7 @@ class HostCodec:
         most recent encode)."""
         torch = _torch()
         if isinstance(src, EncodeJob):
-            slot, job = src.slot, src
+            slot, job = src.slot, src.materialize()
             n, h_payload, h_offsets, h_states = src.n, src.payload, src.offsets, src.states
             cur = torch.cuda.current_stream(self.device)
             for s in slot.streams():

@@ -26,9 +26,9 @@ def main():
     h_msg = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     h_msg.copy_(d[:n])
     outs = [torch.empty(n, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-    hc = HostCodec(n, 65536, 32, 12, dev, batch_bytes=batch, slots=2)
-    for i in range(2):
-        hc.decode_async(hc.encode_async(h_msg, n), outs[i]).wait()
+    hc = HostCodec(n, 65536, 32, 12, dev, batch_bytes=batch, slots=3)
+    for i in range(3):
+        hc.decode_async(hc.encode_async(h_msg, n), outs[i % 2]).wait()
     torch.cuda.synchronize()
     hc.trace = []
     t0 = torch.cuda.Event(enable_timing=True)
@@ -36,9 +36,12 @@ def main():
     w0 = time.perf_counter()
     pend = []
     steps = 6
+    ejs = [hc.encode_async(h_msg, n)]
     for i in range(steps):
         hc._mark(f"step{i}", torch.cuda.current_stream())
-        pend.append(hc.decode_async(hc.encode_async(h_msg, n), outs[i % 2]))
+        if i + 1 < steps:
+            ejs.append(hc.encode_async(h_msg, n))
+        pend.append(hc.decode_async(ejs[i], outs[i % 2]))
         if len(pend) == 2:
             pend.pop(0).wait()
     for p in pend:
