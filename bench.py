@@ -235,6 +235,7 @@ def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: in
         busy = max(r[0] for r in res)
         ok = all(r[1] for r in res)
         workers = len(jobs)
+        per_core = statistics.median((hi - lo) * C / r[0] / 1e9 for (lo, hi), r in zip(jobs, res))
     else:  # oracle port (C restatement), single core
         t0 = time.perf_counter()
         ok = True
@@ -245,6 +246,7 @@ def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: in
             ok &= bool(np.array_equal(out, chunk))
         wall = busy = time.perf_counter() - t0
         workers = 1
+        per_core = n_chunks * C / busy / 1e9
     sample = n_chunks * C
     return {
         "value": sample / (t_model + busy) / 1e9,
@@ -257,6 +259,7 @@ def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: in
                   f"reference ext backend on a fork pool of {workers} workers (slowest "
                   f"worker {busy:.3f}s; wall incl. fork {wall:.2f}s)",
         "round_trip_ok": ok,
+        "single_core_round_trip_GBps": per_core,
         "wall_s": wall,
     }
 
