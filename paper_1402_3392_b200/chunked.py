@@ -518,23 +518,25 @@ class HostCodec:
     user makes with data in host memory. Work is split into chunk-aligned
     batches on per-slot streams so PCIe traffic overlaps the kernels:
 
-    encode(): H2D batch b (copy stream) || histogram of batch b (compute
+    encode: H2D batch b (copy stream) || histogram of batch b (compute
       stream) -> [NCCL all-reduce] -> quantize + tables -> one encode launch
       -> per batch: framing (offsets + packing) -> offsets D2H; the payload
-      of batch b goes D2H as soon as its size is known on the host.
-    decode(): directory H2D -> per batch: payload H2D (copy) || decode
-      (one of four streams: a batch alone cannot fill the GPU, a chunk is one
+      of batch b goes D2H once its size is known on the host.
+    decode: directory H2D -> per batch: payload H2D (copy) || decode (one
+      of four streams: a batch alone cannot fill the GPU, a chunk is one
       warp) || decoded bytes D2H (output stream).
 
     ``slots`` (default 2) independent buffer sets let consecutive calls
-    overlap: ``encode_async`` / ``decode_async`` return jobs, and the upload
-    of the next message runs while the previous round trip's results are
-    still coming down (PCIe is full duplex; a lone call leaves one direction
-    idle while the whole message is uploaded for the histogram). Job
-    results are views of the slot's pinned buffers, valid until the slot is
-    reused ``slots`` calls later. ``encode`` / ``decode`` are the blocking
-    forms. Buffers (device and pinned host) are allocated once for
-    ``capacity`` bytes per slot."""
+    overlap: ``encode_async`` (never blocks) and ``decode_async`` return
+    jobs, so the upload of the next message runs while the previous round
+    trip's results are still coming down (PCIe is full duplex; a lone call
+    leaves one direction idle while the whole message is uploaded for the
+    histogram). An encode job issues its payload downloads in
+    ``materialize()`` (called by ``wait()`` and by a ``decode_async`` of
+    it), which waits for the word offsets. Job results are views of the
+    slot's pinned buffers, valid until the slot is reused ``slots`` calls
+    later. ``encode`` / ``decode`` are the blocking forms. Buffers (device
+    and pinned host) are allocated once for ``capacity`` bytes per slot."""
 
     def __init__(self, capacity: int, chunk_len: int = DEFAULT_CHUNK, lane_count: int = 32,
                  scale_bits: int = 14, device=None, counts_allreduce=None,
@@ -664,12 +666,14 @@ class HostCodec:
         self.d2h_bytes = job.d2h_bytes
         return out
 
-    def decode_async(self, src, h_out, n: int | None = None, h_offsets=None, h_states=None):
+    def decode_async(self, src, h_out, n: int | None = None, h_offsets=None, h_states=None,
+                     table: SymbolTable | None = None):
         """Queue the decode into pinned uint8 h_out. ``src`` is an EncodeJob
         of this codec (its device model; payload batches are uploaded as
         soon as their download finished) or a pinned int16 payload with
-        ``h_offsets``, ``h_states`` and ``n`` (decoded with the model of the
-        most recent encode)."""
+        ``h_offsets``, ``h_states`` and ``n``, decoded with ``table`` (e.g.
+        a ChunkedContainer's) or, without one, with the model of the most
+        recent encode."""
         torch = _torch()
         if isinstance(src, EncodeJob):
             slot, job = src.slot, src.materialize()
@@ -677,9 +681,13 @@ class HostCodec:
             cur = torch.cuda.current_stream(self.device)
             for s in slot.streams():
                 s.wait_stream(cur)
+        elif table is not None:
+            slot, job, h_payload = self._take_slot(), None, src
+            slot.codec.build_table_from_freq(table)
+            self._last = slot
         else:
             if self._last is None:
-                raise RuntimeError("decode needs a device model: encode first")
+                raise RuntimeError("decode needs a device model: encode first or pass table=")
             slot, job, h_payload = self._last, None, src
             cur = torch.cuda.current_stream(self.device)
             for s in slot.streams():
@@ -729,7 +737,8 @@ class HostCodec:
         self.h2d_bytes, self.d2h_bytes = h2d, d2h
         return DecodeJob(slot, h_out[:n], ev_done, h2d, d2h)
 
-    def decode(self, h_payload, h_offsets, h_states, n: int, h_out):
-        """Decode into pinned uint8 tensor h_out (device model = the most
-        recent encode's)."""
-        return self.decode_async(h_payload, h_out, n, h_offsets, h_states).wait()
+    def decode(self, h_payload, h_offsets, h_states, n: int, h_out,
+               table: SymbolTable | None = None):
+        """Decode into pinned uint8 tensor h_out (model: ``table``, else the
+        most recent encode's)."""
+        return self.decode_async(h_payload, h_out, n, h_offsets, h_states, table).wait()

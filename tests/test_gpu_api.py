@@ -161,6 +161,27 @@ def test_host_codec_async_round_trips_overlap():
         assert np.array_equal(dj.wait().numpy(), msgs[i])
 
 
+def test_host_codec_decodes_a_container_with_its_own_table():
+    """HostCodec.decode(..., table=) decodes a stored chunked stream with the
+    model it carries, not with the model of whatever was encoded last."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import ChunkedContainer, HostCodec, encode_chunked
+    from paper_1402_3392_b200.synth import synth_host
+
+    n, C = 1_000_003, 65536
+    a = synth_host(n, 1.3, seed=5)
+    cc = ChunkedContainer.from_bytes(encode_chunked(a, None, 32, C, 12).to_bytes())
+    hc = HostCodec(n, C, 32, 12, batch_bytes=1 << 18)
+    hc.encode(torch.from_numpy(synth_host(n, 0.6, seed=6)).pin_memory(), n)  # other model
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
+    offs = cc.word_offsets.astype(np.int64)
+    h_out = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    hc.decode(pin(cc.payload.view(np.int16)), pin(offs), pin(cc.states.reshape(-1).view(np.int32)),
+              n, h_out, table=cc.table)
+    assert np.array_equal(h_out.numpy(), a)
+
+
 def test_stats_counters_single_digit_property():
     rng = np.random.default_rng(3)
     stats = RenormStats()
