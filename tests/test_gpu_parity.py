@@ -348,6 +348,25 @@ def test_chunked_edge_shapes():
         assert np.array_equal(decode_chunked(back), msg)
 
 
+@pytest.mark.parametrize("C, lanes, sb", [(16, 1, 12), (512, 32, 12), (1024, 32, 14),
+                                           (2048, 32, 13)])
+def test_chunked_many_chunks_per_warp(C, lanes, sb):
+    """More chunks than one wave of warps (the coders run one CTA per SM
+    with at most 28 warps, so each warp walks several chunks): every chunk
+    still matches the oracle's framing and decodes."""
+    from paper_1402_3392_b200.chunked import decode_chunked, encode_chunked
+
+    n = 148 * 28 * 3 * C + 11  # > 3 chunks per warp
+    rng = np.random.default_rng(C + sb)
+    counts = (rng.zipf(1.3, 256) % 1000 + 1).tolist()
+    t = SymbolTable(oracle.quantize(counts, sb), sb)
+    msg = random_message(rng, t, n)
+    cc = encode_chunked(msg, t, lanes, C)
+    ref_p, ref_o, ref_s = oracle.encode_chunks_u16(msg, C, t.freq_u32, t.cum_u32, sb, lanes)
+    assert np.array_equal(cc.payload, ref_p) and np.array_equal(cc.states, ref_s)
+    assert np.array_equal(decode_chunked(cc), msg)
+
+
 @pytest.mark.parametrize("sb", [11, 12, 13])
 def test_chunked_skewed_tables_both_lut_forms(sb):
     """The packed decode entry holds f in 12 bits: a single-symbol source at
