@@ -495,18 +495,25 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
 // Framing
 // ---------------------------------------------------------------------------
 // Single CTA exclusive scan of n_chunks word counts -> offsets[n_chunks + 1].
+// Each thread scans 4 consecutive counts per pass (4096 chunks = one pass of
+// 1024 threads); passes carry the running total.
 __global__ void __launch_bounds__(1024)
 chunk_offsets_kernel(const uint32_t *__restrict__ words, int64_t n_chunks,
                      uint64_t *__restrict__ offsets, int carry_in) {
     __shared__ unsigned long long wsum[32];
     __shared__ unsigned long long carry;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
     if (threadIdx.x == 0) carry = carry_in ? offsets[0] : 0ull;  // batch continuation
     __syncthreads();
-    for (int64_t base = 0; base < n_chunks; base += blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const unsigned long long v = i < n_chunks ? words[i] : 0ull;
-        unsigned long long inc = v;
+    const int64_t per_pass = static_cast<int64_t>(blockDim.x) * 4;
+    for (int64_t base = 0; base < n_chunks; base += per_pass) {
+        const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * 4;
+        unsigned long long v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = i0 + q < n_chunks ? words[i0 + q] : 0ull;
+        const unsigned long long mine = v[0] + v[1] + v[2] + v[3];
+        unsigned long long inc = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long u = __shfl_up_sync(0xffffffffu, inc, o);
@@ -515,7 +522,7 @@ chunk_offsets_kernel(const uint32_t *__restrict__ words, int64_t n_chunks,
         if (lane == 31) wsum[wid] = inc;
         __syncthreads();
         if (wid == 0) {
-            unsigned long long w = lane < int(blockDim.x >> 5) ? wsum[lane] : 0ull;
+            unsigned long long w = lane < nw ? wsum[lane] : 0ull;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned long long u = __shfl_up_sync(0xffffffffu, w, o);
@@ -524,10 +531,14 @@ chunk_offsets_kernel(const uint32_t *__restrict__ words, int64_t n_chunks,
             wsum[lane] = w;
         }
         __syncthreads();
-        const unsigned long long excl = carry + (wid ? wsum[wid - 1] : 0ull) + inc - v;
-        if (i < n_chunks) offsets[i] = excl;
+        unsigned long long run = carry + (wid ? wsum[wid - 1] : 0ull) + inc - mine;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (i0 + q < n_chunks) offsets[i0 + q] = run;
+            run += v[q];
+        }
         __syncthreads();
-        if (threadIdx.x == 0) carry += wsum[(blockDim.x >> 5) - 1];
+        if (threadIdx.x == 0) carry += wsum[nw - 1];
         __syncthreads();
     }
     if (threadIdx.x == 0) offsets[n_chunks] = carry;
