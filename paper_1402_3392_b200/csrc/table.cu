@@ -261,27 +261,49 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         }
         s_cur = lo;
     }
-    for (uint32_t j = j0; j < j1; ++j) {
-        uint32_t s;
-        if (slot_in) {
-            s = slot_in[j];
-        } else {
-            while (s_cur < kMaxSym - 1 && cum[s_cur + 1] <= j) ++s_cur;
-            s = static_cast<uint32_t>(s_cur);
+    if (!slot_in && (per & 3u) == 0 && scale_bits <= kPackedMaxBits) {
+        // common case (model from counts / frequencies, sb <= 12, >= 4 slots
+        // per thread): four slots per step, 16-byte packed and 4-byte symbol
+        // stores
+        for (uint32_t j = j0; j < j1; j += 4) {
+            uint32_t e[4], sy = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t jj = j + q;
+                while (s_cur < kMaxSym - 1 && cum[s_cur + 1] <= jj) ++s_cur;
+                const uint32_t sym = static_cast<uint32_t>(s_cur);
+                const uint32_t f = freq[sym];
+                const uint32_t bias = jj - cum[sym];
+                if (f < 1 || f > 4095 || bias >= 4096) ok = 0;
+                e[q] = sym | (bias & 0xFFFu) << 8 | (f & 0xFFFu) << 20;
+                sy |= sym << (8 * q);
+            }
+            *reinterpret_cast<uint4 *>(t->packed + j) = make_uint4(e[0], e[1], e[2], e[3]);
+            *reinterpret_cast<uint32_t *>(t->slot_sym + j) = sy;
         }
-        t->slot_sym[j] = static_cast<uint8_t>(s);
-        if (scale_bits <= kPackedMaxBits) {
-            const uint32_t f = freq[s];
-            const uint32_t bias = j - cum[s];
-            // f == 4096 (a single-symbol sb=12 table) does not fit 12 bits:
-            // such tables take the two-lookup path
-            if (f < 1 || f > 4095 || bias >= 4096) ok = 0;
-            t->packed[j] = s | (bias & 0xFFFu) << 8 | (f & 0xFFFu) << 20;
-        }
-        if (scale_bits >= kPacked64MinBits && scale_bits <= kPacked64MaxBits) {
-            const uint32_t bias = j - cum[s];  // < 2^24 for every consistent table
-            if (bias >= (1u << 24)) ok64 = 0;
-            t->packed64[j] = make_uint2(s | bias << 8, freq[s]);
+    } else {
+        for (uint32_t j = j0; j < j1; ++j) {
+            uint32_t s;
+            if (slot_in) {
+                s = slot_in[j];
+            } else {
+                while (s_cur < kMaxSym - 1 && cum[s_cur + 1] <= j) ++s_cur;
+                s = static_cast<uint32_t>(s_cur);
+            }
+            t->slot_sym[j] = static_cast<uint8_t>(s);
+            if (scale_bits <= kPackedMaxBits) {
+                const uint32_t f = freq[s];
+                const uint32_t bias = j - cum[s];
+                // f == 4096 (a single-symbol sb=12 table) does not fit 12
+                // bits: such tables take the two-lookup path
+                if (f < 1 || f > 4095 || bias >= 4096) ok = 0;
+                t->packed[j] = s | (bias & 0xFFFu) << 8 | (f & 0xFFFu) << 20;
+            }
+            if (scale_bits >= kPacked64MinBits && scale_bits <= kPacked64MaxBits) {
+                const uint32_t bias = j - cum[s];  // < 2^24 for every consistent table
+                if (bias >= (1u << 24)) ok64 = 0;
+                t->packed64[j] = make_uint2(s | bias << 8, freq[s]);
+            }
         }
     }
     __syncthreads();
