@@ -99,9 +99,19 @@ __device__ __forceinline__ void cp_async_wait() {
 //   q = floor(m * n / 2^(32+l)) = (umulhi(magic, n) + n) >> l   (33-bit sum).
 // m*d - 2^(32+l) lies in (0, 2^l], which makes q exact for all n < 2^32;
 // magic < 2^32 because 2^(l-1) < d. tests/test_host.py checks every d.
-__host__ __device__ inline void divmagic(uint32_t d, uint32_t *magic, uint32_t *l_out) {
+// ceil(log2 d) for d >= 1
+__host__ __device__ inline uint32_t ceil_log2(uint32_t d) {
+#ifdef __CUDA_ARCH__
+    return d <= 1u ? 0u : 32u - static_cast<uint32_t>(__clz(d - 1u));
+#else
     uint32_t l = 0;
-    while ((1ull << l) < d) ++l;  // l = ceil(log2 d)
+    while ((1ull << l) < d) ++l;
+    return l;
+#endif
+}
+
+__host__ __device__ inline void divmagic(uint32_t d, uint32_t *magic, uint32_t *l_out) {
+    const uint32_t l = ceil_log2(d);
     const uint64_t m = ((1ull << (32 + l)) / d) + 1;  // in (2^32, 2^33)
     *magic = static_cast<uint32_t>(m - (1ull << 32));
     *l_out = l;
@@ -167,8 +177,7 @@ struct EncFast {
             sh = 0u;
             bias = cum + m - 1u;
         } else {
-            uint32_t c = 0;
-            while ((1u << c) < f) ++c;
+            const uint32_t c = ceil_log2(f);
             M = static_cast<uint32_t>(((1ull << (31 + c)) + f - 1) / f);
             sh = c - 1u;
         }
@@ -197,8 +206,7 @@ struct EncFast12 {
             sh = 0u;
             bias = cum + m - 1u;
         } else {
-            uint32_t c = 0;
-            while ((1u << c) < f) ++c;
+            const uint32_t c = ceil_log2(f);
             M = static_cast<uint32_t>(((1ull << (31 + c)) + f - 1) / f);
             sh = c - 1u;
         }
