@@ -4,7 +4,9 @@
 // _core.decode_lanes_u16 (_core.pyx:130-173); both produce byte-identical
 // output (_pure.py:69-72), so one group-at-a-time kernel serves both.
 //
-// Warp kernel (N <= 32): one warp per stream (chunk), lane l = rANS lane l.
+// Warp kernel (N <= 32): one warp per stream (chunk), lane l = rANS lane l,
+// one CTA per SM holding all of the SM's chunks (<= 28 warps); the decoded
+// bytes go to a sink (HBM, or a consumer fused into the decoder).
 // Per group of N symbols (lanes.decode_step, lanes.py:138-151):
 //   pop:     slot = x & (m-1); s = LUT[slot]; x = f*(x >> sb) + slot - cum
 //   ballot:  mask = __ballot_sync(x < 2^16)            (lanes.ballot)
@@ -18,9 +20,10 @@
 // 512-word batch read starting anywhere in the ring never wraps: inside a
 // batch the read address is the batch base plus a running byte offset.
 //
-// N = 32 fast path: 16 groups (512 symbols) per batch, fully unrolled; the
-// ring is advanced and the 512 decoded bytes are written (one 16-byte
-// vector store per lane) once per batch, and truncation is checked once per
+// N = 32 fast path: 16 groups (512 symbols) per batch, fully unrolled, with
+// the packed LUT (32-bit entries for sb <= 12, 64-bit for sb 13-14); the
+// ring is advanced and the 512 decoded bytes are handed to the sink (one
+// 16-byte vector store per lane) once per batch, and truncation is checked once per
 // batch (pos is monotone, so "some group overran" == "pos > len at the end
 // of the batch"; reads past the payload hit zero-filled ring words and are
 // never used). Other N and the < 512-symbol tail run the per-group loop.

@@ -11,12 +11,15 @@
 // appear in ascending lane order -- lane i writes at
 // top - popc(mask) + popc(mask & lanemask_lt(i)).
 //
-// Warp kernel (N <= 32): one warp per chunk; message bytes are staged
+// Warp kernel (N <= 32): one warp per chunk, one CTA per SM holding all of
+// the SM's chunks (<= 28 warps; see kEncMaxWarps); message bytes are staged
 // backwards into a per-warp 2 KB shared ring by cp.async (4 x 512 B
-// segments); the per-symbol record {f, cum, magic, shifts} lives in shared
-// memory, and x / f is an exact multiply-high (Granlund-Montgomery), no
-// hardware divide. Block kernel (N > 32): one CTA per stream with a
-// CTA-wide scan over spill counts.
+// segments); the per-symbol records live in shared memory and x / f is an
+// exact multiply-high (Granlund-Montgomery), no hardware divide. For N = 32
+// the 512-byte blocks run as unrolled 16-group batches with the fast record
+// (common.cuh EncFast: 8 bytes, sb <= 13; EncFast12: sb = 14) when the table
+// allows it, else the 33-bit-magic record. Block kernel (N > 32): one CTA
+// per stream with a CTA-wide scan over spill counts.
 //
 // Framing: chunk k's payload sits at scratch[k*C + len_k - w_k, k*C + len_k);
 // an exclusive scan of w_k gives word offsets and a compaction kernel packs
@@ -25,7 +28,6 @@
 #include "kernels.cuh"
 
 namespace ilans {
-
 
 constexpr int kInSeg = 512;            // bytes per cp.async warp-copy
 constexpr int kInRing = 4 * kInSeg;    // 2 KB per warp
