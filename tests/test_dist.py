@@ -64,6 +64,18 @@ def _worker(rank, world, port, out):
                                                      12, 32)
     np.savez(out / f"rank{rank}.npz", total=total, freqs=np.asarray(freqs), payload=payload,
              offsets=offs, states=states)
+    # the cross-rank framing step: global word base and the gathered stream
+    from paper_1402_3392_b200.dist import gather_stream, global_word_base
+    from paper_1402_3392_b200.rans import SymbolTable
+
+    base, total_words = global_word_base(int(offs[-1]))
+    cc = gather_stream(torch.from_numpy(payload.view(np.int16).copy()),
+                       torch.from_numpy(offs.astype(np.int64)),
+                       torch.from_numpy(states.reshape(-1).view(np.int32).copy()),
+                       sh, N_BYTES, CHUNK, 32, SymbolTable(list(freqs), 12), dst=0)
+    np.savez(out / f"frame{rank}.npz", base=base, total_words=total_words,
+             container=np.frombuffer(cc.to_bytes(), np.uint8) if cc is not None
+             else np.zeros(0, np.uint8))
     dist.destroy_process_group()
 
 
@@ -91,3 +103,14 @@ def test_gloo_world2_histogram_allreduce_and_shard_streams(tmp_path):
     k0 = len(parts[0]["offsets"]) - 1
     assert np.array_equal(parts[0]["offsets"], offs[: k0 + 1])
     assert np.array_equal(parts[1]["offsets"] + offs[k0], offs[k0:])
+    # gathered on rank 0: byte-identical to the single-GPU ICH1 stream
+    from paper_1402_3392_b200.chunked import ChunkedContainer
+    from paper_1402_3392_b200.rans import SymbolTable
+
+    frames = [np.load(tmp_path / f"frame{r}.npz") for r in range(world)]
+    assert [int(fr["base"]) for fr in frames] == [0, int(offs[k0])]
+    assert all(int(fr["total_words"]) == int(offs[-1]) for fr in frames)
+    single = ChunkedContainer(32, CHUNK, N_BYTES, SymbolTable(freqs, 12), states,
+                              offs.astype(np.uint64), payload)
+    assert frames[0]["container"].tobytes() == single.to_bytes()
+    assert len(frames[1]["container"]) == 0

@@ -194,3 +194,21 @@ def test_stats_counters_single_digit_property():
     assert stats.encode_symbols == stats.decode_symbols == 250_000
     assert stats.encode_digits == stats.decode_digits > 0
     assert stats.max_encode_digits == stats.max_decode_digits == 1
+
+
+def test_sharded_codec_gather_single_rank_matches_encode_chunked():
+    """ShardedCodec (one rank, no process group): build_global_model +
+    encode + gather gives the same ICH1 bytes as encode_chunked."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import encode_chunked
+    from paper_1402_3392_b200.dist import ShardedCodec
+    from paper_1402_3392_b200.synth import synth_host
+
+    n, C = 2_000_003, 65536
+    msg = synth_host(n, 1.2, seed=9)
+    sc = ShardedCodec(n, 0, 1, C, 32, 12)
+    d = torch.from_numpy(msg).cuda()
+    sc.build_global_model(d)
+    sc.encode(d)
+    assert sc.gather(n).to_bytes() == encode_chunked(msg, None, 32, C, 12).to_bytes()
