@@ -421,3 +421,37 @@ def test_decode_fused_adler32_matches_zlib(n, C, lanes, sb, zipf):
     assert codec.adler32(d_msg, n).cpu().numpy().view(np.uint32).tolist() == want
     offs = codec.offsets[: k + 1].cpu().numpy()
     assert np.array_equal(codec.consumed[:k].cpu().numpy(), offs[1:] - offs[:-1])
+
+
+def test_fuzz_random_shapes_against_oracle():
+    """Randomized sweep over lane counts, chunk lengths, message lengths,
+    table shapes and scale_bits: chunked encode/decode and the single-stream
+    drop-ins agree with the oracle bit for bit."""
+    from paper_1402_3392_b200.chunked import decode_chunked, encode_chunked
+
+    import os
+
+    rng = np.random.default_rng(int(os.environ.get("ILANS_FUZZ_SEED", "2026")))
+    for it in range(int(os.environ.get("ILANS_FUZZ_ITERS", "60"))):
+        sb = int(rng.integers(1, 17))
+        n_sym = int(rng.integers(1, min(256, 1 << sb) + 1))
+        counts = rng.integers(0, 50, size=n_sym) ** int(rng.integers(1, 4))
+        counts[int(rng.integers(0, n_sym))] += 1
+        t = SymbolTable(oracle.quantize(counts, sb), sb)
+        n = int(rng.choice([0, 1, 31, 32, 33, 511, 512, 513, 4097, 70_001, 300_000]))
+        lanes = int(rng.choice([1, 2, 3, 7, 16, 31, 32]))
+        C = int(rng.choice([16, 512, 1024, 4096, 65536]))
+        msg = random_message(rng, t, n)
+        cc = encode_chunked(msg, t, lanes, C)
+        ref_p, ref_o, ref_s = oracle.encode_chunks_u16(msg, C, t.freq_u32, t.cum_u32, sb, lanes)
+        assert np.array_equal(cc.payload, ref_p), (it, sb, n, lanes, C)
+        assert np.array_equal(cc.states, ref_s), (it, sb, n, lanes, C)
+        assert np.array_equal(decode_chunked(cc), msg), (it, sb, n, lanes, C)
+        if n <= 70_001:
+            N = int(rng.choice([1, 5, 32, 33, 100]))
+            p, st = B.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, N)
+            rp, rs = oracle.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, N)
+            assert np.array_equal(p, rp) and np.array_equal(st, rs), (it, sb, n, N)
+            out, used = B.decode_interleaved_u16(p, st, t.slot_u8, t.freq_u32, t.cum_u32, sb,
+                                                 n, N)
+            assert np.array_equal(out, msg) and used == len(p), (it, sb, n, N)
