@@ -580,6 +580,11 @@ def run_b200(a):
                    "roofline_frac": gbs(enc_bytes, enc_ms) / hbm},
         "model_build": {"ms": model_ms, "GBps": gbs(n, model_ms)},
         "ratio": {"bits_per_byte": bpb, "entropy_bpb": H, "vs_entropy": bpb / H,
+                  # the quantized model's ideal code length for this message
+                  # (sum over symbols of sb - log2 f_s, from the counts)
+                  "model_ideal_bpb": float(
+                      (counts[: table.alphabet_size] * (table.scale_bits - np.log2(
+                          np.maximum(table.freq_u32, 1).astype(np.float64)))).sum() / n),
                   "single_stream_bits_per_byte": 8 * (single_hdr + 2 * total_words
                                                       - 4 * N * (k_chunks - 1)) / n,
                   "framed_bytes": framed, "payload_words": total_words},
