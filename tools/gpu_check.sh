@@ -1,8 +1,12 @@
+# One full GPU pass: parity tests, smoke, the bench line and the reference
+# arm, then the ncu evidence for one step (tools/profile_round.sh).
+# usage: bash tools/gpu_check.sh [tag]
 set -x
+tag=${1:-check}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
-timeout 600 python bench.py > gpurun_out/bench_b200.json 2> gpurun_out/bench_b200.err; tail -3 gpurun_out/bench_b200.err; cat gpurun_out/bench_b200.json
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>&1; cat gpurun_out/bench_ref.json | tail -2
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"histogram|build_table|encode_warp|compact|decode_warp|chunk_offsets" -c 6 -f -o gpurun_out/prof_r01c python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_ncu2.log 2>&1
-ls -la gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_tests.log 2>&1; tail -n 3 gpurun_out/${tag}_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()"
+timeout 900 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/${tag}_bench_ref.json 2>&1
+bash tools/profile_round.sh ${tag}
+ls -la gpurun_out | grep ${tag}
