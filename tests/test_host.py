@@ -40,6 +40,24 @@ def test_library_exports_every_declared_symbol():
     assert _lib.lib.ilans_table_bytes() > 65536
 
 
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/ilans_b200.h is a C ABI: a C11 translation unit that includes
+    it compiles and links against libilans_b200.so and runs a host-only
+    entry point (no device needed)."""
+    so_dir = ilb.__path__[0]
+    src = tmp_path / "abi.c"
+    src.write_text(
+        '#include "ilans_b200.h"\n#include <stdio.h>\n'
+        "int main(void) { printf(\"%d %zu\\n\", ilans_abi_version(), ilans_table_bytes());"
+        " return 0; }\n")
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", str(ROOT / "include"), str(src),
+                    "-L", so_dir, "-lilans_b200", f"-Wl,-rpath,{so_dir}", "-o", str(exe)],
+                   check=True, capture_output=True, text=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    assert out[0] == "1" and int(out[1]) == _lib.lib.ilans_table_bytes()
+
+
 def test_library_is_sm100a():
     so = ilb.__path__[0] + "/libilans_b200.so"
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so],
