@@ -210,7 +210,9 @@ __host__ __device__ constexpr size_t decode_warp_smem() { return kRingAllocBytes
 // Not inlined: with both LUT forms inlined into one kernel the packed
 // path's schedule degrades (~8% slower decode, measured); as a call each
 // body keeps its own register allocation.
-template <int KIND, class Sink>
+// SMALL: the instantiation for power-of-two N < 32 (512/N-group batches);
+// a separate body so the N = 32 batch loop keeps its own schedule.
+template <int KIND, class Sink, bool SMALL>
 __device__ __noinline__ void
 decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                  const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -287,11 +289,13 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
         sink.begin(k, cbase, lane);
         int64_t base = 0;
 
-        if (n_lanes == 32 && !trace.states) {
-            // ---------------- fast path: batches of kBatch full groups ------
-            // A batch reads <= 512 words, i.e. up to two segments past the
-            // one holding the cursor, so the ring runs one segment deeper
-            // here (wait<1>: everything but the newest segment has landed).
+        if ((SMALL || n_lanes == 32) && !trace.states) {
+            // ---------------- fast path: batches of 512 symbols -------------
+            // (kBatch groups of 32 lanes, or 512/N groups of N < 32 lanes for
+            // the power-of-two widths.) A batch reads <= 512 words, i.e. up
+            // to two segments past the one holding the cursor, so the ring
+            // runs one segment deeper here (wait<1>: everything but the
+            // newest segment has landed).
             const int64_t full = len / (32 * kBatch);
             uint32_t vb = static_cast<uint32_t>(v) << 1;  // byte cursor (mod 2^32)
             uint32_t seg_cur = 0;                          // vb >> 9 of the cursor
@@ -308,16 +312,36 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                 // past it, which the mirrored slots keep contiguous
                 const uint32_t a0 = ring_addr + (vb & (kRingBytes - 2));
                 uint32_t a = a0;
+                if (!SMALL) {
 #pragma unroll
-                for (int g = 0; g < kBatch; ++g) {
-                    const uint32_t s = lut.pop(x);
-                    const bool need = x < kLow;
-                    const uint32_t mk = __ballot_sync(0xffffffffu, need);
-                    // every lane loads (one wavefront either way), then selects
-                    const uint32_t w = lds_u16(mad_lo(__popc(mk * lt_mul), two, a));
-                    x = need ? x * 65536u + w : x;
-                    a = mad_lo(__popc(mk), two, a);
-                    obuf[g * 32 + lane] = static_cast<uint8_t>(s);
+                    for (int g = 0; g < kBatch; ++g) {
+                        const uint32_t s = lut.pop(x);
+                        const bool need = x < kLow;
+                        const uint32_t mk = __ballot_sync(0xffffffffu, need);
+                        // every lane loads (one wavefront either way), then selects
+                        const uint32_t w = lds_u16(mad_lo(__popc(mk * lt_mul), two, a));
+                        x = need ? x * 65536u + w : x;
+                        a = mad_lo(__popc(mk), two, a);
+                        obuf[g * 32 + lane] = static_cast<uint8_t>(s);
+                    }
+                } else {
+                    // N < 32: lanes >= N idle (their state stays 0, never
+                    // renormalises, never stores); 512/N groups per batch
+                    const bool on = lane < n_lanes;
+                    uint8_t *op = obuf + lane;
+                    for (int gb = 0; gb < 512; gb += 16 * n_lanes) {
+#pragma unroll
+                        for (int g = 0; g < 16; ++g) {
+                            const uint32_t s = lut.pop(x);
+                            const bool need = on && x < kLow;
+                            const uint32_t mk = __ballot_sync(0xffffffffu, need);
+                            const uint32_t w = lds_u16(mad_lo(__popc(mk * lt_mul), two, a));
+                            x = need ? x * 65536u + w : x;
+                            a = mad_lo(__popc(mk), two, a);
+                            if (on) *op = static_cast<uint8_t>(s);
+                            op += n_lanes;
+                        }
+                    }
                 }
                 vb = vb0 + (a - a0);
                 __syncwarp();
@@ -404,6 +428,27 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
     }
 }
 
+template <int MAXKIND, class Sink, bool SMALL>
+__device__ __forceinline__ void
+decode_warp_dispatch(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                     const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                     int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab, Sink out,
+                     uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
+                     DStatus *__restrict__ status, DecodeTrace trace, uint8_t *smem, int sb) {
+    if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
+        decode_warp_body<kLutPacked32, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+                                                    n_chunks, n_lanes, tab, out, consumed,
+                                                    final_states, status, trace, smem, sb);
+    else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
+        decode_warp_body<kLutPacked64, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+                                                    n_chunks, n_lanes, tab, out, consumed,
+                                                    final_states, status, trace, smem, sb);
+    else
+        decode_warp_body<kLutGeneric, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+                                                   n_chunks, n_lanes, tab, out, consumed,
+                                                   final_states, status, trace, smem, sb);
+}
+
 // MAXKIND: the packed form this launch's shared memory was sized for (it
 // also fits the two-lookup form); the device table's flags pick which one
 // runs (a single-symbol sb=12 table has f = 4096, which the 12-bit field of
@@ -422,18 +467,14 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
         return;
     }
-    if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
-        decode_warp_body<kLutPacked32, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
-                                             n_lanes, tab, out, consumed, final_states, status,
-                                             trace, smem, sb);
-    else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
-        decode_warp_body<kLutPacked64, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
-                                             n_lanes, tab, out, consumed, final_states, status,
-                                             trace, smem, sb);
+    if (n_lanes < 32 && (n_lanes & (n_lanes - 1)) == 0)
+        decode_warp_dispatch<MAXKIND, Sink, true>(payload, offsets, states, n, chunk_len,
+                                                  n_chunks, n_lanes, tab, out, consumed,
+                                                  final_states, status, trace, smem, sb);
     else
-        decode_warp_body<kLutGeneric, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
-                                            n_lanes, tab, out, consumed, final_states, status,
-                                            trace, smem, sb);
+        decode_warp_dispatch<MAXKIND, Sink, false>(payload, offsets, states, n, chunk_len,
+                                                   n_chunks, n_lanes, tab, out, consumed,
+                                                   final_states, status, trace, smem, sb);
 }
 
 // ---------------------------------------------------------------------------

@@ -119,7 +119,9 @@ struct SpillStage {
 // format's case; long long only for huge single-stream calls).
 // F12: the sb = 14 instantiation (12-byte fast records); the other one
 // carries the 8-byte fast loop, so neither pays for the other's registers.
-template <typename Idx, bool F12>
+// SMALL: power-of-two N < 32 (512/N-group batches with the fast records),
+// a separate instantiation so the N = 32 loops keep their schedule.
+template <typename Idx, bool F12, bool SMALL>
 __global__ void __launch_bounds__(kEncMaxWarps * 32, 1)
 encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
@@ -178,10 +180,11 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         Idx top = len;
         // N = 32: the 512-byte blocks below `full` run as unrolled batches of
         // 16 groups after the per-group loop has coded the tail [full*512, len)
-        const Idx full = n_lanes == 32 ? (len >> 9) : 0;
+        // (and power-of-two N < 32 with a fast record: 512/N groups each)
+        const Idx full = (SMALL ? (fast || fast12) : n_lanes == 32) ? (len >> 9) : 0;
         const Idx groups = (len + n_lanes - 1) / n_lanes;
         bool bad = false;
-        for (Idx gi = groups - 1; gi >= (full << 4); --gi) {
+        for (Idx gi = groups - 1; gi >= (SMALL ? full * (512 / n_lanes) : full << 4); --gi) {
             const Idx base = gi * n_lanes;
             const Idx left = len - base;
             const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
@@ -240,7 +243,50 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             uint32_t zero_f = 0;
             uint32_t topb = static_cast<uint32_t>(top) << 1;  // ring byte cursor
             const uint32_t topb0 = topb;
-            if (fast) {
+            if (SMALL) {
+                // N < 32 (a power of two): 512/N groups of N lanes; lanes >= N
+                // follow lane 0's symbol (a valid record for macc) and never
+                // spill; their state is never stored
+                const bool on = lane < n_lanes;
+                const uint8_t *bp = blk + (kInSeg - n_lanes) + (on ? lane : 0);
+                uint32_t sym_n = *bp;
+                for (int gb = kInSeg / n_lanes - 1; gb >= 0; gb -= 16) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        // next group's symbol one ahead (below blk on the
+                        // last group: a harmless shared read, never used)
+                        bp -= n_lanes;
+                        const uint32_t sym = sym_n;
+                        sym_n = *bp;
+                        const uint2 a = encf[sym];
+                        macc &= a.x;
+                        bool spill;
+                        uint32_t z = 0;
+                        if (!F12) {
+                            const uint32_t xm = x & ~lowm;
+                            spill = on && xm + a.y < xm;
+                        } else {
+                            z = encz[sym];
+                            spill = on && (x | lowm) >= a.y;
+                        }
+                        const uint32_t mk = __ballot_sync(0xffffffffu, spill);
+                        topb -= two * __popc(mk);
+                        if (spill)
+                            sts16(oring_addr |
+                                      ((topb + two * __popc(mk * lt_mul)) & (kOutRingBytes - 2)),
+                                  x);
+                        x = spill ? x >> 16 : x;
+                        uint32_t q = __umulhi(x, a.x);
+                        if (!F12) {
+                            asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
+                            x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
+                        } else {
+                            asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
+                            x = q * (a.y & lowm) + (x + (z >> 17));
+                        }
+                    }
+                }
+            } else if (fast) {
                 // Records are loaded one group ahead of their use: the spill
                 // stores go to shared memory too, so the compiler cannot
                 // hoist a later group's loads above them by itself.
@@ -481,12 +527,23 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
         // the table's scale_bits is on the device; the sb = 14 instantiation
         // is picked by the caller's scale_bits and re-checks the flag itself
         const bool sb14 = scale_bits == 14;
+        const bool small = n_lanes < 32 && (n_lanes & (n_lanes - 1)) == 0;
         if (chunk_len < (int64_t(1) << 30)) {
-            if (sb14) go(encode_warp_kernel<int, true>);
-            else go(encode_warp_kernel<int, false>);
+            if (small) {
+                if (sb14) go(encode_warp_kernel<int, true, true>);
+                else go(encode_warp_kernel<int, false, true>);
+            } else {
+                if (sb14) go(encode_warp_kernel<int, true, false>);
+                else go(encode_warp_kernel<int, false, false>);
+            }
         } else {
-            if (sb14) go(encode_warp_kernel<long long, true>);
-            else go(encode_warp_kernel<long long, false>);
+            if (small) {
+                if (sb14) go(encode_warp_kernel<long long, true, true>);
+                else go(encode_warp_kernel<long long, false, true>);
+            } else {
+                if (sb14) go(encode_warp_kernel<long long, true, false>);
+                else go(encode_warp_kernel<long long, false, false>);
+            }
         }
     }
     ilans_note_launch();

@@ -169,7 +169,7 @@ def test_max_lanes_65535():
 def test_truncation_raises_like_reference():
     rng = np.random.default_rng(63)
     t = random_table(rng)
-    for lanes in (1, 2, 4, 32, 40):
+    for lanes in (1, 2, 4, 8, 16, 32, 40):
         msg = random_message(rng, t, 1500)
         c = ilb.encode_interleaved(msg, t, lanes, WORD16)
         if len(c.payload) == 0:
@@ -212,9 +212,13 @@ def test_fast_encoder_record_edges(sb):
     for freq in tables:
         t = SymbolTable(freq, sb)
         msg = random_message(rng, t, 70_001)
-        payload, states = B.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, 32)
-        ref_p, ref_s = oracle.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, 32)
-        assert np.array_equal(payload, ref_p) and np.array_equal(states, ref_s), freq
+        for lanes in (32, 16, 8, 4, 1):  # N < 32 powers of two: 512/N-group batches
+            payload, states = B.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, lanes)
+            ref_p, ref_s = oracle.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, lanes)
+            assert np.array_equal(payload, ref_p) and np.array_equal(states, ref_s), (freq, lanes)
+            out, used = B.decode_interleaved_u16(payload, states, t.slot_u8, t.freq_u32,
+                                                 t.cum_u32, sb, len(msg), lanes)
+            assert np.array_equal(out, msg) and used == len(payload), (freq, lanes)
         cc = encode_chunked(msg, t, 32, 4096)
         ref_p, _, ref_s = oracle.encode_chunks_u16(msg, 4096, t.freq_u32, t.cum_u32, sb, 32)
         assert np.array_equal(cc.payload, ref_p) and np.array_equal(cc.states, ref_s), freq
@@ -226,14 +230,15 @@ def test_unencodable_symbol_in_fast_batches():
     names the symbol at the highest offending index (the reference's
     backward walk meets it first, _core.pyx:33-34)."""
     t = SymbolTable([2048, 2047, 0, 0, 1], 12)
-    msg = np.zeros(70_000, dtype=np.uint8)
-    msg[100], msg[60_000] = 2, 3
-    with pytest.raises(UnencodableSymbolError, match="symbol 3"):
-        ilb.encode_interleaved(msg, t, 32, WORD16)
-    msg[60_000] = 1
-    msg[40_000] = 2
-    with pytest.raises(UnencodableSymbolError, match="symbol 2"):
-        ilb.encode_interleaved(msg, t, 32, WORD16)
+    for lanes in (32, 8, 1):
+        msg = np.zeros(70_000, dtype=np.uint8)
+        msg[100], msg[60_000] = 2, 3
+        with pytest.raises(UnencodableSymbolError, match="symbol 3"):
+            ilb.encode_interleaved(msg, t, lanes, WORD16)
+        msg[60_000] = 1
+        msg[40_000] = 2
+        with pytest.raises(UnencodableSymbolError, match="symbol 2"):
+            ilb.encode_interleaved(msg, t, lanes, WORD16)
 
 
 def test_trailing_garbage_warns():
@@ -439,7 +444,7 @@ def test_fuzz_random_shapes_against_oracle():
         counts[int(rng.integers(0, n_sym))] += 1
         t = SymbolTable(oracle.quantize(counts, sb), sb)
         n = int(rng.choice([0, 1, 31, 32, 33, 511, 512, 513, 4097, 70_001, 300_000]))
-        lanes = int(rng.choice([1, 2, 3, 7, 16, 31, 32]))
+        lanes = int(rng.choice([1, 2, 3, 4, 7, 8, 16, 31, 32]))
         C = int(rng.choice([16, 512, 1024, 4096, 65536]))
         msg = random_message(rng, t, n)
         cc = encode_chunked(msg, t, lanes, C)
@@ -448,7 +453,7 @@ def test_fuzz_random_shapes_against_oracle():
         assert np.array_equal(cc.states, ref_s), (it, sb, n, lanes, C)
         assert np.array_equal(decode_chunked(cc), msg), (it, sb, n, lanes, C)
         if n <= 70_001:
-            N = int(rng.choice([1, 5, 32, 33, 100]))
+            N = int(rng.choice([1, 2, 5, 8, 16, 32, 33, 100]))
             p, st = B.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, N)
             rp, rs = oracle.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, N)
             assert np.array_equal(p, rp) and np.array_equal(st, rs), (it, sb, n, N)
