@@ -41,6 +41,7 @@ typedef enum ilans_rc {
     ILANS_ERR_UNSUPPORTED = 4,  /* UnsupportedVariantError                    */
     ILANS_ERR_CUDA = 5,         /* CUDA runtime failure / no device           */
     ILANS_ERR_FORMAT = 6,       /* FormatError (byte8 refill loop runaway)    */
+    ILANS_ERR_SCHEDULE = 7,     /* ScheduleError (mux schedule vs streams)    */
 } ilans_rc;
 
 typedef struct ilans_status {
@@ -250,6 +251,82 @@ int ilans_adler32_chunks_dev(const uint8_t *d_data, int64_t n, int64_t chunk_len
  * Symbol = #{k : d_cdf[k] <= u}, clamped to 255. */
 int ilans_synth_bytes_dev(uint8_t *d_out, int64_t n, uint64_t seed, int64_t first_index,
                           const uint32_t *d_cdf, void *stream);
+
+/* -------------------------------------------------------------------------
+ * 4. Stream multiplexer (reference pkg/src/ilans/mux.py). K independently
+ *    coded streams -- rANS (RansStreamCodec, mux.py:82-128) or raw
+ *    fixed-width values (RawStreamCodec, mux.py:131-163) -- merged into one
+ *    payload in the byte order a decoder following `schedule` consumes them
+ *    (schedule[t] = stream decoded at step t). Host buffers in and out, like
+ *    family 1. The merge is a scan + scatter on the device: per-symbol byte
+ *    counts come from the encoder (the digits spilled while pushing symbol i
+ *    are the ones refilled after popping it), a stable sort of the schedule
+ *    maps steps to stream positions, an exclusive scan gives each step's
+ *    offset in the muxed payload. Schedules are validated by the caller
+ *    (mux.py:259-269); n_steps <= 2^30 - 1, n_streams <= 65535.
+ * ---------------------------------------------------------------------- */
+enum { ILANS_MUX_RANS = 0, ILANS_MUX_RAW = 1 };
+
+typedef struct ilans_mux_stream {
+    int32_t kind;         /* ILANS_MUX_RANS or ILANS_MUX_RAW                        */
+    int32_t nbytes;       /* rANS: bytes per digit (digit_bits / 8); raw: per value */
+    int32_t digit_bits;   /* rANS digit width (8 or 16); raw: width_bits (1..32)    */
+    int32_t scale_bits;   /* rANS table scale_bits                                  */
+    uint32_t lower_bound; /* rANS L: states live in [L, L << digit_bits)            */
+    int32_t n_sym;        /* rANS alphabet size                                     */
+    int64_t freq_off;     /* rANS: freq[freq_off .. +n_sym), cum[cum_off .. +n_sym] */
+    int64_t cum_off;
+    int64_t slot_off;     /* rANS: slot[slot_off .. + 2^scale_bits) (decode calls)  */
+} ilans_mux_stream;
+
+/* Encode every stream in segments and merge them (mux.mux_with_flush,
+ * mux.py:329-433; encode_multistream + mux when flush_interval = 0, and
+ * encode_multistream alone when schedule lists the streams back to back).
+ * symbols: u32 values of stream 0, then stream 1, ... (schedule order within
+ * a stream == message order). A stream's steps in epoch t / flush_interval
+ * form one segment coded from a fresh state; the first segment's final
+ * state is the stream header (stream_state[j]; L for an empty rANS stream),
+ * later ones travel inline (4 bytes LE) ahead of the segment's digits.
+ * Outputs: the muxed payload (payload_cap >= 8 * n_steps suffices),
+ * stream_bytes[j] = stream j's bytes in it, the segment count and the
+ * encoder-side buffering peak (MuxBudget.max_buffered).
+ * Errors: ILANS_ERR_UNENCODABLE (f == 0; st->stream, st->index = position
+ * in the stream, st->symbol), ILANS_ERR_VALUE. */
+int ilans_mux_encode(const ilans_mux_stream *streams, int32_t n_streams, const uint32_t *freq,
+                     int64_t n_freq, const uint32_t *cum, int64_t n_cum,
+                     const uint32_t *symbols, const int32_t *schedule, int64_t n_steps,
+                     int64_t flush_interval, uint8_t *payload_out, int64_t payload_cap,
+                     int64_t *payload_len, uint32_t *stream_state, uint64_t *stream_bytes,
+                     int64_t *segment_count, uint64_t *max_buffered, ilans_status *st);
+
+/* Merge pre-encoded single-segment stream buffers by the schedule
+ * (mux.mux, mux.py:283-313): stream j's header is
+ * headers[header_off[j] .. header_off[j+1]) and its payload
+ * payloads[payload_off[j] .. payload_off[j+1]); symbol_counts[j] symbols.
+ * out receives payload_off[K] bytes. Errors, in the reference's order:
+ * ILANS_ERR_TRUNCATED / ILANS_ERR_FORMAT for the first stream whose header
+ * state cannot load, ILANS_ERR_TRUNCATED when a stream's payload runs out,
+ * ILANS_ERR_SCHEDULE for the first stream not fully consumed. */
+int ilans_mux_merge(const ilans_mux_stream *streams, int32_t n_streams, const uint32_t *freq,
+                    int64_t n_freq, const uint32_t *cum, int64_t n_cum, const uint8_t *slot,
+                    int64_t n_slot, const uint8_t *headers, const uint64_t *header_off,
+                    const uint8_t *payloads, const uint64_t *payload_off,
+                    const int64_t *symbol_counts, const int32_t *schedule, int64_t n_steps,
+                    uint8_t *out, ilans_status *st);
+
+/* Decode every stream back out of a muxed payload (mux.demux_decode,
+ * mux.py:436-475): symbols_out[t] = the value decoded at schedule step t.
+ * A sequential walk by construction (each step's read size depends on the
+ * state of the stream it decodes), run by one device thread. *unread =
+ * payload bytes left after the walk (the caller's TrailingGarbageWarning).
+ * Errors: ILANS_ERR_TRUNCATED, ILANS_ERR_FORMAT (state outside
+ * [L, L << digit_bits); st->stream, st->index = step or -1 for a header). */
+int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_streams, const uint32_t *freq,
+                    int64_t n_freq, const uint32_t *cum, int64_t n_cum, const uint8_t *slot,
+                    int64_t n_slot, const uint8_t *headers, const uint64_t *header_off,
+                    const uint8_t *payload, int64_t payload_len, const int32_t *schedule,
+                    int64_t n_steps, int64_t flush_interval, uint32_t *symbols_out,
+                    int64_t *unread, ilans_status *st);
 
 #ifdef __cplusplus
 }

@@ -8,7 +8,7 @@ libilans_b200.so. Chunked, HBM-resident and multi-GPU entry points live in
 ``chunked`` and ``dist``.
 """
 
-from . import backend, interleave, lanes, rans
+from . import backend, interleave, lanes, mux, rans
 from .errors import (
     CodecError,
     FormatError,

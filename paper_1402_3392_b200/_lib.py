@@ -17,6 +17,7 @@ import numpy as np
 
 from .errors import (
     FormatError,
+    ScheduleError,
     TruncatedStreamError,
     UnencodableSymbolError,
     UnsupportedVariantError,
@@ -24,7 +25,9 @@ from .errors import (
 
 LIB_PATH = Path(os.environ.get("ILANS_B200_LIB", Path(__file__).resolve().parent / "libilans_b200.so"))
 
-OK, ERR_VALUE, ERR_UNENCODABLE, ERR_TRUNCATED, ERR_UNSUPPORTED, ERR_CUDA, ERR_FORMAT = range(7)
+(OK, ERR_VALUE, ERR_UNENCODABLE, ERR_TRUNCATED, ERR_UNSUPPORTED, ERR_CUDA, ERR_FORMAT,
+ ERR_SCHEDULE) = range(8)
+MUX_RANS, MUX_RAW = 0, 1
 
 
 class Status(ctypes.Structure):
@@ -37,6 +40,22 @@ class Status(ctypes.Structure):
         ("max_digits", ctypes.c_int32),
         ("consumed", ctypes.c_int64),
         ("message", ctypes.c_char * 128),
+    ]
+
+
+class MuxStream(ctypes.Structure):
+    """ilans_mux_stream: one multiplexed stream's coder parameters."""
+
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("nbytes", ctypes.c_int32),
+        ("digit_bits", ctypes.c_int32),
+        ("scale_bits", ctypes.c_int32),
+        ("lower_bound", ctypes.c_uint32),
+        ("n_sym", ctypes.c_int32),
+        ("freq_off", ctypes.c_int64),
+        ("cum_off", ctypes.c_int64),
+        ("slot_off", ctypes.c_int64),
     ]
 
 
@@ -100,6 +119,15 @@ PROTOTYPES = [
      [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
     ("ilans_adler32_chunks_dev", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp]),
     ("ilans_synth_bytes_dev", ctypes.c_int, [_vp, _i64, _u64, _i64, _vp, _vp]),
+    ("ilans_mux_encode", ctypes.c_int,
+     [_vp, _i32, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp,
+      _vp, _st]),
+    ("ilans_mux_merge", ctypes.c_int,
+     [_vp, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp,
+      _st]),
+    ("ilans_mux_demux", ctypes.c_int,
+     [_vp, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp,
+      _vp, _st]),
 ]
 
 for _name, _res, _args in PROTOTYPES:
@@ -123,6 +151,8 @@ def raise_for(rc: int, st: Status, what: str = "") -> None:
         raise UnsupportedVariantError(msg)
     if rc == ERR_FORMAT:
         raise FormatError(msg)
+    if rc == ERR_SCHEDULE:
+        raise ScheduleError(msg)
     if rc == ERR_VALUE:
         raise ValueError(msg)
     raise RuntimeError(f"ilans-b200 CUDA failure in {what}: {msg}")

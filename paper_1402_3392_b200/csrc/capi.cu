@@ -75,38 +75,7 @@ cudaError_t launch_build_table(const unsigned long long *d_counts, const uint32_
 
 using namespace ilans;
 
-// ---------------------------------------------------------------------------
-// status helpers
-// ---------------------------------------------------------------------------
-static void st_clear(ilans_status *st) {
-    if (!st) return;
-    std::memset(st, 0, sizeof(*st));
-    st->stream = -1;
-    st->index = -1;
-    st->symbol = -1;
-}
-
-static int st_fail(ilans_status *st, int code, const char *fmt, ...) {
-    if (st) {
-        st->code = code;
-        va_list ap;
-        va_start(ap, fmt);
-        std::vsnprintf(st->message, sizeof(st->message), fmt, ap);
-        va_end(ap);
-    }
-    return code;
-}
-
-static int st_cuda(ilans_status *st, cudaError_t e, const char *where) {
-    if (st) st->cuda_error = static_cast<int32_t>(e);
-    return st_fail(st, ILANS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
-}
-
-#define CK(expr)                                              \
-    do {                                                      \
-        cudaError_t _e = (expr);                              \
-        if (_e != cudaSuccess) return st_cuda(st, _e, #expr); \
-    } while (0)
+#include "status.cuh"
 
 // ---------------------------------------------------------------------------
 // per-device context for the host-buffer drop-ins
@@ -177,6 +146,15 @@ int read_dstatus(const DStatus *d, cudaStream_t s, DStatus *h, ilans_status *st)
 }
 
 }  // namespace
+
+int ilans_host_session(ilans_status *st, cudaStream_t *stream, std::unique_lock<std::mutex> *lock) {
+    Ctx *cp = nullptr;
+    if (int rc = current_device(st, &cp)) return rc;
+    *lock = std::unique_lock<std::mutex>(cp->mu);
+    if (int rc = ctx_init(*cp, st)) return rc;
+    *stream = cp->stream;
+    return ILANS_OK;
+}
 
 // ---------------------------------------------------------------------------
 // library
