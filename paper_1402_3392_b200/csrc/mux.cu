@@ -165,14 +165,28 @@ __global__ void mux_encode_segments_kernel(const ilans_mux_stream *__restrict__ 
     }
 }
 
+// Decode lookup per slot of every rANS stream's table, at the slot array's
+// offsets: lo = symbol | (slot - cum[symbol]) << 8, hi = f[symbol], so a pop
+// is one load: x' = hi * (x >> sb) + (lo >> 8) (rans.pop_symbol).
+__global__ void mux_lut_kernel(const ilans_mux_stream *__restrict__ streams, int K,
+                               const uint32_t *__restrict__ freq, const uint32_t *__restrict__ cum,
+                               const uint8_t *__restrict__ slot, uint2 *lut) {
+    for (int j = blockIdx.x; j < K; j += gridDim.x) {
+        const ilans_mux_stream p = streams[j];
+        if (p.kind != ILANS_MUX_RANS) continue;
+        for (uint32_t i = threadIdx.x; i < (1u << p.scale_bits); i += blockDim.x) {
+            const uint32_t s = slot[p.slot_off + i];
+            lut[p.slot_off + i] = make_uint2(s | (i - cum[p.cum_off + s]) << 8, freq[p.freq_off + s]);
+        }
+    }
+}
+
 // Merge of pre-encoded buffers (mux.mux): one thread per stream replays its
 // decoder (mux._RansStreamDecoder, mux.py:107-128) over its own payload to
 // get each symbol's read count. err[j]: 0 ok, 1 header too short, 2 header
 // state outside [L, limit), 3 payload exhausted, 4 payload not consumed.
 __global__ void mux_replay_streams_kernel(const ilans_mux_stream *__restrict__ streams, int K,
-                                          const uint32_t *__restrict__ freq,
-                                          const uint32_t *__restrict__ cum,
-                                          const uint8_t *__restrict__ slot, const uint8_t *hdr,
+                                          const uint2 *__restrict__ lut, const uint8_t *hdr,
                                           const uint64_t *hdr_off, const uint8_t *pay,
                                           const uint64_t *pay_off, const int64_t *sym_off,
                                           uint8_t *dcnt, uint64_t *srcpos, int32_t *err,
@@ -204,16 +218,13 @@ __global__ void mux_replay_streams_kernel(const ilans_mux_stream *__restrict__ s
             err_val[j] = x;
             continue;
         }
-        const uint32_t *fr = freq + p.freq_off;
-        const uint32_t *cu = cum + p.cum_off;
-        const uint8_t *sl = slot + p.slot_off;
+        const uint2 *lt = lut + p.slot_off;
         const uint32_t mmask = (1u << p.scale_bits) - 1u;
         uint64_t cur = 0;
         int32_t e = 0;
         for (int64_t k = 0; k < n && !e; ++k) {
-            const uint32_t sidx = x & mmask;
-            const uint32_t s = sl[sidx];
-            x = static_cast<uint32_t>(uint64_t(fr[s]) * (x >> p.scale_bits) + sidx - cu[s]);
+            const uint2 en = lt[x & mmask];
+            x = en.y * (x >> p.scale_bits) + (en.x >> 8);
             const uint64_t p0 = cur;
             while (x < L) {
                 if (cur + nb > len) {
@@ -287,30 +298,71 @@ struct DemuxStatus {
     uint64_t pos;    // payload bytes read
 };
 
-// demux_decode (mux.py:436-475) on one thread: headers first, then the
-// schedule; inline segment states at epoch changes (mux.py:459-465).
-__global__ void demux_kernel(const ilans_mux_stream *__restrict__ streams, int K,
-                             const uint32_t *__restrict__ freq, const uint32_t *__restrict__ cum,
-                             const uint8_t *__restrict__ slot, const uint8_t *hdr,
-                             const uint64_t *hdr_off, const uint8_t *pay, uint64_t plen,
-                             const int32_t *__restrict__ sched, int64_t T, int64_t F,
-                             uint32_t *state, int64_t *cur_epoch, uint32_t *out,
-                             DemuxStatus *st) {
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+// Per-stream record for the walk, one 32-bit word per field so the loop
+// does no field extraction: lut offset, L, slot mask, sb, digit_bits,
+// nbytes, digit / value mask, raw flag.
+struct __align__(16) WalkDesc {
+    uint32_t lut_off, L, mask, sb, bits, nb, dmask, raw;
+};
+
+__device__ __forceinline__ bool state_ok(uint32_t x, const WalkDesc &d) {
+    return x >= d.L && (uint64_t(x) >> d.bits) < uint64_t(d.L);
+}
+
+// 4 payload bytes at any byte offset (two aligned words + a funnel shift;
+// the device payload is 8-byte padded and 4-byte aligned)
+__device__ __forceinline__ uint32_t load4(const uint32_t *__restrict__ w, uint32_t pos) {
+    const uint32_t q = pos >> 2;
+    return __funnelshift_r(__ldg(w + q), __ldg(w + q + 1), (pos & 3u) * 8u);
+}
+
+// demux_decode (mux.py:436-475): headers first (stream order), then the
+// schedule; a stream's state reloads inline when its epoch changes
+// (mux.py:459-465). One thread walks: each step's read offset depends on
+// the refill count of the step before, so there is nothing to split; the
+// loop is a latency chain (shared load of the stream's state -> lookup ->
+// multiply-add -> compare -> shift-in), kept in 32-bit arithmetic. SMEM:
+// per-stream records, states, epochs and the decode lookups are staged in
+// shared memory (they fit for up to a few thousand streams / tables). The
+// next 4 payload bytes are loaded before the pop decides how many of them
+// it needs, so that load overlaps the lookup.
+template <bool SMEM>
+__global__ void __launch_bounds__(256) demux_kernel(
+    const WalkDesc *__restrict__ gdesc, int K, const uint2 *__restrict__ glut, int64_t n_lut,
+    const uint8_t *hdr, const uint64_t *hdr_off, const uint32_t *__restrict__ pay, uint32_t plen,
+    const int32_t *__restrict__ sched, int32_t T, int32_t F, uint32_t *gstate, int32_t *gepoch,
+    uint32_t *__restrict__ out, DemuxStatus *st) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    const WalkDesc *desc = gdesc;
+    const uint2 *lut = glut;
+    uint32_t *state = gstate;
+    int32_t *epoch = gepoch;
+    if (SMEM) {
+        WalkDesc *sd = reinterpret_cast<WalkDesc *>(dsm);
+        uint2 *sl = reinterpret_cast<uint2 *>(sd + K);
+        for (int64_t i = threadIdx.x; i < n_lut; i += blockDim.x) sl[i] = glut[i];
+        for (int j = threadIdx.x; j < K; j += blockDim.x) sd[j] = gdesc[j];
+        lut = sl;
+        desc = sd;
+        state = reinterpret_cast<uint32_t *>(sl + n_lut);
+        epoch = reinterpret_cast<int32_t *>(state + K);
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
     st->code = 0;
     st->stream = -1;
     st->step = -1;
     for (int j = 0; j < K; ++j) {
-        const ilans_mux_stream p = streams[j];
-        cur_epoch[j] = -1;
-        if (p.kind == ILANS_MUX_RAW) continue;
+        const WalkDesc d = desc[j];
+        epoch[j] = -1;
+        if (d.raw) continue;  // raw: no state
         if (hdr_off[j + 1] - hdr_off[j] < 4) {
             st->code = ILANS_ERR_TRUNCATED;
             st->stream = j;
             return;
         }
         const uint32_t x = load_le(hdr + hdr_off[j], 4);
-        if (x < p.lower_bound || uint64_t(x) >= (uint64_t(p.lower_bound) << p.digit_bits)) {
+        if (!state_ok(x, d)) {
             st->code = ILANS_ERR_FORMAT;
             st->stream = j;
             st->value = x;
@@ -318,28 +370,31 @@ __global__ void demux_kernel(const ilans_mux_stream *__restrict__ streams, int K
         }
         state[j] = x;
     }
-    uint64_t pos = 0;
-    for (int64_t t = 0; t < T; ++t) {
-        const int sid = sched[t];
-        const ilans_mux_stream p = streams[sid];
-        const int nb = p.nbytes;
-        const int64_t e = F > 0 ? t / F : 0;
-        if (cur_epoch[sid] < 0) {
-            cur_epoch[sid] = e;
-        } else if (e > cur_epoch[sid]) {
-            cur_epoch[sid] = e;
-            if (p.kind != ILANS_MUX_RAW) {  // raw streams have no state to reload
-                if (pos + 4 > plen) {
-                    st->code = ILANS_ERR_TRUNCATED;
-                    st->stream = sid;
-                    st->step = t;
-                    st->pos = pos;
-                    return;
-                }
-                const uint32_t x = load_le(pay + pos, 4);
+    uint32_t pos = 0;
+    int32_t e = 0;
+    int32_t next_b = F;  // F = INT32_MAX: a single epoch
+    int32_t sid_n = sched[0];  // the device schedule is padded
+    int32_t t = 0;
+    for (; t < T; ++t) {
+        const int32_t sid = sid_n;
+        sid_n = sched[t + 1];
+        if (t == next_b) {
+            ++e;
+            next_b += F;
+        }
+        const WalkDesc d = desc[sid];
+        uint32_t x = state[sid];
+        // the two words under the cursor; combined only where a digit is
+        // consumed, so the load's latency hides behind the lookup
+        uint32_t w0 = __ldg(pay + (pos >> 2)), w1 = __ldg(pay + (pos >> 2) + 1);
+        const int32_t ep = epoch[sid];
+        if (ep != e) {
+            epoch[sid] = e;
+            if (ep >= 0 && !d.raw) {  // a later segment: its state inline
+                if (pos + 4 > plen) break;
+                x = __funnelshift_r(w0, w1, (pos & 3u) * 8u);
                 pos += 4;
-                if (x < p.lower_bound ||
-                    uint64_t(x) >= (uint64_t(p.lower_bound) << p.digit_bits)) {
+                if (!state_ok(x, d)) {
                     st->code = ILANS_ERR_FORMAT;
                     st->stream = sid;
                     st->step = t;
@@ -347,39 +402,35 @@ __global__ void demux_kernel(const ilans_mux_stream *__restrict__ streams, int K
                     st->pos = pos;
                     return;
                 }
-                state[sid] = x;
+                w0 = __ldg(pay + (pos >> 2));
+                w1 = __ldg(pay + (pos >> 2) + 1);
             }
         }
-        if (p.kind == ILANS_MUX_RAW) {
-            if (pos + nb > plen) {
-                st->code = ILANS_ERR_TRUNCATED;
-                st->stream = sid;
-                st->step = t;
-                st->pos = pos;
-                return;
-            }
-            out[t] = load_le(pay + pos, nb);
-            pos += nb;
+        if (d.raw) {  // raw value
+            const uint32_t v = __funnelshift_r(w0, w1, (pos & 3u) * 8u);
+            pos += d.nb;
+            if (pos > plen) break;
+            out[t] = v & d.dmask;
             continue;
         }
-        uint32_t x = state[sid];
-        const uint32_t sidx = x & ((1u << p.scale_bits) - 1u);
-        const uint32_t s = slot[p.slot_off + sidx];
-        x = static_cast<uint32_t>(uint64_t(freq[p.freq_off + s]) * (x >> p.scale_bits) + sidx -
-                                  cum[p.cum_off + s]);
-        while (x < p.lower_bound) {
-            if (pos + nb > plen) {
-                st->code = ILANS_ERR_TRUNCATED;
-                st->stream = sid;
-                st->step = t;
-                st->pos = pos;
-                return;
+        const uint2 en = lut[d.lut_off + (x & d.mask)];
+        x = en.y * (x >> d.sb) + (en.x >> 8);
+        if (x < d.L) {
+            x = (x << d.bits) | (__funnelshift_r(w0, w1, (pos & 3u) * 8u) & d.dmask);
+            pos += d.nb;
+            while (x < d.L) {  // byte digits: up to 3 per symbol
+                x = (x << d.bits) | (load4(pay, pos) & d.dmask);
+                pos += d.nb;
             }
-            x = (x << p.digit_bits) | load_le(pay + pos, nb);
-            pos += nb;
+            if (pos > plen) break;
         }
         state[sid] = x;
-        out[t] = s;
+        out[t] = en.x & 0xFF;
+    }
+    if (t < T) {  // a read ran past the payload
+        st->code = ILANS_ERR_TRUNCATED;
+        st->stream = sched[t];
+        st->step = t;
     }
     st->pos = pos;
 }
@@ -699,9 +750,12 @@ extern "C" int ilans_mux_merge(const ilans_mux_stream *streams, int32_t n_stream
     CK(m.alloc(&srcpos, size_t(T)));
     CK(m.alloc(&d_err, size_t(K)));
     CK(m.alloc(&d_err_val, size_t(K)));
+    uint2 *d_lut = nullptr;
+    CK(m.alloc(&d_lut, size_t(n_slot)));
+    mux_lut_kernel<<<K < 1024 ? K : 1024, 256, 0, s>>>(d_streams, K, d_freq, d_cum, d_slot, d_lut);
+    ilans_note_launch();
     mux_replay_streams_kernel<<<mux_blocks(K), kMuxThreads, 0, s>>>(
-        d_streams, K, d_freq, d_cum, d_slot, d_hdr, d_hoff, d_pay, d_poff, d_off, dcnt, srcpos,
-        d_err, d_err_val);
+        d_streams, K, d_lut, d_hdr, d_hoff, d_pay, d_poff, d_off, dcnt, srcpos, d_err, d_err_val);
     ilans_note_launch();
     std::vector<int32_t> err(static_cast<size_t>(K));
     std::vector<uint32_t> err_val(static_cast<size_t>(K));
@@ -756,7 +810,8 @@ extern "C" int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_stream
     const int64_t T = n_steps;
     if (K < 0 || K > 0xFFFF) return st_fail(st, ILANS_ERR_VALUE, "stream count must be <= 65535");
     if (T < 0 || T > kMuxMaxSteps) return st_fail(st, ILANS_ERR_VALUE, "too many schedule steps");
-    if (payload_len < 0 || flush_interval < 0) return st_fail(st, ILANS_ERR_VALUE, "bad arguments");
+    if (payload_len < 0 || payload_len > int64_t(0xFFFFFFF0u) || flush_interval < 0)
+        return st_fail(st, ILANS_ERR_VALUE, "bad arguments (payload must be < 4 GiB)");
     if (int rc = check_streams(streams, K, n_freq, n_cum, n_slot, true, st)) return rc;
     std::vector<int64_t> off;
     if (int rc = schedule_offsets(schedule, T, K, off, st)) return rc;
@@ -769,26 +824,64 @@ extern "C" int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_stream
     AsyncBufs m(s);
     ilans_mux_stream *d_streams = nullptr;
     uint32_t *d_freq = nullptr, *d_cum = nullptr, *d_state = nullptr, *d_out = nullptr;
-    uint8_t *d_slot = nullptr, *d_hdr = nullptr, *d_pay = nullptr;
+    uint8_t *d_slot = nullptr, *d_hdr = nullptr;
     uint64_t *d_hoff = nullptr;
-    int64_t *d_epoch = nullptr;
-    int32_t *d_sched = nullptr;
+    int32_t *d_epoch = nullptr, *d_sched = nullptr;
+    uint2 *d_lut = nullptr;
+    WalkDesc *d_desc = nullptr;
     DemuxStatus *d_st = nullptr;
+    std::vector<WalkDesc> desc(static_cast<size_t>(K));
+    for (int j = 0; j < K; ++j) {
+        const ilans_mux_stream &p = streams[j];
+        WalkDesc &d = desc[j];
+        d.raw = p.kind == ILANS_MUX_RAW;
+        d.nb = uint32_t(p.nbytes);
+        d.dmask = p.nbytes >= 4 ? ~0u : (1u << (8 * p.nbytes)) - 1u;
+        d.lut_off = d.raw ? 0u : uint32_t(p.slot_off);
+        d.L = d.raw ? 0u : p.lower_bound;
+        d.sb = d.raw ? 0u : uint32_t(p.scale_bits);
+        d.mask = d.raw ? 0u : (1u << p.scale_bits) - 1u;
+        d.bits = d.raw ? 0u : uint32_t(p.digit_bits);
+    }
     CK(m.upload(&d_streams, streams, size_t(K)));
+    CK(m.upload(&d_desc, desc.data(), size_t(K)));
     CK(m.upload(&d_freq, freq, size_t(n_freq)));
     CK(m.upload(&d_cum, cum, size_t(n_cum)));
     CK(m.upload(&d_slot, slot, size_t(n_slot)));
+    CK(m.alloc(&d_lut, size_t(n_slot)));
     CK(m.upload(&d_hdr, headers, size_t(header_off[K])));
     CK(m.upload(&d_hoff, header_off, size_t(K) + 1));
-    CK(m.upload(&d_pay, payload, size_t(payload_len)));
-    CK(m.upload(&d_sched, schedule, size_t(T)));
+    // payload as 4-byte words + 8 bytes of padding for the look-ahead loads
+    uint32_t *d_payw = nullptr;
+    const size_t pwords = (size_t(payload_len) + 3) / 4 + 2;
+    CK(m.alloc(&d_payw, pwords));
+    CK(cudaMemsetAsync(d_payw, 0, pwords * 4, s));
+    if (payload_len)
+        CK(cudaMemcpyAsync(d_payw, payload, size_t(payload_len), cudaMemcpyHostToDevice, s));
+    CK(m.alloc(&d_sched, size_t(T) + 2));  // + entries read ahead
+    CK(cudaMemsetAsync(d_sched + T, 0, 8, s));
+    if (T) CK(cudaMemcpyAsync(d_sched, schedule, size_t(T) * 4, cudaMemcpyHostToDevice, s));
     CK(m.alloc(&d_state, size_t(K)));
     CK(m.alloc(&d_epoch, size_t(K)));
     CK(m.alloc(&d_out, size_t(T)));
     CK(m.alloc(&d_st, 1));
-    demux_kernel<<<1, 32, 0, s>>>(d_streams, K, d_freq, d_cum, d_slot, d_hdr, d_hoff, d_pay,
-                                  uint64_t(payload_len), d_sched, T, flush_interval, d_state,
-                                  d_epoch, d_out, d_st);
+    mux_lut_kernel<<<K < 1024 ? K : 1024, 256, 0, s>>>(d_streams, K, d_freq, d_cum, d_slot, d_lut);
+    ilans_note_launch();
+    const size_t smem = size_t(n_slot) * sizeof(uint2) + size_t(K) * (sizeof(WalkDesc) + 8);
+    const int32_t F32 = (flush_interval <= 0 || flush_interval >= T) ? INT32_MAX
+                                                                      : int32_t(flush_interval);
+    if (smem <= size_t(200) * 1024) {
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(demux_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        demux_kernel<true><<<1, 256, smem, s>>>(d_desc, K, d_lut, n_slot, d_hdr, d_hoff, d_payw,
+                                                uint32_t(payload_len), d_sched, int32_t(T), F32,
+                                                d_state, d_epoch, d_out, d_st);
+    } else {
+        demux_kernel<false><<<1, 32, 0, s>>>(d_desc, K, d_lut, n_slot, d_hdr, d_hoff, d_payw,
+                                             uint32_t(payload_len), d_sched, int32_t(T), F32,
+                                             d_state, d_epoch, d_out, d_st);
+    }
     ilans_note_launch();
     DemuxStatus h{};
     CK(cudaMemcpyAsync(&h, d_st, sizeof(h), cudaMemcpyDeviceToHost, s));

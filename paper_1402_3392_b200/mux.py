@@ -201,8 +201,9 @@ def round_robin_schedule(lengths) -> list[int]:
 
 
 def _schedule_array(schedule) -> np.ndarray:
-    return np.asarray(list(schedule) if not isinstance(schedule, np.ndarray) else schedule,
-                      dtype=np.int64).reshape(-1)
+    if not isinstance(schedule, (np.ndarray, list, tuple)):
+        schedule = list(schedule)
+    return np.asarray(schedule, dtype=np.int64).reshape(-1)
 
 
 def _validate_schedule(schedule, lengths) -> np.ndarray:
