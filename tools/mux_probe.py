@@ -24,6 +24,7 @@ from ilans.rans import SymbolTable as RTable  # noqa: E402
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
 F = int(sys.argv[3]) if len(sys.argv) > 3 else 4096
+F = F or None  # 0: no flushing
 
 src = synth_host(K * N, 1.1, seed=7)
 counts = np.bincount(src, minlength=256)
