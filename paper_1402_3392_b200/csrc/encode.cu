@@ -253,11 +253,11 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 for (int gb = kInSeg / n_lanes - 1; gb >= 0; gb -= 16) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        // next group's symbol one ahead (below blk on the
-                        // last group: a harmless shared read, never used)
+                        // next group's symbol one ahead (none after group 0,
+                        // which ends the last outer step, gb == 15)
                         bp -= n_lanes;
                         const uint32_t sym = sym_n;
-                        sym_n = *bp;
+                        if (j < 15 || gb > 15) sym_n = *bp;
                         const uint2 a = encf[sym];
                         macc &= a.x;
                         bool spill;
