@@ -280,3 +280,60 @@ def test_larger_mux_round_trip():
     plain = mux(bufs, coders, sched)
     cont0, b0 = mux_with_flush(msgs, coders, sched)
     assert cont0.payload == plain and b0.max_buffered == len(plain)
+
+
+def test_fuzz_against_reference_mux():
+    """Randomized workloads against the unmodified reference mux.py (from
+    oracle/_ref, the checker): containers, budgets, merged payloads and
+    stream buffers byte for byte; demux round trips."""
+    import os
+
+    import oracle
+
+    if oracle.reference_ilans() is None:
+        pytest.skip("oracle/_ref not built (bash oracle/build_ref.sh)")
+    from ilans import mux as rmux
+    from ilans.rans import BYTE8 as RBYTE8
+    from ilans.rans import WORD16 as RWORD16
+    from ilans.rans import RenormVariant as RVariant
+    from ilans.rans import SymbolTable as RTable
+
+    rng = np.random.default_rng(int(os.environ.get("ILANS_FUZZ_SEED", "77")))
+    variants = [(WORD16, RWORD16), (BYTE8, RBYTE8),
+                (RenormVariant("c8", 8, 1 << 16), RVariant("c8", 8, 1 << 16)),
+                (RenormVariant("c16", 16, 1 << 14), RVariant("c16", 16, 1 << 14))]
+    for it in range(int(os.environ.get("ILANS_FUZZ_ITERS", "40"))):
+        k = int(rng.integers(1, 9))
+        ours, theirs, msgs = [], [], []
+        for _ in range(k):
+            n = int(rng.choice([0, 1, 2, 17, 100, 400]))
+            if rng.random() < 0.3:
+                w = int(rng.integers(1, 33))
+                ours.append(RawStreamCodec(w))
+                theirs.append(rmux.RawStreamCodec(w))
+                msgs.append(rng.integers(0, 1 << w, size=n, dtype=np.uint64)
+                            .astype(np.int64).tolist())
+                continue
+            v, rv = variants[int(rng.integers(0, len(variants)))]
+            top = min(14, v.lower_bound.bit_length() - 1)
+            n_sym = int(rng.integers(1, 65))
+            sb = int(rng.integers(max(1, (n_sym - 1).bit_length()), top + 1))
+            counts = rng.integers(0, 300, size=n_sym)
+            counts[int(rng.integers(0, n_sym))] += 1
+            t = SymbolTable.from_counts(counts.tolist(), sb)
+            ours.append(RansStreamCodec(t, v))
+            theirs.append(rmux.RansStreamCodec(RTable(t.freq, sb), rv))
+            msgs.append(random_message(rng, t, n) if n else [])
+        lengths = [len(m) for m in msgs]
+        sched = shuffled(rng, lengths) if rng.random() < 0.6 else round_robin_schedule(lengths)
+        flush = [None, 1, 2, 7, 50][int(rng.integers(0, 5))]
+        c, b = mux_with_flush(msgs, ours, sched, flush)
+        rc, rb = rmux.mux_with_flush(msgs, theirs, sched, flush)
+        assert c.to_bytes() == rc.to_bytes(), (it, flush, lengths)
+        assert (b.max_buffered, b.segment_count, b.payload_bytes) == \
+            (rb.max_buffered, rb.segment_count, rb.payload_bytes), it
+        assert demux_decode(c.to_bytes(), ours, sched) == msgs, it
+        bufs = encode_multistream(msgs, ours)
+        rbufs = rmux.encode_multistream(msgs, theirs)
+        assert [(x.header, x.payload) for x in bufs] == [(x.header, x.payload) for x in rbufs]
+        assert mux(bufs, ours, sched) == rmux.mux(rbufs, theirs, sched), it
