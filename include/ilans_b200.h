@@ -240,6 +240,27 @@ int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload, const uint64_t *d
                                     uint32_t *d_adler, uint64_t *d_consumed, void *d_status,
                                     void *stream);
 
+/* Chunked BYTE8 (8-bit digits, L = 2^23; ICH1 variant 0): chunk k is the
+ * reference's encode_interleaved(msg[kC:(k+1)C], table, N, BYTE8)
+ * (interleave.py:155-179), one warp per chunk, N in [1, 32].
+ * Encode: d_scratch holds 3 bytes per message byte + 8 (chunk k's digits end
+ * at 3kC + 3 len_k); d_chunk_bytes[k] = its digit count. Frame: exclusive
+ * scan into d_byte_offsets[K + 1] and byte compaction into d_payload (both
+ * 4-byte aligned). Decode: one launch for all chunks, d_consumed[k] = bytes
+ * read; errors land in the device status (zero-frequency symbol, exhausted
+ * chunk, runaway refill = FormatError). */
+int ilans_encode_chunks_u8_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
+                               int32_t n_lanes, const void *d_table, uint8_t *d_scratch,
+                               uint32_t *d_chunk_bytes, uint32_t *d_states, void *d_status,
+                               void *stream);
+int ilans_frame_chunks_u8_dev(const uint8_t *d_scratch, int64_t n, int64_t chunk_len,
+                              const uint32_t *d_chunk_bytes, uint64_t *d_byte_offsets,
+                              uint8_t *d_payload, void *stream);
+int ilans_decode_chunks_u8_dev(const uint8_t *d_payload, const uint64_t *d_byte_offsets,
+                               const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                               int32_t n_lanes, const void *d_table, uint8_t *d_out,
+                               uint64_t *d_consumed, void *d_status, void *stream);
+
 /* Per-chunk Adler-32 of bytes already on the device (the unfused
  * consumer, and a device-side integrity check of raw data). */
 int ilans_adler32_chunks_dev(const uint8_t *d_data, int64_t n, int64_t chunk_len,

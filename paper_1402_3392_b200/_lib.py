@@ -118,6 +118,11 @@ PROTOTYPES = [
     ("ilans_decode_chunks_adler32_dev", ctypes.c_int,
      [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
     ("ilans_adler32_chunks_dev", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp]),
+    ("ilans_encode_chunks_u8_dev", ctypes.c_int,
+     [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("ilans_frame_chunks_u8_dev", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    ("ilans_decode_chunks_u8_dev", ctypes.c_int,
+     [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     ("ilans_synth_bytes_dev", ctypes.c_int, [_vp, _i64, _u64, _i64, _vp, _vp]),
     ("ilans_mux_encode", ctypes.c_int,
      [_vp, _i32, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp,

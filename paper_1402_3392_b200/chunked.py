@@ -17,14 +17,14 @@ ICH1 wire format (little-endian), the on-disk form of a chunked stream:
 
     0   4      magic "ICH1"
     4   1      version (1)
-    5   1      variant (1 = word16)
+    5   1      variant (1 = word16, 0 = byte8; the IEC1 codes, interleave.py:10-20)
     6   2      lane_count N (u16)
     8   8      message_length (u64)
     16  8      chunk_len C (u64)
     24  3+2n   table (rans.serialize_table)
-    -   4K     payload words per chunk (u32), K = ceil(len / C)
+    -   4K     payload digits per chunk (u32), K = ceil(len / C)
     -   4KN    final lane states, chunk-major (u32)
-    -   rest   payloads back to back (u16 LE)
+    -   rest   payloads back to back (u16 LE digits for word16, bytes for byte8)
 """
 
 from __future__ import annotations
@@ -38,7 +38,7 @@ import numpy as np
 from . import _lib, rans
 from .errors import FormatError, TruncatedStreamError
 from .interleave import Container, _as_symbols
-from .rans import WORD16, SymbolTable
+from .rans import BYTE8, WORD16, RenormVariant, SymbolTable
 
 CHUNK_MAGIC = b"ICH1"
 DEFAULT_CHUNK = 64 * 1024
@@ -64,8 +64,9 @@ class ChunkedContainer:
     message_length: int
     table: SymbolTable
     states: np.ndarray        # u32 [n_chunks, N]
-    word_offsets: np.ndarray  # u64 [n_chunks + 1]
-    payload: np.ndarray       # u16 [word_offsets[-1]]
+    word_offsets: np.ndarray  # u64 [n_chunks + 1], in digits (words / bytes)
+    payload: np.ndarray       # u16 (word16) or u8 (byte8) [word_offsets[-1]]
+    variant: RenormVariant = WORD16
 
     @property
     def n_chunks(self) -> int:
@@ -77,16 +78,17 @@ class ChunkedContainer:
     def chunk(self, k: int) -> Container:
         """Chunk k as a standalone IEC1 container (reference-decodable)."""
         a, b = int(self.word_offsets[k]), int(self.word_offsets[k + 1])
-        return Container(WORD16, self.lane_count, self.chunk_length(k), self.table,
+        return Container(self.variant, self.lane_count, self.chunk_length(k), self.table,
                          tuple(int(x) for x in self.states[k]), self.payload[a:b].copy())
 
     def to_bytes(self) -> bytes:
-        head = CHUNK_MAGIC + struct.pack("<BBHQQ", 1, 1, self.lane_count, self.message_length,
-                                         self.chunk_len)
+        byte8 = self.variant == BYTE8
+        head = CHUNK_MAGIC + struct.pack("<BBHQQ", 1, 0 if byte8 else 1, self.lane_count,
+                                         self.message_length, self.chunk_len)
         words = np.diff(self.word_offsets.astype(np.uint64)).astype("<u4")
         return (head + rans.serialize_table(self.table) + words.tobytes()
                 + np.ascontiguousarray(self.states, dtype="<u4").tobytes()
-                + np.ascontiguousarray(self.payload, dtype="<u2").tobytes())
+                + np.ascontiguousarray(self.payload, dtype="u1" if byte8 else "<u2").tobytes())
 
     @classmethod
     def from_bytes(cls, raw: bytes) -> "ChunkedContainer":
@@ -98,8 +100,9 @@ class ChunkedContainer:
         version, variant, lanes, n, chunk_len = struct.unpack_from("<BBHQQ", raw, 4)
         if version != 1:
             raise FormatError(f"unsupported container version {version}")
-        if variant != 1:
+        if variant not in (0, 1):
             raise FormatError(f"unknown variant byte {variant}")
+        var = WORD16 if variant == 1 else BYTE8
         if not 1 <= lanes <= 32 or chunk_len == 0 or chunk_len % 16:
             raise FormatError("invalid lane_count / chunk_len")
         table, off = rans.parse_table(raw, 24)
@@ -112,17 +115,22 @@ class ChunkedContainer:
         states = np.frombuffer(raw, dtype="<u4", count=k * lanes, offset=off).astype(
             np.uint32).reshape(k, lanes)
         off += 4 * k * lanes
-        if ((states < WORD16.lower_bound)).any():
+        if ((states < var.lower_bound) | (states.astype(np.uint64) >= var.state_limit)).any():
             raise FormatError("lane state outside the coder interval")
         offsets = np.zeros(k + 1, dtype=np.uint64)
         np.cumsum(words, out=offsets[1:])
         tail = raw[off:]
-        if len(tail) % 2:
-            raise FormatError("word16 payload has odd byte length")
-        if len(tail) // 2 < int(offsets[-1]):
-            raise TruncatedStreamError("payload truncated")
-        payload = np.frombuffer(tail, dtype="<u2").astype(np.uint16)
-        return cls(lanes, chunk_len, n, table, states, offsets, payload)
+        if var == BYTE8:
+            if len(tail) < int(offsets[-1]):
+                raise TruncatedStreamError("payload truncated")
+            payload = np.frombuffer(tail, dtype=np.uint8).copy()
+        else:
+            if len(tail) % 2:
+                raise FormatError("word16 payload has odd byte length")
+            if len(tail) // 2 < int(offsets[-1]):
+                raise TruncatedStreamError("payload truncated")
+            payload = np.frombuffer(tail, dtype="<u2").astype(np.uint16)
+        return cls(lanes, chunk_len, n, table, states, offsets, payload, var)
 
 
 # ---------------------------------------------------------------------------
@@ -354,12 +362,20 @@ class DeviceCodec:
 
 
 def encode_chunked(message, table: SymbolTable | None = None, lane_count: int = 32,
-                   chunk_len: int = DEFAULT_CHUNK, scale_bits: int = 14) -> ChunkedContainer:
+                   chunk_len: int = DEFAULT_CHUNK, scale_bits: int = 14,
+                   variant: RenormVariant = WORD16) -> ChunkedContainer:
     """Encode host bytes as independent N-lane chunks under one table. With
     table=None the model is built on the device (histogram + quantize), as
-    cli._build_table does on the host (cli.py:31-37)."""
+    cli._build_table does on the host (cli.py:31-37). variant=BYTE8 codes
+    every chunk with byte digits (the reference's scalar byte8 path)."""
     torch = _torch()
     _check_chunking(chunk_len, lane_count)
+    if variant == BYTE8:
+        return _encode_chunked_u8(message, table, lane_count, chunk_len, scale_bits)
+    if variant != WORD16:
+        from .errors import UnsupportedVariantError
+
+        raise UnsupportedVariantError(f"chunked streams are word16 or byte8, not {variant.tag!r}")
     if table is not None:
         msg = _as_symbols(message, table)
         WORD16.check_table(table)
@@ -388,6 +404,8 @@ def decode_chunked(cc: ChunkedContainer) -> np.ndarray:
     """Decode a ChunkedContainer on the device (one launch for all chunks)."""
     torch = _torch()
     _check_chunking(cc.chunk_len, cc.lane_count)
+    if cc.variant == BYTE8:
+        return _decode_chunked_u8(cc)
     n = cc.message_length
     if n == 0:
         return np.zeros(0, dtype=np.uint8)
@@ -410,6 +428,132 @@ def decode_chunked(cc: ChunkedContainer) -> np.ndarray:
     codec.check_status()
     consumed = codec.consumed[:k].cpu().numpy()
     if (consumed != np.diff(cc.word_offsets.astype(np.int64))).any():
+        import warnings
+
+        from .errors import TrailingGarbageWarning
+
+        warnings.warn("unread digits after chunk decode", TrailingGarbageWarning, stacklevel=2)
+    return out.cpu().numpy()
+
+
+class _Model:
+    """Device table + status blobs for the one-shot byte8 calls."""
+
+    def __init__(self, torch, dev):
+        self.torch, self.dev = torch, dev
+        self.table = torch.empty(int(_lib.lib.ilans_table_bytes()), dtype=torch.uint8, device=dev)
+        self.status = torch.empty(int(_lib.lib.ilans_dstatus_bytes()), dtype=torch.uint8,
+                                  device=dev)
+        self.s = int(torch.cuda.current_stream(dev).cuda_stream)
+
+    def from_freq(self, table: SymbolTable):
+        f = self.torch.from_numpy(table.freq_u32.view(np.int32).copy()).to(self.dev)
+        self._keep = f
+        _lib.check_dev(_lib.lib.ilans_table_from_freq_dev(
+            int(f.data_ptr()), table.alphabet_size, table.scale_bits, int(self.table.data_ptr()),
+            self.s), "table_from_freq")
+
+    def from_message(self, d_msg, n: int, scale_bits: int) -> SymbolTable:
+        counts = self.torch.zeros(256, dtype=self.torch.int64, device=self.dev)
+        _lib.check_dev(_lib.lib.ilans_histogram_u8_dev(int(d_msg.data_ptr()), int(n),
+                                                       int(counts.data_ptr()), self.s),
+                       "histogram")
+        _lib.check_dev(_lib.lib.ilans_table_from_counts_dev(
+            int(counts.data_ptr()), scale_bits, int(self.table.data_ptr()), self.s), "table")
+        alpha, sb = ctypes.c_int32(0), ctypes.c_int32(0)
+        freq = np.zeros(256, dtype=np.uint32)
+        st = _lib.Status()
+        rc = _lib.lib.ilans_table_read_host(int(self.table.data_ptr()), ctypes.byref(alpha),
+                                            ctypes.byref(sb), _lib.ptr(freq), self.s,
+                                            ctypes.byref(st))
+        _lib.raise_for(rc, st, "table")
+        return SymbolTable(freq[: alpha.value].tolist(), sb.value)
+
+    def reset(self):
+        _lib.check_dev(_lib.lib.ilans_dstatus_reset_dev(int(self.status.data_ptr()), self.s),
+                       "status")
+
+    def check(self):
+        st = _lib.Status()
+        rc = _lib.lib.ilans_dstatus_read_host(int(self.status.data_ptr()), self.s,
+                                              ctypes.byref(st))
+        _lib.raise_for(rc, st, "device status")
+
+
+def _encode_chunked_u8(message, table, lane_count: int, chunk_len: int,
+                       scale_bits: int) -> ChunkedContainer:
+    """Chunked byte8: one warp per chunk (csrc/byte8.cu), byte framing."""
+    torch = _torch()
+    if table is not None:
+        msg = _as_symbols(message, table)
+        BYTE8.check_table(table)
+    else:
+        msg = np.frombuffer(message, dtype=np.uint8) if isinstance(
+            message, (bytes, bytearray, memoryview)) else np.asarray(message, dtype=np.uint8)
+    n = len(msg)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    m = _Model(torch, dev)
+    d_msg = torch.zeros(max(16, n), dtype=torch.uint8, device=dev)
+    if n:
+        d_msg[:n].copy_(torch.from_numpy(np.ascontiguousarray(msg)))
+    if table is None:
+        table = m.from_message(d_msg, n, scale_bits)
+        BYTE8.check_table(table)
+    else:
+        m.from_freq(table)
+    k = n_chunks_for(n, chunk_len)
+    cap = 3 * max(n, 1) + 16
+    scratch = torch.empty(cap, dtype=torch.uint8, device=dev)
+    payload = torch.empty(cap, dtype=torch.uint8, device=dev)
+    nbytes = torch.zeros(max(k, 1), dtype=torch.int32, device=dev)
+    offsets = torch.zeros(k + 1, dtype=torch.int64, device=dev)
+    states = torch.empty(max(k, 1) * lane_count, dtype=torch.int32, device=dev)
+    m.reset()
+    p = lambda t: int(t.data_ptr())  # noqa: E731
+    if n:
+        _lib.check_dev(_lib.lib.ilans_encode_chunks_u8_dev(
+            p(d_msg), n, chunk_len, lane_count, p(m.table), p(scratch), p(nbytes), p(states),
+            p(m.status), m.s), "encode_chunks_u8")
+        m.check()
+        _lib.check_dev(_lib.lib.ilans_frame_chunks_u8_dev(
+            p(scratch), n, chunk_len, p(nbytes), p(offsets), p(payload), m.s), "frame_u8")
+    offs = offsets.cpu().numpy().view(np.uint64).copy()
+    total = int(offs[-1]) if k else 0
+    return ChunkedContainer(lane_count, chunk_len, n, table,
+                            states[: k * lane_count].cpu().numpy().view(np.uint32)
+                            .reshape(k, lane_count).copy(),
+                            offs if k else np.zeros(1, np.uint64),
+                            payload[:total].cpu().numpy().copy(), BYTE8)
+
+
+def _decode_chunked_u8(cc: ChunkedContainer) -> np.ndarray:
+    torch = _torch()
+    n = cc.message_length
+    if n == 0:
+        return np.zeros(0, dtype=np.uint8)
+    k = cc.n_chunks
+    if cc.states.shape != (k, cc.lane_count) or len(cc.word_offsets) != k + 1:
+        raise FormatError("chunk directory does not match the message length")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    m = _Model(torch, dev)
+    m.from_freq(cc.table)
+    pay = torch.zeros(max(len(cc.payload), 1) + 8, dtype=torch.uint8, device=dev)
+    if len(cc.payload):
+        pay[: len(cc.payload)].copy_(torch.from_numpy(np.ascontiguousarray(cc.payload,
+                                                                           dtype=np.uint8)))
+    offs = torch.from_numpy(np.ascontiguousarray(cc.word_offsets, dtype=np.uint64)
+                            .view(np.int64)).to(dev)
+    states = torch.from_numpy(np.ascontiguousarray(cc.states, dtype=np.uint32).view(np.int32)
+                              .reshape(-1)).to(dev)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    consumed = torch.zeros(k, dtype=torch.int64, device=dev)
+    m.reset()
+    p = lambda t: int(t.data_ptr())  # noqa: E731
+    _lib.check_dev(_lib.lib.ilans_decode_chunks_u8_dev(
+        p(pay), p(offs), p(states), n, cc.chunk_len, cc.lane_count, p(m.table), p(out),
+        p(consumed), p(m.status), m.s), "decode_chunks_u8")
+    m.check()
+    if (consumed.cpu().numpy() != np.diff(cc.word_offsets.astype(np.int64))).any():
         import warnings
 
         from .errors import TrailingGarbageWarning

@@ -395,4 +395,83 @@ cudaError_t launch_decode_u8(const uint8_t *d_payload, uint64_t pay_len, const u
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Chunked byte8 (the ICH1 framing of encode.cu with byte digits): chunk k is
+// an independent byte8 stream; its digits sit at
+// scratch[3kC + 3 len_k - b_k, 3kC + 3 len_k) after the encode, and the
+// framing packs them back to back at the scanned byte offsets.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+compact_u8_kernel(const uint8_t *__restrict__ scratch, int64_t n, int64_t chunk_len,
+                  const uint32_t *__restrict__ bytes, const uint64_t *__restrict__ offsets,
+                  uint8_t *__restrict__ payload) {
+    for (int64_t k = blockIdx.x; k * chunk_len < n; k += gridDim.x) {
+        const int64_t cbase = k * chunk_len;
+        const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+        const uint32_t b = bytes[k];
+        const uint64_t s = uint64_t(3 * cbase + 3 * len) - b;  // source byte
+        const uint64_t d = offsets[k];                          // destination byte
+        // head bytes up to a 4-byte aligned destination, then whole words
+        // assembled from two aligned source words, then the tail bytes
+        uint32_t head = uint32_t((4u - (d & 3u)) & 3u);
+        if (head > b) head = b;
+        if (threadIdx.x < head) payload[d + threadIdx.x] = scratch[s + threadIdx.x];
+        const uint32_t words = (b - head) >> 2;
+        const uint64_t s0 = s + head;
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(scratch + (s0 & ~uint64_t(3)));
+        const uint32_t sh = uint32_t(s0 & 3u) * 8u;
+        uint32_t *dst = reinterpret_cast<uint32_t *>(payload + d + head);
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
+            dst[i] = sh ? __funnelshift_r(src[i], src[i + 1], sh) : src[i];
+        const uint32_t done = head + 4 * words;
+        if (threadIdx.x < b - done) payload[d + done + threadIdx.x] = scratch[s + done + threadIdx.x];
+    }
+}
+
+cudaError_t launch_encode_chunks_u8(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
+                                    int n_lanes, const TableDev *d_table, uint8_t *d_scratch,
+                                    uint32_t *d_bytes, uint32_t *d_states, DStatus *d_status,
+                                    cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
+    int64_t blocks = (n_chunks + 7) / 8;  // 8 warps (streams) per CTA
+    const int64_t cap = int64_t(sm_count()) * 8;
+    if (blocks > cap) blocks = cap;
+    encode_u8_warp_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_bytes, d_states, d_status);
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_frame_u8(const uint8_t *d_scratch, int64_t n, int64_t chunk_len,
+                            const uint32_t *d_bytes, uint64_t *d_offsets, uint8_t *d_payload,
+                            cudaStream_t stream) {
+    const int64_t n_chunks = n <= 0 ? 0 : (n + chunk_len - 1) / chunk_len;
+    chunk_offsets_kernel<<<1, 1024, 0, stream>>>(d_bytes, n_chunks, d_offsets, 0);
+    ilans_note_launch();
+    if (n_chunks > 0) {
+        const int64_t cap = int64_t(sm_count()) * 8;
+        compact_u8_kernel<<<static_cast<unsigned>(n_chunks < cap ? n_chunks : cap), 256, 0,
+                            stream>>>(d_scratch, n, chunk_len, d_bytes, d_offsets, d_payload);
+        ilans_note_launch();
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_chunks_u8(const uint8_t *d_payload, const uint64_t *d_offsets,
+                                    const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                    int n_lanes, const TableDev *d_table, uint8_t *d_out,
+                                    uint64_t *d_consumed, DStatus *d_status, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
+    int64_t blocks = (n_chunks + 7) / 8;
+    const int64_t cap = int64_t(sm_count()) * 8;
+    if (blocks > cap) blocks = cap;
+    decode_u8_warp_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        d_payload, d_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table, d_out,
+        d_consumed, d_status, DecodeTrace{nullptr, nullptr, nullptr});
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace ilans

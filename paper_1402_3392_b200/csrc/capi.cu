@@ -764,6 +764,8 @@ extern "C" int ilans_dstatus_parse(const void *h_status, ilans_status *st) {
         return st_fail(st, ILANS_ERR_TRUNCATED, "payload exhausted mid-decode (chunk %lld)",
                        static_cast<long long>(h.trunc_stream));
     }
+    if (h.value_error == ILANS_ERR_FORMAT)  // byte8: a refill loop that does not terminate
+        return st_fail(st, ILANS_ERR_FORMAT, "renormalization does not terminate; corrupt stream");
     if (h.value_error) {
         return st_fail(st, ILANS_ERR_VALUE, "table does not match the launch (scale_bits / layout)");
     }
@@ -814,6 +816,39 @@ extern "C" int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t
                          static_cast<const TableDev *>(d_table), scale_bits, packed, d_out,
                          d_consumed, d_final_states, static_cast<DStatus *>(d_status), nullptr,
                          ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_encode_chunks_u8_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
+                                          int32_t n_lanes, const void *d_table,
+                                          uint8_t *d_scratch, uint32_t *d_chunk_bytes,
+                                          uint32_t *d_states, void *d_status, void *stream) {
+    if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    return launch_encode_chunks_u8(d_msg, n, chunk_len, n_lanes,
+                                   static_cast<const TableDev *>(d_table), d_scratch,
+                                   d_chunk_bytes, d_states, static_cast<DStatus *>(d_status),
+                                   ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_frame_chunks_u8_dev(const uint8_t *d_scratch, int64_t n, int64_t chunk_len,
+                                         const uint32_t *d_chunk_bytes, uint64_t *d_byte_offsets,
+                                         uint8_t *d_payload, void *stream) {
+    if (chunk_len <= 0 || (reinterpret_cast<uintptr_t>(d_scratch) & 3) ||
+        (reinterpret_cast<uintptr_t>(d_payload) & 3))
+        return ILANS_ERR_VALUE;
+    return launch_frame_u8(d_scratch, n, chunk_len, d_chunk_bytes, d_byte_offsets, d_payload,
+                           ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_decode_chunks_u8_dev(const uint8_t *d_payload, const uint64_t *d_byte_offsets,
+                                          const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                          int32_t n_lanes, const void *d_table, uint8_t *d_out,
+                                          uint64_t *d_consumed, void *d_status, void *stream) {
+    if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    return launch_decode_chunks_u8(d_payload, d_byte_offsets, d_states, n, chunk_len, n_lanes,
+                                   static_cast<const TableDev *>(d_table), d_out, d_consumed,
+                                   static_cast<DStatus *>(d_status), ST(stream)) == cudaSuccess
+               ? ILANS_OK
+               : ILANS_ERR_CUDA;
 }
 
 extern "C" int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload,

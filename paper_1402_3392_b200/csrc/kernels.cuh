@@ -56,12 +56,27 @@ cudaError_t launch_decode_u8(const uint8_t *d_payload, uint64_t pay_len, const u
                              const TableDev *d_table, uint8_t *d_out, uint64_t *d_consumed,
                              DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream,
                              DecodeTrace trace);
+// chunked byte8: one warp per chunk, byte framing (ICH1 variant 0)
+cudaError_t launch_encode_chunks_u8(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
+                                    int n_lanes, const TableDev *d_table, uint8_t *d_scratch,
+                                    uint32_t *d_bytes, uint32_t *d_states, DStatus *d_status,
+                                    cudaStream_t stream);
+cudaError_t launch_frame_u8(const uint8_t *d_scratch, int64_t n, int64_t chunk_len,
+                            const uint32_t *d_bytes, uint64_t *d_offsets, uint8_t *d_payload,
+                            cudaStream_t stream);
+cudaError_t launch_decode_chunks_u8(const uint8_t *d_payload, const uint64_t *d_offsets,
+                                    const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                    int n_lanes, const TableDev *d_table, uint8_t *d_out,
+                                    uint64_t *d_consumed, DStatus *d_status, cudaStream_t stream);
 
 // synth.cu
 cudaError_t launch_synth(uint8_t *d_out, int64_t n, uint64_t seed, int64_t first_index,
                          const uint32_t *d_cdf, cudaStream_t stream);
 
 __global__ void dstatus_reset_kernel(DStatus *s);
+// encode.cu: exclusive scan of per-chunk sizes into u64 offsets (one CTA)
+__global__ void chunk_offsets_kernel(const uint32_t *__restrict__ words, int64_t n_chunks,
+                                     uint64_t *__restrict__ offsets, int carry_in);
 
 int sm_count();
 

@@ -109,3 +109,57 @@ def test_byte8_steps_and_stats():
         _, used, xs = oracle.decode_u8_full(c.payload, c.final_states, slot, f, cum,
                                             t.scale_bits, upto, 8)
         assert steps[g][1] == tuple(int(v) for v in xs) and steps[g][2] == used
+
+
+# ------------------------------------------------------- chunked byte8 ---
+@pytest.mark.parametrize("n, C, lanes", [(0, 1024, 2), (1, 16, 1), (1000, 16, 3),
+                                         (70_001, 4096, 2), (300_000, 65536, 32),
+                                         (148 * 8 * 2 * 512 + 7, 512, 8)])
+def test_chunked_byte8_matches_reference_per_chunk(n, C, lanes):
+    """Chunked byte8 (ICH1 variant 0): every chunk's payload and states equal
+    the reference's byte8 encode of that chunk alone (oracle restatement of
+    interleave.py:155-179), the byte framing packs them back to back, the
+    container round-trips through bytes and every chunk re-wraps as a
+    standalone IEC1 byte8 container."""
+    from paper_1402_3392_b200.chunked import ChunkedContainer, decode_chunked, encode_chunked
+
+    rng = np.random.default_rng(n + C + lanes)
+    t = random_table(rng)
+    msg = random_message(rng, t, n)
+    cc = encode_chunked(msg, t, lanes, C, variant=BYTE8)
+    assert cc.variant == BYTE8 and cc.payload.dtype == np.uint8
+    k = cc.n_chunks
+    for j in range(k):
+        chunk = msg[j * C:(j + 1) * C]
+        p, s = oracle.encode_interleaved_u8(chunk, t.freq_u32, t.cum_u32, t.scale_bits, lanes)
+        a, b = int(cc.word_offsets[j]), int(cc.word_offsets[j + 1])
+        assert np.array_equal(cc.payload[a:b], p), j
+        assert np.array_equal(cc.states[j], s), j
+    back = ChunkedContainer.from_bytes(cc.to_bytes())
+    assert back.variant == BYTE8
+    assert np.array_equal(decode_chunked(back), msg)
+    for j in {0, k - 1} if k else ():
+        one = Container.from_bytes(cc.chunk(j).to_bytes())
+        assert np.array_equal(ilb.decode_interleaved(one), msg[j * C:(j + 1) * C])
+
+
+def test_chunked_byte8_device_model_and_errors():
+    from paper_1402_3392_b200.chunked import ChunkedContainer, decode_chunked, encode_chunked
+    from paper_1402_3392_b200.errors import UnencodableSymbolError
+
+    msg = zipf_1mib()
+    cc = encode_chunked(msg, None, 2, 65536, 12, variant=BYTE8)  # config 1 shape, chunked
+    counts, alpha = oracle.histogram(msg)
+    assert cc.table == SymbolTable(oracle.quantize(counts[:alpha], 12), 12)
+    assert np.array_equal(decode_chunked(cc), msg)
+    t = SymbolTable([2048, 2047, 0, 1], 12)
+    bad = np.zeros(10_000, dtype=np.uint8)
+    bad[7777] = 2
+    with pytest.raises(UnencodableSymbolError):
+        encode_chunked(bad, t, 4, 1024, variant=BYTE8)
+    good = encode_chunked(np.zeros(10_000, dtype=np.uint8), t, 4, 1024, variant=BYTE8)
+    short = ChunkedContainer(good.lane_count, good.chunk_len, good.message_length, good.table,
+                             good.states, good.word_offsets.copy(), good.payload, BYTE8)
+    short.word_offsets[-1] -= 1  # last chunk one byte short
+    with pytest.raises(TruncatedStreamError):
+        decode_chunked(short)
