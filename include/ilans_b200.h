@@ -336,10 +336,13 @@ int ilans_mux_merge(const ilans_mux_stream *streams, int32_t n_streams, const ui
                     uint8_t *out, ilans_status *st);
 
 /* Decode every stream back out of a muxed payload (mux.demux_decode,
- * mux.py:436-475): symbols_out[t] = the value decoded at schedule step t.
- * A sequential walk by construction (each step's read size depends on the
- * state of the stream it decodes), run by one device thread. *unread =
- * payload bytes left after the walk (the caller's TrailingGarbageWarning).
+ * mux.py:436-475). symbols_out[t] = the value decoded at schedule step t
+ * and/or symbols_by_stream = the same values stream by stream (stream 0's
+ * symbols in order, then stream 1's, ...); either pointer may be NULL.
+ * Sequential by construction -- each step's read offset depends on the
+ * refill counts of all earlier steps -- so one warp walks the schedule,
+ * decoding runs of consecutive steps on distinct streams together. *unread
+ * = payload bytes left after the walk (the caller's TrailingGarbageWarning).
  * Errors: ILANS_ERR_TRUNCATED, ILANS_ERR_FORMAT (state outside
  * [L, L << digit_bits); st->stream, st->index = step or -1 for a header). */
 int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_streams, const uint32_t *freq,
@@ -347,7 +350,7 @@ int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_streams, const ui
                     int64_t n_slot, const uint8_t *headers, const uint64_t *header_off,
                     const uint8_t *payload, int64_t payload_len, const int32_t *schedule,
                     int64_t n_steps, int64_t flush_interval, uint32_t *symbols_out,
-                    int64_t *unread, ilans_status *st);
+                    uint32_t *symbols_by_stream, int64_t *unread, ilans_status *st);
 
 #ifdef __cplusplus
 }

@@ -132,7 +132,7 @@ PROTOTYPES = [
       _st]),
     ("ilans_mux_demux", ctypes.c_int,
      [_vp, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp,
-      _vp, _st]),
+      _vp, _vp, _st]),
 ]
 
 for _name, _res, _args in PROTOTYPES:

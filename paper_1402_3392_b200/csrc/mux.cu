@@ -300,10 +300,15 @@ struct DemuxStatus {
 
 // Per-stream record for the walk, one 32-bit word per field so the loop
 // does no field extraction: lut offset, L, slot mask, sb, digit_bits,
-// nbytes, digit / value mask, raw flag.
+// nbytes, digit / value mask, flags = raw | pure << 1 | rmax << 8.
+// pure: the refill count after a pop is a function of the popped state
+// alone (x' R^(k-1) < L decides refill k exactly when R^(k-1) divides L:
+// every power-of-two L, i.e. WORD16, BYTE8 and most custom variants);
+// rmax: most refills one pop can need (x' = 1).
 struct __align__(16) WalkDesc {
-    uint32_t lut_off, L, mask, sb, bits, nb, dmask, raw;
+    uint32_t lut_off, L, mask, sb, bits, nb, dmask, flags;
 };
+constexpr uint32_t kWalkRaw = 1u, kWalkPure = 2u;
 
 __device__ __forceinline__ bool state_ok(uint32_t x, const WalkDesc &d) {
     return x >= d.L && (uint64_t(x) >> d.bits) < uint64_t(d.L);
@@ -316,123 +321,261 @@ __device__ __forceinline__ uint32_t load4(const uint32_t *__restrict__ w, uint32
     return __funnelshift_r(__ldg(w + q), __ldg(w + q + 1), (pos & 3u) * 8u);
 }
 
+// refills after a pop to x' >= 1 on a pure stream: #{k < rmax : x' < L >> (bits k)}
+__device__ __forceinline__ uint32_t pure_refills(uint32_t x, const WalkDesc &d) {
+    uint32_t r = 0;
+    const uint32_t rmax = d.flags >> 8;
+    for (uint32_t k = 0; k < rmax; ++k) r += x < (d.L >> (d.bits * k)) ? 1u : 0u;
+    return r;
+}
+
+// Per-step word for the walk, built in parallel from the stable sort of
+// the schedule: stream id | reload << 16 | min(t - prev, 63) << 17, where
+// prev is the stream's previous step (none: 63) and reload marks a stream
+// whose previous step lies in an earlier epoch (its state is inline here,
+// mux.py:459-465).
+__global__ void walk_prep_kernel(const int32_t *__restrict__ keys,
+                                 const int32_t *__restrict__ perm, int64_t T, int32_t F,
+                                 uint32_t *__restrict__ word) {
+    MUX_FOR(i, T) {
+        const int32_t t = perm[i];
+        const bool has_prev = i > 0 && keys[i - 1] == keys[i];
+        const int32_t prev = has_prev ? perm[i - 1] : -1;
+        const uint32_t dist = has_prev ? min(t - prev, 63) : 63u;
+        const uint32_t reload = has_prev && (prev / F != t / F) ? 1u : 0u;
+        word[t] = uint32_t(keys[i]) | reload << 16 | dist << 17;
+    }
+}
+
+// Walk staging rings in shared memory, refilled by cp.async half a ring
+// ahead of the walker: the per-step words (2 x 2048) and the payload
+// (2 x 4 KB). The device arrays are padded to whole halves plus one.
+constexpr uint32_t kWordHalf = 2048;                // words per half
+constexpr uint32_t kPayHalf = 4096;                 // payload bytes per half
+constexpr size_t kWalkRingBytes = 2 * kWordHalf * 4 + 2 * kPayHalf;
+
+// 4 payload bytes at absolute byte offset b from the payload ring
+__device__ __forceinline__ uint32_t ring4(const uint32_t *pr, uint32_t b) {
+    const uint32_t q = b >> 2;
+    return __funnelshift_r(pr[q & (2 * kPayHalf / 4 - 1)], pr[(q + 1) & (2 * kPayHalf / 4 - 1)],
+                           (b & 3u) * 8u);
+}
+
+// one half (kWordHalf words or kPayHalf bytes) of a ring, 16 bytes a lane
+__device__ __forceinline__ void ring_fill(void *dst, const void *src, uint32_t bytes, int lane) {
+    for (uint32_t o = 16u * lane; o < bytes; o += 512u)
+        cp_async16(static_cast<uint8_t *>(dst) + o, static_cast<const uint8_t *>(src) + o, 16u);
+}
+
 // demux_decode (mux.py:436-475): headers first (stream order), then the
-// schedule; a stream's state reloads inline when its epoch changes
-// (mux.py:459-465). One thread walks: each step's read offset depends on
-// the refill count of the step before, so there is nothing to split; the
-// loop is a latency chain (shared load of the stream's state -> lookup ->
-// multiply-add -> compare -> shift-in), kept in 32-bit arithmetic. SMEM:
-// per-stream records, states, epochs and the decode lookups are staged in
-// shared memory (they fit for up to a few thousand streams / tables). The
-// next 4 payload bytes are loaded before the pop decides how many of them
-// it needs, so that load overlaps the lookup.
+// schedule.
+//
+// Each step's read offset is the sum of the read sizes of all earlier
+// steps, and a step's read size depends on its stream's state -- but only
+// on that stream's. So a run of consecutive steps that touch DISTINCT
+// streams decodes together: warp 0 takes up to 32 steps and cuts the
+// window at the first step whose stream already occurs in it (t - prev <=
+// lane), at the first inline state reload after lane 0, and at an impure
+// stream; every lane pops its stream's state, its refill count follows from
+// the popped state, three ballots give the prefix sum of the read sizes
+// (< 8 bytes a step), and every lane shifts in its own digits from the
+// window's 256 payload bytes, staged in registers when the window opens.
+// Round-robin schedules over K >= 32 streams run 32 steps per window. A
+// window that starts at an impure stream takes one step with the
+// reference's digit loop. Records, states and lookups sit in shared memory
+// when they fit (SMEM).
 template <bool SMEM>
 __global__ void __launch_bounds__(256) demux_kernel(
     const WalkDesc *__restrict__ gdesc, int K, const uint2 *__restrict__ glut, int64_t n_lut,
     const uint8_t *hdr, const uint64_t *hdr_off, const uint32_t *__restrict__ pay, uint32_t plen,
-    const int32_t *__restrict__ sched, int32_t T, int32_t F, uint32_t *gstate, int32_t *gepoch,
-    uint32_t *__restrict__ out, DemuxStatus *st) {
+    const uint32_t *__restrict__ word, int32_t T, uint32_t *gstate, uint32_t *__restrict__ out,
+    DemuxStatus *st) {
     extern __shared__ __align__(16) uint8_t dsm[];
+    uint8_t *ring_smem = dsm;  // kWalkRingBytes, then the SMEM tables
     const WalkDesc *desc = gdesc;
     const uint2 *lut = glut;
     uint32_t *state = gstate;
-    int32_t *epoch = gepoch;
     if (SMEM) {
-        WalkDesc *sd = reinterpret_cast<WalkDesc *>(dsm);
+        WalkDesc *sd = reinterpret_cast<WalkDesc *>(dsm + kWalkRingBytes);
         uint2 *sl = reinterpret_cast<uint2 *>(sd + K);
         for (int64_t i = threadIdx.x; i < n_lut; i += blockDim.x) sl[i] = glut[i];
         for (int j = threadIdx.x; j < K; j += blockDim.x) sd[j] = gdesc[j];
         lut = sl;
         desc = sd;
         state = reinterpret_cast<uint32_t *>(sl + n_lut);
-        epoch = reinterpret_cast<int32_t *>(state + K);
         __syncthreads();
     }
-    if (threadIdx.x != 0) return;
-    st->code = 0;
-    st->stream = -1;
-    st->step = -1;
-    for (int j = 0; j < K; ++j) {
-        const WalkDesc d = desc[j];
-        epoch[j] = -1;
-        if (d.raw) continue;  // raw: no state
-        if (hdr_off[j + 1] - hdr_off[j] < 4) {
-            st->code = ILANS_ERR_TRUNCATED;
-            st->stream = j;
-            return;
-        }
-        const uint32_t x = load_le(hdr + hdr_off[j], 4);
-        if (!state_ok(x, d)) {
-            st->code = ILANS_ERR_FORMAT;
-            st->stream = j;
-            st->value = x;
-            return;
-        }
-        state[j] = x;
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const uint32_t lt = lanemask_lt();
+    if (lane == 0) {
+        st->code = 0;
+        st->stream = -1;
+        st->step = -1;
     }
-    uint32_t pos = 0;
-    int32_t e = 0;
-    int32_t next_b = F;  // F = INT32_MAX: a single epoch
-    int32_t sid_n = sched[0];  // the device schedule is padded
-    int32_t t = 0;
-    for (; t < T; ++t) {
-        const int32_t sid = sid_n;
-        sid_n = sched[t + 1];
-        if (t == next_b) {
-            ++e;
-            next_b += F;
-        }
-        const WalkDesc d = desc[sid];
-        uint32_t x = state[sid];
-        // the two words under the cursor; combined only where a digit is
-        // consumed, so the load's latency hides behind the lookup
-        uint32_t w0 = __ldg(pay + (pos >> 2)), w1 = __ldg(pay + (pos >> 2) + 1);
-        const int32_t ep = epoch[sid];
-        if (ep != e) {
-            epoch[sid] = e;
-            if (ep >= 0 && !d.raw) {  // a later segment: its state inline
-                if (pos + 4 > plen) break;
-                x = __funnelshift_r(w0, w1, (pos & 3u) * 8u);
-                pos += 4;
-                if (!state_ok(x, d)) {
-                    st->code = ILANS_ERR_FORMAT;
-                    st->stream = sid;
-                    st->step = t;
-                    st->value = x;
-                    st->pos = pos;
-                    return;
+    // stream headers, in stream order (the first failing stream reports)
+    for (int j0 = 0; j0 < K; j0 += 32) {
+        const int j = j0 + lane;
+        int err = 0;
+        uint32_t x = 0;
+        if (j < K) {
+            const WalkDesc d = desc[j];
+            if (!(d.flags & kWalkRaw)) {
+                if (hdr_off[j + 1] - hdr_off[j] < 4) {
+                    err = ILANS_ERR_TRUNCATED;
+                } else {
+                    x = load_le(hdr + hdr_off[j], 4);
+                    if (!state_ok(x, d)) err = ILANS_ERR_FORMAT;
+                    state[j] = x;
                 }
-                w0 = __ldg(pay + (pos >> 2));
-                w1 = __ldg(pay + (pos >> 2) + 1);
             }
         }
-        if (d.raw) {  // raw value
-            const uint32_t v = __funnelshift_r(w0, w1, (pos & 3u) * 8u);
-            pos += d.nb;
-            if (pos > plen) break;
-            out[t] = v & d.dmask;
-            continue;
-        }
-        const uint2 en = lut[d.lut_off + (x & d.mask)];
-        x = en.y * (x >> d.sb) + (en.x >> 8);
-        if (x < d.L) {
-            x = (x << d.bits) | (__funnelshift_r(w0, w1, (pos & 3u) * 8u) & d.dmask);
-            pos += d.nb;
-            while (x < d.L) {  // byte digits: up to 3 per symbol
-                x = (x << d.bits) | (load4(pay, pos) & d.dmask);
-                pos += d.nb;
+        const uint32_t eb = __ballot_sync(0xffffffffu, err != 0);
+        if (eb) {
+            if (lane == __ffs(eb) - 1) {
+                st->code = err;
+                st->stream = j;
+                st->value = x;
             }
-            if (pos > plen) break;
+            return;
         }
-        state[sid] = x;
-        out[t] = en.x & 0xFF;
     }
-    if (t < T) {  // a read ran past the payload
-        st->code = ILANS_ERR_TRUNCATED;
-        st->stream = sched[t];
-        st->step = t;
+    __syncwarp();
+
+    uint32_t pos = 0;
+    int32_t t = 0;
+    // rings: words [wbase, wbase + 2 halves), payload bytes [pbase, pbase +
+    // 2 halves); *_ready: end of what has landed
+    uint32_t *wring = reinterpret_cast<uint32_t *>(ring_smem);
+    uint32_t *pring = wring + 2 * kWordHalf;
+    uint32_t wbase = 0, wissued = 2 * kWordHalf, wready = 0;
+    uint32_t pbase = 0, pissued = 2 * kPayHalf, pready = 0;
+    ring_fill(wring, word, 2 * kWordHalf * 4, lane);
+    ring_fill(pring, pay, 2 * kPayHalf, lane);
+    cp_async_commit();
+    while (t < T) {
+        // refill the half behind the walker, wait only when the window
+        // needs what is still in flight
+        if (uint32_t(t) >= wbase + kWordHalf) {
+            ring_fill(wring + (wissued / kWordHalf & 1u) * kWordHalf, word + wissued,
+                      kWordHalf * 4, lane);
+            cp_async_commit();
+            wbase += kWordHalf;
+            wissued += kWordHalf;
+        }
+        if (pos >= pbase + kPayHalf) {
+            ring_fill(reinterpret_cast<uint8_t *>(pring) + (pissued / kPayHalf & 1u) * kPayHalf,
+                      reinterpret_cast<const uint8_t *>(pay) + pissued, kPayHalf, lane);
+            cp_async_commit();
+            pbase += kPayHalf;
+            pissued += kPayHalf;
+        }
+        if (uint32_t(t) + 32 > wready || pos + 264 > pready) {
+            cp_async_wait<0>();
+            __syncwarp();
+            wready = wissued;
+            pready = pissued;
+        }
+        const int32_t step = t + lane;
+        const bool valid = step < T;
+        const uint32_t cur = wring[uint32_t(step) & (2 * kWordHalf - 1)];
+        const int32_t sid = valid ? int32_t(cur & 0xFFFFu) : 0;
+        const WalkDesc d = desc[sid];
+        const bool raw = d.flags & kWalkRaw;
+        const bool reload = valid && !raw && ((cur >> 16) & 1u);
+        const bool dup = (cur >> 17) <= uint32_t(lane);
+        const bool impure = !raw && !(d.flags & kWalkPure);
+        const bool impure0 = __shfl_sync(0xffffffffu, impure, 0);  // lane 0 goes alone
+        const bool stop = !valid || dup || (lane > 0 && (reload || impure || impure0));
+        const uint32_t sbal = __ballot_sync(0xffffffffu, stop);
+        const int W = sbal ? __ffs(sbal) - 1 : 32;  // >= 1: lane 0 is valid and first
+        const bool on = lane < W;
+        uint32_t x = raw ? 0u : state[sid];
+        uint32_t extra = 0;
+        int err = 0;
+        if (on && reload) {  // lane 0 only: the state inline at the window start
+            if (pos + 4 > plen) {
+                err = ILANS_ERR_TRUNCATED;
+            } else {
+                x = ring4(pring, pos);
+                extra = 4;
+                if (!state_ok(x, d)) err = ILANS_ERR_FORMAT;
+            }
+        }
+        uint32_t sym = 0, bytes = 0;
+        if (on && !err) {
+            if (raw) {
+                bytes = d.nb;
+            } else {
+                const uint2 en = lut[d.lut_off + (x & d.mask)];
+                x = en.y * (x >> d.sb) + (en.x >> 8);
+                sym = en.x & 0xFFu;
+                if (!impure0) bytes = pure_refills(x, d) * d.nb;
+            }
+        }
+        if (impure0 && lane == 0 && !err) {
+            // lane 0 alone, the digits decide the count: the reference's loop
+            uint32_t p = pos + extra;
+            while (x < d.L) {
+                if (p + d.nb > plen) {
+                    err = ILANS_ERR_TRUNCATED;
+                    break;
+                }
+                x = (x << d.bits) | (load4(pay, p) & d.dmask);
+                p += d.nb;
+            }
+            bytes = p - pos - extra;
+        }
+        // offsets: prefix sum of the window's read sizes (< 8 bytes a step:
+        // a 4-byte reload + 3 byte digits at most), three ballots
+        const uint32_t mine = on ? extra + bytes : 0u;
+        const uint32_t b0 = __ballot_sync(0xffffffffu, mine & 1u);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, mine & 2u);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, mine & 4u);
+        const uint32_t at = pos + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
+        const uint32_t wtot = __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
+        if (on && !err && at + mine > plen) err = ILANS_ERR_TRUNCATED;
+        const uint32_t ebal = __ballot_sync(0xffffffffu, err != 0);
+        if (ebal) {
+            const int f = __ffs(ebal) - 1;
+            if (lane == f) {
+                st->code = err;
+                st->stream = sid;
+                st->step = step;
+                st->value = x;
+                st->pos = at;
+            }
+            return;
+        }
+        if (on) {
+            // this step's 4 bytes after its reload (impure lane 0 is done)
+            const uint32_t w = ring4(pring, at + extra);
+            if (raw) {
+                out[step] = w & d.dmask;
+            } else {
+                if (!impure0 && bytes) {
+                    if (d.nb == 2) {
+                        x = (x << 16) | (w & 0xFFFFu);
+                    } else {  // byte digits, read in order
+                        for (uint32_t k = 0; k < bytes; ++k) x = (x << 8) | ((w >> (8 * k)) & 0xFFu);
+                    }
+                }
+                state[sid] = x;
+                out[step] = sym;
+            }
+        }
+        pos += wtot;
+        t += W;
+        __syncwarp();
     }
-    st->pos = pos;
+    cp_async_wait<0>();
+    if (lane == 0) st->pos = pos;
+}
+
+// stream-major order of the decoded values: dst[i] = src[perm[i]]
+__global__ void gather_kernel(const int32_t *__restrict__ perm, const uint32_t *__restrict__ src,
+                              int64_t T, uint32_t *__restrict__ dst) {
+    MUX_FOR(i, T) dst[i] = src[perm[i]];
 }
 
 // cudaMallocAsync'd scratch, released on the call's stream
@@ -804,7 +947,8 @@ extern "C" int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_stream
                                const uint8_t *headers, const uint64_t *header_off,
                                const uint8_t *payload, int64_t payload_len,
                                const int32_t *schedule, int64_t n_steps, int64_t flush_interval,
-                               uint32_t *symbols_out, int64_t *unread, ilans_status *st) {
+                               uint32_t *symbols_out, uint32_t *symbols_by_stream,
+                               int64_t *unread, ilans_status *st) {
     st_clear(st);
     const int K = n_streams;
     const int64_t T = n_steps;
@@ -826,7 +970,7 @@ extern "C" int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_stream
     uint32_t *d_freq = nullptr, *d_cum = nullptr, *d_state = nullptr, *d_out = nullptr;
     uint8_t *d_slot = nullptr, *d_hdr = nullptr;
     uint64_t *d_hoff = nullptr;
-    int32_t *d_epoch = nullptr, *d_sched = nullptr;
+    int32_t *d_sched = nullptr;
     uint2 *d_lut = nullptr;
     WalkDesc *d_desc = nullptr;
     DemuxStatus *d_st = nullptr;
@@ -834,14 +978,25 @@ extern "C" int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_stream
     for (int j = 0; j < K; ++j) {
         const ilans_mux_stream &p = streams[j];
         WalkDesc &d = desc[j];
-        d.raw = p.kind == ILANS_MUX_RAW;
+        const bool raw = p.kind == ILANS_MUX_RAW;
         d.nb = uint32_t(p.nbytes);
         d.dmask = p.nbytes >= 4 ? ~0u : (1u << (8 * p.nbytes)) - 1u;
-        d.lut_off = d.raw ? 0u : uint32_t(p.slot_off);
-        d.L = d.raw ? 0u : p.lower_bound;
-        d.sb = d.raw ? 0u : uint32_t(p.scale_bits);
-        d.mask = d.raw ? 0u : (1u << p.scale_bits) - 1u;
-        d.bits = d.raw ? 0u : uint32_t(p.digit_bits);
+        d.lut_off = raw ? 0u : uint32_t(p.slot_off);
+        d.L = raw ? 0u : p.lower_bound;
+        d.sb = raw ? 0u : uint32_t(p.scale_bits);
+        d.mask = raw ? 0u : (1u << p.scale_bits) - 1u;
+        d.bits = raw ? 0u : uint32_t(p.digit_bits);
+        uint32_t rmax = 0;
+        bool pure = true;
+        if (!raw) {  // refills from x' = 1, and whether R^(k-1) | L for each
+            uint64_t v = 1;
+            while (v < p.lower_bound) {
+                if (p.lower_bound % v) pure = false;
+                v <<= p.digit_bits;
+                ++rmax;
+            }
+        }
+        d.flags = (raw ? kWalkRaw : 0u) | (raw || pure ? kWalkPure : 0u) | rmax << 8;
     }
     CK(m.upload(&d_streams, streams, size_t(K)));
     CK(m.upload(&d_desc, desc.data(), size_t(K)));
@@ -853,39 +1008,59 @@ extern "C" int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_stream
     CK(m.upload(&d_hoff, header_off, size_t(K) + 1));
     // payload as 4-byte words + 8 bytes of padding for the look-ahead loads
     uint32_t *d_payw = nullptr;
-    const size_t pwords = (size_t(payload_len) + 3) / 4 + 2;
+    // whole ring halves past the end (the rings copy halves; reads stop at plen)
+    const size_t pwords = ((size_t(payload_len) + kPayHalf - 1) / kPayHalf + 2) * (kPayHalf / 4);
     CK(m.alloc(&d_payw, pwords));
     CK(cudaMemsetAsync(d_payw, 0, pwords * 4, s));
     if (payload_len)
         CK(cudaMemcpyAsync(d_payw, payload, size_t(payload_len), cudaMemcpyHostToDevice, s));
-    CK(m.alloc(&d_sched, size_t(T) + 2));  // + entries read ahead
-    CK(cudaMemsetAsync(d_sched + T, 0, 8, s));
+    CK(m.alloc(&d_sched, size_t(T) + 128));  // + entries read ahead
+    CK(cudaMemsetAsync(d_sched + T, 0, 128 * 4, s));
     if (T) CK(cudaMemcpyAsync(d_sched, schedule, size_t(T) * 4, cudaMemcpyHostToDevice, s));
     CK(m.alloc(&d_state, size_t(K)));
-    CK(m.alloc(&d_epoch, size_t(K)));
     CK(m.alloc(&d_out, size_t(T)));
     CK(m.alloc(&d_st, 1));
     mux_lut_kernel<<<K < 1024 ? K : 1024, 256, 0, s>>>(d_streams, K, d_freq, d_cum, d_slot, d_lut);
     ilans_note_launch();
-    const size_t smem = size_t(n_slot) * sizeof(uint2) + size_t(K) * (sizeof(WalkDesc) + 8);
+    // per-step words from the stable sort of the schedule
+    uint32_t *d_word = nullptr;
+    const size_t nwords = ((size_t(T) + kWordHalf - 1) / kWordHalf + 2) * kWordHalf;
+    CK(m.alloc(&d_word, nwords));
+    CK(cudaMemsetAsync(d_word, 0, nwords * 4, s));
     const int32_t F32 = (flush_interval <= 0 || flush_interval >= T) ? INT32_MAX
                                                                       : int32_t(flush_interval);
+    int32_t *perm = nullptr;
+    if (T > 0) {
+        int32_t *keys = nullptr;
+        if (int rc = sort_schedule(m, d_sched, T, K, &keys, &perm, st)) return rc;
+        walk_prep_kernel<<<mux_blocks(T), kMuxThreads, 0, s>>>(keys, perm, T, F32, d_word);
+        ilans_note_launch();
+    }
+    const size_t smem = kWalkRingBytes + size_t(n_slot) * sizeof(uint2) +
+                        size_t(K) * (sizeof(WalkDesc) + 4);
     if (smem <= size_t(200) * 1024) {
-        if (smem > 48 * 1024)
-            CK(cudaFuncSetAttribute(demux_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CK(cudaFuncSetAttribute(demux_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(smem)));
         demux_kernel<true><<<1, 256, smem, s>>>(d_desc, K, d_lut, n_slot, d_hdr, d_hoff, d_payw,
-                                                uint32_t(payload_len), d_sched, int32_t(T), F32,
-                                                d_state, d_epoch, d_out, d_st);
+                                                uint32_t(payload_len), d_word, int32_t(T),
+                                                d_state, d_out, d_st);
     } else {
-        demux_kernel<false><<<1, 32, 0, s>>>(d_desc, K, d_lut, n_slot, d_hdr, d_hoff, d_payw,
-                                             uint32_t(payload_len), d_sched, int32_t(T), F32,
-                                             d_state, d_epoch, d_out, d_st);
+        demux_kernel<false><<<1, 32, kWalkRingBytes, s>>>(
+            d_desc, K, d_lut, n_slot, d_hdr, d_hoff, d_payw, uint32_t(payload_len), d_word,
+            int32_t(T), d_state, d_out, d_st);
     }
     ilans_note_launch();
     DemuxStatus h{};
     CK(cudaMemcpyAsync(&h, d_st, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(symbols_out, d_out, size_t(T) * 4, cudaMemcpyDeviceToHost, s));
+    if (symbols_out && T)
+        CK(cudaMemcpyAsync(symbols_out, d_out, size_t(T) * 4, cudaMemcpyDeviceToHost, s));
+    if (symbols_by_stream && T) {  // stream-major: out[perm[i]]
+        uint32_t *d_sm = nullptr;
+        CK(m.alloc(&d_sm, size_t(T)));
+        gather_kernel<<<mux_blocks(T), kMuxThreads, 0, s>>>(perm, d_out, T, d_sm);
+        ilans_note_launch();
+        CK(cudaMemcpyAsync(symbols_by_stream, d_sm, size_t(T) * 4, cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaStreamSynchronize(s));
     if (h.code) {
         st->stream = h.stream;

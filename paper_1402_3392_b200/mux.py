@@ -412,12 +412,12 @@ def demux_decode(muxed, coders, schedule=None) -> list[list[int]]:
     st = _lib.Status()
     rc = _lib.lib.ilans_mux_demux(
         *streams.table_args(True), _lib.ptr(hcat), _lib.ptr(hoff), _lib.ptr(pbuf), len(payload),
-        _lib.ptr(sched_buf), t, flush, _lib.ptr(out), ctypes.byref(unread), ctypes.byref(st))
+        _lib.ptr(sched_buf), t, flush, None, _lib.ptr(out), ctypes.byref(unread),
+        ctypes.byref(st))
     _lib.raise_for(rc, st, "demux")
     if unread.value:
         warnings.warn(f"{unread.value} unread bytes after demux", TrailingGarbageWarning,
                       stacklevel=2)
-    order = np.argsort(sched, kind="stable")
-    values = out[:t][order]
+    values = out[:t]  # stream by stream (the device's stable sort of the schedule)
     ends = np.cumsum(lengths)
     return [values[e - n: e].tolist() for n, e in zip(lengths, ends)]

@@ -5,7 +5,7 @@ from paper_1402_3392_b200.synth import synth_host
 import ilans as ref
 msg = synth_host(1 << 20, 1.1, seed=1)
 counts = np.bincount(msg, minlength=256)
-for N in (1, 2, 4, 8, 16, 32):
+for N in [int(v) for v in (sys.argv[1].split(",") if len(sys.argv) > 1 else "1,2,4,8,16,32".split(","))]:
     t = ilb.SymbolTable.from_counts(counts.tolist(), 14)
     rt = ref.rans.SymbolTable.from_counts(counts.tolist(), 14)
     c = ilb.encode_interleaved(msg, t, N); ilb.decode_interleaved(c)
