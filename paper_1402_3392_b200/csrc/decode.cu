@@ -210,7 +210,8 @@ __host__ __device__ constexpr size_t decode_warp_smem() { return kRingAllocBytes
 // Not inlined: with both LUT forms inlined into one kernel the packed
 // path's schedule degrades (~8% slower decode, measured); as a call each
 // body keeps its own register allocation.
-// SMALL: the instantiation for power-of-two N < 32 (512/N-group batches);
+// SMALL: the instantiation for N < 32 (512/N-group batches for powers of two,
+// floor(256/N)-group batches otherwise);
 // a separate body so the N = 32 batch loop keeps its own schedule.
 template <int KIND, class Sink, bool SMALL>
 __device__ __noinline__ void
@@ -296,7 +297,12 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
             // to two segments past the one holding the cursor, so the ring
             // runs one segment deeper here (wait<1>: everything but the
             // newest segment has landed).
-            const int64_t full = len / (32 * kBatch);
+            // N < 32 not a power of two: batches of floor(256/N) groups
+            // (<= 256 symbols), flushed by 256-byte halves like the loop below
+            const bool pow2n = (n_lanes & (n_lanes - 1)) == 0;
+            const int gpb = pow2n ? 512 / n_lanes : 256 / n_lanes;
+            const int64_t spb = !SMALL ? int64_t(32 * kBatch) : int64_t(gpb) * n_lanes;
+            const int64_t full = len / spb;
             uint32_t vb = static_cast<uint32_t>(v) << 1;  // byte cursor (mod 2^32)
             uint32_t seg_cur = 0;                          // vb >> 9 of the cursor
             uint32_t next_seg = 4;                         // next segment to issue
@@ -324,6 +330,20 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                         a = mad_lo(__popc(mk), two, a);
                         obuf[g * 32 + lane] = static_cast<uint8_t>(s);
                     }
+                } else if (!pow2n) {
+                    const bool on = lane < n_lanes;
+                    uint32_t oi = static_cast<uint32_t>(b * spb) + lane;  // obuf index mod 512
+#pragma unroll 4
+                    for (int g = 0; g < gpb; ++g) {
+                        const uint32_t s = lut.pop(x);
+                        const bool need = on && x < kLow;
+                        const uint32_t mk = __ballot_sync(0xffffffffu, need);
+                        const uint32_t w = lds_u16(mad_lo(__popc(mk * lt_mul), two, a));
+                        x = need ? x * 65536u + w : x;
+                        a = mad_lo(__popc(mk), two, a);
+                        if (on) obuf[oi & (kObufBytes - 1)] = static_cast<uint8_t>(s);
+                        oi += n_lanes;
+                    }
                 } else {
                     // N < 32: lanes >= N idle (their state stays 0, never
                     // renormalises, never stores); 512/N groups per batch
@@ -345,7 +365,13 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                 }
                 vb = vb0 + (a - a0);
                 __syncwarp();
-                sink.block512(obuf, b * (32 * kBatch), lane);
+                if (!SMALL || pow2n) {
+                    sink.block512(obuf, b * (32 * kBatch), lane);
+                } else {
+                    const int64_t blk = (b * spb) >> 8;
+                    if (((b * spb + spb) >> 8) != blk)  // a 256-byte half is complete
+                        sink.block256(obuf + (blk & 1) * kObufHalf, blk << 8, lane);
+                }
                 v += (vb - vb0) >> 1;
                 const uint32_t seg = (vb >> 9) & 0x7FFFFFu;
                 if (seg != seg_cur) {  // one or two segments were finished
@@ -367,7 +393,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                 __syncwarp();
             }
             cur = next_seg - 4;  // == v / kSegWords; cur + 1.. cur + 3 issued
-            base = full * (32 * kBatch);
+            base = full * spb;
         }
         // ---------------- generic per-group loop (any N <= 32, tails) ------
         bool truncated = (v - delta) > wlen;
@@ -467,7 +493,7 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
         return;
     }
-    if (n_lanes < 32 && (n_lanes & (n_lanes - 1)) == 0)
+    if (n_lanes < 32)
         decode_warp_dispatch<MAXKIND, Sink, true>(payload, offsets, states, n, chunk_len,
                                                   n_chunks, n_lanes, tab, out, consumed,
                                                   final_states, status, trace, smem, sb);
