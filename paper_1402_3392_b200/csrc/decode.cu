@@ -210,10 +210,10 @@ __host__ __device__ constexpr size_t decode_warp_smem() { return kRingAllocBytes
 // Not inlined: with both LUT forms inlined into one kernel the packed
 // path's schedule degrades (~8% slower decode, measured); as a call each
 // body keeps its own register allocation.
-// SMALL: the instantiation for N < 32 (512/N-group batches for powers of two,
-// floor(256/N)-group batches otherwise);
-// a separate body so the N = 32 batch loop keeps its own schedule.
-template <int KIND, class Sink, bool SMALL>
+// MODE 0: N = 32; 1: power-of-two N < 32 (512/N-group batches); 2: other
+// N < 32 (floor(256/N)-group batches). Separate bodies (and mode 2 a
+// separate kernel) so the N = 32 batch loop keeps its own schedule.
+template <int KIND, class Sink, int MODE>
 __device__ __noinline__ void
 decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                  const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -221,6 +221,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                  Sink sink, uint64_t *__restrict__ consumed,
                  uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
                  DecodeTrace trace, uint8_t *smem, int sb) {
+    constexpr bool SMALL = MODE != 0;
     const uint32_t m = 1u << sb;
     const int nw = blockDim.x >> 5;
     uint8_t *lut_base = smem + nw * (kRingAllocBytes + kObufBytes);
@@ -299,9 +300,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
             // newest segment has landed).
             // N < 32 not a power of two: batches of floor(256/N) groups
             // (<= 256 symbols), flushed by 256-byte halves like the loop below
-            const bool pow2n = (n_lanes & (n_lanes - 1)) == 0;
-            const int gpb = pow2n ? 512 / n_lanes : 256 / n_lanes;
-            const int64_t spb = !SMALL ? int64_t(32 * kBatch) : int64_t(gpb) * n_lanes;
+            const int64_t spb = MODE == 2 ? int64_t(256 / n_lanes) * n_lanes : int64_t(32 * kBatch);
             const int64_t full = len / spb;
             uint32_t vb = static_cast<uint32_t>(v) << 1;  // byte cursor (mod 2^32)
             uint32_t seg_cur = 0;                          // vb >> 9 of the cursor
@@ -330,7 +329,8 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                         a = mad_lo(__popc(mk), two, a);
                         obuf[g * 32 + lane] = static_cast<uint8_t>(s);
                     }
-                } else if (!pow2n) {
+                } else if (MODE == 2) {
+                    const int gpb = 256 / n_lanes;
                     const bool on = lane < n_lanes;
                     uint32_t oi = static_cast<uint32_t>(b * spb) + lane;  // obuf index mod 512
 #pragma unroll 4
@@ -365,7 +365,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                 }
                 vb = vb0 + (a - a0);
                 __syncwarp();
-                if (!SMALL || pow2n) {
+                if (MODE != 2) {
                     sink.block512(obuf, b * (32 * kBatch), lane);
                 } else {
                     const int64_t blk = (b * spb) >> 8;
@@ -454,7 +454,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
     }
 }
 
-template <int MAXKIND, class Sink, bool SMALL>
+template <int MAXKIND, class Sink, int MODE>
 __device__ __forceinline__ void
 decode_warp_dispatch(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                      const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -462,15 +462,15 @@ decode_warp_dispatch(const uint16_t *__restrict__ payload, const uint64_t *__res
                      uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
                      DStatus *__restrict__ status, DecodeTrace trace, uint8_t *smem, int sb) {
     if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
-        decode_warp_body<kLutPacked32, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+        decode_warp_body<kLutPacked32, Sink, MODE>(payload, offsets, states, n, chunk_len,
                                                     n_chunks, n_lanes, tab, out, consumed,
                                                     final_states, status, trace, smem, sb);
     else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
-        decode_warp_body<kLutPacked64, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+        decode_warp_body<kLutPacked64, Sink, MODE>(payload, offsets, states, n, chunk_len,
                                                     n_chunks, n_lanes, tab, out, consumed,
                                                     final_states, status, trace, smem, sb);
     else
-        decode_warp_body<kLutGeneric, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+        decode_warp_body<kLutGeneric, Sink, MODE>(payload, offsets, states, n, chunk_len,
                                                    n_chunks, n_lanes, tab, out, consumed,
                                                    final_states, status, trace, smem, sb);
 }
@@ -479,7 +479,7 @@ decode_warp_dispatch(const uint16_t *__restrict__ payload, const uint64_t *__res
 // also fits the two-lookup form); the device table's flags pick which one
 // runs (a single-symbol sb=12 table has f = 4096, which the 12-bit field of
 // the 32-bit entry cannot hold).
-template <int MAXKIND, class Sink>
+template <int MAXKIND, class Sink, bool NP2>
 __global__ void __launch_bounds__(1024)
 decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                    const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -493,14 +493,18 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
         return;
     }
-    if (n_lanes < 32)
-        decode_warp_dispatch<MAXKIND, Sink, true>(payload, offsets, states, n, chunk_len,
-                                                  n_chunks, n_lanes, tab, out, consumed,
-                                                  final_states, status, trace, smem, sb);
+    if (NP2)
+        decode_warp_dispatch<MAXKIND, Sink, 2>(payload, offsets, states, n, chunk_len,
+                                               n_chunks, n_lanes, tab, out, consumed,
+                                               final_states, status, trace, smem, sb);
+    else if (n_lanes < 32)
+        decode_warp_dispatch<MAXKIND, Sink, 1>(payload, offsets, states, n, chunk_len,
+                                               n_chunks, n_lanes, tab, out, consumed,
+                                               final_states, status, trace, smem, sb);
     else
-        decode_warp_dispatch<MAXKIND, Sink, false>(payload, offsets, states, n, chunk_len,
-                                                   n_chunks, n_lanes, tab, out, consumed,
-                                                   final_states, status, trace, smem, sb);
+        decode_warp_dispatch<MAXKIND, Sink, 0>(payload, offsets, states, n, chunk_len,
+                                               n_chunks, n_lanes, tab, out, consumed,
+                                               final_states, status, trace, smem, sb);
 }
 
 // ---------------------------------------------------------------------------
@@ -668,24 +672,25 @@ static cudaError_t launch_decode_warp(const uint16_t *d_payload, const uint64_t 
     const int64_t max_blocks = sms * (per_sm < 1 ? 1 : per_sm);
     if (blocks > max_blocks) blocks = max_blocks;
     const unsigned g = static_cast<unsigned>(blocks);
+    auto go = [&](auto kernel) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        kernel<<<g, warps * 32, smem, stream>>>(d_payload, d_word_offsets, d_states, n,
+                                                chunk_len, n_chunks, n_lanes, d_table, sink,
+                                                d_consumed, d_final_states, d_status,
+                                                scale_bits, trace);
+    };
+    // N < 32 not a power of two: its own kernel (mode 2), so the N = 32
+    // kernel's call graph -- and register allocation -- stays as it was
+    const bool np2 = n_lanes < 32 && (n_lanes & (n_lanes - 1)) != 0;
     if (maxkind == kLutPacked32) {
-        cudaFuncSetAttribute(decode_warp_kernel<kLutPacked32, Sink>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        decode_warp_kernel<kLutPacked32, Sink><<<g, warps * 32, smem, stream>>>(
-            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
-            sink, d_consumed, d_final_states, d_status, scale_bits, trace);
+        if (np2) go(decode_warp_kernel<kLutPacked32, Sink, true>);
+        else go(decode_warp_kernel<kLutPacked32, Sink, false>);
     } else if (maxkind == kLutPacked64) {
-        cudaFuncSetAttribute(decode_warp_kernel<kLutPacked64, Sink>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        decode_warp_kernel<kLutPacked64, Sink><<<g, warps * 32, smem, stream>>>(
-            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
-            sink, d_consumed, d_final_states, d_status, scale_bits, trace);
+        if (np2) go(decode_warp_kernel<kLutPacked64, Sink, true>);
+        else go(decode_warp_kernel<kLutPacked64, Sink, false>);
     } else {
-        cudaFuncSetAttribute(decode_warp_kernel<kLutGeneric, Sink>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        decode_warp_kernel<kLutGeneric, Sink><<<g, warps * 32, smem, stream>>>(
-            d_payload, d_word_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table,
-            sink, d_consumed, d_final_states, d_status, scale_bits, trace);
+        if (np2) go(decode_warp_kernel<kLutGeneric, Sink, true>);
+        else go(decode_warp_kernel<kLutGeneric, Sink, false>);
     }
     ilans_note_launch();
     return cudaGetLastError();

@@ -119,15 +119,17 @@ struct SpillStage {
 // format's case; long long only for huge single-stream calls).
 // F12: the sb = 14 instantiation (12-byte fast records); the other one
 // carries the 8-byte fast loop, so neither pays for the other's registers.
-// SMALL: power-of-two N < 32 (512/N-group batches with the fast records),
-// a separate instantiation so the N = 32 loops keep their schedule.
-template <typename Idx, bool F12, bool SMALL>
+// MODE 0: N = 32; 1: power-of-two N < 32 (512/N-group batches with the
+// fast records); 2: other N < 32 (floor(256/N)-group batches with the fast
+// records). Separate instantiations so the N = 32 loops keep their schedule.
+template <typename Idx, bool F12, int MODE>
 __global__ void __launch_bounds__(kEncMaxWarps * 32, 1)
 encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                    uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
                    uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
     extern __shared__ __align__(16) uint8_t esmem[];
+    constexpr bool SMALL = MODE == 1;
     const int nw = blockDim.x >> 5;
     uint2 *enc = reinterpret_cast<uint2 *>(esmem);
     uint2 *encf = enc + kMaxSym;  // EncFast {M, Z} / EncFast12 {M, Y}
@@ -181,10 +183,15 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         // N = 32: the 512-byte blocks below `full` run as unrolled batches of
         // 16 groups after the per-group loop has coded the tail [full*512, len)
         // (and power-of-two N < 32 with a fast record: 512/N groups each)
-        const Idx full = (SMALL ? (fast || fast12) : n_lanes == 32) ? (len >> 9) : 0;
+        const Idx full =
+            (MODE == 1 ? (fast || fast12) : MODE == 0 && n_lanes == 32) ? (len >> 9) : 0;
         const Idx groups = (len + n_lanes - 1) / n_lanes;
+        // MODE 2: the full groups below nbat * G run as batches of G groups
+        const int G = MODE == 2 ? 256 / n_lanes : 1;
+        const Idx nbat = MODE == 2 && (fast || fast12) ? (len / n_lanes) / G : 0;
+        const Idx gstop = MODE == 2 ? nbat * G : SMALL ? full * (512 / n_lanes) : full << 4;
         bool bad = false;
-        for (Idx gi = groups - 1; gi >= (SMALL ? full * (512 / n_lanes) : full << 4); --gi) {
+        for (Idx gi = groups - 1; gi >= gstop; --gi) {
             const Idx base = gi * n_lanes;
             const Idx left = len - base;
             const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
@@ -371,13 +378,71 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             }
             st.drain(top, lane);
         }
+        if (MODE == 2) {
+            // Batches of G groups (<= 256 bytes: inside the segment holding
+            // their top byte and the one below, both landed after wait<2>),
+            // records one group ahead; lanes >= N follow lane 0's symbol.
+            const bool on = lane < n_lanes;
+            const uint32_t lidx = on ? lane : 0u;
+            for (Idx bt = nbat - 1; !bad && bt >= 0; --bt) {
+                const Idx g_hi = bt * G + G - 1;
+                const Idx hs = (g_hi * n_lanes + n_lanes - 1) >> 9;
+                if (hs != cur) {  // segment cur fully consumed: recycle its slot
+                    cur = hs;
+                    __syncwarp();
+                    issue_msg_segment(ring, g, len, cur - 3, lane);
+                    cp_async_commit();
+                    cp_async_wait<2>();
+                    __syncwarp();
+                }
+                uint32_t topb = static_cast<uint32_t>(top) << 1;
+                const uint32_t topb0 = topb;
+                uint32_t ri = static_cast<uint32_t>(g_hi * n_lanes) + lidx;  // ring index
+                uint32_t sym_n = ring[ri & (kInRing - 1)];
+#pragma unroll 4
+                for (int j = 0; j < G; ++j) {
+                    const uint32_t sym = sym_n;
+                    ri -= n_lanes;
+                    if (j + 1 < G) sym_n = ring[ri & (kInRing - 1)];
+                    const uint2 a = encf[sym];
+                    macc &= a.x;
+                    bool spill;
+                    uint32_t z = 0;
+                    if (!F12) {
+                        const uint32_t xm = x & ~lowm;
+                        spill = on && xm + a.y < xm;
+                    } else {
+                        z = encz[sym];
+                        spill = on && (x | lowm) >= a.y;
+                    }
+                    const uint32_t mk = __ballot_sync(0xffffffffu, spill);
+                    topb -= two * __popc(mk);
+                    if (spill)
+                        sts16(oring_addr | ((topb + two * __popc(mk * lt_mul)) & (kOutRingBytes - 2)),
+                              x);
+                    x = spill ? x >> 16 : x;
+                    uint32_t q = __umulhi(x, a.x);
+                    if (!F12) {
+                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
+                        x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
+                    } else {
+                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
+                        x = q * (a.y & lowm) + (x + (z >> 17));
+                    }
+                }
+                top -= static_cast<Idx>((topb0 - topb) >> 1);
+                st.drain(top, lane);
+            }
+        }
         if ((fast || fast12) && !bad && __ballot_sync(0xffffffffu, (macc >> 31) == 0u)) {
             // rare: some symbol of the fast region has f = 0 (its scratch is
             // garbage but stayed inside the chunk: at most 32 spills per
             // group). The highest offending index, as the reference's
             // backward walk meets it first (_core.pyx:33-34):
-            for (Idx i0 = (full << 9) - 32; i0 >= 0; i0 -= 32) {
-                const uint32_t bm = __ballot_sync(0xffffffffu, enc[g[i0 + lane]].x == 0u);
+            const Idx fast_end = MODE == 2 ? nbat * G * n_lanes : full << 9;
+            for (Idx i0 = fast_end - 32; i0 > -32; i0 -= 32) {
+                const Idx i = i0 + lane;
+                const uint32_t bm = __ballot_sync(0xffffffffu, i >= 0 && enc[g[i]].x == 0u);
                 if (bm) {
                     if (lane == 0)
                         atomicMax(&status->unenc_index,
@@ -527,24 +592,23 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
         // the table's scale_bits is on the device; the sb = 14 instantiation
         // is picked by the caller's scale_bits and re-checks the flag itself
         const bool sb14 = scale_bits == 14;
-        const bool small = n_lanes < 32 && (n_lanes & (n_lanes - 1)) == 0;
-        if (chunk_len < (int64_t(1) << 30)) {
-            if (small) {
-                if (sb14) go(encode_warp_kernel<int, true, true>);
-                else go(encode_warp_kernel<int, false, true>);
+        // mode 1: power-of-two N < 32, mode 2: other N < 32, mode 0: N = 32
+        const int mode = n_lanes >= 32 ? 0 : (n_lanes & (n_lanes - 1)) == 0 ? 1 : 2;
+        auto pick = [&](auto idx) {
+            using I = decltype(idx);
+            if (mode == 1) {
+                if (sb14) go(encode_warp_kernel<I, true, 1>);
+                else go(encode_warp_kernel<I, false, 1>);
+            } else if (mode == 2) {
+                if (sb14) go(encode_warp_kernel<I, true, 2>);
+                else go(encode_warp_kernel<I, false, 2>);
             } else {
-                if (sb14) go(encode_warp_kernel<int, true, false>);
-                else go(encode_warp_kernel<int, false, false>);
+                if (sb14) go(encode_warp_kernel<I, true, 0>);
+                else go(encode_warp_kernel<I, false, 0>);
             }
-        } else {
-            if (small) {
-                if (sb14) go(encode_warp_kernel<long long, true, true>);
-                else go(encode_warp_kernel<long long, false, true>);
-            } else {
-                if (sb14) go(encode_warp_kernel<long long, true, false>);
-                else go(encode_warp_kernel<long long, false, false>);
-            }
-        }
+        };
+        if (chunk_len < (int64_t(1) << 30)) pick(int(0));
+        else pick(static_cast<long long>(0));
     }
     ilans_note_launch();
     return cudaGetLastError();

@@ -212,7 +212,7 @@ def test_fast_encoder_record_edges(sb):
     for freq in tables:
         t = SymbolTable(freq, sb)
         msg = random_message(rng, t, 70_001)
-        for lanes in (32, 16, 8, 4, 1):  # N < 32 powers of two: 512/N-group batches
+        for lanes in (32, 16, 8, 4, 1, 31, 7, 3):  # N < 32: 512/N- or 256/N-group batches
             payload, states = B.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, lanes)
             ref_p, ref_s = oracle.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, sb, lanes)
             assert np.array_equal(payload, ref_p) and np.array_equal(states, ref_s), (freq, lanes)
@@ -230,7 +230,7 @@ def test_unencodable_symbol_in_fast_batches():
     names the symbol at the highest offending index (the reference's
     backward walk meets it first, _core.pyx:33-34)."""
     t = SymbolTable([2048, 2047, 0, 0, 1], 12)
-    for lanes in (32, 8, 1):
+    for lanes in (32, 8, 1, 7, 3):
         msg = np.zeros(70_000, dtype=np.uint8)
         msg[100], msg[60_000] = 2, 3
         with pytest.raises(UnencodableSymbolError, match="symbol 3"):
