@@ -545,20 +545,30 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
                     int n_lanes, const TableDev *__restrict__ tab, uint8_t *__restrict__ out,
                     uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
                     DStatus *__restrict__ status, uint32_t *__restrict__ ws_all,
-                    DecodeTrace trace) {
+                    DecodeTrace trace, int ws_in_smem) {
     __shared__ uint32_t scan_sh[32];
+    // dynamic smem: dec[256] | slot -> symbol [2^sb] | lane states [N] (when
+    // ws_in_smem; else they stay in the global scratch)
+    extern __shared__ __align__(16) uint8_t bsm[];
+    const int sb = static_cast<int>(tab->scale_bits);
+    const uint32_t mask = (1u << sb) - 1u;
+    uint2 *dec = reinterpret_cast<uint2 *>(bsm);
+    uint8_t *slot_sym = bsm + kMaxSym * sizeof(uint2);
+    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) dec[i] = tab->dec[i];
+    for (uint32_t i = threadIdx.x; i < (1u << sb); i += blockDim.x) slot_sym[i] = tab->slot_sym[i];
     const int64_t k = blockIdx.x;
     const int64_t cbase = k * chunk_len;
     const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
     const uint64_t woff = offsets[k];
     const uint64_t wlen = offsets[k + 1] - woff;
     const uint16_t *pay = payload + woff;
-    uint32_t *ws = ws_all + k * n_lanes;
-    const int sb = static_cast<int>(tab->scale_bits);
-    const uint32_t mask = (1u << sb) - 1u;
+    uint32_t *ws = ws_in_smem
+                       ? reinterpret_cast<uint32_t *>(slot_sym + ((size_t(1) << sb) + 15 & ~size_t(15)))
+                       : ws_all + k * n_lanes;
     const int per = (n_lanes + blockDim.x - 1) / blockDim.x;
     const int lo = threadIdx.x * per;
     for (int l = lo; l < lo + per && l < n_lanes; ++l) ws[l] = states[k * n_lanes + l];
+    __syncthreads();
     uint64_t pos = 0;
     bool truncated = false;
     int64_t base = 0;
@@ -571,8 +581,8 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
         for (int l = lo; l < hi; ++l) {
             uint32_t x = ws[l];
             const uint32_t slot = x & mask;
-            const uint32_t s = tab->slot_sym[slot];
-            const uint2 d = tab->dec[s];
+            const uint32_t s = slot_sym[slot];
+            const uint2 d = dec[s];
             x = d.x * (x >> sb) + slot - d.y;
             out[cbase + base + l] = static_cast<uint8_t>(s);
             ws[l] = x;
@@ -610,6 +620,73 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
     }
     if (final_states)
         for (int l = lo; l < lo + per && l < n_lanes; ++l) final_states[k * n_lanes + l] = ws[l];
+}
+
+// 32 < N <= kWideMax, no trace: one warp per stream walks each group in
+// sub-groups of 32 lanes (lanes ascending, so the refill order is the
+// reference's), the lane states in shared memory. A sub-group costs about
+// what an N = 32 group does, with no CTA-wide scan per group.
+constexpr int kWideMax = 64;  // beyond this the CTA kernel wins (measured)
+__global__ void __launch_bounds__(32)
+decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                   const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                   int n_lanes, const TableDev *__restrict__ tab, uint8_t *__restrict__ out,
+                   uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
+                   DStatus *__restrict__ status) {
+    extern __shared__ __align__(16) uint8_t wsm[];  // dec[256] | slot [2^sb] | ws [N]
+    const int lane = threadIdx.x;
+    const uint32_t lt = lanemask_lt();
+    const int sb = static_cast<int>(tab->scale_bits);
+    const uint32_t mask = (1u << sb) - 1u;
+    uint2 *dec = reinterpret_cast<uint2 *>(wsm);
+    uint8_t *slot_sym = wsm + kMaxSym * sizeof(uint2);
+    uint32_t *ws = reinterpret_cast<uint32_t *>(slot_sym + (((size_t(1) << sb) + 15) & ~size_t(15)));
+    for (int i = lane; i < kMaxSym; i += 32) dec[i] = tab->dec[i];
+    for (uint32_t i = lane; i < (1u << sb); i += 32) slot_sym[i] = tab->slot_sym[i];
+    const int64_t k = blockIdx.x;
+    const int64_t cbase = k * chunk_len;
+    const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+    const uint64_t woff = offsets[k];
+    const uint64_t wlen = offsets[k + 1] - woff;
+    const uint16_t *pay = payload + woff;
+    for (int l = lane; l < n_lanes; l += 32) ws[l] = states[k * n_lanes + l];
+    __syncwarp();
+    uint64_t pos = 0;
+    bool truncated = false;
+    for (int64_t base = 0; base < len && !truncated; base += n_lanes) {
+        const int active = (len - base) < n_lanes ? static_cast<int>(len - base) : n_lanes;
+        for (int j0 = 0; j0 < active; j0 += 32) {
+            const int l = j0 + lane;
+            const bool on = l < active;
+            uint32_t x = on ? ws[l] : 0u, s = 0;
+            if (on) {
+                const uint32_t slot = x & mask;
+                s = slot_sym[slot];
+                const uint2 d = dec[s];
+                x = d.x * (x >> sb) + slot - d.y;
+            }
+            const bool need = on && x < kLow;
+            const uint32_t mk = __ballot_sync(0xffffffffu, need);
+            const uint32_t cnt = __popc(mk);
+            if (pos + cnt > wlen) {
+                truncated = true;
+                break;
+            }
+            if (need) x = (x << 16) | pay[pos + __popc(mk & lt)];
+            pos += cnt;
+            if (on) {
+                ws[l] = x;
+                out[cbase + base + l] = static_cast<uint8_t>(s);
+            }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        if (truncated) atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
+        if (consumed) consumed[k] = pos;
+    }
+    if (final_states)
+        for (int l = lane; l < n_lanes; l += 32) final_states[k * n_lanes + l] = ws[l];
 }
 
 static size_t decode_lut_bytes(int scale_bits, int kind) {
@@ -704,11 +781,29 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
                           DecodeTrace trace) {
     if (n <= 0) return cudaSuccess;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
+    if (n_lanes > 32 && n_lanes <= kWideMax && !trace.states) {
+        const size_t smem = kMaxSym * sizeof(uint2) +
+                            (((size_t(1) << scale_bits) + 15) & ~size_t(15)) +
+                            size_t(n_lanes) * 4;
+        cudaFuncSetAttribute(decode_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+        decode_wide_kernel<<<static_cast<unsigned>(n_chunks), 32, smem, stream>>>(
+            d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table, d_out,
+            d_consumed, d_final_states, d_status);
+        ilans_note_launch();
+        return cudaGetLastError();
+    }
     if (n_lanes > 32) {
         const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
-        decode_block_kernel<<<static_cast<unsigned>(n_chunks), threads, 0, stream>>>(
+        // tables (and the lane states when they fit) in shared memory
+        const size_t tabs = kMaxSym * sizeof(uint2) + (((size_t(1) << scale_bits) + 15) & ~size_t(15));
+        const int ws_smem = tabs + size_t(n_lanes) * 4 <= size_t(200) * 1024;
+        const size_t smem = tabs + (ws_smem ? size_t(n_lanes) * 4 : 0);
+        cudaFuncSetAttribute(decode_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+        decode_block_kernel<<<static_cast<unsigned>(n_chunks), threads, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table, d_out,
-            d_consumed, d_final_states, d_status, d_lane_ws, trace);
+            d_consumed, d_final_states, d_status, d_lane_ws, trace, ws_smem);
         ilans_note_launch();
         return cudaGetLastError();
     }

@@ -496,9 +496,10 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
                     int n_lanes, const TableDev *__restrict__ tab,
                     uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
                     uint32_t *__restrict__ states_out, DStatus *__restrict__ status,
-                    uint32_t *__restrict__ ws_all) {
+                    uint32_t *__restrict__ ws_all, int ws_in_smem) {
     __shared__ uint32_t scan_sh[32];
     __shared__ uint2 enc[kMaxSym];
+    extern __shared__ __align__(16) uint32_t bws[];  // lane states, when they fit
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
     __syncthreads();
     const EncCtx ctx(tab->scale_bits);
@@ -507,7 +508,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
     const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
     const uint8_t *g = msg + cbase;
     uint16_t *out = scratch + cbase;
-    uint32_t *ws = ws_all + k * n_lanes;
+    uint32_t *ws = ws_in_smem ? bws : ws_all + k * n_lanes;
     const int per = (n_lanes + blockDim.x - 1) / blockDim.x;
     const int lo = threadIdx.x * per;
     for (int l = lo; l < lo + per && l < n_lanes; ++l) ws[l] = kLow;
@@ -558,17 +559,81 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
     }
 }
 
+// 32 < N <= kWideMaxE: one warp per stream walks each group backwards in
+// sub-groups of 32 lanes (highest first; inside one, the packed store puts
+// the spills in ascending lane order), the lane states in shared memory.
+constexpr int kWideMaxE = 64;  // beyond this the CTA kernel wins (measured)
+__global__ void __launch_bounds__(32)
+encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len, int n_lanes,
+                   const TableDev *__restrict__ tab, uint16_t *__restrict__ scratch,
+                   uint32_t *__restrict__ chunk_words, uint32_t *__restrict__ states_out,
+                   DStatus *__restrict__ status) {
+    __shared__ uint2 enc[kMaxSym];
+    extern __shared__ __align__(16) uint32_t wws[];  // lane states [N]
+    const int lane = threadIdx.x;
+    const uint32_t lt = lanemask_lt();
+    for (int i = lane; i < kMaxSym; i += 32) enc[i] = tab->enc[i];
+    const EncCtx ctx(tab->scale_bits);
+    const int64_t k = blockIdx.x;
+    const int64_t cbase = k * chunk_len;
+    const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+    const uint8_t *g = msg + cbase;
+    uint16_t *out = scratch + cbase;
+    for (int l = lane; l < n_lanes; l += 32) wws[l] = kLow;
+    __syncwarp();
+    int64_t top = len;
+    bool bad = false;
+    for (int64_t gi = (len + n_lanes - 1) / n_lanes - 1; gi >= 0 && !bad; --gi) {
+        const int64_t base = gi * n_lanes;
+        const int active = (len - base) < n_lanes ? static_cast<int>(len - base) : n_lanes;
+        for (int j0 = ((active - 1) >> 5) << 5; j0 >= 0; j0 -= 32) {
+            const int l = j0 + lane;
+            const bool on = l < active;
+            const uint2 e = enc[on ? g[base + l] : 0u];
+            const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.x == 0u);
+            if (badmask) {  // the highest offending index (the reference walks down)
+                if (lane == 0)
+                    atomicMax(&status->unenc_index,
+                              static_cast<long long>(cbase + base + j0 + 31 - __clz(badmask)));
+                bad = true;
+                break;
+            }
+            uint32_t x = on ? wws[l] : 0u;
+            const bool spill = on && enc_spill(ctx, x, e);
+            const uint32_t mk = __ballot_sync(0xffffffffu, spill);
+            top -= __popc(mk);
+            if (spill) {
+                out[top + __popc(mk & lt)] = static_cast<uint16_t>(x & 0xFFFFu);
+                x >>= 16;
+            }
+            if (on) wws[l] = enc_push(ctx, x, e);
+        }
+    }
+    __syncwarp();
+    if (!bad) {
+        if (lane == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
+        for (int l = lane; l < n_lanes; l += 32) states_out[k * n_lanes + l] = wws[l];
+    }
+}
+
 cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, int n_lanes,
                           const TableDev *d_table, int scale_bits, uint16_t *d_scratch,
                           uint32_t *d_chunk_words, uint32_t *d_states, DStatus *d_status,
                           uint32_t *d_lane_ws, cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
-    if (n_lanes > 32) {
+    if (n_lanes > 32 && n_lanes <= kWideMaxE) {
+        encode_wide_kernel<<<static_cast<unsigned>(n_chunks), 32, size_t(n_lanes) * 4, stream>>>(
+            d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states, d_status);
+    } else if (n_lanes > 32) {
         const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
-        encode_block_kernel<<<static_cast<unsigned>(n_chunks), threads, 0, stream>>>(
+        const int ws_smem = size_t(n_lanes) * 4 <= size_t(200) * 1024;
+        const size_t smem = ws_smem ? size_t(n_lanes) * 4 : 0;
+        cudaFuncSetAttribute(encode_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+        encode_block_kernel<<<static_cast<unsigned>(n_chunks), threads, smem, stream>>>(
             d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states,
-            d_status, d_lane_ws);
+            d_status, d_lane_ws, ws_smem);
     } else {
         // one CTA per SM with the SM's share of the streams (<= 28 warps);
         // more streams than 28 per SM: grid-stride over CTA-sized groups
