@@ -94,7 +94,14 @@ decode_u8_warp_kernel(const uint8_t *__restrict__ payload, const uint64_t *__res
                     err = ILANS_ERR_TRUNCATED;
                 } else {
                     const uint64_t p = pos + __popc(b0 & lt) + 2u * __popc(b1 & lt);
-                    for (uint32_t j = 0; j < r; ++j) x = (x << 8) | pay[p + j];
+                    if (r) {  // the r digits at once: 4 bytes from two aligned
+                        // words of the (4-aligned, padded) payload, byte-reversed
+                        const uint64_t ab = static_cast<uint64_t>(pay - payload) + p;
+                        const uint32_t *w = reinterpret_cast<const uint32_t *>(payload) + (ab >> 2);
+                        const uint32_t v = __funnelshift_r(__ldg(w), __ldg(w + 1),
+                                                           static_cast<uint32_t>(ab & 3u) * 8u);
+                        x = (x << (8u * r)) | (__byte_perm(v, 0u, 0x0123u) >> (32u - 8u * r));
+                    }
                     pos += tot;
                     most = max(most, r);
                 }
