@@ -210,10 +210,9 @@ __host__ __device__ constexpr size_t decode_warp_smem() { return kRingAllocBytes
 // Not inlined: with both LUT forms inlined into one kernel the packed
 // path's schedule degrades (~8% slower decode, measured); as a call each
 // body keeps its own register allocation.
-// MODE 0: N = 32; 1: power-of-two N < 32 (512/N-group batches); 2: other
-// N < 32 (floor(256/N)-group batches). Separate bodies (and mode 2 a
-// separate kernel) so the N = 32 batch loop keeps its own schedule.
-template <int KIND, class Sink, int MODE>
+// SMALL: the instantiation for power-of-two N < 32 (512/N-group batches);
+// a separate body so the N = 32 batch loop keeps its own schedule.
+template <int KIND, class Sink, bool SMALL>
 __device__ __noinline__ void
 decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                  const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -221,7 +220,275 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
                  Sink sink, uint64_t *__restrict__ consumed,
                  uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
                  DecodeTrace trace, uint8_t *smem, int sb) {
-    constexpr bool SMALL = MODE != 0;
+    const uint32_t m = 1u << sb;
+    const int nw = blockDim.x >> 5;
+    uint8_t *lut_base = smem + nw * (kRingAllocBytes + kObufBytes);
+
+    // ---- stage the lookup tables in shared memory ------------------------
+    Lut<KIND> lut;
+    lut.mask = m - 1u;
+    lut.sb = static_cast<uint32_t>(sb);
+    if (KIND == kLutPacked32) {
+        uint32_t *p = reinterpret_cast<uint32_t *>(lut_base);
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) p[i] = tab->packed[i];
+        lut.packed = p;
+    } else if (KIND == kLutPacked64) {
+        uint4 *p = reinterpret_cast<uint4 *>(lut_base);
+        const uint4 *src = reinterpret_cast<const uint4 *>(tab->packed64);
+        for (uint32_t i = threadIdx.x; i < m / 2; i += blockDim.x) p[i] = src[i];
+        lut.packed64 = reinterpret_cast<const uint2 *>(lut_base);
+    } else {
+        uint2 *d = reinterpret_cast<uint2 *>(lut_base);
+        uint8_t *s = lut_base + kMaxSym * sizeof(uint2);
+        for (uint32_t i = threadIdx.x; i < kMaxSym; i += blockDim.x) d[i] = tab->dec[i];
+        if (m >= 4) {
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(tab->slot_sym);
+            uint32_t *dst = reinterpret_cast<uint32_t *>(s);
+            for (uint32_t i = threadIdx.x; i < m / 4; i += blockDim.x) dst[i] = src[i];
+        } else {
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) s[i] = tab->slot_sym[i];
+        }
+        lut.dec = d;
+        lut.sym = s;
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    uint16_t *ring = reinterpret_cast<uint16_t *>(smem + wib * kRingAllocBytes);
+    const uint32_t ring_addr = smem_addr(ring);
+    uint8_t *obuf = smem + nw * kRingAllocBytes + wib * kObufBytes;
+    const uint32_t lt = lanemask_lt();
+    // popc(mk & lanemask_lt) == popc(mk << (32 - lane)): a multiply (FMA
+    // pipe) instead of a LOP3 (ALU pipe); lane 0 multiplies by 0
+    const uint32_t lt_mul = lane ? 1u << (32 - lane) : 0u;
+    // 2 as an opaque register: keeps the cursor updates as IMADs (FMA pipe)
+    uint32_t two;
+    asm volatile("mov.u32 %0, 2;" : "=r"(two));
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nw;
+
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * nw + wib; k < n_chunks;
+         k += warps_total) {
+        const int64_t cbase = k * chunk_len;
+        const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+        const uint64_t woff = offsets[k];
+        const uint64_t wlen = offsets[k + 1] - woff;
+        const uint32_t delta = static_cast<uint32_t>(woff & 7u);
+        SegSrc src{payload + (woff & ~7ull), wlen + delta};
+#pragma unroll
+        for (uint32_t s = 0; s < 4; ++s) {
+            issue_segment(ring, src, s, lane);
+            cp_async_commit();
+        }
+        cp_async_wait<2>();
+        __syncwarp();
+
+        uint64_t cur = 0;            // ring segment holding the read cursor
+        uint64_t v = delta;          // read cursor in words from src.g
+        uint32_t x = lane < n_lanes ? states[k * n_lanes + lane] : 0u;
+        sink.begin(k, cbase, lane);
+        int64_t base = 0;
+
+        if ((SMALL || n_lanes == 32) && !trace.states) {
+            // ---------------- fast path: batches of 512 symbols -------------
+            // (kBatch groups of 32 lanes, or 512/N groups of N < 32 lanes for
+            // the power-of-two widths.) A batch reads <= 512 words, i.e. up
+            // to two segments past the one holding the cursor, so the ring
+            // runs one segment deeper here (wait<1>: everything but the
+            // newest segment has landed).
+            const int64_t full = len / (32 * kBatch);
+            uint32_t vb = static_cast<uint32_t>(v) << 1;  // byte cursor (mod 2^32)
+            uint32_t seg_cur = 0;                          // vb >> 9 of the cursor
+            uint32_t next_seg = 4;                         // next segment to issue
+            // segments wholly inside the payload are issued without bounds
+            // arithmetic from a running source pointer (the common case)
+            const uint64_t segs_whole = src.avail / kSegWords;
+            const uint16_t *seg_g = src.g + 4 * kSegWords + lane * 8;
+            cp_async_wait<1>();
+            __syncwarp();
+            for (int64_t b = 0; b < full; ++b) {
+                const uint32_t vb0 = vb;
+                // shared address of the cursor; the batch reads < 512 words
+                // past it, which the mirrored slots keep contiguous
+                const uint32_t a0 = ring_addr + (vb & (kRingBytes - 2));
+                uint32_t a = a0;
+                if (!SMALL) {
+#pragma unroll
+                    for (int g = 0; g < kBatch; ++g) {
+                        const uint32_t s = lut.pop(x);
+                        const bool need = x < kLow;
+                        const uint32_t mk = __ballot_sync(0xffffffffu, need);
+                        // every lane loads (one wavefront either way), then selects
+                        const uint32_t w = lds_u16(mad_lo(__popc(mk * lt_mul), two, a));
+                        x = need ? x * 65536u + w : x;
+                        a = mad_lo(__popc(mk), two, a);
+                        obuf[g * 32 + lane] = static_cast<uint8_t>(s);
+                    }
+                } else {
+                    // N < 32: lanes >= N idle (their state stays 0, never
+                    // renormalises, never stores); 512/N groups per batch
+                    const bool on = lane < n_lanes;
+                    uint8_t *op = obuf + lane;
+                    for (int gb = 0; gb < 512; gb += 16 * n_lanes) {
+#pragma unroll
+                        for (int g = 0; g < 16; ++g) {
+                            const uint32_t s = lut.pop(x);
+                            const bool need = on && x < kLow;
+                            const uint32_t mk = __ballot_sync(0xffffffffu, need);
+                            const uint32_t w = lds_u16(mad_lo(__popc(mk * lt_mul), two, a));
+                            x = need ? x * 65536u + w : x;
+                            a = mad_lo(__popc(mk), two, a);
+                            if (on) *op = static_cast<uint8_t>(s);
+                            op += n_lanes;
+                        }
+                    }
+                }
+                vb = vb0 + (a - a0);
+                __syncwarp();
+                sink.block512(obuf, b * (32 * kBatch), lane);
+                v += (vb - vb0) >> 1;
+                const uint32_t seg = (vb >> 9) & 0x7FFFFFu;
+                if (seg != seg_cur) {  // one or two segments were finished
+                    do {
+                        seg_cur = (seg_cur + 1) & 0x7FFFFFu;
+                        if (next_seg < segs_whole) {
+                            uint16_t *dst = ring + (next_seg & 3u) * kSegWords + lane * 8;
+                            cp_async16(dst, seg_g, 16u);
+                            if ((next_seg & 3u) < 2u) cp_async16(dst + kRingWords, seg_g, 16u);
+                        } else {
+                            issue_segment(ring, src, next_seg, lane);
+                        }
+                        ++next_seg;
+                        seg_g += kSegWords;
+                        cp_async_commit();
+                    } while (seg_cur != seg);
+                    cp_async_wait<1>();
+                }
+                __syncwarp();
+            }
+            cur = next_seg - 4;  // == v / kSegWords; cur + 1.. cur + 3 issued
+            base = full * (32 * kBatch);
+        }
+        // ---------------- generic per-group loop (any N <= 32, tails) ------
+        bool truncated = (v - delta) > wlen;
+        for (; !truncated && base < len; base += n_lanes) {
+            const int64_t left = len - base;
+            const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
+            const bool on = lane < active;
+            uint32_t s = 0;
+            if (on) s = lut.pop(x);
+            const bool need = on && x < kLow;
+            const uint32_t mk = __ballot_sync(0xffffffffu, need);
+            const uint32_t cnt = __popc(mk);
+            if (v - delta + cnt > wlen) {
+                truncated = true;
+                break;
+            }
+            if (need)
+                x = (x << 16) | ring_load(ring_addr, static_cast<uint32_t>(v + __popc(mk & lt)) << 1);
+            v += cnt;
+            if (trace.states) {
+                const int64_t gi = base / n_lanes;
+                if (lane < n_lanes) trace.states[gi * n_lanes + lane] = x;
+                if (lane == 0) trace.pos[gi] = v - delta;
+            }
+            if (on) obuf[(base + lane) & (kObufBytes - 1)] = static_cast<uint8_t>(s);
+            const int64_t nb = base + active;
+            if ((nb >> 8) != (base >> 8)) {  // a 256-byte half is complete
+                __syncwarp();
+                const int64_t blk = base >> 8;
+                sink.block256(obuf + (blk & 1) * kObufHalf, blk << 8, lane);
+                __syncwarp();
+            }
+            const uint64_t seg = v / kSegWords;
+            if (seg != cur) {  // segment cur-1 fully read: refill its slot
+                cur = seg;
+                __syncwarp();
+                issue_segment(ring, src, static_cast<uint32_t>(cur + 3), lane);
+                cp_async_commit();
+                cp_async_wait<2>();
+                __syncwarp();
+            }
+        }
+        if (truncated && lane == 0)
+            atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
+        {   // bytes of the last partial 256-byte block (all groups done so far)
+            const int64_t end = truncated ? base : len;
+            __syncwarp();
+            const int64_t tail0 = (end >> 8) << 8;
+            const uint8_t *half = obuf + ((end >> 8) & 1) * kObufHalf;
+            sink.tail(half, tail0, end, lane);
+            sink.end(k, end, lane);
+        }
+        if (trace.groups && lane == 0) trace.groups[k] = (base < len ? base : len + n_lanes - 1) / n_lanes;
+        if (lane == 0 && consumed) consumed[k] = v - delta;
+        if (final_states && lane < n_lanes) final_states[k * n_lanes + lane] = x;
+        cp_async_wait<0>();
+        __syncwarp();
+    }
+}
+
+template <int MAXKIND, class Sink, bool SMALL>
+__device__ __forceinline__ void
+decode_warp_dispatch(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                     const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                     int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab, Sink out,
+                     uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
+                     DStatus *__restrict__ status, DecodeTrace trace, uint8_t *smem, int sb) {
+    if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
+        decode_warp_body<kLutPacked32, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+                                                    n_chunks, n_lanes, tab, out, consumed,
+                                                    final_states, status, trace, smem, sb);
+    else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
+        decode_warp_body<kLutPacked64, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+                                                    n_chunks, n_lanes, tab, out, consumed,
+                                                    final_states, status, trace, smem, sb);
+    else
+        decode_warp_body<kLutGeneric, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+                                                   n_chunks, n_lanes, tab, out, consumed,
+                                                   final_states, status, trace, smem, sb);
+}
+
+// MAXKIND: the packed form this launch's shared memory was sized for (it
+// also fits the two-lookup form); the device table's flags pick which one
+// runs (a single-symbol sb=12 table has f = 4096, which the 12-bit field of
+// the 32-bit entry cannot hold).
+template <int MAXKIND, class Sink>
+__global__ void __launch_bounds__(1024)
+decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                   const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                   int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                   Sink out, uint64_t *__restrict__ consumed,
+                   uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
+                   int launch_sb, DecodeTrace trace) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int sb = static_cast<int>(tab->scale_bits);
+    if (sb != launch_sb || tab->status != ILANS_OK) {
+        if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
+        return;
+    }
+    if (n_lanes < 32 && (n_lanes & (n_lanes - 1)) == 0)
+        decode_warp_dispatch<MAXKIND, Sink, true>(payload, offsets, states, n, chunk_len,
+                                                  n_chunks, n_lanes, tab, out, consumed,
+                                                  final_states, status, trace, smem, sb);
+    else
+        decode_warp_dispatch<MAXKIND, Sink, false>(payload, offsets, states, n, chunk_len,
+                                                   n_chunks, n_lanes, tab, out, consumed,
+                                                   final_states, status, trace, smem, sb);
+}
+
+// N < 32 not a power of two (floor(256/N)-group batches): a separate body
+// and kernel, so the N = 32 / power-of-two kernels keep their code.
+template <int KIND, class Sink>
+__device__ __noinline__ void
+decode_warp_body_np2(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                 const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                 int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                 Sink sink, uint64_t *__restrict__ consumed,
+                 uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
+                 DecodeTrace trace, uint8_t *smem, int sb) {
+    constexpr int MODE = 2;  // N < 32, not a power of two
+    constexpr bool SMALL = true;
     const uint32_t m = 1u << sb;
     const int nw = blockDim.x >> 5;
     uint8_t *lut_base = smem + nw * (kRingAllocBytes + kObufBytes);
@@ -454,57 +721,32 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
     }
 }
 
-template <int MAXKIND, class Sink, int MODE>
-__device__ __forceinline__ void
-decode_warp_dispatch(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
-                     const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
-                     int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab, Sink out,
-                     uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
-                     DStatus *__restrict__ status, DecodeTrace trace, uint8_t *smem, int sb) {
-    if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
-        decode_warp_body<kLutPacked32, Sink, MODE>(payload, offsets, states, n, chunk_len,
-                                                    n_chunks, n_lanes, tab, out, consumed,
-                                                    final_states, status, trace, smem, sb);
-    else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
-        decode_warp_body<kLutPacked64, Sink, MODE>(payload, offsets, states, n, chunk_len,
-                                                    n_chunks, n_lanes, tab, out, consumed,
-                                                    final_states, status, trace, smem, sb);
-    else
-        decode_warp_body<kLutGeneric, Sink, MODE>(payload, offsets, states, n, chunk_len,
-                                                   n_chunks, n_lanes, tab, out, consumed,
-                                                   final_states, status, trace, smem, sb);
-}
-
-// MAXKIND: the packed form this launch's shared memory was sized for (it
-// also fits the two-lookup form); the device table's flags pick which one
-// runs (a single-symbol sb=12 table has f = 4096, which the 12-bit field of
-// the 32-bit entry cannot hold).
-template <int MAXKIND, class Sink, bool NP2>
+template <int MAXKIND, class Sink>
 __global__ void __launch_bounds__(1024)
-decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
-                   const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
-                   int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
-                   Sink out, uint64_t *__restrict__ consumed,
-                   uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
-                   int launch_sb, DecodeTrace trace) {
+decode_warp_np2_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                       const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                       int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                       Sink out, uint64_t *__restrict__ consumed,
+                       uint32_t *__restrict__ final_states, DStatus *__restrict__ status,
+                       int launch_sb, DecodeTrace trace) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int sb = static_cast<int>(tab->scale_bits);
     if (sb != launch_sb || tab->status != ILANS_OK) {
         if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
         return;
     }
-    if (NP2)
-        decode_warp_dispatch<MAXKIND, Sink, 2>(payload, offsets, states, n, chunk_len,
-                                               n_chunks, n_lanes, tab, out, consumed,
-                                               final_states, status, trace, smem, sb);
-    else if (n_lanes < 32)
-        decode_warp_dispatch<MAXKIND, Sink, 1>(payload, offsets, states, n, chunk_len,
-                                               n_chunks, n_lanes, tab, out, consumed,
-                                               final_states, status, trace, smem, sb);
+    if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
+        decode_warp_body_np2<kLutPacked32, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
+                                                 n_lanes, tab, out, consumed, final_states,
+                                                 status, trace, smem, sb);
+    else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
+        decode_warp_body_np2<kLutPacked64, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
+                                                 n_lanes, tab, out, consumed, final_states,
+                                                 status, trace, smem, sb);
     else
-        decode_warp_dispatch<MAXKIND, Sink, 0>(payload, offsets, states, n, chunk_len,
-                                               n_chunks, n_lanes, tab, out, consumed,
-                                               final_states, status, trace, smem, sb);
+        decode_warp_body_np2<kLutGeneric, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
+                                                n_lanes, tab, out, consumed, final_states,
+                                                status, trace, smem, sb);
 }
 
 // ---------------------------------------------------------------------------
@@ -756,18 +998,16 @@ static cudaError_t launch_decode_warp(const uint16_t *d_payload, const uint64_t 
                                                 d_consumed, d_final_states, d_status,
                                                 scale_bits, trace);
     };
-    // N < 32 not a power of two: its own kernel (mode 2), so the N = 32
-    // kernel's call graph -- and register allocation -- stays as it was
     const bool np2 = n_lanes < 32 && (n_lanes & (n_lanes - 1)) != 0;
     if (maxkind == kLutPacked32) {
-        if (np2) go(decode_warp_kernel<kLutPacked32, Sink, true>);
-        else go(decode_warp_kernel<kLutPacked32, Sink, false>);
+        if (np2) go(decode_warp_np2_kernel<kLutPacked32, Sink>);
+        else go(decode_warp_kernel<kLutPacked32, Sink>);
     } else if (maxkind == kLutPacked64) {
-        if (np2) go(decode_warp_kernel<kLutPacked64, Sink, true>);
-        else go(decode_warp_kernel<kLutPacked64, Sink, false>);
+        if (np2) go(decode_warp_np2_kernel<kLutPacked64, Sink>);
+        else go(decode_warp_kernel<kLutPacked64, Sink>);
     } else {
-        if (np2) go(decode_warp_kernel<kLutGeneric, Sink, true>);
-        else go(decode_warp_kernel<kLutGeneric, Sink, false>);
+        if (np2) go(decode_warp_np2_kernel<kLutGeneric, Sink>);
+        else go(decode_warp_kernel<kLutGeneric, Sink>);
     }
     ilans_note_launch();
     return cudaGetLastError();
