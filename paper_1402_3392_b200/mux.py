@@ -13,8 +13,10 @@ byte order directly (libilans_b200.so ``ilans_mux_*``, csrc/mux.cu):
 * ``mux`` (pre-encoded buffers) -- one device thread per stream replays its
   decoder over its own payload for the per-symbol counts, then the same
   scan + scatter;
-* ``demux_decode`` -- a sequential walk by construction (each step's read
-  size depends on the state of the stream it decodes), one device thread.
+* ``demux_decode`` -- sequential by construction (each step's read offset
+  depends on every earlier step's read size), but consecutive steps on
+  distinct streams decode together: one warp walks the schedule in windows
+  of up to 32 steps.
 
 Streams are ``RansStreamCodec`` (rANS over a SymbolTable, byte-multiple
 digits: BYTE8, WORD16 or a custom RenormVariant with 8/16-bit digits) or
