@@ -490,7 +490,9 @@ __global__ void __launch_bounds__(256) demux_kernel(
         const uint32_t sbal = __ballot_sync(0xffffffffu, stop);
         const int W = sbal ? __ffs(sbal) - 1 : 32;  // >= 1: lane 0 is valid and first
         const bool on = lane < W;
-        uint32_t x = raw ? 0u : state[sid];
+        // lanes past the window may name a stream a window lane updates
+        // below: they do not read its state
+        uint32_t x = (raw || !on) ? 0u : state[sid];
         uint32_t extra = 0;
         int err = 0;
         if (on && reload) {  // lane 0 only: the state inline at the window start
