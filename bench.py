@@ -189,6 +189,17 @@ class Clocks:
 
 
 # --------------------------------------------------------- CPU reference ---
+def _ref_hist_worker(args):
+    """Fork-pool worker: np.bincount of a contiguous byte range (the
+    reference's model-build call site, cli._build_table / bench._table_for,
+    split over the pool); returns (seconds, counts)."""
+    lo, hi = args
+    msg = _REF_STATE[0]
+    t0 = time.perf_counter()
+    counts = np.bincount(msg[lo:hi], minlength=256)
+    return time.perf_counter() - t0, counts
+
+
 def _ref_worker(args):
     """Fork-pool worker: round-trip a contiguous range of chunks with the
     reference ext kernels on fork-inherited data; returns (seconds, ok)."""
@@ -210,11 +221,18 @@ def _ref_worker(args):
 _REF_STATE = None
 
 
-def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: int = 8):
-    """Time the reference CPU path on a bounded sample of the same workload:
-    its model build (np.bincount + SymbolTable.from_counts, as
-    cli._build_table does) plus an encode+decode round trip of every sampled
-    chunk, on a fork pool over all host cores (per_core_mib per core)."""
+def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: int = 16):
+    """Time the reference CPU path on a bounded sample of the same workload,
+    on a fork pool over all host cores (per_core_mib per core):
+
+    1. model build -- np.bincount of each worker's byte range (the
+       reference's call site, cli._build_table, split over the pool), summed,
+       then SymbolTable.from_counts (one thread);
+    2. an encode + decode round trip of every sampled chunk with the
+       reference ext kernels (reference bench.py:86-93 per chunk).
+
+    ``value`` covers both; ``coding_only_GBps`` is step 2 alone and
+    ``single_thread_model_build_s`` is the reference's own unsplit bincount."""
     global _REF_STATE
     import multiprocessing as mp
 
@@ -237,24 +255,25 @@ def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: in
     if kind != "reference":
         n_chunks = min(total_chunks, chunks_per_core)
     sample_msg = msg[: n_chunks * C]
-    # model build, timed, at the reference's own call site semantics
-    # (cli._build_table: np.bincount(minlength=max+1) -> SymbolTable.from_counts)
+    sample = n_chunks * C
     t0 = time.perf_counter()
-    counts = np.bincount(sample_msg, minlength=int(sample_msg.max()) + 1)
+    np.bincount(sample_msg, minlength=int(sample_msg.max()) + 1)
+    t_model_1t = time.perf_counter() - t0
     if kind == "reference":
+        ctx = mp.get_context("fork")
+        _REF_STATE = (sample_msg, None, C, lanes)
+        bounds = np.linspace(0, sample, cores + 1).astype(np.int64)
+        with ctx.Pool(cores) as pool:
+            hres = pool.map(_ref_hist_worker, [(int(bounds[i]), int(bounds[i + 1]))
+                                               for i in range(cores)])
+        t0 = time.perf_counter()
+        counts = np.sum([h[1] for h in hres], axis=0)
+        counts = counts[: int(np.nonzero(counts)[0][-1]) + 1]
         table = RefTable.from_counts(counts.tolist(), sb)
-    else:
-        sys.path.insert(0, str(ROOT / "oracle"))
-        import oracle
-
-        freqs_s = oracle.quantize(counts, sb)
-        f, cum, slot = oracle.table_views(freqs_s, sb)
-    t_model = time.perf_counter() - t0
-    if kind == "reference":
+        t_model = max(h[0] for h in hres) + time.perf_counter() - t0
         _REF_STATE = (msg, table, C, lanes)
         ranges = np.array_split(np.arange(n_chunks), cores)
         jobs = [(int(r[0]), int(r[-1]) + 1) for r in ranges if len(r)]
-        ctx = mp.get_context("fork")
         t0 = time.perf_counter()
         with ctx.Pool(len(jobs)) as pool:
             res = pool.map(_ref_worker, jobs)
@@ -264,6 +283,14 @@ def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: in
         workers = len(jobs)
         per_core = statistics.median((hi - lo) * C / r[0] / 1e9 for (lo, hi), r in zip(jobs, res))
     else:  # oracle port (C restatement), single core
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle
+
+        t0 = time.perf_counter()
+        counts = np.bincount(sample_msg, minlength=int(sample_msg.max()) + 1)
+        freqs_s = oracle.quantize(counts, sb)
+        f, cum, slot = oracle.table_views(freqs_s, sb)
+        t_model = time.perf_counter() - t0
         t0 = time.perf_counter()
         ok = True
         for k in range(n_chunks):
@@ -274,18 +301,21 @@ def cpu_reference(msg: np.ndarray, sb: int, C: int, lanes: int, per_core_mib: in
         wall = busy = time.perf_counter() - t0
         workers = 1
         per_core = n_chunks * C / busy / 1e9
-    sample = n_chunks * C
     return {
         "value": sample / (t_model + busy) / 1e9,
         "unit": "GB/s",
         "cores": workers,
         "kind": kind,
         "sample": f"{n_chunks} x {C // 1024} KiB chunks ({sample / MIB:.0f} MiB) of the same "
-                  f"workload: model build (np.bincount + SymbolTable.from_counts, "
-                  f"{t_model:.3f}s, 1 thread) then encode+decode round trip per chunk with the "
-                  f"reference ext backend on a fork pool of {workers} workers (slowest "
-                  f"worker {busy:.3f}s; wall incl. fork {wall:.2f}s)",
+                  f"workload: model build (np.bincount split over {workers} workers + "
+                  f"SymbolTable.from_counts, {t_model:.3f}s) then encode+decode round trip per "
+                  f"chunk with the reference "
+                  f"{'ext backend' if kind == 'reference' else 'C port'} on {workers} "
+                  f"worker(s) (slowest worker {busy:.3f}s; wall incl. fork {wall:.2f}s)",
         "round_trip_ok": ok,
+        "coding_only_GBps": sample / busy / 1e9,
+        "model_build_s": t_model,
+        "single_thread_model_build_s": t_model_1t,
         "single_core_round_trip_GBps": per_core,
         "wall_s": wall,
     }
@@ -412,6 +442,9 @@ def run_b200(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {a.gpus}; using WORLD_SIZE",
+              file=sys.stderr)
     # one process per GPU; --dist-backend gloo (+ wrap-around device index)
     # only exists to smoke-test the multi-rank logic on a single-GPU box
     local = local % max(1, torch.cuda.device_count()) if a.dist_backend == "gloo" else local
@@ -755,14 +788,22 @@ def stress(a, dev):
 
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(max(1, a.gpus))))
     if rank != 0:
         return
-    from paper_1402_3392_b200.synth import synth_host
+    # the reference arm must not import this package (its __init__ loads
+    # libilans_b200.so): the host sampler is loaded by file path
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "ilans_b200_synth_host", ROOT / "paper_1402_3392_b200" / "synth.py")
+    synth = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(synth)
+    synth_host = synth.synth_host
 
     n = a.global_mib * MIB // world if a.global_mib else a.mib * MIB
     cores = len(os.sched_getaffinity(0))
-    per_core = 4  # MiB per core per step -> a bounded sample of the workload
+    per_core = 16  # MiB per core per step -> a bounded sample (16 cores: all 256 MiB)
     sample = min(n, cores * per_core * MIB)
     msg = synth_host(sample, a.zipf_s, a.seed)
     vals = []
@@ -785,10 +826,35 @@ def run_reference(a):
     }))
 
 
+def launch_ranks(a) -> int:
+    """``--gpus N`` (N > 1) outside torchrun: start N ranks, one per GPU,
+    with torch.distributed.run on 127.0.0.1 (the driver's own launch form)
+    and return their exit code. N larger than the visible GPUs is an error
+    (``--dist-backend gloo`` may wrap ranks onto fewer GPUs for testing)."""
+    import socket
+
+    import torch
+
+    visible = torch.cuda.device_count()
+    if a.gpus > visible and a.dist_backend == "nccl":
+        print(f"bench.py: --gpus {a.gpus} but only {visible} CUDA device(s) visible",
+              file=sys.stderr)
+        return 2
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(a))
     else:
         run_b200(a)
 

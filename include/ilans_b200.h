@@ -233,7 +233,8 @@ int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t *d_word_of
  * but the decoded bytes are consumed in registers instead of written to
  * HBM -- here by a zlib-compatible Adler-32 per chunk, d_adler[k] =
  * adler32(chunk k) (after the whole chunk, or after its decoded prefix when
- * the chunk is truncated, which is also recorded in the status). */
+ * the chunk is truncated, which is also recorded in the status).
+ * chunk_len <= 2^27 (the position sums are exact in u64 up to there). */
 int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload, const uint64_t *d_word_offsets,
                                     const uint32_t *d_states, int64_t n, int64_t chunk_len,
                                     int32_t n_lanes, const void *d_table, int32_t scale_bits,
@@ -246,7 +247,9 @@ int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload, const uint64_t *d
  * Encode: d_scratch holds 3 bytes per message byte + 8 (chunk k's digits end
  * at 3kC + 3 len_k); d_chunk_bytes[k] = its digit count. Frame: exclusive
  * scan into d_byte_offsets[K + 1] and byte compaction into d_payload (both
- * 4-byte aligned). Decode: one launch for all chunks, d_consumed[k] = bytes
+ * 4-byte aligned). Decode: d_payload must be 4-byte aligned (ILANS_ERR_VALUE
+ * otherwise) and readable for 8 bytes past its last payload byte (the
+ * refill loads two aligned words); one launch for all chunks, d_consumed[k] = bytes
  * read; errors land in the device status (zero-frequency symbol, exhausted
  * chunk, runaway refill = FormatError). */
 int ilans_encode_chunks_u8_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
@@ -262,7 +265,7 @@ int ilans_decode_chunks_u8_dev(const uint8_t *d_payload, const uint64_t *d_byte_
                                uint64_t *d_consumed, void *d_status, void *stream);
 
 /* Per-chunk Adler-32 of bytes already on the device (the unfused
- * consumer, and a device-side integrity check of raw data). */
+ * consumer, and a device-side integrity check of raw data); chunk_len <= 2^27. */
 int ilans_adler32_chunks_dev(const uint8_t *d_data, int64_t n, int64_t chunk_len,
                              uint32_t *d_adler, void *stream);
 

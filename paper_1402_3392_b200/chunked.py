@@ -833,9 +833,17 @@ class HostCodec:
             if self._last is None:
                 raise RuntimeError("decode needs a device model: encode first or pass table=")
             slot, job, h_payload = self._last, None, src
-            cur = torch.cuda.current_stream(self.device)
+            # the slot's buffers are reused in place (they hold the model):
+            # issue a pending encode's payload downloads first, then order
+            # every slot stream after all of its earlier work (the encode
+            # kernels on s_comp, the downloads on s_out, earlier decodes)
+            if slot.pending is not None:
+                slot.pending.materialize()
+            fence = [self._event(s) for s in slot.streams()]
+            fence.append(self._event(torch.cuda.current_stream(self.device)))
             for s in slot.streams():
-                s.wait_stream(cur)
+                for e in fence:
+                    s.wait_event(e)
         c = slot.codec
         C, N = c.chunk_len, c.lane_count
         k = n_chunks_for(n, C)

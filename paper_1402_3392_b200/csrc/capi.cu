@@ -844,12 +844,18 @@ extern "C" int ilans_decode_chunks_u8_dev(const uint8_t *d_payload, const uint64
                                           int32_t n_lanes, const void *d_table, uint8_t *d_out,
                                           uint64_t *d_consumed, void *d_status, void *stream) {
     if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    // the refill reads two aligned u32 words of the payload (byte8.cu)
+    if (reinterpret_cast<uintptr_t>(d_payload) & 3) return ILANS_ERR_VALUE;
     return launch_decode_chunks_u8(d_payload, d_byte_offsets, d_states, n, chunk_len, n_lanes,
                                    static_cast<const TableDev *>(d_table), d_out, d_consumed,
                                    static_cast<DStatus *>(d_status), ST(stream)) == cudaSuccess
                ? ILANS_OK
                : ILANS_ERR_CUDA;
 }
+
+// the Adler-32 sinks keep sum(i * b_i) of a chunk in u64 (~255 C^2 / 2):
+// exact for chunks up to 2^27 bytes
+constexpr int64_t kAdlerMaxChunk = int64_t(1) << 27;
 
 extern "C" int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload,
                                                const uint64_t *d_word_offsets,
@@ -861,6 +867,7 @@ extern "C" int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload,
     if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
     if (scale_bits < 1 || scale_bits > kMaxScaleBits) return ILANS_ERR_VALUE;
     if (reinterpret_cast<uintptr_t>(d_payload) & 15) return ILANS_ERR_VALUE;
+    if (chunk_len > kAdlerMaxChunk) return ILANS_ERR_VALUE;
     return launch_decode_adler32(d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes,
                                  static_cast<const TableDev *>(d_table), scale_bits, d_adler,
                                  d_consumed, static_cast<DStatus *>(d_status), ST(stream)) ==
@@ -871,7 +878,8 @@ extern "C" int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload,
 
 extern "C" int ilans_adler32_chunks_dev(const uint8_t *d_data, int64_t n, int64_t chunk_len,
                                         uint32_t *d_adler, void *stream) {
-    if (chunk_len <= 0 || (chunk_len & 15) || (reinterpret_cast<uintptr_t>(d_data) & 15))
+    if (chunk_len <= 0 || (chunk_len & 15) || (reinterpret_cast<uintptr_t>(d_data) & 15) ||
+        chunk_len > kAdlerMaxChunk)
         return ILANS_ERR_VALUE;
     return launch_adler32_chunks(d_data, n, chunk_len, d_adler, ST(stream)) == cudaSuccess
                ? ILANS_OK

@@ -156,7 +156,7 @@ struct StoreSink {
 // warp reduces once per chunk.
 struct Adler32Sink {
     uint32_t *adler;
-    unsigned long long s1, si;  // per-lane partial sums (exact: < 2^40 per chunk)
+    unsigned long long s1, si;  // per-lane partial sums (exact for chunks <= 2^27 B: < 2^62)
     __device__ __forceinline__ void begin(int64_t, int64_t, int) { s1 = si = 0; }
     __device__ __forceinline__ void words(const uint32_t *w, int nw, int64_t pos0) {
         uint32_t t1 = 0, tj = 0;

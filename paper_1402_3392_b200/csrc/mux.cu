@@ -956,8 +956,10 @@ extern "C" int ilans_mux_demux(const ilans_mux_stream *streams, int32_t n_stream
     const int64_t T = n_steps;
     if (K < 0 || K > 0xFFFF) return st_fail(st, ILANS_ERR_VALUE, "stream count must be <= 65535");
     if (T < 0 || T > kMuxMaxSteps) return st_fail(st, ILANS_ERR_VALUE, "too many schedule steps");
-    if (payload_len < 0 || payload_len > int64_t(0xFFFFFFF0u) || flush_interval < 0)
-        return st_fail(st, ILANS_ERR_VALUE, "bad arguments (payload must be < 4 GiB)");
+    // u32 ring cursors run up to 2 halves + 264 bytes past the payload end
+    if (payload_len < 0 || payload_len > int64_t(0xFFFFFFFFu) - 4 * int64_t(kPayHalf) ||
+        flush_interval < 0)
+        return st_fail(st, ILANS_ERR_VALUE, "bad arguments (payload must be < 4 GiB - 16 KiB)");
     if (int rc = check_streams(streams, K, n_freq, n_cum, n_slot, true, st)) return rc;
     std::vector<int64_t> off;
     if (int rc = schedule_offsets(schedule, T, K, off, st)) return rc;

@@ -182,6 +182,34 @@ def test_host_codec_decodes_a_container_with_its_own_table():
     assert np.array_equal(h_out.numpy(), a)
 
 
+def test_host_codec_raw_decode_after_async_encode_keeps_both():
+    """encode_async(A) then decode_async(raw payload of B, no table=): B is
+    decoded with A's model in A's slot without corrupting A's pending
+    payload downloads (the raw branch fences every slot stream)."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import HostCodec, encode_chunked
+    from paper_1402_3392_b200.synth import synth_host
+
+    n, C = 2_500_009, 65536
+    a = synth_host(n, 1.2, seed=11)
+    b = synth_host(n, 1.25, seed=12)
+    hc = HostCodec(n, C, 32, 12, batch_bytes=1 << 19, slots=2)
+    ej = hc.encode_async(torch.from_numpy(a).pin_memory(), n)
+    ta = encode_chunked(a, None, 32, C, 12)
+    cb = encode_chunked(b, ta.table, 32, C, 12)  # B under A's model
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
+    h_out = torch.zeros(n, dtype=torch.uint8, pin_memory=True)
+    dj = hc.decode_async(pin(cb.payload.view(np.int16)), h_out, n,
+                         pin(cb.word_offsets.astype(np.int64)),
+                         pin(cb.states.reshape(-1).view(np.int32)))
+    assert np.array_equal(dj.wait().numpy(), b)
+    pay, offs, states = ej.wait()
+    assert np.array_equal(pay.numpy().view(np.uint16), ta.payload)
+    assert np.array_equal(offs.numpy().view(np.uint64), ta.word_offsets)
+    assert np.array_equal(states.numpy().view(np.uint32).reshape(-1, 32), ta.states)
+
+
 def test_stats_counters_single_digit_property():
     rng = np.random.default_rng(3)
     stats = RenormStats()
