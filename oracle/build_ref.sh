@@ -22,6 +22,10 @@ python -m pip install --quiet --no-index --no-build-isolation --no-deps \
 rm -rf "$out"
 mkdir -p "$out"
 cp -r "$tmp/site/ilans" "$out/ilans"
+# the reference's own test suite travels with it (git-ignored like the rest
+# of _ref): integration/install_into_reference.py runs it against the B200
+# backend on the GPU box, where /root/reference does not exist
+cp -r "$src/tests" "$out/tests"
 python - "$out" <<'PY'
 import sys
 sys.path.insert(0, sys.argv[1])
