@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-plugin", action="store_true")
+    ap.add_argument("--plugin-only", action="store_true",
+                    help="only the plugin_e2e leg (threads 1,2,4,8,16)")
     ap.add_argument("--sweep", action="store_true", help="config 4: entropy x precision sweep")
     ap.add_argument("--stress", action="store_true",
                     help="config 5: small chunks x many streams (framing / tail overhead)")
@@ -349,6 +352,72 @@ def fused_consumer(codec, d_out, n, dev, reps=5):
             "fused_GBps": n / (f_ms * 1e-3) / 1e9, "fused_ms": f_ms,
             "unfused_GBps": n / (u_ms * 1e-3) / 1e9, "unfused_ms": u_ms,
             "hbm_bytes_avoided": 2 * n}
+
+
+_PLUGIN = None
+
+
+def _plugin_range(job):
+    """The reference's per-chunk loop (reference bench.py:86-93 shape, the
+    _ref_worker below) over chunks [lo, hi), through the reference kernel
+    boundary Backend("b200") with host buffers; returns (seconds, ok)."""
+    from paper_1402_3392_b200.interleave import decode_interleaved, encode_interleaved
+    from paper_1402_3392_b200.rans import WORD16
+
+    lo, hi = job
+    msg, table, C, lanes = _PLUGIN
+    ok = True
+    t0 = time.perf_counter()
+    for k in range(lo, hi):
+        chunk = msg[k * C:(k + 1) * C]
+        c = encode_interleaved(chunk, table, lanes, WORD16, backend="b200")
+        out = decode_interleaved(c, backend="b200")
+        ok &= bool(np.array_equal(out, chunk))
+    return time.perf_counter() - t0, ok
+
+
+def plugin_e2e(msg_h, table, C, N, threads_list=(1, 8, 16), sample_mib=256):
+    """SURVEY 8b drop-in path: the reference's per-chunk loop
+    (encode_interleaved + decode_interleaved per 64 KiB chunk, one Container
+    each) through Backend("b200") -- one warp per call, host buffers in and
+    out, every call synchronous -- on T host threads (ctypes releases the
+    GIL during each call; the library keeps one stream, staging buffer and
+    cached model per thread, so T calls are in flight at once). Each thread
+    warms its own context up first; the clock runs from a barrier to the
+    last thread's end."""
+    global _PLUGIN
+    import threading
+
+    k = min(len(msg_h) // C, (sample_mib * MIB) // C)
+    _PLUGIN = (msg_h, table, C, N)
+    rows = {}
+    for T in threads_list:
+        ranges = [r for r in np.array_split(np.arange(k), T) if len(r)]
+        bar = threading.Barrier(len(ranges) + 1)
+        res = [None] * len(ranges)
+
+        def worker(i, r):
+            _plugin_range((int(r[0]), int(r[0]) + min(2, len(r))))  # context + model warm-up
+            bar.wait()
+            res[i] = _plugin_range((int(r[0]), int(r[-1]) + 1))
+            bar.wait()
+
+        ths = [threading.Thread(target=worker, args=(i, r)) for i, r in enumerate(ranges)]
+        for t in ths:
+            t.start()
+        bar.wait()
+        t0 = time.perf_counter()
+        bar.wait()
+        wall = time.perf_counter() - t0
+        for t in ths:
+            t.join()
+        if not all(r[1] for r in res):
+            raise SystemExit("plugin round-trip mismatch")
+        rows[f"threads_{T}"] = {"GBps": k * C / wall / 1e9, "s": wall,
+                                "us_per_chunk_round_trip": 1e6 * wall * len(ranges) / k}
+    return {"what": f"reference per-chunk loop through Backend('b200'): {k} x {C // 1024} KiB "
+                    f"chunks, encode_interleaved + decode_interleaved (one Container per chunk, "
+                    f"N={N}), host numpy buffers, wall clock", **rows}
 
 
 def e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes):
@@ -681,6 +750,8 @@ def run_b200(a):
 
     if not a.no_e2e:
         out["e2e"] = e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes)
+    if rank == 0 and world == 1 and not a.no_plugin:
+        out["plugin_e2e"] = plugin_e2e(d_msg[:n].cpu().numpy(), table, C, N)
 
     if rank == 0 and world == 1 and not a.no_cpu:
         msg_h = d_msg[:n].cpu().numpy()
@@ -849,9 +920,23 @@ def launch_ranks(a) -> int:
     return subprocess.call(cmd)
 
 
+def run_plugin_only(a):
+    from paper_1402_3392_b200.rans import SymbolTable
+    from paper_1402_3392_b200.synth import synth_host
+
+    msg = synth_host(256 * MIB, a.zipf_s, a.seed)
+    counts = np.bincount(msg, minlength=256)
+    table = SymbolTable.from_counts(counts[: int(np.nonzero(counts)[0][-1]) + 1].tolist(),
+                                    a.scale_bits)
+    print(json.dumps(plugin_e2e(msg, table, a.chunk, a.lanes,
+                                threads_list=(1, 2, 4, 8, 16, 32))))
+
+
 def main():
     a = parse()
-    if a.impl == "reference":
+    if a.plugin_only:
+        run_plugin_only(a)
+    elif a.impl == "reference":
         run_reference(a)
     elif a.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(launch_ranks(a))

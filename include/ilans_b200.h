@@ -50,7 +50,7 @@ typedef struct ilans_status {
     int64_t stream;     /* chunk/stream index of the first failing stream, or -1 */
     int64_t index;      /* message index of the offending symbol, or -1          */
     int32_t symbol;     /* offending symbol value (unencodable), or -1           */
-    int32_t max_digits; /* byte8 calls: most digits spilled / refilled by a symbol */
+    int32_t max_digits; /* most digits spilled / refilled by one symbol (byte8, *_stats) */
     int64_t consumed;   /* words consumed (single-stream decode)                 */
     char message[128];  /* human-readable detail                                 */
 } ilans_status;
@@ -104,6 +104,28 @@ int ilans_decode_lanes_u16(const uint16_t *payload, int64_t pay_len, const uint3
                            const uint32_t *cum, int32_t n_freq, int32_t scale_bits,
                            int64_t msg_len, int32_t n_lanes, uint8_t *out,
                            int64_t *consumed, ilans_status *st);
+
+/* Instrumented forms for interleave.encode_interleaved / decode_interleaved
+ * with stats= (the reference's RenormStats path, rans.py:235-314): same
+ * arguments and results as the two calls above, and the kernel MEASURES the
+ * most digits any one symbol moved under the reference's spill / refill
+ * loops (rans.py:284-287, :305-309) into st->max_digits (word16: 1 whenever
+ * any digit moved; 2 would mean a symbol needed a second digit). These run
+ * the generic per-group loop, not the batched fast path.
+ * Host-buffer calls are per host thread: each thread gets its own stream,
+ * device buffers, pinned staging and cached device model (rebuilt only when
+ * freq / cum / slot / scale_bits change), and one synchronisation per call. */
+int ilans_encode_interleaved_u16_stats(const uint8_t *msg, int64_t n, const uint32_t *freq,
+                                       int32_t n_freq, const uint32_t *cum, int32_t scale_bits,
+                                       int32_t n_lanes, uint16_t *payload_out,
+                                       int64_t *payload_words, uint32_t *states_out,
+                                       ilans_status *st);
+int ilans_decode_interleaved_u16_stats(const uint16_t *payload, int64_t pay_len,
+                                       const uint32_t *states, const uint8_t *slot_sym,
+                                       int64_t n_slots, const uint32_t *freq, const uint32_t *cum,
+                                       int32_t n_freq, int32_t scale_bits, int64_t msg_len,
+                                       int32_t n_lanes, uint8_t *out, int64_t *consumed,
+                                       ilans_status *st);
 
 /* Instrumented decode: the device form of interleave.decode_interleaved_steps
  * (interleave.py:251-268) and lanes.decode_lanes_steps (lanes.py:221-232).

@@ -55,7 +55,27 @@ def encode_interleaved_u16(msg, freq, cum, scale_bits: int, n_lanes: int):
     return payload[: words.value].copy(), states
 
 
-def _decode(fn, payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):
+def encode_interleaved_u16_stats(msg, freq, cum, scale_bits: int, n_lanes: int):
+    """encode_interleaved_u16 + the kernel-measured most digits one symbol
+    spilled (RenormStats, rans.py:235-263): (payload, states, max_digits)."""
+    m = np.ascontiguousarray(msg, dtype=np.uint8)
+    f = _u32(freq)
+    c = _u32(cum)
+    if len(c) < len(f) + 1:
+        raise ValueError("cum must have len(freq) + 1 entries")
+    payload = np.empty(max(1, len(m)), dtype=np.uint16)
+    states = np.empty(n_lanes, dtype=np.uint32) if n_lanes > 0 else np.empty(0, np.uint32)
+    words = ctypes.c_int64(0)
+    st = _lib.Status()
+    rc = _lib.lib.ilans_encode_interleaved_u16_stats(
+        _lib.ptr(m), len(m), _lib.ptr(f), len(f), _lib.ptr(c), int(scale_bits), int(n_lanes),
+        _lib.ptr(payload), ctypes.byref(words), _lib.ptr(states), ctypes.byref(st))
+    _lib.raise_for(rc, st, "encode_interleaved_u16")
+    return payload[: words.value].copy(), states, int(st.max_digits)
+
+
+def _decode(fn, payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes,
+            with_stats=False):
     pay = np.ascontiguousarray(payload, dtype=np.uint16)
     xs = np.array(states, dtype=np.uint32)  # copied: inputs are never mutated
     slot = np.ascontiguousarray(slot_sym, dtype=np.uint8)
@@ -72,6 +92,8 @@ def _decode(fn, payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lan
             _lib.ptr(c), len(f), int(scale_bits), int(msg_len), int(n_lanes), _lib.ptr(out),
             ctypes.byref(consumed), ctypes.byref(st))
     _lib.raise_for(rc, st, "decode")
+    if with_stats:
+        return out[:msg_len], int(consumed.value), int(st.max_digits)
     return out[:msg_len], int(consumed.value)
 
 
@@ -84,6 +106,14 @@ def decode_interleaved_u16(payload, states, slot_sym, freq, cum, scale_bits, msg
     words read) -- contract of _pure.decode_interleaved_u16 (_pure.py:42-66)."""
     return _decode(_dec_serial, payload, states, slot_sym, freq, cum, scale_bits, msg_len,
                    n_lanes)
+
+
+def decode_interleaved_u16_stats(payload, states, slot_sym, freq, cum, scale_bits, msg_len,
+                                 n_lanes):
+    """decode_interleaved_u16 + the kernel-measured most digits one symbol
+    refilled: (message, words read, max_digits)."""
+    return _decode(_lib.lib.ilans_decode_interleaved_u16_stats, payload, states, slot_sym, freq,
+                   cum, scale_bits, msg_len, n_lanes, with_stats=True)
 
 
 def decode_lanes_u16(payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lanes):

@@ -476,7 +476,7 @@ cudaError_t launch_decode_chunks_u8(const uint8_t *d_payload, const uint64_t *d_
     if (blocks > cap) blocks = cap;
     decode_u8_warp_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
         d_payload, d_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table, d_out,
-        d_consumed, d_status, DecodeTrace{nullptr, nullptr, nullptr});
+        d_consumed, d_status, DecodeTrace{nullptr, nullptr, nullptr, 0});
     ilans_note_launch();
     return cudaGetLastError();
 }

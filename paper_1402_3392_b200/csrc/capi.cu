@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <sched.h>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -19,12 +21,31 @@ void ilans_note_launch(int n) { g_launches.fetch_add(static_cast<unsigned long l
 
 namespace ilans {
 
+__global__ void flag_kernel(uint32_t *flag, uint32_t v) {
+    __threadfence_system();
+    *reinterpret_cast<volatile uint32_t *>(flag) = v;
+}
+
 __global__ void dstatus_reset_kernel(DStatus *s) {
     s->trunc_stream = ~0ull;
     s->unenc_index = -1;
     s->unenc_symbol = 0;
     s->value_error = 0;
     s->max_digits = 0;
+}
+
+cudaError_t smem_limit(const void *kernel, int bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void *, int> set_to[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    int &cur = set_to[dev & 63][kernel];
+    if (cur >= bytes) return cudaSuccess;
+    const cudaError_t e =
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
 }
 
 int sm_count() {
@@ -100,15 +121,70 @@ struct DevBuf {
     T *as() const { return static_cast<T *>(p); }
 };
 
+// pinned host staging for the single-stream drop-ins: inputs are packed
+// into it and every result (status, counts, states, payload / decoded bytes)
+// comes back into it with ONE stream synchronisation per call
+struct HostBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = bytes + bytes / 4;
+        if (want < (size_t(1) << 20)) want = size_t(1) << 20;
+        cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocDefault);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    uint8_t *at(size_t off) const { return static_cast<uint8_t *>(p) + off; }
+};
+constexpr size_t kStageMax = size_t(256) << 20;  // larger calls copy pageable memory directly
+
+// One context per (host thread, device): its own stream, device buffers,
+// pinned staging and cached device model, so calls from different host
+// threads (ctypes releases the GIL) run concurrently on the GPU.
 struct Ctx {
     std::mutex mu;
     bool init = false;
+    int dev = 0;
     cudaStream_t stream = nullptr;
+    // completion flag in mapped pinned memory, written by a one-thread
+    // kernel after the call's last copy; the host polls it with no driver
+    // call (many threads waiting at once do not contend in the driver)
+    uint32_t *hflag = nullptr, *dflag = nullptr;
+    uint32_t seq = 0;
     DevBuf msg, scratch, payload, out, states, ws, slot, freq, cum, table, status, counts,
-        offsets, consumed, words, trace;
+        offsets, consumed, words, trace, io;
+    HostBuf stage, tstage;
+    // the model currently built in `table` (drop-in calls pass the same
+    // freq / cum / slot arrays call after call: rebuilt only on change)
+    bool tab_valid = false, tab_has_slot = false, tab_packed = false;
+    int tab_sb = 0, tab_nfreq = 0;
+    uint32_t tab_f[kMaxSym] = {0}, tab_c[kMaxSym + 1] = {0};
+    std::vector<uint8_t> tab_slot;
+    ~Ctx() {
+        if (!init || cudaSetDevice(dev) != cudaSuccess) return;
+        for (DevBuf *b : {&msg, &scratch, &payload, &out, &states, &ws, &slot, &freq, &cum, &table,
+                          &status, &counts, &offsets, &consumed, &words, &trace, &io})
+            if (b->p) cudaFree(b->p);
+        for (HostBuf *b : {&stage, &tstage})
+            if (b->p) cudaFreeHost(b->p);
+        if (hflag) cudaFreeHost(hflag);
+        cudaStreamDestroy(stream);
+    }
 };
 
-Ctx g_ctx[64];
+thread_local Ctx *t_ctx[64] = {nullptr};
+thread_local struct CtxOwner {
+    ~CtxOwner() {
+        for (Ctx *&c : t_ctx) {
+            delete c;
+            c = nullptr;
+        }
+    }
+} t_ctx_owner;
 thread_local int t_device = -1;
 
 int current_device(ilans_status *st, Ctx **out) {
@@ -125,14 +201,21 @@ int current_device(ilans_status *st, Ctx **out) {
     if (dev >= n || dev >= 64) return st_fail(st, ILANS_ERR_VALUE, "bad device %d", dev);
     e = cudaSetDevice(dev);
     if (e != cudaSuccess) return st_cuda(st, e, "cudaSetDevice");
-    Ctx &c = g_ctx[dev];
-    *out = &c;
+    (void)t_ctx_owner;  // constructs the owner (frees this thread's contexts at exit)
+    if (!t_ctx[dev]) {
+        t_ctx[dev] = new Ctx();
+        t_ctx[dev]->dev = dev;
+    }
+    *out = t_ctx[dev];
     return ILANS_OK;
 }
 
 int ctx_init(Ctx &c, ilans_status *st) {
     if (c.init) return ILANS_OK;
     CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    CK(cudaHostAlloc(reinterpret_cast<void **>(&c.hflag), 64, cudaHostAllocMapped));
+    *c.hflag = 0;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&c.dflag), c.hflag, 0));
     CK(c.table.ensure(sizeof(TableDev)));
     CK(c.status.ensure(sizeof(DStatus)));
     c.init = true;
@@ -189,6 +272,69 @@ extern "C" size_t ilans_dstatus_bytes(void) { return sizeof(DStatus); }
 // 1. host-buffer drop-ins
 // ---------------------------------------------------------------------------
 
+// sb <= 12 packed LUT is valid only for self-consistent tables (every slot's
+// symbol s has 1 <= f[s] <= 4095 and 0 <= slot - cum[s] < 4096).
+static bool host_packable(const uint8_t *slot_sym, const uint32_t *f, const uint32_t *cum,
+                          int scale_bits) {
+    if (scale_bits > kPackedMaxBits) return false;
+    const uint32_t m = 1u << scale_bits;
+    for (uint32_t j = 0; j < m; ++j) {
+        const uint32_t s = slot_sym[j];
+        if (f[s] < 1 || f[s] > 4095 || j - cum[s] >= 4096u) return false;
+    }
+    return true;
+}
+
+static size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
+
+// Make c.table the model of (freq, cum[, slot]) at scale_bits: a no-op when
+// it already is (the drop-in callers pass the same table arrays call after
+// call), else the arrays go up through pinned staging and build_table runs.
+// slot == nullptr (encode): the slot LUT is derived from cum on the device.
+static int ensure_table(Ctx &c, const uint32_t *freq, int n_freq, const uint32_t *cum,
+                        const uint8_t *slot, int scale_bits, cudaStream_t s, ilans_status *st) {
+    const size_t m = size_t(1) << scale_bits;
+    if (c.tab_valid && c.tab_sb == scale_bits && c.tab_nfreq == n_freq &&
+        std::memcmp(c.tab_f, freq, size_t(n_freq) * 4) == 0 &&
+        std::memcmp(c.tab_c, cum, size_t(n_freq + 1) * 4) == 0 &&
+        (!slot || (c.tab_has_slot && std::memcmp(c.tab_slot.data(), slot, m) == 0)))
+        return ILANS_OK;
+    c.tab_valid = false;
+    CK(c.freq.ensure(kMaxSym * 4));
+    CK(c.cum.ensure((kMaxSym + 1) * 4));
+    if (slot) CK(c.slot.ensure(m));
+    // the previous call's uploads from tstage completed before it returned
+    CK(c.tstage.ensure(kMaxSym * 4 + (kMaxSym + 1) * 4 + m + 16));
+    uint32_t *hf = reinterpret_cast<uint32_t *>(c.tstage.at(0));
+    uint32_t *hc = reinterpret_cast<uint32_t *>(c.tstage.at(kMaxSym * 4));
+    std::memset(hf, 0, kMaxSym * 4 + (kMaxSym + 1) * 4);
+    std::memcpy(hf, freq, size_t(n_freq) * 4);
+    std::memcpy(hc, cum, size_t(n_freq + 1) * 4);
+    CK(cudaMemcpyAsync(c.freq.p, hf, kMaxSym * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.cum.p, hc, (kMaxSym + 1) * 4, cudaMemcpyHostToDevice, s));
+    if (slot) {
+        uint8_t *hs = c.tstage.at(kMaxSym * 4 + (kMaxSym + 1) * 4);
+        std::memcpy(hs, slot, m);
+        CK(cudaMemcpyAsync(c.slot.p, hs, m, cudaMemcpyHostToDevice, s));
+    }
+    CK(launch_build_table(nullptr, c.freq.as<uint32_t>(), n_freq, c.cum.as<uint32_t>(),
+                          slot ? c.slot.as<uint8_t>() : nullptr, scale_bits,
+                          c.table.as<TableDev>(), s));
+    c.tab_sb = scale_bits;
+    c.tab_nfreq = n_freq;
+    std::memcpy(c.tab_f, freq, size_t(n_freq) * 4);
+    std::memcpy(c.tab_c, cum, size_t(n_freq + 1) * 4);
+    c.tab_has_slot = slot != nullptr;
+    if (slot) {
+        c.tab_slot.assign(slot, slot + m);
+        c.tab_packed = host_packable(slot, hf, hc, scale_bits);
+    }
+    c.tab_valid = true;
+    return ILANS_OK;
+}
+
+static void table_clobbered(Ctx &c) { c.tab_valid = false; }
+
 // The encoder's 8-byte symbol record holds f - 1 and cum in 16 bits each
 // (common.cuh EncSym): true for every SymbolTable (f <= m, cum < m <= 2^16);
 // hand-made tables outside that range are rejected instead of mis-coded.
@@ -199,12 +345,47 @@ static bool encode_table_fits(const uint32_t *freq, const uint32_t *cum, int n_f
         if (freq[s] && (freq[s] > m || cum[s] > 0xFFFFu)) return false;
     return true;
 }
-extern "C" int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const uint32_t *freq,
-                                            int32_t n_freq, const uint32_t *cum,
-                                            int32_t scale_bits, int32_t n_lanes,
-                                            uint16_t *payload_out, int64_t *payload_words,
-                                            uint32_t *states_out, ilans_status *st) {
-    st_clear(st);
+
+// Wait for everything queued on the context's stream: a one-thread kernel
+// stores the call's sequence number into mapped pinned memory after the
+// last copy, and the host polls that word, yielding its core between polls
+// (no driver lock, no spinning thread starving the Python threads). The
+// stream is queried now and then so a failed launch cannot hang the wait.
+static cudaError_t ctx_wait(Ctx &c) {
+    const uint32_t want = ++c.seq;
+    flag_kernel<<<1, 1, 0, c.stream>>>(c.dflag, want);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ilans_note_launch();
+    for (uint32_t i = 1;; ++i) {
+        if (__atomic_load_n(c.hflag, __ATOMIC_ACQUIRE) == want) return cudaSuccess;
+        if ((i & 1023u) == 0) {
+            e = cudaStreamQuery(c.stream);
+            if (e != cudaSuccess && e != cudaErrorNotReady) return e;
+            if (e == cudaSuccess && __atomic_load_n(c.hflag, __ATOMIC_ACQUIRE) != want)
+                return cudaStreamSynchronize(c.stream);  // (flag store not yet visible)
+        }
+        sched_yield();
+    }
+}
+
+static void dstatus_init(DStatus *h) {  // dstatus_reset_kernel's image
+    std::memset(h, 0, sizeof(DStatus));
+    h->trunc_stream = ~0ull;
+    h->unenc_index = -1;
+}
+
+// stats: measure the most digits any symbol spilled (RenormStats.note_encode,
+// rans.py:246-250) in the kernel -> st->max_digits
+//
+// Small calls (the per-chunk plugin loop) are one upload, one launch, one
+// download and one synchronisation: message and status image travel in one
+// copy, and status | words | states | scratch come back in one. The device
+// buffer `io` mirrors the pinned staging layout byte for byte.
+static int encode_u16_common(const uint8_t *msg, int64_t n, const uint32_t *freq, int32_t n_freq,
+                             const uint32_t *cum, int32_t scale_bits, int32_t n_lanes,
+                             uint16_t *payload_out, int64_t *payload_words, uint32_t *states_out,
+                             bool stats, ilans_status *st) {
     if (n < 0) return st_fail(st, ILANS_ERR_VALUE, "negative message length");
     if (n_lanes < 1 || n_lanes > 0xFFFF)
         return st_fail(st, ILANS_ERR_VALUE, "lane_count must be in [1, 65535]");
@@ -222,59 +403,99 @@ extern "C" int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const
     if (n == 0) {  // states stay at L, empty payload (_core.pyx:28-29)
         for (int l = 0; l < n_lanes; ++l) states_out[l] = kLow;
         *payload_words = 0;
+        st->max_digits = 0;
         return ILANS_OK;
     }
     cudaStream_t s = c.stream;
-    CK(c.msg.ensure(size_t(n)));
-    CK(c.scratch.ensure(size_t(n) * 2 + 16));  // + 8 words of block-store slack
-    CK(c.states.ensure(size_t(n_lanes) * 4));
     CK(c.ws.ensure(size_t(n_lanes) * 4));
-    CK(c.freq.ensure(kMaxSym * 4));
-    CK(c.cum.ensure((kMaxSym + 1) * 4));
-    CK(c.words.ensure(8));
-    uint32_t hf[kMaxSym] = {0}, hc[kMaxSym + 1] = {0};
-    std::memcpy(hf, freq, size_t(n_freq) * 4);
-    std::memcpy(hc, cum, size_t(n_freq + 1) * 4);
-    CK(cudaMemcpyAsync(c.msg.p, msg, size_t(n), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c.freq.p, hf, sizeof(hf), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c.cum.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
-    CK(launch_build_table(nullptr, c.freq.as<uint32_t>(), n_freq, c.cum.as<uint32_t>(), nullptr,
-                          scale_bits, c.table.as<TableDev>(), s));
-    dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
-    ilans_note_launch();
-    CK(launch_encode(c.msg.as<uint8_t>(), n, n, n_lanes, c.table.as<TableDev>(), scale_bits,
-                     c.scratch.as<uint16_t>(), c.words.as<uint32_t>(), c.states.as<uint32_t>(),
-                     c.status.as<DStatus>(), c.ws.as<uint32_t>(), s));
+    // layout: msg | status | words | states | scratch (n words + slack)
+    const size_t o_st = al16(size_t(n)), o_words = o_st + al16(sizeof(DStatus)),
+                 o_states = o_words + 16, o_pay = al16(o_states + size_t(n_lanes) * 4),
+                 total = o_pay + size_t(n) * 2 + 32;
+    const bool staged = total <= kStageMax;
+    uint8_t *dmsg, *dscr, *dwords, *dstates;
+    DStatus *dst;
+    if (staged) {
+        CK(c.stage.ensure(total));
+        CK(c.io.ensure(total));
+        std::memcpy(c.stage.at(0), msg, size_t(n));
+        dstatus_init(reinterpret_cast<DStatus *>(c.stage.at(o_st)));
+        CK(cudaMemcpyAsync(c.io.p, c.stage.at(0), o_words, cudaMemcpyHostToDevice, s));
+        uint8_t *io = c.io.as<uint8_t>();
+        dmsg = io;
+        dst = reinterpret_cast<DStatus *>(io + o_st);
+        dwords = io + o_words;
+        dstates = io + o_states;
+        dscr = io + o_pay;
+    } else {
+        CK(c.msg.ensure(size_t(n)));
+        CK(c.scratch.ensure(size_t(n) * 2 + 32));
+        CK(c.states.ensure(size_t(n_lanes) * 4));
+        CK(c.words.ensure(8));
+        CK(cudaMemcpyAsync(c.msg.p, msg, size_t(n), cudaMemcpyHostToDevice, s));
+        dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
+        ilans_note_launch();
+        dmsg = c.msg.as<uint8_t>();
+        dst = c.status.as<DStatus>();
+        dwords = c.words.as<uint8_t>();
+        dstates = c.states.as<uint8_t>();
+        dscr = c.scratch.as<uint8_t>();
+    }
+    if (int rc = ensure_table(c, freq, n_freq, cum, nullptr, scale_bits, s, st)) return rc;
+    CK(launch_encode(dmsg, n, n, n_lanes, c.table.as<TableDev>(), scale_bits,
+                     reinterpret_cast<uint16_t *>(dscr), reinterpret_cast<uint32_t *>(dwords),
+                     reinterpret_cast<uint32_t *>(dstates), dst, c.ws.as<uint32_t>(), s, stats));
     DStatus hs;
-    if (int rc = read_dstatus(c.status.as<DStatus>(), s, &hs, st)) return rc;
+    uint32_t w = 0;
+    if (staged) {  // status | words | states | scratch in one download
+        CK(cudaMemcpyAsync(c.stage.at(o_st), dst, total - 32 - o_st, cudaMemcpyDeviceToHost, s));
+        CK(ctx_wait(c));
+        std::memcpy(&hs, c.stage.at(o_st), sizeof(DStatus));
+        std::memcpy(&w, c.stage.at(o_words), 4);
+    } else {
+        if (int rc = read_dstatus(dst, s, &hs, st)) return rc;
+        CK(cudaMemcpyAsync(&w, dwords, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
     if (hs.unenc_index >= 0) {
         st->index = hs.unenc_index;
         st->symbol = msg[hs.unenc_index];
         return st_fail(st, ILANS_ERR_UNENCODABLE, "symbol %d has frequency 0", st->symbol);
     }
-    uint32_t w = 0;
-    CK(cudaMemcpyAsync(&w, c.words.p, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (w)
-        CK(cudaMemcpyAsync(payload_out, c.scratch.as<uint16_t>() + (n - w), size_t(w) * 2,
-                           cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(states_out, c.states.p, size_t(n_lanes) * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    st->max_digits = int32_t(hs.max_digits);
+    if (staged) {  // the payload is the right-aligned tail of the scratch
+        std::memcpy(payload_out, c.stage.at(o_pay) + size_t(n - w) * 2, size_t(w) * 2);
+        std::memcpy(states_out, c.stage.at(o_states), size_t(n_lanes) * 4);
+    } else {
+        if (w)
+            CK(cudaMemcpyAsync(payload_out, dscr + size_t(n - w) * 2, size_t(w) * 2,
+                               cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(states_out, dstates, size_t(n_lanes) * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
     *payload_words = w;
     return ILANS_OK;
 }
 
-// sb <= 12 packed LUT is valid only for self-consistent tables (every slot's
-// symbol s has 1 <= f[s] <= 4095 and 0 <= slot - cum[s] < 4096).
-static bool host_packable(const uint8_t *slot_sym, const uint32_t *f, const uint32_t *cum,
-                          int scale_bits) {
-    if (scale_bits > kPackedMaxBits) return false;
-    const uint32_t m = 1u << scale_bits;
-    for (uint32_t j = 0; j < m; ++j) {
-        const uint32_t s = slot_sym[j];
-        if (f[s] < 1 || f[s] > 4095 || j - cum[s] >= 4096u) return false;
-    }
-    return true;
+extern "C" int ilans_encode_interleaved_u16(const uint8_t *msg, int64_t n, const uint32_t *freq,
+                                            int32_t n_freq, const uint32_t *cum,
+                                            int32_t scale_bits, int32_t n_lanes,
+                                            uint16_t *payload_out, int64_t *payload_words,
+                                            uint32_t *states_out, ilans_status *st) {
+    st_clear(st);
+    return encode_u16_common(msg, n, freq, n_freq, cum, scale_bits, n_lanes, payload_out,
+                             payload_words, states_out, false, st);
+}
+
+extern "C" int ilans_encode_interleaved_u16_stats(const uint8_t *msg, int64_t n,
+                                                  const uint32_t *freq, int32_t n_freq,
+                                                  const uint32_t *cum, int32_t scale_bits,
+                                                  int32_t n_lanes, uint16_t *payload_out,
+                                                  int64_t *payload_words, uint32_t *states_out,
+                                                  ilans_status *st) {
+    st_clear(st);
+    return encode_u16_common(msg, n, freq, n_freq, cum, scale_bits, n_lanes, payload_out,
+                             payload_words, states_out, true, st);
 }
 
 struct HostTrace {  // host buffers for ilans_decode_trace_u16 (all null = no trace)
@@ -287,7 +508,8 @@ static int decode_common(const uint16_t *payload, int64_t pay_len, const uint32_
                          const uint8_t *slot_sym, int64_t n_slots, const uint32_t *freq,
                          const uint32_t *cum, int32_t n_freq, int32_t scale_bits,
                          int64_t msg_len, int32_t n_lanes, uint8_t *out, int64_t *consumed,
-                         ilans_status *st, HostTrace ht = HostTrace{nullptr, nullptr, nullptr}) {
+                         ilans_status *st, HostTrace ht = HostTrace{nullptr, nullptr, nullptr},
+                         bool stats = false) {
     if (msg_len < 0 || pay_len < 0) return st_fail(st, ILANS_ERR_VALUE, "negative length");
     if (n_lanes < 1 || n_lanes > 0xFFFF)
         return st_fail(st, ILANS_ERR_VALUE, "lane_count must be in [1, 65535]");
@@ -305,12 +527,13 @@ static int decode_common(const uint16_t *payload, int64_t pay_len, const uint32_
     if (msg_len == 0) {
         *consumed = 0;
         st->consumed = 0;
+        st->max_digits = 0;
         if (ht.groups) *ht.groups = 0;
         return ILANS_OK;
     }
     cudaStream_t s = c.stream;
     const int64_t n_groups = (msg_len + n_lanes - 1) / n_lanes;
-    DecodeTrace dt{nullptr, nullptr, nullptr};
+    DecodeTrace dt{nullptr, nullptr, nullptr, stats ? 1 : 0};
     if (ht.states) {
         CK(c.trace.ensure(size_t(n_groups) * n_lanes * 4 + size_t(n_groups) * 8 + 16));
         dt.states = c.trace.as<uint32_t>();
@@ -319,40 +542,70 @@ static int decode_common(const uint16_t *payload, int64_t pay_len, const uint32_
         CK(c.words.ensure(8));
         dt.groups = reinterpret_cast<uint64_t *>(c.words.p);
     }
-    CK(c.payload.ensure(size_t(pay_len) * 2 + 16));
-    CK(c.offsets.ensure(16));
-    CK(c.states.ensure(size_t(n_lanes) * 4));
     CK(c.ws.ensure(size_t(n_lanes) * 4));
-    CK(c.slot.ensure(size_t(m)));
-    CK(c.freq.ensure(kMaxSym * 4));
-    CK(c.cum.ensure((kMaxSym + 1) * 4));
-    CK(c.out.ensure(size_t(msg_len)));
-    CK(c.consumed.ensure(8));
-    uint32_t hf[kMaxSym] = {0}, hc[kMaxSym + 1] = {0};
-    std::memcpy(hf, freq, size_t(n_freq) * 4);
-    std::memcpy(hc, cum, size_t(n_freq + 1) * 4);
+    // layout: offsets | states | payload | status | consumed | out -- the
+    // first four go up in one copy, the last three come back in one
+    const size_t o_states = 16, o_pay = al16(o_states + size_t(n_lanes) * 4),
+                 o_st = al16(o_pay + size_t(pay_len) * 2 + 16),
+                 o_used = o_st + al16(sizeof(DStatus)), o_out = o_used + 16,
+                 total = o_out + size_t(msg_len);
+    const bool staged = !ht.states && total <= kStageMax;
     const uint64_t offs[2] = {0, uint64_t(pay_len)};
-    if (pay_len)
-        CK(cudaMemcpyAsync(c.payload.p, payload, size_t(pay_len) * 2, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c.offsets.p, offs, sizeof(offs), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c.states.p, states, size_t(n_lanes) * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c.slot.p, slot_sym, size_t(m), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c.freq.p, hf, sizeof(hf), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c.cum.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
-    CK(launch_build_table(nullptr, c.freq.as<uint32_t>(), n_freq, c.cum.as<uint32_t>(),
-                          c.slot.as<uint8_t>(), scale_bits, c.table.as<TableDev>(), s));
-    dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
-    ilans_note_launch();
-    const bool packed = host_packable(slot_sym, hf, hc, scale_bits);
-    CK(launch_decode(c.payload.as<uint16_t>(), c.offsets.as<uint64_t>(), c.states.as<uint32_t>(),
-                     msg_len, msg_len, n_lanes, c.table.as<TableDev>(), scale_bits, packed,
-                     c.out.as<uint8_t>(), c.consumed.as<uint64_t>(), nullptr,
-                     c.status.as<DStatus>(), c.ws.as<uint32_t>(), s, dt));
+    uint8_t *dpay, *doffs, *dstates, *dout, *dused;
+    DStatus *dst;
+    if (staged) {
+        CK(c.stage.ensure(total));
+        CK(c.io.ensure(total));
+        std::memcpy(c.stage.at(0), offs, sizeof(offs));
+        std::memcpy(c.stage.at(o_states), states, size_t(n_lanes) * 4);
+        if (pay_len) std::memcpy(c.stage.at(o_pay), payload, size_t(pay_len) * 2);
+        dstatus_init(reinterpret_cast<DStatus *>(c.stage.at(o_st)));
+        CK(cudaMemcpyAsync(c.io.p, c.stage.at(0), o_used, cudaMemcpyHostToDevice, s));
+        uint8_t *io = c.io.as<uint8_t>();
+        doffs = io;
+        dstates = io + o_states;
+        dpay = io + o_pay;
+        dst = reinterpret_cast<DStatus *>(io + o_st);
+        dused = io + o_used;
+        dout = io + o_out;
+    } else {
+        CK(c.payload.ensure(size_t(pay_len) * 2 + 16));
+        CK(c.offsets.ensure(16));
+        CK(c.states.ensure(size_t(n_lanes) * 4));
+        CK(c.out.ensure(size_t(msg_len)));
+        CK(c.consumed.ensure(8));
+        if (pay_len)
+            CK(cudaMemcpyAsync(c.payload.p, payload, size_t(pay_len) * 2, cudaMemcpyHostToDevice,
+                               s));
+        CK(cudaMemcpyAsync(c.offsets.p, offs, sizeof(offs), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(c.states.p, states, size_t(n_lanes) * 4, cudaMemcpyHostToDevice, s));
+        dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
+        ilans_note_launch();
+        doffs = c.offsets.as<uint8_t>();
+        dstates = c.states.as<uint8_t>();
+        dpay = c.payload.as<uint8_t>();
+        dst = c.status.as<DStatus>();
+        dused = c.consumed.as<uint8_t>();
+        dout = c.out.as<uint8_t>();
+    }
+    if (int rc = ensure_table(c, freq, n_freq, cum, slot_sym, scale_bits, s, st)) return rc;
+    CK(launch_decode(reinterpret_cast<uint16_t *>(dpay), reinterpret_cast<uint64_t *>(doffs),
+                     reinterpret_cast<uint32_t *>(dstates), msg_len, msg_len, n_lanes,
+                     c.table.as<TableDev>(), scale_bits, c.tab_packed, dout,
+                     reinterpret_cast<uint64_t *>(dused), nullptr, dst, c.ws.as<uint32_t>(), s,
+                     dt));
     DStatus hs;
-    if (int rc = read_dstatus(c.status.as<DStatus>(), s, &hs, st)) return rc;
     uint64_t used = 0;
-    CK(cudaMemcpyAsync(&used, c.consumed.p, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if (staged) {  // status | words read | decoded bytes in one download
+        CK(cudaMemcpyAsync(c.stage.at(o_st), dst, total - o_st, cudaMemcpyDeviceToHost, s));
+        CK(ctx_wait(c));
+        std::memcpy(&hs, c.stage.at(o_st), sizeof(DStatus));
+        std::memcpy(&used, c.stage.at(o_used), 8);
+    } else {
+        if (int rc = read_dstatus(dst, s, &hs, st)) return rc;
+        CK(cudaMemcpyAsync(&used, dused, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
     if (ht.states) {  // trace + decoded bytes of every completed group, even on truncation
         uint64_t g = 0;
         CK(cudaMemcpyAsync(&g, dt.groups, 8, cudaMemcpyDeviceToHost, s));
@@ -363,17 +616,22 @@ static int decode_common(const uint16_t *payload, int64_t pay_len, const uint32_
                                cudaMemcpyDeviceToHost, s));
             CK(cudaMemcpyAsync(ht.pos, dt.pos, size_t(g) * 8, cudaMemcpyDeviceToHost, s));
             const int64_t done = int64_t(g) * n_lanes < msg_len ? int64_t(g) * n_lanes : msg_len;
-            CK(cudaMemcpyAsync(out, c.out.p, size_t(done), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(out, dout, size_t(done), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
         }
     }
+    st->max_digits = int32_t(hs.max_digits);
     if (hs.trunc_stream != ~0ull) {
         st->stream = int64_t(hs.trunc_stream);
         st->consumed = int64_t(used);
         return st_fail(st, ILANS_ERR_TRUNCATED, "payload exhausted mid-decode");
     }
-    CK(cudaMemcpyAsync(out, c.out.p, size_t(msg_len), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if (staged) {
+        std::memcpy(out, c.stage.at(o_out), size_t(msg_len));
+    } else {
+        CK(cudaMemcpyAsync(out, dout, size_t(msg_len), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
     *consumed = int64_t(used);
     st->consumed = int64_t(used);
     return ILANS_OK;
@@ -389,6 +647,19 @@ extern "C" int ilans_decode_interleaved_u16(const uint16_t *payload, int64_t pay
     st_clear(st);
     return decode_common(payload, pay_len, states, slot_sym, n_slots, freq, cum, n_freq,
                          scale_bits, msg_len, n_lanes, out, consumed, st);
+}
+
+extern "C" int ilans_decode_interleaved_u16_stats(const uint16_t *payload, int64_t pay_len,
+                                                  const uint32_t *states, const uint8_t *slot_sym,
+                                                  int64_t n_slots, const uint32_t *freq,
+                                                  const uint32_t *cum, int32_t n_freq,
+                                                  int32_t scale_bits, int64_t msg_len,
+                                                  int32_t n_lanes, uint8_t *out,
+                                                  int64_t *consumed, ilans_status *st) {
+    st_clear(st);
+    return decode_common(payload, pay_len, states, slot_sym, n_slots, freq, cum, n_freq,
+                         scale_bits, msg_len, n_lanes, out, consumed, st,
+                         HostTrace{nullptr, nullptr, nullptr}, true);
 }
 
 extern "C" int ilans_decode_trace_u16(const uint16_t *payload, int64_t pay_len,
@@ -460,6 +731,7 @@ extern "C" int ilans_encode_interleaved_u8(const uint8_t *msg, int64_t n, const 
     CK(cudaMemcpyAsync(c.msg.p, msg, size_t(n), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(c.freq.p, hf, sizeof(hf), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(c.cum.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    table_clobbered(c);
     CK(launch_build_table(nullptr, c.freq.as<uint32_t>(), n_freq, c.cum.as<uint32_t>(), nullptr,
                           scale_bits, c.table.as<TableDev>(), s));
     dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
@@ -513,7 +785,7 @@ static int decode_u8_common(const uint8_t *payload, int64_t pay_len, const uint3
     }
     cudaStream_t s = c.stream;
     const int64_t n_groups = (msg_len + n_lanes - 1) / n_lanes;
-    DecodeTrace dt{nullptr, nullptr, nullptr};
+    DecodeTrace dt{nullptr, nullptr, nullptr, 0};
     if (ht.states) {
         CK(c.trace.ensure(size_t(n_groups) * n_lanes * 4 + size_t(n_groups) * 8 + 16));
         CK(c.words.ensure(8));
@@ -542,6 +814,7 @@ static int decode_u8_common(const uint8_t *payload, int64_t pay_len, const uint3
     CK(cudaMemcpyAsync(c.slot.p, slot_sym, size_t(m), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(c.freq.p, hf, sizeof(hf), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(c.cum.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    table_clobbered(c);
     CK(launch_build_table(nullptr, c.freq.as<uint32_t>(), n_freq, c.cum.as<uint32_t>(),
                           c.slot.as<uint8_t>(), scale_bits, c.table.as<TableDev>(), s));
     dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
@@ -629,6 +902,7 @@ extern "C" int ilans_quantize(const uint64_t *counts, int32_t n, int32_t scale_b
     uint64_t hc[kMaxSym] = {0};
     std::memcpy(hc, counts, size_t(n) * 8);
     CK(cudaMemcpyAsync(c.counts.p, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    table_clobbered(c);
     CK(launch_build_table(c.counts.as<unsigned long long>(), nullptr, 0, nullptr, nullptr,
                           scale_bits, c.table.as<TableDev>(), s));
     TableDev *h = static_cast<TableDev *>(std::malloc(sizeof(TableDev)));

@@ -55,6 +55,7 @@ struct DecodeTrace {
     uint32_t *states;  // [groups][N]
     uint64_t *pos;     // [groups]
     uint64_t *groups;  // [1] completed groups
+    int stats;         // measure digits per symbol -> DStatus::max_digits (generic loop)
 };
 
 // Device status blob (first error wins, deterministic by index).
@@ -63,7 +64,7 @@ struct alignas(16) DStatus {
     long long unenc_index;            // max offending message index, -1 = none
     uint32_t unenc_symbol;
     uint32_t value_error;
-    uint32_t max_digits;              // byte8: most digits moved for one symbol
+    uint32_t max_digits;              // most digits moved for one symbol (byte8; word16 stats calls)
     uint32_t pad[3];
 };
 

@@ -265,9 +265,14 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
     // 2 as an opaque register: keeps the cursor updates as IMADs (FMA pipe)
     uint32_t two;
     asm volatile("mov.u32 %0, 2;" : "=r"(two));
-    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nw;
+    // warps that own chunks: a launch over few chunks adds staging-only
+    // warps (the LUT copy above) that stop here
+    int64_t nwk = (n_chunks + gridDim.x - 1) / gridDim.x;
+    if (nwk > nw) nwk = nw;
+    if (wib >= nwk) return;
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nwk;
 
-    for (int64_t k = static_cast<int64_t>(blockIdx.x) * nw + wib; k < n_chunks;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * nwk + wib; k < n_chunks;
          k += warps_total) {
         const int64_t cbase = k * chunk_len;
         const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
@@ -289,7 +294,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
         sink.begin(k, cbase, lane);
         int64_t base = 0;
 
-        if ((SMALL || n_lanes == 32) && !trace.states) {
+        if ((SMALL || n_lanes == 32) && !trace.states && !trace.stats) {
             // ---------------- fast path: batches of 512 symbols -------------
             // (kBatch groups of 32 lanes, or 512/N groups of N < 32 lanes for
             // the power-of-two widths.) A batch reads <= 512 words, i.e. up
@@ -371,6 +376,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
         }
         // ---------------- generic per-group loop (any N <= 32, tails) ------
         bool truncated = (v - delta) > wlen;
+        uint32_t most = 0;  // stats: most digits one symbol needed (rans.py:305-309 loop)
         for (; !truncated && base < len; base += n_lanes) {
             const int64_t left = len - base;
             const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
@@ -387,6 +393,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
             if (need)
                 x = (x << 16) | ring_load(ring_addr, static_cast<uint32_t>(v + __popc(mk & lt)) << 1);
             v += cnt;
+            if (trace.stats && need) most = max(most, x < kLow ? 2u : 1u);
             if (trace.states) {
                 const int64_t gi = base / n_lanes;
                 if (lane < n_lanes) trace.states[gi * n_lanes + lane] = x;
@@ -422,6 +429,10 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
         }
         if (trace.groups && lane == 0) trace.groups[k] = (base < len ? base : len + n_lanes - 1) / n_lanes;
         if (lane == 0 && consumed) consumed[k] = v - delta;
+        if (trace.stats) {
+            most = __reduce_max_sync(0xffffffffu, most);
+            if (lane == 0 && most) atomicMax(&status->max_digits, most);
+        }
         if (final_states && lane < n_lanes) final_states[k * n_lanes + lane] = x;
         cp_async_wait<0>();
         __syncwarp();
@@ -534,9 +545,14 @@ decode_warp_body_np2(const uint16_t *__restrict__ payload, const uint64_t *__res
     // 2 as an opaque register: keeps the cursor updates as IMADs (FMA pipe)
     uint32_t two;
     asm volatile("mov.u32 %0, 2;" : "=r"(two));
-    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nw;
+    // warps that own chunks: a launch over few chunks adds staging-only
+    // warps (the LUT copy above) that stop here
+    int64_t nwk = (n_chunks + gridDim.x - 1) / gridDim.x;
+    if (nwk > nw) nwk = nw;
+    if (wib >= nwk) return;
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nwk;
 
-    for (int64_t k = static_cast<int64_t>(blockIdx.x) * nw + wib; k < n_chunks;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * nwk + wib; k < n_chunks;
          k += warps_total) {
         const int64_t cbase = k * chunk_len;
         const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
@@ -558,7 +574,7 @@ decode_warp_body_np2(const uint16_t *__restrict__ payload, const uint64_t *__res
         sink.begin(k, cbase, lane);
         int64_t base = 0;
 
-        if ((SMALL || n_lanes == 32) && !trace.states) {
+        if ((SMALL || n_lanes == 32) && !trace.states && !trace.stats) {
             // ---------------- fast path: batches of 512 symbols -------------
             // (kBatch groups of 32 lanes, or 512/N groups of N < 32 lanes for
             // the power-of-two widths.) A batch reads <= 512 words, i.e. up
@@ -664,6 +680,7 @@ decode_warp_body_np2(const uint16_t *__restrict__ payload, const uint64_t *__res
         }
         // ---------------- generic per-group loop (any N <= 32, tails) ------
         bool truncated = (v - delta) > wlen;
+        uint32_t most = 0;  // stats: most digits one symbol needed (rans.py:305-309 loop)
         for (; !truncated && base < len; base += n_lanes) {
             const int64_t left = len - base;
             const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
@@ -680,6 +697,7 @@ decode_warp_body_np2(const uint16_t *__restrict__ payload, const uint64_t *__res
             if (need)
                 x = (x << 16) | ring_load(ring_addr, static_cast<uint32_t>(v + __popc(mk & lt)) << 1);
             v += cnt;
+            if (trace.stats && need) most = max(most, x < kLow ? 2u : 1u);
             if (trace.states) {
                 const int64_t gi = base / n_lanes;
                 if (lane < n_lanes) trace.states[gi * n_lanes + lane] = x;
@@ -715,6 +733,10 @@ decode_warp_body_np2(const uint16_t *__restrict__ payload, const uint64_t *__res
         }
         if (trace.groups && lane == 0) trace.groups[k] = (base < len ? base : len + n_lanes - 1) / n_lanes;
         if (lane == 0 && consumed) consumed[k] = v - delta;
+        if (trace.stats) {
+            most = __reduce_max_sync(0xffffffffu, most);
+            if (lane == 0 && most) atomicMax(&status->max_digits, most);
+        }
         if (final_states && lane < n_lanes) final_states[k * n_lanes + lane] = x;
         cp_async_wait<0>();
         __syncwarp();
@@ -814,6 +836,7 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
     uint64_t pos = 0;
     bool truncated = false;
     int64_t base = 0;
+    uint32_t most = 0;
     for (; base < len; base += n_lanes) {
         const int64_t left = len - base;
         const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
@@ -846,6 +869,7 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
             const int l = lo + j;
             ws[l] = (ws[l] << 16) | pay[pos + excl + r];
             ++r;
+            if (trace.stats) most = max(most, ws[l] < kLow ? 2u : 1u);
         }
         pos += total;
         if (trace.states) {
@@ -855,6 +879,7 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
             if (threadIdx.x == 0) trace.pos[gi] = pos;
         }
     }
+    if (most) atomicMax(&status->max_digits, most);
     if (threadIdx.x == 0) {
         if (truncated) atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
         if (consumed) consumed[k] = pos;
@@ -985,15 +1010,19 @@ static cudaError_t launch_decode_warp(const uint16_t *d_payload, const uint64_t 
     if (warps < 1) warps = 1;
     const size_t smem_cap = 227 * 1024;
     while (warps > 1 && lut + size_t(warps) * decode_warp_smem() > smem_cap) --warps;
-    const size_t smem = lut + size_t(warps) * decode_warp_smem();
     int64_t blocks = (n_chunks + warps - 1) / warps;
+    // few chunks per CTA (single streams, small inputs): staging-only warps
+    // help copy the LUT into shared memory, then exit (the kernel gives the
+    // chunks to the first ceil(n_chunks / blocks) warps)
+    const int cta_warps = warps < 8 && lut >= 4096 ? 8 : warps;
+    const size_t smem = lut + size_t(cta_warps) * decode_warp_smem();
     const int64_t per_sm = static_cast<int64_t>(smem_cap / (smem + 1024));
     const int64_t max_blocks = sms * (per_sm < 1 ? 1 : per_sm);
     if (blocks > max_blocks) blocks = max_blocks;
     const unsigned g = static_cast<unsigned>(blocks);
     auto go = [&](auto kernel) {
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        kernel<<<g, warps * 32, smem, stream>>>(d_payload, d_word_offsets, d_states, n,
+        smem_limit(reinterpret_cast<const void *>(kernel), int(smem));
+        kernel<<<g, cta_warps * 32, smem, stream>>>(d_payload, d_word_offsets, d_states, n,
                                                 chunk_len, n_chunks, n_lanes, d_table, sink,
                                                 d_consumed, d_final_states, d_status,
                                                 scale_bits, trace);
@@ -1021,12 +1050,11 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
                           DecodeTrace trace) {
     if (n <= 0) return cudaSuccess;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
-    if (n_lanes > 32 && n_lanes <= kWideMax && !trace.states) {
+    if (n_lanes > 32 && n_lanes <= kWideMax && !trace.states && !trace.stats) {
         const size_t smem = kMaxSym * sizeof(uint2) +
                             (((size_t(1) << scale_bits) + 15) & ~size_t(15)) +
                             size_t(n_lanes) * 4;
-        cudaFuncSetAttribute(decode_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
+        smem_limit(reinterpret_cast<const void *>(decode_wide_kernel), int(smem));
         decode_wide_kernel<<<static_cast<unsigned>(n_chunks), 32, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table, d_out,
             d_consumed, d_final_states, d_status);
@@ -1039,8 +1067,7 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
         const size_t tabs = kMaxSym * sizeof(uint2) + (((size_t(1) << scale_bits) + 15) & ~size_t(15));
         const int ws_smem = tabs + size_t(n_lanes) * 4 <= size_t(200) * 1024;
         const size_t smem = tabs + (ws_smem ? size_t(n_lanes) * 4 : 0);
-        cudaFuncSetAttribute(decode_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
+        smem_limit(reinterpret_cast<const void *>(decode_block_kernel), int(smem));
         decode_block_kernel<<<static_cast<unsigned>(n_chunks), threads, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table, d_out,
             d_consumed, d_final_states, d_status, d_lane_ws, trace, ws_smem);
@@ -1075,7 +1102,7 @@ cudaError_t launch_decode_adler32(const uint16_t *d_payload, const uint64_t *d_w
     return launch_decode_warp(d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table,
                               scale_bits, scale_bits <= kPackedMaxBits,
                               Adler32Sink{d_adler, 0ull, 0ull}, d_consumed, nullptr, d_status,
-                              stream, DecodeTrace{nullptr, nullptr, nullptr});
+                              stream, DecodeTrace{nullptr, nullptr, nullptr, 0});
 }
 
 }  // namespace ilans

@@ -496,7 +496,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
                     int n_lanes, const TableDev *__restrict__ tab,
                     uint16_t *__restrict__ scratch, uint32_t *__restrict__ chunk_words,
                     uint32_t *__restrict__ states_out, DStatus *__restrict__ status,
-                    uint32_t *__restrict__ ws_all, int ws_in_smem) {
+                    uint32_t *__restrict__ ws_all, int ws_in_smem, int stats) {
     __shared__ uint32_t scan_sh[32];
     __shared__ uint2 enc[kMaxSym];
     extern __shared__ __align__(16) uint32_t bws[];  // lane states, when they fit
@@ -515,6 +515,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
     int64_t top = len;
     const int64_t groups = (len + n_lanes - 1) / n_lanes;
     bool bad = false;
+    uint32_t most = 0;
     for (int64_t gi = groups - 1; gi >= 0; --gi) {
         const int64_t base = gi * n_lanes;
         const int64_t left = len - base;
@@ -546,6 +547,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
             out[top - total + excl + r] = static_cast<uint16_t>(ws[l] & 0xFFFFu);
             ws[l] >>= 16;
             ++r;
+            if (stats) most = max(most, enc_spill(ctx, ws[l], enc[g[base + l]]) ? 2u : 1u);
         }
         top -= total;
         for (int l = lo; l < hi; ++l) {
@@ -553,6 +555,7 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
             ws[l] = enc_push(ctx, ws[l], e);
         }
     }
+    if (most) atomicMax(&status->max_digits, most);
     if (!bad) {
         if (threadIdx.x == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
         for (int l = lo; l < lo + per && l < n_lanes; ++l) states_out[k * n_lanes + l] = ws[l];
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(32)
 encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len, int n_lanes,
                    const TableDev *__restrict__ tab, uint16_t *__restrict__ scratch,
                    uint32_t *__restrict__ chunk_words, uint32_t *__restrict__ states_out,
-                   DStatus *__restrict__ status) {
+                   DStatus *__restrict__ status, int stats) {
     __shared__ uint2 enc[kMaxSym];
     extern __shared__ __align__(16) uint32_t wws[];  // lane states [N]
     const int lane = threadIdx.x;
@@ -583,6 +586,7 @@ encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     __syncwarp();
     int64_t top = len;
     bool bad = false;
+    uint32_t most = 0;
     for (int64_t gi = (len + n_lanes - 1) / n_lanes - 1; gi >= 0 && !bad; --gi) {
         const int64_t base = gi * n_lanes;
         const int active = (len - base) < n_lanes ? static_cast<int>(len - base) : n_lanes;
@@ -606,10 +610,17 @@ encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 out[top + __popc(mk & lt)] = static_cast<uint16_t>(x & 0xFFFFu);
                 x >>= 16;
             }
+            // stats: digits this symbol moves under the reference's spill
+            // loop (rans.py:284-287): one per pass while x >= threshold
+            if (stats && spill) most = max(most, enc_spill(ctx, x, e) ? 2u : 1u);
             if (on) wws[l] = enc_push(ctx, x, e);
         }
     }
     __syncwarp();
+    if (stats) {
+        most = __reduce_max_sync(0xffffffffu, most);
+        if (lane == 0 && most) atomicMax(&status->max_digits, most);
+    }
     if (!bad) {
         if (lane == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
         for (int l = lane; l < n_lanes; l += 32) states_out[k * n_lanes + l] = wws[l];
@@ -619,21 +630,23 @@ encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
 cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, int n_lanes,
                           const TableDev *d_table, int scale_bits, uint16_t *d_scratch,
                           uint32_t *d_chunk_words, uint32_t *d_states, DStatus *d_status,
-                          uint32_t *d_lane_ws, cudaStream_t stream) {
+                          uint32_t *d_lane_ws, cudaStream_t stream, bool stats) {
     if (n <= 0) return cudaSuccess;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
-    if (n_lanes > 32 && n_lanes <= kWideMaxE) {
+    // stats (instrumented calls): the one-warp sub-group walk measures the
+    // digits per symbol for every N <= 64, the CTA kernel beyond
+    if ((n_lanes > 32 || stats) && n_lanes <= kWideMaxE) {
         encode_wide_kernel<<<static_cast<unsigned>(n_chunks), 32, size_t(n_lanes) * 4, stream>>>(
-            d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states, d_status);
+            d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states, d_status,
+            stats ? 1 : 0);
     } else if (n_lanes > 32) {
         const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
         const int ws_smem = size_t(n_lanes) * 4 <= size_t(200) * 1024;
         const size_t smem = ws_smem ? size_t(n_lanes) * 4 : 0;
-        cudaFuncSetAttribute(encode_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
+        smem_limit(reinterpret_cast<const void *>(encode_block_kernel), int(smem));
         encode_block_kernel<<<static_cast<unsigned>(n_chunks), threads, smem, stream>>>(
             d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states,
-            d_status, d_lane_ws, ws_smem);
+            d_status, d_lane_ws, ws_smem, stats ? 1 : 0);
     } else {
         // one CTA per SM with the SM's share of the streams (<= 28 warps);
         // more streams than 28 per SM: grid-stride over CTA-sized groups
@@ -649,7 +662,7 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
         const size_t smem = encode_smem_bytes(warps);
         const unsigned g = static_cast<unsigned>(blocks);
         auto go = [&](auto kernel) {
-            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            smem_limit(reinterpret_cast<const void *>(kernel), int(smem));
             kernel<<<g, warps * 32, smem, stream>>>(d_msg, n, chunk_len, n_chunks, n_lanes,
                                                     d_table, d_scratch, d_chunk_words, d_states,
                                                     d_status);

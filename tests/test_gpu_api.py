@@ -224,6 +224,62 @@ def test_stats_counters_single_digit_property():
     assert stats.max_encode_digits == stats.max_decode_digits == 1
 
 
+def test_stats_are_measured_by_the_kernel():
+    """max_decode_digits comes from the kernel: a lane state of 0 (below L,
+    handed in directly) pops to x' = 0, one refill leaves it below L, and the
+    reference's refill loop (rans.py:305-309) would need a second digit --
+    the kernel reports 2. Outputs still follow the compiled kernel
+    (_core.pyx:107-112: one refill)."""
+    import warnings
+
+    t = SymbolTable([3, 1], 2)
+    c = Container(WORD16, 1, 1, t, (0,), np.array([5, 7], dtype=np.uint16))
+    stats = RenormStats()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        out = ilb.decode_interleaved(c, stats=stats)
+    ref, used = oracle.decode_interleaved_u16(c.payload, np.array([0], np.uint32), t.slot_u8,
+                                              t.freq_u32, t.cum_u32, 2, 1, 1)
+    assert np.array_equal(out, ref) and used == 1
+    assert stats.max_decode_digits == 2 and stats.decode_digits == 1
+    # N > 32 and N = 32 go through the CTA / warp kernels' measuring loops too
+    rng = np.random.default_rng(5)
+    for lanes in (3, 32, 40, 100):
+        tt = random_table(rng)
+        msg = random_message(rng, tt, 20_000)
+        st2 = RenormStats()
+        cc = ilb.encode_interleaved(msg, tt, lanes, WORD16, stats=st2)
+        assert cc.to_bytes() == ilb.encode_interleaved(msg, tt, lanes, WORD16).to_bytes()
+        assert np.array_equal(ilb.decode_interleaved(cc, stats=st2), msg)
+        assert st2.max_encode_digits == st2.max_decode_digits == 1
+        assert st2.encode_digits == st2.decode_digits == len(cc.payload)
+
+
+def test_drop_in_calls_from_many_threads():
+    """The host-buffer drop-ins keep one context (stream, buffers, pinned
+    staging, cached model) per host thread: concurrent calls from 8 threads
+    with two alternating tables all return the oracle's bytes."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(77)
+    tables = [random_table(rng, max_scale=12), random_table(rng, max_scale=14)]
+    jobs = []
+    for i in range(64):
+        t = tables[i % 2]
+        jobs.append((t, random_message(rng, t, int(rng.integers(0, 70_000))), 1 + i % 32))
+
+    def run(job):
+        t, msg, lanes = job
+        c = ilb.encode_interleaved(msg, t, lanes)
+        ref_p, ref_s = oracle.encode_interleaved_u16(msg, t.freq_u32, t.cum_u32, t.scale_bits,
+                                                     lanes)
+        ok = np.array_equal(c.payload, ref_p) and c.final_states == tuple(ref_s.tolist())
+        return ok and np.array_equal(ilb.decode_interleaved(c), msg)
+
+    with ThreadPoolExecutor(8) as ex:
+        assert all(ex.map(run, jobs))
+
+
 def test_sharded_codec_gather_single_rank_matches_encode_chunked():
     """ShardedCodec (one rank, no process group): build_global_model +
     encode + gather gives the same ICH1 bytes as encode_chunked."""
