@@ -376,6 +376,47 @@ def _plugin_range(job):
     return time.perf_counter() - t0, ok
 
 
+CONFIG1_DIGEST = "1ea63c4d860a4650"  # byte8 N=2 sb=12 container
+
+
+def config1(ref: bool, repeats: int = 3):
+    """BASELINE config 1: byte8 (8-bit digits, L = 2^23), N = 2 lanes, sb =
+    12, 1 MiB of Zipf(1.1) bytes -- the reference's scalar path
+    (interleave.py:155-179). Input: default_rng(1).choice, the BASELINE.md
+    section 3 known-answer input, so the container digest is checked too.
+    ref=True times the unmodified reference (oracle/_ref, pure Python);
+    otherwise the single-stream drop-in call on the B200 (one warp, 2 lanes)."""
+    import hashlib
+
+    if ref:
+        sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+        from ilans.interleave import decode_interleaved, encode_interleaved
+        from ilans.rans import BYTE8, SymbolTable
+    else:
+        from paper_1402_3392_b200.interleave import decode_interleaved, encode_interleaved
+        from paper_1402_3392_b200.rans import BYTE8, SymbolTable
+    p = (np.arange(256) + 1.0) ** -1.1
+    msg = np.random.default_rng(1).choice(256, 1 << 20, p=p / p.sum()).astype(np.uint8)
+    table = SymbolTable.from_counts(np.bincount(msg, minlength=int(msg.max()) + 1).tolist(), 12)
+    enc, dec = [], []
+    for _ in range(1 if ref else repeats):
+        t0 = time.perf_counter()
+        c = encode_interleaved(msg, table, 2, BYTE8)
+        t1 = time.perf_counter()
+        out = decode_interleaved(c)
+        t2 = time.perf_counter()
+        enc.append(t1 - t0)
+        dec.append(t2 - t1)
+    digest = hashlib.sha256(c.to_bytes()).hexdigest()[:16]
+    return {"workload": "config1: byte8 N=2 sb=12, 1 MiB Zipf(1.1) (default_rng(1).choice), "
+                        "one container", "impl": "reference pure-Python scalar path" if ref
+            else "B200 single-stream drop-in (one warp, 2 lanes)",
+            "encode_MBps": len(msg) / min(enc) / 1e6, "decode_MBps": len(msg) / min(dec) / 1e6,
+            "round_trip_MBps": len(msg) / (min(enc) + min(dec)) / 1e6,
+            "container_sha256_16": digest, "digest_ok": digest == CONFIG1_DIGEST,
+            "round_trip_ok": bool(np.array_equal(out, msg))}
+
+
 def plugin_e2e(msg_h, table, C, N, threads_list=(1, 8, 16), sample_mib=256):
     """SURVEY 8b drop-in path: the reference's per-chunk loop
     (encode_interleaved + decode_interleaved per 64 KiB chunk, one Container
@@ -752,6 +793,8 @@ def run_b200(a):
         out["e2e"] = e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes)
     if rank == 0 and world == 1 and not a.no_plugin:
         out["plugin_e2e"] = plugin_e2e(d_msg[:n].cpu().numpy(), table, C, N)
+    if rank == 0 and world == 1:
+        out["config1"] = config1(ref=False)
 
     if rank == 0 and world == 1 and not a.no_cpu:
         msg_h = d_msg[:n].cpu().numpy()
@@ -887,7 +930,9 @@ def run_reference(a):
     base = vals[-1]
     base["value"] = v
     base.pop("wall_s", None)
+    cfg1 = config1(ref=True)
     print(json.dumps({
+        "config1": cfg1,
         "metric": METRIC, "impl": "reference", "value": v, "unit": "GB/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8 symbols / u32 states / u16 digits",

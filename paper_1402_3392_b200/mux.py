@@ -22,8 +22,9 @@ Streams are ``RansStreamCodec`` (rANS over a SymbolTable, byte-multiple
 digits: BYTE8, WORD16 or a custom RenormVariant with 8/16-bit digits) or
 ``RawStreamCodec`` (fixed-width little-endian values). The reference's
 coder interface is duck-typed (any object with encode_segment /
-new_decoder); the per-symbol scalar decoder it calls is not a B200 path, so
-other coder types raise TypeError and ``new_decoder`` is not provided.
+new_decoder); the B200 kernels know these two coder types, so other coder
+types raise TypeError. ``new_decoder()`` returns the reference's per-symbol
+scalar decoders (host helpers; containers decode on the GPU).
 """
 
 from __future__ import annotations
@@ -86,9 +87,36 @@ class RansStreamCodec:
         return buf.header, buf.payload
 
     def new_decoder(self):
-        raise NotImplementedError(
-            "per-symbol stream decoders are not part of the B200 path; use demux_decode"
-        )
+        """Per-symbol decoder of this stream's segments (reference
+        mux.py:100-128): load_state(read) / decode_symbol(read), the
+        duck-typed interface of the reference's coder objects. A scalar host
+        helper for callers that walk a schedule themselves; demux_decode
+        decodes whole containers on the B200."""
+        return _RansStreamDecoder(self)
+
+
+class _RansStreamDecoder:
+    def __init__(self, codec: RansStreamCodec):
+        self._codec = codec
+        self._state = None
+
+    def load_state(self, read) -> None:
+        state = int.from_bytes(read(4), "little")
+        v = self._codec.variant
+        if not v.lower_bound <= state < v.state_limit:
+            raise FormatError(f"stream state {state} outside the coder interval")
+        self._state = state
+
+    def decode_symbol(self, read) -> int:
+        from .rans import pop_symbol
+
+        c = self._codec
+        low, bits, nb = c.variant.lower_bound, c.variant.digit_bits, c.digit_nbytes
+        symbol, state = pop_symbol(c.table, self._state)
+        while state < low:
+            state = (state << bits) | int.from_bytes(read(nb), "little")
+        self._state = state
+        return symbol
 
 
 class RawStreamCodec:
@@ -106,9 +134,19 @@ class RawStreamCodec:
         return buf.header, buf.payload
 
     def new_decoder(self):
-        raise NotImplementedError(
-            "per-symbol stream decoders are not part of the B200 path; use demux_decode"
-        )
+        """Per-value decoder (reference mux.py:150-163); stateless."""
+        return _RawStreamDecoder(self.value_nbytes)
+
+
+class _RawStreamDecoder:
+    def __init__(self, nbytes: int):
+        self._nbytes = nbytes
+
+    def load_state(self, read) -> None:
+        pass  # stateless: reloading at a segment boundary costs nothing
+
+    def decode_symbol(self, read) -> int:
+        return int.from_bytes(read(self._nbytes), "little")
 
 
 # ------------------------------------------------------------ containers

@@ -181,8 +181,9 @@ class SymbolTable:
 
 class RenormStats:
     """Spill / refill counters (reference rans.py:235-263). The B200 path
-    fills them from kernel totals: word16 moves at most one digit per symbol,
-    so symbols, digits and the per-symbol maximum follow from the counts."""
+    fills them from the kernels: symbol and digit totals, and the most
+    digits one symbol moved, measured by the instrumented kernel calls
+    (ilans_*_u16_stats; byte8 always reports it)."""
 
     def __init__(self):
         self.encode_symbols = 0
@@ -213,6 +214,101 @@ class RenormStats:
 def encode_threshold(table: SymbolTable, variant: RenormVariant, symbol: int) -> int:
     """Exclusive upper state bound before pushing ``symbol`` (rans.py:229-232)."""
     return table.freq[symbol] * (variant.state_limit >> table.scale_bits)
+
+
+# ---------------------------------------------------------------------------
+# Scalar per-symbol helpers (reference rans.py:214-329). These are the
+# reference's building blocks for custom coders (raw-bit bypass, the mux's
+# per-stream decoders, user code): one exact integer state transition per
+# call on Python ints. No bulk path of this package calls them -- message
+# coding runs in the B200 kernels -- and they are tested against the
+# reference's own known answers (tests/test_host.py).
+# ---------------------------------------------------------------------------
+def push_symbol(table: SymbolTable, symbol: int, state: int) -> int:
+    """Bare rANS push, no renormalisation (rans.py:214-219)."""
+    f = table.freq[symbol]
+    if f == 0:
+        raise UnencodableSymbolError(f"symbol {symbol} has frequency 0")
+    q, r = divmod(state, f)
+    return (q << table.scale_bits) + table.cum[symbol] + r
+
+
+def pop_symbol(table: SymbolTable, state: int) -> tuple[int, int]:
+    """Bare rANS pop, no renormalisation (rans.py:222-226)."""
+    slot = state & (table.total - 1)
+    symbol = table.slot_to_symbol[slot]
+    return symbol, table.freq[symbol] * (state >> table.scale_bits) + slot - table.cum[symbol]
+
+
+def encode_symbol_renorm(state: int, symbol: int, table: SymbolTable, variant: RenormVariant,
+                         sink: list, stats: RenormStats | None = None) -> int:
+    """Spill digits to ``sink`` (emission order) until ``state`` is below the
+    symbol's threshold f * (state_limit >> sb), then push (rans.py:266-290)."""
+    f = table.freq[symbol]
+    if f == 0:
+        raise UnencodableSymbolError(f"symbol {symbol} has frequency 0")
+    limit = f * (variant.state_limit >> table.scale_bits)
+    spilled = 0
+    while state >= limit:
+        sink.append(state & variant.digit_mask)
+        state >>= variant.digit_bits
+        spilled += 1
+    if stats is not None:
+        stats.note_encode(spilled)
+    return push_symbol(table, symbol, state)
+
+
+def decode_symbol_renorm(state: int, table: SymbolTable, variant: RenormVariant, source,
+                         stats: RenormStats | None = None) -> tuple[int, int]:
+    """Pop one symbol, then refill digits from ``source`` (anything with
+    ``.read()``) until the state is back in [L, R*L) (rans.py:293-314)."""
+    symbol, state = pop_symbol(table, state)
+    low = variant.lower_bound
+    # a valid pop never lands on 0; more refills than a state has digits
+    # (+ 2) only happen on corrupt input
+    max_refills = (low.bit_length() + variant.digit_bits - 1) // variant.digit_bits + 2
+    refills = 0
+    while state < low:
+        state = (state << variant.digit_bits) | source.read()
+        refills += 1
+        if refills > max_refills:
+            raise FormatError("renormalization does not terminate; corrupt stream")
+    if stats is not None:
+        stats.note_decode(refills)
+    return symbol, state
+
+
+@dataclass(frozen=True)
+class Coder:
+    """A code / decode pair with its normalisation interval -- the fields of
+    the reference's generic ``ans.Coder`` (ans.py:41-67) that rans_coder
+    fills; the generic teaching framework itself is out of scope."""
+
+    alphabet_size: int
+    code: object
+    decode: object
+    lower_bound: int
+    radix: int
+
+    def __post_init__(self):
+        if self.radix < 2:
+            raise ValueError("radix must be >= 2")
+        if self.lower_bound < 1:
+            raise ValueError("lower_bound must be >= 1")
+        if self.alphabet_size < 1:
+            raise ValueError("alphabet_size must be >= 1")
+
+    def in_interval(self, state: int) -> bool:
+        return self.lower_bound <= state < self.radix * self.lower_bound
+
+
+def rans_coder(table: SymbolTable, variant: RenormVariant) -> Coder:
+    """A table + variant as a Coder (rans.py:317-329)."""
+    variant.check_table(table)
+    return Coder(alphabet_size=table.alphabet_size,
+                 code=lambda s, x: push_symbol(table, s, x),
+                 decode=lambda x: pop_symbol(table, x),
+                 lower_bound=variant.lower_bound, radix=variant.radix)
 
 
 def serialize_table(table: SymbolTable) -> bytes:
