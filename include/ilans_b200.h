@@ -232,7 +232,8 @@ int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
  * (capacity n words) at those offsets. carry_in != 0 continues a previous
  * batch: d_word_offsets[0] is read as the starting offset instead of being
  * set to 0 (so batches of chunks pack into one stream). d_payload may be a
- * mapped pinned host pointer (the packing then streams over PCIe). */
+ * mapped pinned host pointer (the packing then streams over PCIe).
+ * d_payload == NULL computes the word offsets (the ICH1 directory) only. */
 int ilans_frame_chunks_dev(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
                            const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
                            uint16_t *d_payload, int32_t carry_in, void *stream);
@@ -250,6 +251,25 @@ int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t *d_word_of
                             uint8_t *d_out,
                             uint64_t *d_consumed, uint32_t *d_final_states, void *d_status,
                             void *stream);
+
+/* Chunked decode straight from the encoder's slot layout (no framing pass):
+ * d_scratch / d_chunk_words / d_states exactly as ilans_encode_chunks_dev
+ * left them -- chunk k's w_k = d_chunk_words[k] words right-aligned in its
+ * slot [kC + len_k - w_k, kC + len_k). Otherwise as ilans_decode_chunks_dev
+ * (d_consumed[k] == w_k on valid input). The packed ICH1 payload is built
+ * only when the stream leaves HBM (ilans_frame_chunks_dev). */
+int ilans_decode_chunks_slots_dev(const uint16_t *d_scratch, const uint32_t *d_chunk_words,
+                                  const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                  int32_t n_lanes, const void *d_table, int32_t scale_bits,
+                                  uint8_t *d_out, uint64_t *d_consumed, uint32_t *d_final_states,
+                                  void *d_status, void *stream);
+/* The fused Adler-32 consumer over the slot layout (see below). */
+int ilans_decode_chunks_slots_adler32_dev(const uint16_t *d_scratch,
+                                          const uint32_t *d_chunk_words,
+                                          const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                          int32_t n_lanes, const void *d_table,
+                                          int32_t scale_bits, uint32_t *d_adler,
+                                          uint64_t *d_consumed, void *d_status, void *stream);
 
 /* Decode fused with a consumer: the same chunked decode,
  * but the decoded bytes are consumed in registers instead of written to

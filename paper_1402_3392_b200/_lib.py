@@ -119,6 +119,10 @@ PROTOTYPES = [
     ("ilans_frame_chunks_dev", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
     ("ilans_decode_chunks_dev", ctypes.c_int,
      [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),
+    ("ilans_decode_chunks_slots_dev", ctypes.c_int,
+     [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),
+    ("ilans_decode_chunks_slots_adler32_dev", ctypes.c_int,
+     [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
     ("ilans_decode_chunks_adler32_dev", ctypes.c_int,
      [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
     ("ilans_adler32_chunks_dev", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp]),

@@ -318,7 +318,30 @@ class DeviceCodec:
             self._p(self.consumed), self._p(self.final_states) if final_states else None,
             self._p(self.status), self._s()), "decode")
 
-    def decode_adler32(self, n: int, adler=None, payload=None, offsets=None, states=None):
+    def decode_slots(self, d_out, n: int, final_states: bool = False):
+        """Decode n bytes into d_out straight from this codec's encode scratch
+        (each chunk's words right-aligned in its slot, counts in
+        chunk_words): the device-resident round trip needs no packing pass;
+        the packed ICH1 payload is built when the stream leaves HBM
+        (frame_range into mapped pinned host memory)."""
+        _lib.check_dev(_lib.lib.ilans_decode_chunks_slots_dev(
+            self._p(self.scratch), self._p(self.chunk_words), self._p(self.states), int(n),
+            self.chunk_len, self.lane_count, self._p(self.table), self.scale_bits,
+            self._p(d_out), self._p(self.consumed),
+            self._p(self.final_states) if final_states else None, self._p(self.status),
+            self._s()), "decode_slots")
+
+    def directory(self, n: int):
+        """Word offsets of the framed stream (the ICH1 directory) from the
+        encoder's chunk word counts, without packing the payload."""
+        k = n_chunks_for(n, self.chunk_len)
+        _lib.check_dev(_lib.lib.ilans_frame_chunks_dev(
+            self._p(self.scratch), int(n), self.chunk_len, self._p(self.chunk_words),
+            self._p(self.offsets), None, 0, self._s()), "directory")
+        return self.offsets[: k + 1]
+
+    def decode_adler32(self, n: int, adler=None, payload=None, offsets=None, states=None,
+                       slots: bool = False):
         """Decode fused with its consumer: the zlib Adler-32
         of every decoded chunk (uint32 per chunk, as int32 tensor), computed
         in registers -- the decoded bytes never reach HBM."""
@@ -326,6 +349,13 @@ class DeviceCodec:
         k = n_chunks_for(n, self.chunk_len)
         if adler is None:
             adler = torch.empty(max(1, k), dtype=torch.int32, device=self.device)
+        if slots:  # straight from the encode scratch (see decode_slots)
+            _lib.check_dev(_lib.lib.ilans_decode_chunks_slots_adler32_dev(
+                self._p(self.scratch), self._p(self.chunk_words), self._p(self.states), int(n),
+                self.chunk_len, self.lane_count, self._p(self.table), self.scale_bits,
+                self._p(adler), self._p(self.consumed), self._p(self.status), self._s()),
+                "decode_slots_adler32")
+            return adler[:k]
         payload = self.payload if payload is None else payload
         offsets = self.offsets if offsets is None else offsets
         states = self.states if states is None else states

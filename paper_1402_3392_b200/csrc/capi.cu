@@ -959,6 +959,11 @@ extern "C" int ilans_histogram_u8(const uint8_t *msg, int64_t n, uint64_t *count
 // ---------------------------------------------------------------------------
 #define ST(x) static_cast<cudaStream_t>(x)
 
+// the Adler-32 sinks keep sum(i * b_i) of a chunk in u64 (~255 C^2 / 2):
+// exact for chunks up to 2^27 bytes
+constexpr int64_t kAdlerMaxChunk = int64_t(1) << 27;
+
+
 extern "C" int ilans_counts_zero_dev(uint64_t *d_counts, void *stream) {
     return cudaMemsetAsync(d_counts, 0, kMaxSym * 8, ST(stream)) == cudaSuccess ? ILANS_OK
                                                                                : ILANS_ERR_CUDA;
@@ -1092,6 +1097,43 @@ extern "C" int ilans_decode_chunks_dev(const uint16_t *d_payload, const uint64_t
                          ST(stream)) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
 }
 
+extern "C" int ilans_decode_chunks_slots_dev(const uint16_t *d_scratch,
+                                             const uint32_t *d_chunk_words,
+                                             const uint32_t *d_states, int64_t n,
+                                             int64_t chunk_len, int32_t n_lanes,
+                                             const void *d_table, int32_t scale_bits,
+                                             uint8_t *d_out, uint64_t *d_consumed,
+                                             uint32_t *d_final_states, void *d_status,
+                                             void *stream) {
+    if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits || !d_chunk_words) return ILANS_ERR_VALUE;
+    if ((reinterpret_cast<uintptr_t>(d_scratch) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
+        return ILANS_ERR_VALUE;
+    const bool packed = scale_bits <= kPackedMaxBits;
+    return launch_decode(d_scratch, nullptr, d_states, n, chunk_len, n_lanes,
+                         static_cast<const TableDev *>(d_table), scale_bits, packed, d_out,
+                         d_consumed, d_final_states, static_cast<DStatus *>(d_status), nullptr,
+                         ST(stream), DecodeTrace{nullptr, nullptr, nullptr, 0},
+                         d_chunk_words) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_decode_chunks_slots_adler32_dev(const uint16_t *d_scratch,
+                                                     const uint32_t *d_chunk_words,
+                                                     const uint32_t *d_states, int64_t n,
+                                                     int64_t chunk_len, int32_t n_lanes,
+                                                     const void *d_table, int32_t scale_bits,
+                                                     uint32_t *d_adler, uint64_t *d_consumed,
+                                                     void *d_status, void *stream) {
+    if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits || !d_chunk_words) return ILANS_ERR_VALUE;
+    if (reinterpret_cast<uintptr_t>(d_scratch) & 15) return ILANS_ERR_VALUE;
+    if (chunk_len > kAdlerMaxChunk) return ILANS_ERR_VALUE;
+    return launch_decode_adler32(d_scratch, nullptr, d_states, n, chunk_len, n_lanes,
+                                 static_cast<const TableDev *>(d_table), scale_bits, d_adler,
+                                 d_consumed, static_cast<DStatus *>(d_status), ST(stream),
+                                 d_chunk_words) == cudaSuccess ? ILANS_OK : ILANS_ERR_CUDA;
+}
+
 extern "C" int ilans_encode_chunks_u8_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
                                           int32_t n_lanes, const void *d_table,
                                           uint8_t *d_scratch, uint32_t *d_chunk_bytes,
@@ -1126,10 +1168,6 @@ extern "C" int ilans_decode_chunks_u8_dev(const uint8_t *d_payload, const uint64
                ? ILANS_OK
                : ILANS_ERR_CUDA;
 }
-
-// the Adler-32 sinks keep sum(i * b_i) of a chunk in u64 (~255 C^2 / 2):
-// exact for chunks up to 2^27 bytes
-constexpr int64_t kAdlerMaxChunk = int64_t(1) << 27;
 
 extern "C" int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload,
                                                const uint64_t *d_word_offsets,

@@ -51,6 +51,26 @@ struct alignas(16) TableDev {
 // the read position after every group, plus the number of completed groups
 // -- the device form of interleave.decode_interleaved_steps /
 // lanes.decode_lanes_steps (interleave.py:251-268, lanes.py:221-232).
+// Where chunk k's payload words are: packed back to back at word offsets
+// offsets[k] .. offsets[k + 1] (the framed stream), or -- slot_words set --
+// in the encoder's slot layout, right-aligned in chunk k's C-word slot:
+// [kC + len_k - w_k, kC + len_k) with w_k = slot_words[k] (decode straight
+// from the encode scratch; the packed stream is only built on egress).
+struct ChunkDir {
+    const uint64_t *offsets;
+    const uint32_t *slot_words;
+    __device__ __forceinline__ void span(int64_t k, int64_t cbase, int64_t len, uint64_t &woff,
+                                         uint64_t &wlen) const {
+        if (slot_words) {
+            wlen = slot_words[k];
+            woff = static_cast<uint64_t>(cbase + len) - wlen;
+        } else {
+            woff = offsets[k];
+            wlen = offsets[k + 1] - woff;
+        }
+    }
+};
+
 struct DecodeTrace {
     uint32_t *states;  // [groups][N]
     uint64_t *pos;     // [groups]

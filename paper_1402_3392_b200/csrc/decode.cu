@@ -214,7 +214,7 @@ __host__ __device__ constexpr size_t decode_warp_smem() { return kRingAllocBytes
 // a separate body so the N = 32 batch loop keeps its own schedule.
 template <int KIND, class Sink, bool SMALL>
 __device__ __noinline__ void
-decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+decode_warp_body(const uint16_t *__restrict__ payload, ChunkDir dir,
                  const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
                  int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                  Sink sink, uint64_t *__restrict__ consumed,
@@ -276,8 +276,8 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
          k += warps_total) {
         const int64_t cbase = k * chunk_len;
         const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
-        const uint64_t woff = offsets[k];
-        const uint64_t wlen = offsets[k + 1] - woff;
+        uint64_t woff, wlen;
+        dir.span(k, cbase, len, woff, wlen);
         const uint32_t delta = static_cast<uint32_t>(woff & 7u);
         SegSrc src{payload + (woff & ~7ull), wlen + delta};
 #pragma unroll
@@ -441,21 +441,21 @@ decode_warp_body(const uint16_t *__restrict__ payload, const uint64_t *__restric
 
 template <int MAXKIND, class Sink, bool SMALL>
 __device__ __forceinline__ void
-decode_warp_dispatch(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+decode_warp_dispatch(const uint16_t *__restrict__ payload, ChunkDir dir,
                      const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
                      int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab, Sink out,
                      uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
                      DStatus *__restrict__ status, DecodeTrace trace, uint8_t *smem, int sb) {
     if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
-        decode_warp_body<kLutPacked32, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+        decode_warp_body<kLutPacked32, Sink, SMALL>(payload, dir, states, n, chunk_len,
                                                     n_chunks, n_lanes, tab, out, consumed,
                                                     final_states, status, trace, smem, sb);
     else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
-        decode_warp_body<kLutPacked64, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+        decode_warp_body<kLutPacked64, Sink, SMALL>(payload, dir, states, n, chunk_len,
                                                     n_chunks, n_lanes, tab, out, consumed,
                                                     final_states, status, trace, smem, sb);
     else
-        decode_warp_body<kLutGeneric, Sink, SMALL>(payload, offsets, states, n, chunk_len,
+        decode_warp_body<kLutGeneric, Sink, SMALL>(payload, dir, states, n, chunk_len,
                                                    n_chunks, n_lanes, tab, out, consumed,
                                                    final_states, status, trace, smem, sb);
 }
@@ -466,7 +466,7 @@ decode_warp_dispatch(const uint16_t *__restrict__ payload, const uint64_t *__res
 // the 32-bit entry cannot hold).
 template <int MAXKIND, class Sink>
 __global__ void __launch_bounds__(1024)
-decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+decode_warp_kernel(const uint16_t *__restrict__ payload, ChunkDir dir,
                    const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                    Sink out, uint64_t *__restrict__ consumed,
@@ -479,11 +479,11 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         return;
     }
     if (n_lanes < 32 && (n_lanes & (n_lanes - 1)) == 0)
-        decode_warp_dispatch<MAXKIND, Sink, true>(payload, offsets, states, n, chunk_len,
+        decode_warp_dispatch<MAXKIND, Sink, true>(payload, dir, states, n, chunk_len,
                                                   n_chunks, n_lanes, tab, out, consumed,
                                                   final_states, status, trace, smem, sb);
     else
-        decode_warp_dispatch<MAXKIND, Sink, false>(payload, offsets, states, n, chunk_len,
+        decode_warp_dispatch<MAXKIND, Sink, false>(payload, dir, states, n, chunk_len,
                                                    n_chunks, n_lanes, tab, out, consumed,
                                                    final_states, status, trace, smem, sb);
 }
@@ -492,7 +492,7 @@ decode_warp_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
 // and kernel, so the N = 32 / power-of-two kernels keep their code.
 template <int KIND, class Sink>
 __device__ __noinline__ void
-decode_warp_body_np2(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+decode_warp_body_np2(const uint16_t *__restrict__ payload, ChunkDir dir,
                  const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
                  int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                  Sink sink, uint64_t *__restrict__ consumed,
@@ -556,8 +556,8 @@ decode_warp_body_np2(const uint16_t *__restrict__ payload, const uint64_t *__res
          k += warps_total) {
         const int64_t cbase = k * chunk_len;
         const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
-        const uint64_t woff = offsets[k];
-        const uint64_t wlen = offsets[k + 1] - woff;
+        uint64_t woff, wlen;
+        dir.span(k, cbase, len, woff, wlen);
         const uint32_t delta = static_cast<uint32_t>(woff & 7u);
         SegSrc src{payload + (woff & ~7ull), wlen + delta};
 #pragma unroll
@@ -745,7 +745,7 @@ decode_warp_body_np2(const uint16_t *__restrict__ payload, const uint64_t *__res
 
 template <int MAXKIND, class Sink>
 __global__ void __launch_bounds__(1024)
-decode_warp_np2_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+decode_warp_np2_kernel(const uint16_t *__restrict__ payload, ChunkDir dir,
                        const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
                        int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                        Sink out, uint64_t *__restrict__ consumed,
@@ -758,15 +758,15 @@ decode_warp_np2_kernel(const uint16_t *__restrict__ payload, const uint64_t *__r
         return;
     }
     if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
-        decode_warp_body_np2<kLutPacked32, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
+        decode_warp_body_np2<kLutPacked32, Sink>(payload, dir, states, n, chunk_len, n_chunks,
                                                  n_lanes, tab, out, consumed, final_states,
                                                  status, trace, smem, sb);
     else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
-        decode_warp_body_np2<kLutPacked64, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
+        decode_warp_body_np2<kLutPacked64, Sink>(payload, dir, states, n, chunk_len, n_chunks,
                                                  n_lanes, tab, out, consumed, final_states,
                                                  status, trace, smem, sb);
     else
-        decode_warp_body_np2<kLutGeneric, Sink>(payload, offsets, states, n, chunk_len, n_chunks,
+        decode_warp_body_np2<kLutGeneric, Sink>(payload, dir, states, n, chunk_len, n_chunks,
                                                 n_lanes, tab, out, consumed, final_states,
                                                 status, trace, smem, sb);
 }
@@ -986,7 +986,7 @@ adler32_chunks_kernel(const uint8_t *__restrict__ data, int64_t n, int64_t chunk
 }
 
 template <class Sink>
-static cudaError_t launch_decode_warp(const uint16_t *d_payload, const uint64_t *d_word_offsets,
+static cudaError_t launch_decode_warp(const uint16_t *d_payload, ChunkDir dir,
                                      const uint32_t *d_states, int64_t n, int64_t chunk_len,
                                      int n_lanes, const TableDev *d_table, int scale_bits,
                                      bool packed, Sink sink, uint64_t *d_consumed,
@@ -1022,7 +1022,7 @@ static cudaError_t launch_decode_warp(const uint16_t *d_payload, const uint64_t 
     const unsigned g = static_cast<unsigned>(blocks);
     auto go = [&](auto kernel) {
         smem_limit(reinterpret_cast<const void *>(kernel), int(smem));
-        kernel<<<g, cta_warps * 32, smem, stream>>>(d_payload, d_word_offsets, d_states, n,
+        kernel<<<g, cta_warps * 32, smem, stream>>>(d_payload, dir, d_states, n,
                                                 chunk_len, n_chunks, n_lanes, d_table, sink,
                                                 d_consumed, d_final_states, d_status,
                                                 scale_bits, trace);
@@ -1047,9 +1047,10 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
                           const TableDev *d_table, int scale_bits, bool packed,
                           uint8_t *d_out, uint64_t *d_consumed, uint32_t *d_final_states,
                           DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream,
-                          DecodeTrace trace) {
+                          DecodeTrace trace, const uint32_t *d_slot_words) {
     if (n <= 0) return cudaSuccess;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
+    if (d_slot_words && n_lanes > 32) return cudaErrorInvalidValue;  // chunked streams: N <= 32
     if (n_lanes > 32 && n_lanes <= kWideMax && !trace.states && !trace.stats) {
         const size_t smem = kMaxSym * sizeof(uint2) +
                             (((size_t(1) << scale_bits) + 15) & ~size_t(15)) +
@@ -1074,7 +1075,8 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
         ilans_note_launch();
         return cudaGetLastError();
     }
-    return launch_decode_warp(d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table,
+    return launch_decode_warp(d_payload, ChunkDir{d_word_offsets, d_slot_words}, d_states, n,
+                              chunk_len, n_lanes, d_table,
                               scale_bits, packed, StoreSink{d_out, nullptr}, d_consumed,
                               d_final_states, d_status, stream, trace);
 }
@@ -1096,10 +1098,12 @@ cudaError_t launch_decode_adler32(const uint16_t *d_payload, const uint64_t *d_w
                                   const uint32_t *d_states, int64_t n, int64_t chunk_len,
                                   int n_lanes, const TableDev *d_table, int scale_bits,
                                   uint32_t *d_adler, uint64_t *d_consumed, DStatus *d_status,
-                                  cudaStream_t stream) {
+                                  cudaStream_t stream, const uint32_t *d_slot_words) {
     if (n <= 0) return cudaSuccess;
     if (n_lanes > 32) return cudaErrorInvalidValue;
-    return launch_decode_warp(d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table,
+    return launch_decode_warp(d_payload, ChunkDir{d_word_offsets, d_slot_words}, d_states, n,
+                              chunk_len,
+                              n_lanes, d_table,
                               scale_bits, scale_bits <= kPackedMaxBits,
                               Adler32Sink{d_adler, 0ull, 0ull}, d_consumed, nullptr, d_status,
                               stream, DecodeTrace{nullptr, nullptr, nullptr, 0});

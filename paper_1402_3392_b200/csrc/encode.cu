@@ -808,7 +808,7 @@ cudaError_t launch_frame(const uint16_t *d_scratch, int64_t n, int64_t chunk_len
     chunk_offsets_kernel<<<1, 1024, 0, stream>>>(d_chunk_words, n_chunks, d_word_offsets,
                                                   carry_in);
     ilans_note_launch();
-    if (n_chunks > 0) {
+    if (n_chunks > 0 && d_payload) {  // d_payload == nullptr: the directory only
         compact_kernel<<<static_cast<unsigned>(n_chunks), 256, 0, stream>>>(
             d_scratch, n, chunk_len, d_chunk_words, d_word_offsets, d_payload);
         ilans_note_launch();

@@ -40,7 +40,8 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
                           const TableDev *d_table, int scale_bits, bool packed,
                           uint8_t *d_out, uint64_t *d_consumed, uint32_t *d_final_states,
                           DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream,
-                          DecodeTrace trace = DecodeTrace{nullptr, nullptr, nullptr});
+                          DecodeTrace trace = DecodeTrace{nullptr, nullptr, nullptr, 0},
+                          const uint32_t *d_slot_words = nullptr);
 cudaError_t launch_adler32_chunks(const uint8_t *d_data, int64_t n, int64_t chunk_len,
                                   uint32_t *d_adler, cudaStream_t stream);
 // decode fused with its consumer: per-chunk Adler-32 of the decoded bytes,
@@ -49,7 +50,7 @@ cudaError_t launch_decode_adler32(const uint16_t *d_payload, const uint64_t *d_w
                                   const uint32_t *d_states, int64_t n, int64_t chunk_len,
                                   int n_lanes, const TableDev *d_table, int scale_bits,
                                   uint32_t *d_adler, uint64_t *d_consumed, DStatus *d_status,
-                                  cudaStream_t stream);
+                                  cudaStream_t stream, const uint32_t *d_slot_words = nullptr);
 
 // byte8.cu -- single-stream byte8 codec (N <= 32 warp, N > 32 CTA)
 cudaError_t launch_encode_u8(const uint8_t *d_msg, int64_t n, int n_lanes, const TableDev *d_table,

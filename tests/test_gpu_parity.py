@@ -460,3 +460,44 @@ def test_fuzz_random_shapes_against_oracle():
             out, used = B.decode_interleaved_u16(p, st, t.slot_u8, t.freq_u32, t.cum_u32, sb,
                                                  n, N)
             assert np.array_equal(out, msg) and used == len(p), (it, sb, n, N)
+
+
+def test_decode_from_slot_layout_matches_packed_decode():
+    """DeviceCodec.decode_slots (straight from the encode scratch, no
+    packing pass) returns the message, consumes exactly each chunk's word
+    count, and matches the packed-stream decode and its final states; the
+    fused Adler-32 over the slot layout equals zlib per chunk."""
+    import zlib
+
+    import torch
+
+    from paper_1402_3392_b200.chunked import DeviceCodec
+    from paper_1402_3392_b200.synth import synth_host
+
+    for n, C, N, sb in ((3_000_017, 65536, 32, 12), (1_000_000, 16384, 32, 14),
+                        (700_001, 4096, 7, 11), (250_000, 1024, 16, 15)):
+        msg = synth_host(n, 1.2, seed=n)
+        d = torch.from_numpy(msg).cuda()
+        codec = DeviceCodec(n, C, N, sb)
+        codec.histogram(d, n)
+        codec.build_table_from_counts()
+        codec.reset_status()
+        codec.encode(d, n, frame=False)
+        offs = codec.directory(n).clone()
+        k = len(offs) - 1
+        out = torch.empty(n, dtype=torch.uint8, device="cuda")
+        codec.decode_slots(out, n, final_states=True)
+        codec.check_status()
+        assert np.array_equal(out.cpu().numpy(), msg)
+        words = codec.chunk_words[:k].to(torch.int64)
+        assert torch.equal(codec.consumed[:k], words)
+        assert torch.equal(offs[1:] - offs[:-1], words)
+        fs_slots = codec.final_states[: k * N].clone()
+        codec.frame_range(n, 0, k, codec.payload.data_ptr())
+        out2 = torch.empty_like(out)
+        codec.decode(out2, n, final_states=True)
+        codec.check_status()
+        assert torch.equal(out, out2) and torch.equal(codec.final_states[: k * N], fs_slots)
+        ad = codec.decode_adler32(n, slots=True).cpu().numpy().view(np.uint32)
+        ref = [zlib.adler32(msg[i * C:(i + 1) * C].tobytes()) for i in range(k)]
+        assert ad.tolist() == ref
