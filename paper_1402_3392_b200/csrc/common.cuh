@@ -16,10 +16,10 @@ namespace ilans {
 constexpr uint32_t kLow = 1u << 16;          // WORD16.lower_bound (rans.py:87)
 constexpr int kMaxSym = 256;                 // MAX_ALPHABET (rans.py:24)
 constexpr int kMaxScaleBits = 16;            // MAX_SCALE_BITS (rans.py:25)
-constexpr int kPackedMaxBits = 12;           // packed 32-bit slot entry: sym|f-1|bias
+constexpr int kPackedMaxBits = 15;           // packed 32-bit slot entry: sym|bias|f (f < 4096)
 
 // Table flags
-constexpr uint32_t kTabPacked = 1u;          // packed[] valid (sb <= 12, consistent)
+constexpr uint32_t kTabPacked = 1u;          // packed[] valid (sb <= 15, every f < 4096, consistent)
 constexpr uint32_t kTabEncFast = 2u;         // encf valid (sb <= 13, every f <= m/2)
 constexpr uint32_t kTabPacked64 = 4u;        // packed64[] valid (13 <= sb <= 14)
 constexpr uint32_t kTabEncFast12 = 8u;       // encf = {M, Y} + encz valid (sb = 14, f <= m/2)

@@ -85,6 +85,15 @@ __device__ __forceinline__ uint32_t ring_load(uint32_t ring_addr, uint32_t byte_
 // (13 <= sb <= 14: one LDS.64 per lane instead of two dependent lookups),
 // and the two-lookup form slot -> symbol -> {f, cum} (any sb).
 enum : int { kLutGeneric = 0, kLutPacked32 = 1, kLutPacked64 = 2 };
+// launch-only kind (13 <= sb <= 14): shared memory sized for the 64-bit LUT;
+// the 32-bit entries run when every f < 4096, else the 64-bit ones
+constexpr int kLutPacked3264 = 3;
+__host__ __device__ constexpr bool allows32(int maxkind) {
+    return maxkind == kLutPacked32 || maxkind == kLutPacked3264;
+}
+__host__ __device__ constexpr bool allows64(int maxkind) {
+    return maxkind == kLutPacked64 || maxkind == kLutPacked3264;
+}
 
 template <int KIND>
 struct Lut {
@@ -446,11 +455,11 @@ decode_warp_dispatch(const uint16_t *__restrict__ payload, ChunkDir dir,
                      int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab, Sink out,
                      uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
                      DStatus *__restrict__ status, DecodeTrace trace, uint8_t *smem, int sb) {
-    if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
+    if (allows32(MAXKIND) && (tab->flags & kTabPacked))
         decode_warp_body<kLutPacked32, Sink, SMALL>(payload, dir, states, n, chunk_len,
                                                     n_chunks, n_lanes, tab, out, consumed,
                                                     final_states, status, trace, smem, sb);
-    else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
+    else if (allows64(MAXKIND) && (tab->flags & kTabPacked64))
         decode_warp_body<kLutPacked64, Sink, SMALL>(payload, dir, states, n, chunk_len,
                                                     n_chunks, n_lanes, tab, out, consumed,
                                                     final_states, status, trace, smem, sb);
@@ -757,11 +766,11 @@ decode_warp_np2_kernel(const uint16_t *__restrict__ payload, ChunkDir dir,
         if (threadIdx.x == 0) status->value_error = 1;  // smem was sized for launch_sb
         return;
     }
-    if (MAXKIND == kLutPacked32 && (tab->flags & kTabPacked))
+    if (allows32(MAXKIND) && (tab->flags & kTabPacked))
         decode_warp_body_np2<kLutPacked32, Sink>(payload, dir, states, n, chunk_len, n_chunks,
                                                  n_lanes, tab, out, consumed, final_states,
                                                  status, trace, smem, sb);
-    else if (MAXKIND == kLutPacked64 && (tab->flags & kTabPacked64))
+    else if (allows64(MAXKIND) && (tab->flags & kTabPacked64))
         decode_warp_body_np2<kLutPacked64, Sink>(payload, dir, states, n, chunk_len, n_chunks,
                                                  n_lanes, tab, out, consumed, final_states,
                                                  status, trace, smem, sb);
@@ -959,7 +968,7 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
 static size_t decode_lut_bytes(int scale_bits, int kind) {
     const size_t m = size_t(1) << scale_bits;
     size_t b = kind == kLutPacked32 ? m * 4
-             : kind == kLutPacked64 ? m * 8
+             : kind == kLutPacked64 || kind == kLutPacked3264 ? m * 8
                                     : kMaxSym * sizeof(uint2) + (m < 16 ? 16 : m);
     return (b + 15) & ~size_t(15);
 }
@@ -995,9 +1004,10 @@ static cudaError_t launch_decode_warp(const uint16_t *d_payload, ChunkDir dir,
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
     // the packed form this launch allows (the device table's flags decide
     // whether it runs; its shared memory always fits the two-lookup form too)
-    const int maxkind = (packed && scale_bits <= kPackedMaxBits) ? kLutPacked32
-                      : (scale_bits >= kPacked64MinBits && scale_bits <= kPacked64MaxBits)
-                          ? kLutPacked64 : kLutGeneric;
+    const bool sb64 = scale_bits >= kPacked64MinBits && scale_bits <= kPacked64MaxBits;
+    const bool sb32 = packed && scale_bits <= kPackedMaxBits;
+    const int maxkind = sb32 && sb64 ? kLutPacked3264 : sb32 ? kLutPacked32
+                      : sb64 ? kLutPacked64 : kLutGeneric;
     size_t lut = decode_lut_bytes(scale_bits, kLutGeneric);
     if (decode_lut_bytes(scale_bits, maxkind) > lut) lut = decode_lut_bytes(scale_bits, maxkind);
     // One CTA per SM with that SM's share of the streams (up to 28 warps;
@@ -1031,6 +1041,9 @@ static cudaError_t launch_decode_warp(const uint16_t *d_payload, ChunkDir dir,
     if (maxkind == kLutPacked32) {
         if (np2) go(decode_warp_np2_kernel<kLutPacked32, Sink>);
         else go(decode_warp_kernel<kLutPacked32, Sink>);
+    } else if (maxkind == kLutPacked3264) {
+        if (np2) go(decode_warp_np2_kernel<kLutPacked3264, Sink>);
+        else go(decode_warp_kernel<kLutPacked3264, Sink>);
     } else if (maxkind == kLutPacked64) {
         if (np2) go(decode_warp_np2_kernel<kLutPacked64, Sink>);
         else go(decode_warp_kernel<kLutPacked64, Sink>);

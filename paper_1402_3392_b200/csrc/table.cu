@@ -262,9 +262,11 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         s_cur = lo;
     }
     if (!slot_in && (per & 3u) == 0 && scale_bits <= kPackedMaxBits) {
-        // common case (model from counts / frequencies, sb <= 12, >= 4 slots
-        // per thread): four slots per step, 16-byte packed and 4-byte symbol
-        // stores
+        // common case (model from counts / frequencies, >= 4 slots per
+        // thread): four slots per step, 16-byte packed and 4-byte symbol
+        // stores (and the 64-bit entries for 13 <= sb <= 14, the fallback
+        // when some f >= 4096 does not fit the 32-bit entry)
+        const bool p64 = scale_bits >= kPacked64MinBits && scale_bits <= kPacked64MaxBits;
         for (uint32_t j = j0; j < j1; j += 4) {
             uint32_t e[4], sy = 0;
 #pragma unroll
@@ -277,6 +279,7 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
                 if (f < 1 || f > 4095 || bias >= 4096) ok = 0;
                 e[q] = sym | (bias & 0xFFFu) << 8 | (f & 0xFFFu) << 20;
                 sy |= sym << (8 * q);
+                if (p64) t->packed64[jj] = make_uint2(sym | bias << 8, f);
             }
             *reinterpret_cast<uint4 *>(t->packed + j) = make_uint4(e[0], e[1], e[2], e[3]);
             *reinterpret_cast<uint32_t *>(t->slot_sym + j) = sy;
@@ -294,8 +297,8 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
             if (scale_bits <= kPackedMaxBits) {
                 const uint32_t f = freq[s];
                 const uint32_t bias = j - cum[s];
-                // f == 4096 (a single-symbol sb=12 table) does not fit 12
-                // bits: such tables take the two-lookup path
+                // f >= 4096 (e.g. a single-symbol sb=12 table) does not fit
+                // 12 bits: such tables take the 64-bit or two-lookup path
                 if (f < 1 || f > 4095 || bias >= 4096) ok = 0;
                 t->packed[j] = s | (bias & 0xFFFu) << 8 | (f & 0xFFFu) << 20;
             }
