@@ -822,6 +822,8 @@ def run_b200(a):
                                     "source": "ncu smsp__inst_executed.sum / live kernel time"}
 
     out["fused_consumer"] = fused_consumer(codec, d_out, n, dev)
+    if rank == 0 and world == 1 and a.scale_bits != 14:
+        out["sb14"] = other_precision(a, dev, d_msg, n, 14)
 
     if not a.no_e2e:
         out["e2e"] = e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes)
@@ -843,6 +845,60 @@ def run_b200(a):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out))
+
+
+def other_precision(a, dev, d_msg, n, sb, steps=10):
+    """The same device-resident step at another probability precision
+    (sb = 14 is the reference's default, rans.py:131-133 / CLI
+    --scale-bits 14): step, encode and decode times on the same input."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import DeviceCodec, n_chunks_for
+
+    codec = DeviceCodec(n, a.chunk, a.lanes, sb, dev)
+    d_out = torch.empty(n, dtype=torch.uint8, device=dev)
+    k = n_chunks_for(n, a.chunk)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(m=None):
+        if m: m[0].record(stream)
+        codec.histogram(d_msg, n)
+        codec.build_table_from_counts()
+        if m: m[1].record(stream)
+        codec.encode(d_msg, n, frame=False)
+        if m: m[2].record(stream)
+        codec.directory(n)
+        if m: m[3].record(stream)
+        codec.decode_slots(d_out, n)
+        if m: m[4].record(stream)
+
+    codec.reset_status()
+    step()
+    codec.check_status()
+    torch.cuda.synchronize(dev)
+    if not torch.equal(d_out, d_msg[:n]):
+        raise SystemExit(f"sb={sb} round-trip mismatch")
+    for _ in range(3):
+        step()
+    marks = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(steps)]
+    for m in marks:
+        step(m)
+    torch.cuda.synchronize(dev)
+    ph = np.array([[m[j].elapsed_time(m[j + 1]) for j in range(4)] for m in marks]).mean(0)
+    ms = float(np.mean([m[0].elapsed_time(m[4]) for m in marks]))
+    words = int(codec.offsets[k])
+    hbm, _ = hbm_peak()
+    dec_bytes = 2 * words + 4 * a.lanes * k + n
+    enc_bytes = n + 2 * words + 4 * a.lanes * k
+    flags = int(codec.table.view(torch.int32)[3].item())
+    return {"scale_bits": sb, "ms_per_step_eager": ms, "GBps": n / (ms * 1e-3) / 1e9,
+            "model_ms": ph[0], "encode_kernel_ms": ph[1], "decode_ms": ph[3],
+            "decode_GBps": n / (ph[3] * 1e-3) / 1e9, "encode_GBps": n / (ph[1] * 1e-3) / 1e9,
+            "decode_roofline_frac": dec_bytes / (ph[3] * 1e-3) / 1e9 / hbm,
+            "encode_roofline_frac": enc_bytes / (ph[1] * 1e-3) / 1e9 / hbm,
+            "decode_lut": "packed32" if flags & 1 else "packed64" if flags & 4 else "two-lookup",
+            "encode_record": "fast12" if flags & 8 else "fast" if flags & 2 else "generic",
+            "payload_bits_per_byte": 16 * words / n}
 
 
 def sweep(a, dev):

@@ -64,6 +64,88 @@ __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<uint16_t>(v)));
 }
 
+// One group's spill step in PTX: the spill predicate feeds the ballot and
+// the predicated store / shift directly (as C++ the compiler computed it
+// twice and moved the shifted state through a temporary), and the store
+// address is computed unconditionally (predicated temporaries cost SELs).
+//   TEST 0 (EncFast):   spill = (~x | (2^t - 1)) < Z   (carry of (x & ~(2^t-1)) + Z)
+//   TEST 1 (EncFast12): spill = (x | (2^t - 1)) >= Y
+// ON: lanes with on == 0 never spill (N < 32). topb is the ring byte cursor
+// (decremented by two per spilled word); the spilled lanes store their low
+// 16 bits at topb_new + 2 * (spilling lanes below them), ring-wrapped.
+template <int TEST, bool ON>
+__device__ __forceinline__ void spill_group(uint32_t &x, uint32_t &topb, uint32_t lowm,
+                                            uint32_t key, uint32_t on, uint32_t lt_mul,
+                                            uint32_t ring_addr, uint32_t neg2, uint32_t two) {
+    static_assert(kOutRingBytes == 2048, "ring mask below");
+    if (TEST == 0 && !ON)
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t, mk, c, cl, ad;\n\t"
+            "lop3.b32 t, %0, %2, 0, 0xcf;\n\t"
+            "setp.lt.u32 p, t, %3;\n\t"
+            "vote.sync.ballot.b32 mk, p, 0xffffffff;\n\t"
+            "popc.b32 c, mk;\n\t"
+            "mad.lo.u32 %1, c, %6, %1;\n\t"
+            "mul.lo.u32 cl, mk, %4;\n\t"
+            "popc.b32 cl, cl;\n\t"
+            "mad.lo.u32 ad, cl, %7, %1;\n\t"
+            "lop3.b32 ad, ad, 0x7fe, %5, 0xea;\n\t"
+            "@p st.shared.u16 [ad], %0;\n\t"
+            "@p shr.b32 %0, %0, 16;\n\t}"
+            : "+r"(x), "+r"(topb)
+            : "r"(lowm), "r"(key), "r"(lt_mul), "r"(ring_addr), "r"(neg2), "r"(two)
+            : "memory");
+    else if (TEST == 0)
+        asm("{\n\t.reg .pred p, q;\n\t.reg .b32 t, mk, c, cl, ad;\n\t"
+            "lop3.b32 t, %0, %2, 0, 0xcf;\n\t"
+            "setp.ne.u32 q, %8, 0;\n\t"
+            "setp.lt.and.u32 p, t, %3, q;\n\t"
+            "vote.sync.ballot.b32 mk, p, 0xffffffff;\n\t"
+            "popc.b32 c, mk;\n\t"
+            "mad.lo.u32 %1, c, %6, %1;\n\t"
+            "mul.lo.u32 cl, mk, %4;\n\t"
+            "popc.b32 cl, cl;\n\t"
+            "mad.lo.u32 ad, cl, %7, %1;\n\t"
+            "lop3.b32 ad, ad, 0x7fe, %5, 0xea;\n\t"
+            "@p st.shared.u16 [ad], %0;\n\t"
+            "@p shr.b32 %0, %0, 16;\n\t}"
+            : "+r"(x), "+r"(topb)
+            : "r"(lowm), "r"(key), "r"(lt_mul), "r"(ring_addr), "r"(neg2), "r"(two), "r"(on)
+            : "memory");
+    else if (!ON)
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t, mk, c, cl, ad;\n\t"
+            "or.b32 t, %0, %2;\n\t"
+            "setp.ge.u32 p, t, %3;\n\t"
+            "vote.sync.ballot.b32 mk, p, 0xffffffff;\n\t"
+            "popc.b32 c, mk;\n\t"
+            "mad.lo.u32 %1, c, %6, %1;\n\t"
+            "mul.lo.u32 cl, mk, %4;\n\t"
+            "popc.b32 cl, cl;\n\t"
+            "mad.lo.u32 ad, cl, %7, %1;\n\t"
+            "lop3.b32 ad, ad, 0x7fe, %5, 0xea;\n\t"
+            "@p st.shared.u16 [ad], %0;\n\t"
+            "@p shr.b32 %0, %0, 16;\n\t}"
+            : "+r"(x), "+r"(topb)
+            : "r"(lowm), "r"(key), "r"(lt_mul), "r"(ring_addr), "r"(neg2), "r"(two)
+            : "memory");
+    else
+        asm("{\n\t.reg .pred p, q;\n\t.reg .b32 t, mk, c, cl, ad;\n\t"
+            "or.b32 t, %0, %2;\n\t"
+            "setp.ne.u32 q, %8, 0;\n\t"
+            "setp.ge.and.u32 p, t, %3, q;\n\t"
+            "vote.sync.ballot.b32 mk, p, 0xffffffff;\n\t"
+            "popc.b32 c, mk;\n\t"
+            "mad.lo.u32 %1, c, %6, %1;\n\t"
+            "mul.lo.u32 cl, mk, %4;\n\t"
+            "popc.b32 cl, cl;\n\t"
+            "mad.lo.u32 ad, cl, %7, %1;\n\t"
+            "lop3.b32 ad, ad, 0x7fe, %5, 0xea;\n\t"
+            "@p st.shared.u16 [ad], %0;\n\t"
+            "@p shr.b32 %0, %0, 16;\n\t}"
+            : "+r"(x), "+r"(topb)
+            : "r"(lowm), "r"(key), "r"(lt_mul), "r"(ring_addr), "r"(neg2), "r"(two), "r"(on)
+            : "memory");
+}
+
 // Spilled words are staged in a per-warp shared ring (2 KB aligned, so an
 // address is base | (byte_offset & mask)) indexed by their final scratch
 // position w & 1023, and written to HBM as aligned 16-byte blocks. `flushed`
@@ -153,6 +235,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     const uint32_t lt_mul = lane ? 1u << (32 - lane) : 0u;
     uint32_t two;  // opaque 2: keeps the cursor arithmetic as IMADs
     asm volatile("mov.u32 %0, 2;" : "=r"(two));
+    const uint32_t neg2 = 0u - two;
     const int wib = threadIdx.x >> 5;
     uint8_t *ring = rings + wib * kInRing;
     const uint32_t oraw = smem_addr(oring_raw);
@@ -267,22 +350,15 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         if (j < 15 || gb > 15) sym_n = *bp;
                         const uint2 a = encf[sym];
                         macc &= a.x;
-                        bool spill;
                         uint32_t z = 0;
                         if (!F12) {
-                            const uint32_t xm = x & ~lowm;
-                            spill = on && xm + a.y < xm;
+                            spill_group<0, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr,
+                                                 neg2, two);
                         } else {
                             z = encz[sym];
-                            spill = on && (x | lowm) >= a.y;
+                            spill_group<1, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr,
+                                                 neg2, two);
                         }
-                        const uint32_t mk = __ballot_sync(0xffffffffu, spill);
-                        topb -= two * __popc(mk);
-                        if (spill)
-                            sts16(oring_addr |
-                                      ((topb + two * __popc(mk * lt_mul)) & (kOutRingBytes - 2)),
-                                  x);
-                        x = spill ? x >> 16 : x;
                         uint32_t q = __umulhi(x, a.x);
                         if (!F12) {
                             asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
@@ -308,14 +384,8 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         if (gg > 1) sym_n = blk[(gg - 2) * 32 + lane];
                     }
                     macc &= a.x;
-                    const uint32_t xm = x & ~lowm;
-                    const bool spill = xm + a.y < xm;  // carry out of (x & ~(2^t-1)) + Z
-                    const uint32_t mk = __ballot_sync(0xffffffffu, spill);
-                    topb -= two * __popc(mk);
-                    if (spill)
-                        sts16(oring_addr | ((topb + two * __popc(mk * lt_mul)) & (kOutRingBytes - 2)),
-                              x);
-                    x = spill ? x >> 16 : x;
+                    // spill iff carry out of (x & ~(2^t-1)) + Z
+                    spill_group<0, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2, two);
                     uint32_t q = __umulhi(x, a.x);
                     asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
                     x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
@@ -335,13 +405,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         if (gg > 1) sym_n = blk[(gg - 2) * 32 + lane];
                     }
                     macc &= a.x;
-                    const bool spill = (x | lowm) >= a.y;
-                    const uint32_t mk = __ballot_sync(0xffffffffu, spill);
-                    topb -= two * __popc(mk);
-                    if (spill)
-                        sts16(oring_addr | ((topb + two * __popc(mk * lt_mul)) & (kOutRingBytes - 2)),
-                              x);
-                    x = spill ? x >> 16 : x;
+                    spill_group<1, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2, two);
                     uint32_t q = __umulhi(x, a.x);
                     asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
                     x = q * (a.y & lowm) + (x + (z >> 17));
@@ -406,21 +470,15 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                     if (j + 1 < G) sym_n = ring[ri & (kInRing - 1)];
                     const uint2 a = encf[sym];
                     macc &= a.x;
-                    bool spill;
                     uint32_t z = 0;
                     if (!F12) {
-                        const uint32_t xm = x & ~lowm;
-                        spill = on && xm + a.y < xm;
+                        spill_group<0, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr, neg2,
+                                             two);
                     } else {
                         z = encz[sym];
-                        spill = on && (x | lowm) >= a.y;
+                        spill_group<1, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr, neg2,
+                                             two);
                     }
-                    const uint32_t mk = __ballot_sync(0xffffffffu, spill);
-                    topb -= two * __popc(mk);
-                    if (spill)
-                        sts16(oring_addr | ((topb + two * __popc(mk * lt_mul)) & (kOutRingBytes - 2)),
-                              x);
-                    x = spill ? x >> 16 : x;
                     uint32_t q = __umulhi(x, a.x);
                     if (!F12) {
                         asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
