@@ -227,6 +227,17 @@ int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
                             int32_t n_lanes, const void *d_table, int32_t scale_bits,
                             uint16_t *d_scratch, uint32_t *d_chunk_words, uint32_t *d_states,
                             void *d_status, void *stream);
+/* As ilans_encode_chunks_dev, for a table quantized on the device from this
+ * very message's histogram (ilans_histogram_u8_dev -> ilans_table_from_counts_dev,
+ * also after a histogram all-reduce over shards of one message): every
+ * symbol of the message then has f >= 1 (rans.py:197-199), so the kernel
+ * skips its per-symbol zero-frequency check. With any other table the
+ * result is undefined for symbols of frequency 0 -- use
+ * ilans_encode_chunks_dev, which reports them. */
+int ilans_encode_chunks_covered_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
+                                    int32_t n_lanes, const void *d_table, int32_t scale_bits,
+                                    uint16_t *d_scratch, uint32_t *d_chunk_words,
+                                    uint32_t *d_states, void *d_status, void *stream);
 /* Framing: d_word_offsets[0..n_chunks] = exclusive prefix sum of chunk
  * words, and the chunk payloads packed back to back into d_payload
  * (capacity n words) at those offsets. carry_in != 0 continues a previous

@@ -116,6 +116,8 @@ PROTOTYPES = [
     ("ilans_dstatus_parse", ctypes.c_int, [_vp, _st]),
     ("ilans_encode_chunks_dev", ctypes.c_int,
      [_vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),
+    ("ilans_encode_chunks_covered_dev", ctypes.c_int,
+     [_vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),
     ("ilans_frame_chunks_dev", ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
     ("ilans_decode_chunks_dev", ctypes.c_int,
      [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),

@@ -194,6 +194,7 @@ class DeviceCodec:
     # -- model ------------------------------------------------------------
     def histogram(self, d_msg, n: int, accumulate: bool = False):
         """counts[b] (+)= #{i < n : d_msg[i] == b} (int64 view of u64)."""
+        self._counts_of = None if accumulate else (self._p(d_msg), int(n))
         s = self._s()
         if not accumulate:
             _lib.check_dev(_lib.lib.ilans_counts_zero_dev(self._p(self.counts), s), "counts_zero")
@@ -202,6 +203,9 @@ class DeviceCodec:
         return self.counts
 
     def build_table_from_counts(self):
+        # a model quantized from a message's own histogram gives every byte
+        # of that message f >= 1: its encode may skip the zero-frequency check
+        self._covers = getattr(self, "_counts_of", None)
         _lib.check_dev(_lib.lib.ilans_table_from_counts_dev(
             self._p(self.counts), self.scale_bits, self._p(self.table), self._s()), "table")
 
@@ -209,6 +213,7 @@ class DeviceCodec:
         torch = _torch()
         if table.scale_bits != self.scale_bits:
             raise ValueError("table scale_bits differs from the codec's")
+        self._covers = None
         f = torch.from_numpy(table.freq_u32.view(np.int32).copy()).to(self.device,
                                                                       non_blocking=False)
         self._freq_keepalive = f
@@ -253,7 +258,8 @@ class DeviceCodec:
         """Encode n bytes at d_msg with the current table: one launch for all
         chunks, then (frame=True) the offset scan + payload compaction."""
         k = n_chunks_for(n, self.chunk_len)
-        self.encode_range(self._p(d_msg), n, 0, k)
+        covered = getattr(self, "_covers", None) == (self._p(d_msg), int(n))
+        self.encode_range(self._p(d_msg), n, 0, k, covered=covered)
         if frame:
             self.frame_range(n, 0, k, self._p(self.payload))
 
@@ -264,12 +270,16 @@ class DeviceCodec:
         lo = k0 * self.chunk_len
         return lo, min(n, k1 * self.chunk_len) - lo
 
-    def encode_range(self, msg_ptr: int, n: int, k0: int, k1: int):
-        """Encode chunks [k0, k1) of the n-byte message starting at msg_ptr."""
+    def encode_range(self, msg_ptr: int, n: int, k0: int, k1: int, covered: bool = False):
+        """Encode chunks [k0, k1) of the n-byte message starting at msg_ptr.
+        covered=True: the current table was quantized from this message's
+        own histogram (every byte has f >= 1), so the per-symbol
+        zero-frequency check is skipped."""
         lo, nb = self._range(n, k0, k1)
         if nb <= 0:
             return
-        _lib.check_dev(_lib.lib.ilans_encode_chunks_dev(
+        fn = _lib.lib.ilans_encode_chunks_covered_dev if covered else _lib.lib.ilans_encode_chunks_dev
+        _lib.check_dev(fn(
             msg_ptr + lo, nb, self.chunk_len, self.lane_count, self._p(self.table),
             self.scale_bits, self._p(self.scratch) + 2 * lo, self._p(self.chunk_words) + 4 * k0,
             self._p(self.states) + 4 * k0 * self.lane_count, self._p(self.status), self._s()),
@@ -809,7 +819,7 @@ class HostCodec:
         # sequential work, so splitting it would only serialise), then per
         # batch: pack into HBM + copy its word offsets out; as soon as a
         # batch's offsets are on the host its payload D2H is issued.
-        c.encode_range(p_msg, n, 0, k)
+        c.encode_range(p_msg, n, 0, k, covered=True)  # model from this message's histogram
         self._mark("enc.kernel.end", slot.s_comp)
         if k == 0:
             c.frame_range(n, 0, 0, c.payload.data_ptr())

@@ -1056,18 +1056,36 @@ extern "C" int ilans_dstatus_parse(const void *h_status, ilans_status *st) {
     return ILANS_OK;
 }
 
-extern "C" int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
-                                       int32_t n_lanes, const void *d_table, int32_t scale_bits,
-                                       uint16_t *d_scratch, uint32_t *d_chunk_words,
-                                       uint32_t *d_states, void *d_status, void *stream) {
+static int encode_chunks(const uint8_t *d_msg, int64_t n, int64_t chunk_len, int32_t n_lanes,
+                         const void *d_table, int32_t scale_bits, uint16_t *d_scratch,
+                         uint32_t *d_chunk_words, uint32_t *d_states, void *d_status,
+                         void *stream, bool covered) {
     if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
     if (scale_bits < 1 || scale_bits > kMaxScaleBits) return ILANS_ERR_VALUE;
     if (reinterpret_cast<uintptr_t>(d_msg) & 15) return ILANS_ERR_VALUE;
     return launch_encode(d_msg, n, chunk_len, n_lanes, static_cast<const TableDev *>(d_table),
                          scale_bits, d_scratch, d_chunk_words, d_states,
-                         static_cast<DStatus *>(d_status), nullptr, ST(stream)) == cudaSuccess
+                         static_cast<DStatus *>(d_status), nullptr, ST(stream), false,
+                         covered) == cudaSuccess
                ? ILANS_OK
                : ILANS_ERR_CUDA;
+}
+
+extern "C" int ilans_encode_chunks_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,
+                                       int32_t n_lanes, const void *d_table, int32_t scale_bits,
+                                       uint16_t *d_scratch, uint32_t *d_chunk_words,
+                                       uint32_t *d_states, void *d_status, void *stream) {
+    return encode_chunks(d_msg, n, chunk_len, n_lanes, d_table, scale_bits, d_scratch,
+                         d_chunk_words, d_states, d_status, stream, false);
+}
+
+extern "C" int ilans_encode_chunks_covered_dev(const uint8_t *d_msg, int64_t n,
+                                               int64_t chunk_len, int32_t n_lanes,
+                                               const void *d_table, int32_t scale_bits,
+                                               uint16_t *d_scratch, uint32_t *d_chunk_words,
+                                               uint32_t *d_states, void *d_status, void *stream) {
+    return encode_chunks(d_msg, n, chunk_len, n_lanes, d_table, scale_bits, d_scratch,
+                         d_chunk_words, d_states, d_status, stream, true);
 }
 
 extern "C" int ilans_frame_chunks_dev(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,

@@ -204,7 +204,10 @@ struct SpillStage {
 // MODE 0: N = 32; 1: power-of-two N < 32 (512/N-group batches with the
 // fast records); 2: other N < 32 (floor(256/N)-group batches with the fast
 // records). Separate instantiations so the N = 32 loops keep their schedule.
-template <typename Idx, bool F12, int MODE>
+// COVERED: the table was quantized from this message's own histogram, so
+// every symbol in it has f >= 1 (rans.py:197-199) and the fast loops skip
+// the per-group zero-frequency check (the AND of every record's M).
+template <typename Idx, bool F12, int MODE, bool COVERED = false>
 __global__ void __launch_bounds__(kEncMaxWarps * 32, 1)
 encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
@@ -319,7 +322,8 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         uint32_t macc = ~0u;
         for (Idx b = full - 1; !bad && b >= 0; --b) {
             if (b - 3 < issued_lo) {  // segments below `full` are whole 512-byte blocks
-                __syncwarp();
+                // (no __syncwarp: every lane's reads of this slot -- segment
+                // b + 1 -- were consumed before the previous batch's ballots)
                 const Idx sg = b - 3;
                 if (sg >= 0)
                     cp_async16(ring + (static_cast<uint32_t>(sg) & 3u) * kInSeg + lane * 16,
@@ -349,7 +353,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         const uint32_t sym = sym_n;
                         if (j < 15 || gb > 15) sym_n = *bp;
                         const uint2 a = encf[sym];
-                        macc &= a.x;
+                        if (!COVERED) macc &= a.x;
                         uint32_t z = 0;
                         if (!F12) {
                             spill_group<0, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr,
@@ -383,7 +387,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         a_n = encf[sym_n];
                         if (gg > 1) sym_n = blk[(gg - 2) * 32 + lane];
                     }
-                    macc &= a.x;
+                    if (!COVERED) macc &= a.x;
                     // spill iff carry out of (x & ~(2^t-1)) + Z
                     spill_group<0, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2, two);
                     uint32_t q = __umulhi(x, a.x);
@@ -404,7 +408,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         z_n = encz[sym_n];
                         if (gg > 1) sym_n = blk[(gg - 2) * 32 + lane];
                     }
-                    macc &= a.x;
+                    if (!COVERED) macc &= a.x;
                     spill_group<1, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2, two);
                     uint32_t q = __umulhi(x, a.x);
                     asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
@@ -469,7 +473,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                     ri -= n_lanes;
                     if (j + 1 < G) sym_n = ring[ri & (kInRing - 1)];
                     const uint2 a = encf[sym];
-                    macc &= a.x;
+                    if (!COVERED) macc &= a.x;
                     uint32_t z = 0;
                     if (!F12) {
                         spill_group<0, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr, neg2,
@@ -688,7 +692,7 @@ encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
 cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, int n_lanes,
                           const TableDev *d_table, int scale_bits, uint16_t *d_scratch,
                           uint32_t *d_chunk_words, uint32_t *d_states, DStatus *d_status,
-                          uint32_t *d_lane_ws, cudaStream_t stream, bool stats) {
+                          uint32_t *d_lane_ws, cudaStream_t stream, bool stats, bool covered) {
     if (n <= 0) return cudaSuccess;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
     // stats (instrumented calls): the one-warp sub-group walk measures the
@@ -738,6 +742,9 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
             } else if (mode == 2) {
                 if (sb14) go(encode_warp_kernel<I, true, 2>);
                 else go(encode_warp_kernel<I, false, 2>);
+            } else if (covered && sizeof(I) == 4) {
+                if (sb14) go(encode_warp_kernel<int, true, 0, true>);
+                else go(encode_warp_kernel<int, false, 0, true>);
             } else {
                 if (sb14) go(encode_warp_kernel<I, true, 0>);
                 else go(encode_warp_kernel<I, false, 0>);

@@ -29,7 +29,8 @@ cudaError_t smem_limit(const void *kernel, int bytes);
 cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, int n_lanes,
                           const TableDev *d_table, int scale_bits, uint16_t *d_scratch,
                           uint32_t *d_chunk_words, uint32_t *d_states, DStatus *d_status,
-                          uint32_t *d_lane_ws, cudaStream_t stream, bool stats = false);
+                          uint32_t *d_lane_ws, cudaStream_t stream, bool stats = false,
+                          bool covered = false);
 cudaError_t launch_frame(const uint16_t *d_scratch, int64_t n, int64_t chunk_len,
                          const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
                          uint16_t *d_payload, int carry_in, cudaStream_t stream);
