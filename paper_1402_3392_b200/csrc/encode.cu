@@ -181,11 +181,17 @@ struct SpillStage {
     __device__ __forceinline__ void drain(Idx top, int lane) {
         while (flushed - top >= 512) {
             __syncwarp();
-            const Idx blk = flushed - 512 + Idx(lane) * 8;
-            const uint4 lo = *reinterpret_cast<const uint4 *>(ring + (blk & (kOutRing - 1)));
-            const uint4 hi = *reinterpret_cast<const uint4 *>(ring + ((blk + 256) & (kOutRing - 1)));
-            *reinterpret_cast<uint4 *>(out + blk) = lo;
-            *reinterpret_cast<uint4 *>(out + blk + 256) = hi;
+            const uint32_t wb = (static_cast<uint32_t>(flushed) - 512u + lane * 8u) << 1;
+            uint4 lo, hi;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w)
+                         : "r"(ring_addr | (wb & (kOutRingBytes - 1))));
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                         : "r"(ring_addr | ((wb + 512u) & (kOutRingBytes - 1))));
+            uint16_t *d = out + (flushed - 512) + lane * 8;
+            *reinterpret_cast<uint4 *>(d) = lo;
+            *reinterpret_cast<uint4 *>(d + 256) = hi;
             flushed -= 512;
         }
     }
@@ -320,14 +326,21 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         // fast records: AND of every record's M over the whole fast region;
         // bit 31 clears iff some symbol had f = 0 (checked once, after it)
         uint32_t macc = ~0u;
+        // next segment to issue (issued_lo - 1): running source pointer and
+        // the lane's 32-bit shared slot address (no per-batch conversions)
+        const uint8_t *seg_src = g + (issued_lo - 1) * kInSeg + lane * 16;
+        const uint32_t ring_sa = smem_addr(ring) + lane * 16;
         for (Idx b = full - 1; !bad && b >= 0; --b) {
             if (b - 3 < issued_lo) {  // segments below `full` are whole 512-byte blocks
                 // (no __syncwarp: every lane's reads of this slot -- segment
-                // b + 1 -- were consumed before the previous batch's ballots)
+                // b + 1 -- were consumed before the previous batch's ballots;
+                // below segment 0 the copy reads nothing and zero-fills)
                 const Idx sg = b - 3;
-                if (sg >= 0)
-                    cp_async16(ring + (static_cast<uint32_t>(sg) & 3u) * kInSeg + lane * 16,
-                               g + sg * kInSeg + lane * 16, 16u);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                                 ring_sa + ((static_cast<uint32_t>(sg) & 3u) << 9)),
+                             "l"(sg >= 0 ? seg_src : g), "r"(sg >= 0 ? 16u : 0u)
+                             : "memory");
+                seg_src -= kInSeg;
                 cp_async_commit();
                 issued_lo = sg;
             }
