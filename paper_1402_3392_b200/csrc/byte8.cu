@@ -29,9 +29,9 @@ __device__ __forceinline__ uint32_t refills_for(uint32_t x) {  // x >= 1
     return (x < (1u << 23)) + (x < (1u << 15)) + (x < (1u << 7));
 }
 
-// One warp per stream, N <= 32 lanes; payload / message read straight from
-// global memory (the byte8 path is the reference's CPU config, not the
-// throughput path, so no staging rings).
+// Traced single-stream decode (interleave.decode_interleaved_steps for byte8):
+// one warp, N <= 32 lanes, payload read straight from global memory; the
+// untraced calls run the staged kernels below.
 __global__ void __launch_bounds__(256)
 decode_u8_warp_kernel(const uint8_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                       const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -125,39 +125,304 @@ decode_u8_warp_kernel(const uint8_t *__restrict__ payload, const uint64_t *__res
     }
 }
 
-// Backward encode, one warp per stream, N <= 32. Spilled digits go to the
-// stream's scratch (capacity 3 bytes per symbol) growing downwards from len*3.
-__global__ void __launch_bounds__(256)
-encode_u8_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
+// ---------------------------------------------------------------------------
+// Staged byte8 coders (N <= 32): the word16 kernels' structure with byte
+// digits. One CTA per SM holds all of the SM's streams (<= 28 warps, one
+// warp per chunk); the payload (decode) / message (encode) stream through a
+// per-warp 2 KB shared ring filled by cp.async, the slot LUT and records sit
+// in shared memory, the decoded bytes leave through a per-warp 512-byte
+// staging buffer as 16-byte stores, and the spilled digits drain from a
+// per-warp 2 KB ring as aligned 16-byte blocks. Digit order and counts are
+// the two-ballot exclusive prefix above.
+// ---------------------------------------------------------------------------
+constexpr int kSeg8 = 512;                 // ring segment (bytes)
+constexpr int kRing8 = 4 * kSeg8;          // per-warp ring
+constexpr int kObuf8 = 512;                // decoded-byte staging per warp
+constexpr int kMaxWarps8 = 28;
+constexpr int64_t kRingMaxChunk8 = int64_t(1) << 29;  // 32-bit chunk cursors (3 len < 2^31)
+
+__device__ __forceinline__ void issue_seg8(uint32_t ring_sa, const uint8_t *gbase, uint64_t avail,
+                                           uint64_t seg, int lane) {
+    const uint64_t b0 = seg * kSeg8 + lane * 16;
+    uint32_t bytes = 0;
+    if (avail > b0) bytes = (avail - b0) >= 16 ? 16u : static_cast<uint32_t>(avail - b0);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                     ring_sa + static_cast<uint32_t>(seg & 3u) * kSeg8 + lane * 16),
+                 "l"(bytes ? gbase + b0 : gbase), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"(static_cast<uint16_t>(v)) : "memory");
+}
+
+// PACKED: the 32-bit slot entries sym | bias << 8 | f << 20 (every f < 4096;
+// table flag kTabPacked), else the two lookups slot -> symbol -> {f, cum}.
+template <bool PACKED>
+__device__ __noinline__ void
+decode_u8_ring_body(const uint8_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
+                    const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                    uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
+                    DStatus *__restrict__ status, uint8_t *sm8) {
+    const int nw = blockDim.x >> 5;
+    const int sb = static_cast<int>(tab->scale_bits);
+    const uint32_t m = 1u << sb, mask = m - 1u;
+    uint8_t *lut = sm8 + nw * (kRing8 + kObuf8);
+    if (PACKED) {
+        uint32_t *p = reinterpret_cast<uint32_t *>(lut);
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) p[i] = tab->packed[i];
+    } else {
+        uint2 *d = reinterpret_cast<uint2 *>(lut);
+        for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) d[i] = tab->dec[i];
+        uint8_t *ss = lut + kMaxSym * sizeof(uint2);
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) ss[i] = tab->slot_sym[i];
+    }
+    __syncthreads();
+    const uint32_t lut_sa = smem_addr(lut);
+    const uint2 *dec = reinterpret_cast<const uint2 *>(lut);
+    const uint8_t *slot_sym = lut + kMaxSym * sizeof(uint2);
+    const uint32_t *packed = reinterpret_cast<const uint32_t *>(lut);
+    (void)lut_sa;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const uint32_t lt = lanemask_lt();
+    const uint32_t ring_sa = smem_addr(sm8 + wib * kRing8);
+    uint8_t *obuf = sm8 + nw * kRing8 + wib * kObuf8;
+    int64_t nwk = (n_chunks + gridDim.x - 1) / gridDim.x;
+    if (nwk > nw) nwk = nw;
+    if (wib >= nwk) return;
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nwk;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * nwk + wib; k < n_chunks;
+         k += warps_total) {
+        const int64_t cbase = k * chunk_len;
+        const uint32_t len = static_cast<uint32_t>((n - cbase) < chunk_len ? (n - cbase) : chunk_len);
+        const uint64_t off = offsets[k];
+        const uint32_t plen = static_cast<uint32_t>(offsets[k + 1] - off);  // <= 3 len < 2^31
+        const uint32_t delta = static_cast<uint32_t>(off & 15u);
+        const uint8_t *gbase = payload + (off - delta);
+        const uint64_t avail = uint64_t(plen) + delta;
+        uint8_t *outk = out + cbase;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            issue_seg8(ring_sa, gbase, avail, q, lane);
+            cp_async_commit();
+        }
+        cp_async_wait<2>();
+        __syncwarp();
+        uint32_t x = lane < n_lanes ? states[k * n_lanes + lane] : 0u;
+        uint32_t pos = delta;  // byte cursor from gbase
+        uint32_t cur = 0;      // ring segment holding the cursor
+        const uint32_t pend = plen + delta;  // cursor limit
+        int err = 0;
+        uint32_t most = 0;
+        uint32_t base = 0;
+        const uint32_t obuf_sa = smem_addr(obuf);
+        for (; base < len; base += n_lanes) {
+            const uint32_t left = len - base;
+            const bool on = static_cast<uint32_t>(lane) < left && lane < n_lanes;
+            uint32_t s = 0;
+            if (on) {
+                const uint32_t slot = x & mask;
+                if (PACKED) {
+                    const uint32_t e = packed[slot];
+                    x = (e >> 20) * ((x >> sb) - 4096u) + (e >> 8);
+                    s = e;
+                } else {
+                    s = slot_sym[slot];
+                    const uint2 d = dec[s];
+                    x = d.x * (x >> sb) + slot - d.y;
+                }
+            }
+            if (__any_sync(0xffffffffu, on && x == 0u)) {
+                // byte-dependent refills (corrupt input): lane by lane
+                const int active = left < static_cast<uint32_t>(n_lanes) ? int(left) : n_lanes;
+                for (int l = 0; l < active && !err; ++l) {
+                    if (lane == l) {
+                        int r = 0;
+                        while (x < kLow8) {
+                            if (pos >= pend) { err = ILANS_ERR_TRUNCATED; break; }
+                            x = (x << 8) | lds8(ring_sa + (pos & (kRing8 - 1)));
+                            ++pos;
+                            if (++r > kRefillLimit8) { err = ILANS_ERR_FORMAT; break; }
+                        }
+                        most = max(most, static_cast<uint32_t>(r));
+                    }
+                    pos = __shfl_sync(0xffffffffu, pos, l);
+                    err = __shfl_sync(0xffffffffu, err, l);
+                }
+            } else {
+                const uint32_t r = on ? refills_for(x) : 0u;
+                const uint32_t b0 = __ballot_sync(0xffffffffu, r & 1u);
+                const uint32_t b1 = __ballot_sync(0xffffffffu, r & 2u);
+                const uint32_t q = pos + __popc(b0 & lt) + 2u * __popc(b1 & lt);
+                pos += __popc(b0) + 2u * __popc(b1);
+                if (pos > pend) {
+                    err = ILANS_ERR_TRUNCATED;
+                    pos -= __popc(b0) + 2u * __popc(b1);
+                } else {
+                    // r digits: 4 bytes from two ring words, byte-reversed
+                    const uint32_t w0 = lds32(ring_sa + (q & (kRing8 - 4)));
+                    const uint32_t w1 = lds32(ring_sa + ((q + 4u) & (kRing8 - 4)));
+                    const uint32_t v = __byte_perm(__funnelshift_r(w0, w1, (q & 3u) * 8u), 0u,
+                                                   0x0123u);
+                    if (r) x = (x << (8u * r)) | (v >> (32u - 8u * r));
+                    most = max(most, r);
+                }
+            }
+            if (err) break;
+            if (on) sts8(obuf_sa + ((base + lane) & (kObuf8 - 1)), s);
+            const uint32_t nb = base + n_lanes;
+            if ((nb >> 8) != (base >> 8)) {  // a 256-byte half is complete
+                __syncwarp();
+                const uint32_t blk = base >> 8;
+                const uint2 o = reinterpret_cast<const uint2 *>(obuf + (blk & 1) * 256)[lane];
+                *reinterpret_cast<uint2 *>(outk + (blk << 8) + 8 * lane) = o;
+                __syncwarp();
+            }
+            const uint32_t seg = pos >> 9;
+            if (seg != cur) {  // segments below the cursor are read: refill them
+                __syncwarp();
+                while (cur < seg) {
+                    ++cur;
+                    issue_seg8(ring_sa, gbase, avail, cur + 3, lane);
+                    cp_async_commit();
+                }
+                cp_async_wait<2>();
+                __syncwarp();
+            }
+        }
+        {  // bytes of the last partial 256-byte block
+            const uint32_t end = err ? base : len;
+            __syncwarp();
+            const uint32_t t0 = (end >> 8) << 8;
+            const uint8_t *half = obuf + ((end >> 8) & 1) * 256;
+            for (uint32_t i = t0 + lane; i < end; i += 32) outk[i] = half[i - t0];
+        }
+        most = __reduce_max_sync(0xffffffffu, most);
+        if (lane == 0) {
+            atomicMax(&status->max_digits, most);
+            if (err == ILANS_ERR_TRUNCATED)
+                atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
+            if (err == ILANS_ERR_FORMAT) status->value_error = ILANS_ERR_FORMAT;
+            if (consumed) consumed[k] = pos - delta;
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+    }
+}
+
+// the device table's flags pick the LUT form (shared memory is sized for the
+// larger of the two on the host)
+__global__ void __launch_bounds__(kMaxWarps8 * 32, 1)
+decode_u8_dispatch_kernel(const uint8_t *__restrict__ payload,
+                          const uint64_t *__restrict__ offsets,
+                          const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
+                          int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
+                          uint8_t *__restrict__ out, uint64_t *__restrict__ consumed,
+                          DStatus *__restrict__ status) {
+    extern __shared__ __align__(16) uint8_t sm8[];
+    if (tab->status != ILANS_OK) {
+        if (threadIdx.x == 0) status->value_error = 1;
+        return;
+    }
+    if (tab->flags & kTabPacked)
+        decode_u8_ring_body<true>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes, tab,
+                                  out, consumed, status, sm8);
+    else
+        decode_u8_ring_body<false>(payload, offsets, states, n, chunk_len, n_chunks, n_lanes, tab,
+                                   out, consumed, status, sm8);
+}
+
+// Backward encode: message segments through the ring (highest first), the
+// spilled digits through a 2 KB byte ring (positions in stack coordinates:
+// byte p of chunk k lands at scratch[3kC + p], the stack growing down from
+// 3 len_k), drained as aligned 16-byte blocks while 512 or more are pending.
+__global__ void __launch_bounds__(kMaxWarps8 * 32, 1)
+encode_u8_ring_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
                       int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
                       uint8_t *__restrict__ scratch, uint32_t *__restrict__ chunk_bytes,
                       uint32_t *__restrict__ states_out, DStatus *__restrict__ status) {
-    __shared__ uint2 enc[kMaxSym];
+    extern __shared__ __align__(16) uint8_t sm8[];
+    const int nw = blockDim.x >> 5;
+    uint2 *enc = reinterpret_cast<uint2 *>(sm8);
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
     __syncthreads();
     const EncCtx ctx(tab->scale_bits);
     const uint32_t thr8 = 31u - tab->scale_bits;  // spill while x >= f << (31 - sb)
     const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
     const uint32_t lt = lanemask_lt();
-    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-         k < n_chunks; k += warps_total) {
+    // [enc 2 KB][W message rings][pad to 2 KB][W spill rings, 2 KB aligned]
+    const uint32_t in_sa = smem_addr(sm8 + kMaxSym * sizeof(uint2) + wib * kRing8);
+    const uint32_t raw = smem_addr(sm8 + kMaxSym * sizeof(uint2) + nw * kRing8);
+    const uint32_t out_sa = ((raw + kRing8 - 1) & ~uint32_t(kRing8 - 1)) + wib * kRing8;
+    const uint8_t *out_ring = sm8 + (out_sa - smem_addr(sm8));
+    int64_t nwk = (n_chunks + gridDim.x - 1) / gridDim.x;
+    if (nwk > nw) nwk = nw;
+    if (wib >= nwk) return;
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * nwk;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * nwk + wib; k < n_chunks;
+         k += warps_total) {
+        // chunk-local cursors in 32 bits (chunks < 2^29 bytes: 3 len < 2^31)
         const int64_t cbase = k * chunk_len;
-        const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
+        const int len = static_cast<int>((n - cbase) < chunk_len ? (n - cbase) : chunk_len);
         const uint8_t *g = msg + cbase;
         uint8_t *o = scratch + 3 * cbase;
+        int cur = (len - 1) >> 9;  // segment holding the current group's top byte
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int sg = cur - q;
+            const int b0 = sg * kSeg8 + lane * 16;
+            uint32_t bytes = 0;
+            if (sg >= 0 && b0 < len) bytes = (len - b0) >= 16 ? 16u : static_cast<uint32_t>(len - b0);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                             in_sa + static_cast<uint32_t>(sg & 3) * kSeg8 + lane * 16),
+                         "l"(bytes ? g + b0 : g), "r"(bytes)
+                         : "memory");
+            cp_async_commit();
+        }
+        cp_async_wait<2>();  // segments cur and cur - 1 (a group may straddle)
+        __syncwarp();
         uint32_t x = kLow8;
-        int64_t top = 3 * len;
+        int top = 3 * len;                 // stack top (bytes)
+        int flushed = (top + 15) & ~15;    // [flushed, ...) is in HBM
         bool bad = false;
-        uint32_t most = 0;  // RenormStats.max_encode_digits
-        for (int64_t gi = (len + n_lanes - 1) / n_lanes - 1; gi >= 0; --gi) {
-            const int64_t base = gi * n_lanes;
-            const int64_t left = len - base;
-            const int active = left < n_lanes ? static_cast<int>(left) : n_lanes;
-            const bool on = lane < active;
-            const uint2 e = enc[on ? g[base + lane] : 0u];
-            const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.x == 0u);
-            if (badmask) {
+        uint32_t most = 0;
+        const int groups = (len + n_lanes - 1) / n_lanes;
+        int base = (groups - 1) * n_lanes;
+        for (; base >= 0; base -= n_lanes) {
+            const int left = len - base;
+            const bool on = lane < left && lane < n_lanes;
+            const int hs = (base + (left < n_lanes ? left : n_lanes) - 1) >> 9;
+            if (hs != cur) {  // segment cur consumed: prefetch cur - 4 into its slot
+                __syncwarp();
+                while (cur > hs) {
+                    const int sg = cur - 4;
+                    const bool ok = sg >= 0;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                                     in_sa + static_cast<uint32_t>(sg & 3) * kSeg8 + lane * 16),
+                                 "l"(ok ? g + sg * kSeg8 + lane * 16 : g), "r"(ok ? 16u : 0u)
+                                 : "memory");
+                    cp_async_commit();
+                    --cur;
+                }
+                cp_async_wait<2>();
+                __syncwarp();
+            }
+            const uint2 e = enc[on ? lds8(in_sa + ((base + lane) & (kRing8 - 1))) : 0u];
+            if (__any_sync(0xffffffffu, on && e.x == 0u)) {
+                const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.x == 0u);
                 if (lane == 0)
                     atomicMax(&status->unenc_index,
                               static_cast<long long>(cbase + base + 31 - __clz(badmask)));
@@ -165,28 +430,80 @@ encode_u8_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_
                 break;
             }
             const uint32_t fm1 = e.y & 0xFFFFu;  // spill while (x >> 8j) >> thr8 > f - 1
-            uint32_t sp = 0;
-            if (on) sp = ((x >> thr8) > fm1) + (((x >> 8) >> thr8) > fm1) +
-                         (((x >> 16) >> thr8) > fm1);
+            const uint32_t sp = on ? ((x >> thr8) > fm1) + (((x >> 8) >> thr8) > fm1) +
+                                         (((x >> 16) >> thr8) > fm1)
+                                   : 0u;
             const uint32_t b0 = __ballot_sync(0xffffffffu, sp & 1u);
             const uint32_t b1 = __ballot_sync(0xffffffffu, sp & 2u);
             top -= __popc(b0) + 2 * __popc(b1);
-            const int64_t p = top + __popc(b0 & lt) + 2 * __popc(b1 & lt);
-            // read order is most significant spilled byte first
-            for (uint32_t j = 0; j < sp; ++j) o[p + j] = static_cast<uint8_t>(x >> (8 * (sp - 1 - j)));
-            if (on) x = enc_push(ctx, sp ? x >> (8 * sp) : x, e);
+            // read order is most significant spilled byte first: byte j of the
+            // lane's sp digits (j < sp) is x >> 8 (sp - 1 - j)
+            const uint32_t pe = out_sa + ((static_cast<uint32_t>(top) + __popc(b0 & lt) +
+                                           2u * __popc(b1 & lt) + sp - 1u) & (kRing8 - 1));
+            if (sp >= 1u) sts8(pe, x);
+            if (sp >= 2u) sts8(out_sa + ((pe - out_sa - 1u) & (kRing8 - 1)), x >> 8);
+            if (sp >= 3u) sts8(out_sa + ((pe - out_sa - 2u) & (kRing8 - 1)), x >> 16);
+            if (on) x = enc_push(ctx, x >> (8u * sp), e);
             most = max(most, sp);
+            if (flushed - top >= 512) {  // drain 512 bytes: 16 per lane
+                __syncwarp();
+                const uint32_t ro = static_cast<uint32_t>(flushed - 512) + lane * 16;
+                uint4 v;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                             : "r"(out_sa + (ro & (kRing8 - 1))));
+                *reinterpret_cast<uint4 *>(o + (flushed - 512) + lane * 16) = v;
+                flushed -= 512;
+                __syncwarp();
+            }
         }
         most = __reduce_max_sync(0xffffffffu, most);
         if (lane == 0) atomicMax(&status->max_digits, most);
         if (!bad) {
+            __syncwarp();
+            // whole 16-byte blocks of [roundup16(top), flushed), then the head bytes
+            const int lo16 = (top + 15) & ~15;
+            for (int b = lo16 + lane * 16; b < flushed; b += 512) {
+                uint4 v;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                             : "r"(out_sa + (static_cast<uint32_t>(b) & (kRing8 - 1))));
+                *reinterpret_cast<uint4 *>(o + b) = v;
+            }
+            for (int b = top + lane; b < lo16 && b < flushed; b += 32)
+                o[b] = out_ring[b & (kRing8 - 1)];
             if (lane == 0) chunk_bytes[k] = static_cast<uint32_t>(3 * len - top);
             if (lane < n_lanes) states_out[k * n_lanes + lane] = x;
         }
+        cp_async_wait<0>();
+        __syncwarp();
     }
 }
 
-// N > 32: one CTA per stream, thread t owns lanes [t*k, t*k + k) (k <= 64),
+static size_t ring8_decode_smem(int warps, int sb, bool packed) {
+    const size_t m = size_t(1) << sb;
+    const size_t lut = packed ? m * 4 : kMaxSym * sizeof(uint2) + (m < 16 ? 16 : m);
+    return size_t(warps) * (kRing8 + kObuf8) + ((lut + 15) & ~size_t(15));
+}
+
+static size_t ring8_encode_smem(int warps) {
+    return kMaxSym * sizeof(uint2) + size_t(warps) * kRing8 + kRing8 + size_t(warps) * kRing8;
+}
+
+// one CTA per SM with the SM's share of the streams (as the word16 coders)
+static void ring8_shape(int64_t n_chunks, int *warps, int *cta_warps, int64_t *blocks) {
+    const int64_t sms = sm_count();
+    int w = static_cast<int>((n_chunks + sms - 1) / sms);
+    if (w > kMaxWarps8) w = kMaxWarps8;
+    if (w < 1) w = 1;
+    int64_t b = (n_chunks + w - 1) / w;
+    if (b > sms) b = sms;  // grid-stride beyond one wave
+    *warps = w;
+    *cta_warps = w;
+    *blocks = b;
+}
+
+// N > 32: one CTA per stream, thread t owns lanes [t*k, t*k + k) (k <= 64),// N > 32: one CTA per stream, thread t owns lanes [t*k, t*k + k) (k <= 64),
 // CTA-wide exclusive scans of the digit counts; states live in ws.
 __device__ __forceinline__ uint32_t block_excl_scan_8(uint32_t v, uint32_t *total,
                                                       uint32_t *sh) {
@@ -366,17 +683,39 @@ encode_u8_block_kernel(const uint8_t *__restrict__ g, int64_t len, int n_lanes,
     }
 }
 
+static cudaError_t launch_decode_ring8(const uint8_t *d_payload, const uint64_t *d_offsets,
+                                       const uint32_t *d_states, int64_t n, int64_t chunk_len,
+                                       int64_t n_chunks, int n_lanes, const TableDev *d_table,
+                                       uint8_t *d_out, uint64_t *d_consumed, DStatus *d_status,
+                                       cudaStream_t stream) {
+    int warps, cta_warps;
+    int64_t blocks;
+    ring8_shape(n_chunks, &warps, &cta_warps, &blocks);
+    (void)warps;
+    // scale_bits and the packed flag are device-side: size for the larger
+    // LUT (32-bit entries at sb = 15 vs the two-lookup form at sb = 16)
+    size_t smem = ring8_decode_smem(cta_warps, kMaxScaleBits, false);
+    const size_t smem32 = ring8_decode_smem(cta_warps, kPackedMaxBits, true);
+    if (smem32 > smem) smem = smem32;
+    smem_limit(reinterpret_cast<const void *>(decode_u8_dispatch_kernel), int(smem));
+    decode_u8_dispatch_kernel<<<static_cast<unsigned>(blocks), cta_warps * 32, smem, stream>>>(
+        d_payload, d_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table, d_out,
+        d_consumed, d_status);
+    ilans_note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_encode_u8(const uint8_t *d_msg, int64_t n, int n_lanes, const TableDev *d_table,
                              uint8_t *d_scratch, uint32_t *d_bytes, uint32_t *d_states,
                              DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
-    if (n_lanes > 32) {
+    if (n_lanes > 32 || n > kRingMaxChunk8) {
         const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
         encode_u8_block_kernel<<<1, threads, 0, stream>>>(d_msg, n, n_lanes, d_table, d_scratch,
                                                           d_bytes, d_states, d_status, d_lane_ws);
-    } else {
-        encode_u8_warp_kernel<<<1, 32, 0, stream>>>(d_msg, n, n, 1, n_lanes, d_table, d_scratch,
-                                                    d_bytes, d_states, d_status);
+    } else {  // the staged kernel, one stream = one chunk
+        return launch_encode_chunks_u8(d_msg, n, n, n_lanes, d_table, d_scratch, d_bytes,
+                                       d_states, d_status, stream);
     }
     ilans_note_launch();
     return cudaGetLastError();
@@ -388,6 +727,9 @@ cudaError_t launch_decode_u8(const uint8_t *d_payload, uint64_t pay_len, const u
                              DStatus *d_status, uint32_t *d_lane_ws, cudaStream_t stream,
                              DecodeTrace trace) {
     if (n <= 0) return cudaSuccess;
+    if (n_lanes <= 32 && !trace.states && n <= kRingMaxChunk8)  // staged: one stream = one chunk
+        return launch_decode_ring8(d_payload, d_offsets, d_states, n, n, 1, n_lanes, d_table,
+                                   d_out, d_consumed, d_status, stream);
     if (n_lanes > 32) {
         const int threads = n_lanes >= 1024 ? 1024 : ((n_lanes + 31) / 32) * 32;
         decode_u8_block_kernel<<<1, threads, 0, stream>>>(
@@ -440,11 +782,14 @@ cudaError_t launch_encode_chunks_u8(const uint8_t *d_msg, int64_t n, int64_t chu
                                     uint32_t *d_bytes, uint32_t *d_states, DStatus *d_status,
                                     cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
+    if (chunk_len > kRingMaxChunk8) return cudaErrorInvalidValue;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
-    int64_t blocks = (n_chunks + 7) / 8;  // 8 warps (streams) per CTA
-    const int64_t cap = int64_t(sm_count()) * 8;
-    if (blocks > cap) blocks = cap;
-    encode_u8_warp_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+    int warps, cta_warps;
+    int64_t blocks;
+    ring8_shape(n_chunks, &warps, &cta_warps, &blocks);
+    const size_t smem = ring8_encode_smem(cta_warps);
+    smem_limit(reinterpret_cast<const void *>(encode_u8_ring_kernel), int(smem));
+    encode_u8_ring_kernel<<<static_cast<unsigned>(blocks), cta_warps * 32, smem, stream>>>(
         d_msg, n, chunk_len, n_chunks, n_lanes, d_table, d_scratch, d_bytes, d_states, d_status);
     ilans_note_launch();
     return cudaGetLastError();
@@ -470,15 +815,10 @@ cudaError_t launch_decode_chunks_u8(const uint8_t *d_payload, const uint64_t *d_
                                     int n_lanes, const TableDev *d_table, uint8_t *d_out,
                                     uint64_t *d_consumed, DStatus *d_status, cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
+    if (chunk_len > kRingMaxChunk8) return cudaErrorInvalidValue;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
-    int64_t blocks = (n_chunks + 7) / 8;
-    const int64_t cap = int64_t(sm_count()) * 8;
-    if (blocks > cap) blocks = cap;
-    decode_u8_warp_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-        d_payload, d_offsets, d_states, n, chunk_len, n_chunks, n_lanes, d_table, d_out,
-        d_consumed, d_status, DecodeTrace{nullptr, nullptr, nullptr, 0});
-    ilans_note_launch();
-    return cudaGetLastError();
+    return launch_decode_ring8(d_payload, d_offsets, d_states, n, chunk_len, n_chunks, n_lanes,
+                               d_table, d_out, d_consumed, d_status, stream);
 }
 
 }  // namespace ilans
