@@ -467,7 +467,7 @@ def plugin_e2e(msg_h, table, C, N, threads_list=(1, 8, 16), sample_mib=256):
                     f"N={N}), host numpy buffers, wall clock", **rows}
 
 
-def e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes):
+def e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes, slots=3):
     """The same round trip through the public host API (chunked.HostCodec)
     from pinned host memory: every step uploads its message, builds the
     model, encodes, downloads the framed payload, uploads it again, decodes
@@ -480,7 +480,7 @@ def e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes):
 
     from paper_1402_3392_b200.chunked import HostCodec
 
-    hc = HostCodec(n, C, N, sb, dev, counts_allreduce=allreduce, slots=3)
+    hc = HostCodec(n, C, N, sb, dev, counts_allreduce=allreduce, slots=slots)
     h_msg = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     h_msg.copy_(d_msg[:n])
     h_outs = [torch.empty(n, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
@@ -542,7 +542,7 @@ def e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes):
     vs, _, _ = timed(sequential)
     return {"value": v, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "api": "chunked.HostCodec encode_async()+decode_async() from pinned host memory, "
-                   "up to 3 round trips in flight",
+                   f"up to {slots} round trips in flight",
             "sequential_GBps": vs, "steps": steps,
             "timing": "wall clock around synchronized steps, max over ranks"}
 
@@ -822,11 +822,16 @@ def run_b200(a):
                                     "source": "ncu smsp__inst_executed.sum / live kernel time"}
 
     out["fused_consumer"] = fused_consumer(codec, d_out, n, dev)
-    if rank == 0 and world == 1 and a.scale_bits != 14:
+    big = n > (2 << 30)  # config 3 sizes: free the step's buffers for the legs below
+    if rank == 0 and world == 1 and a.scale_bits != 14 and not big:
         out["sb14"] = other_precision(a, dev, d_msg, n, 14)
+    if big:
+        del codec, d_out
+        torch.cuda.empty_cache()
 
     if not a.no_e2e:
-        out["e2e"] = e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes)
+        out["e2e"] = e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes,
+                         slots=2 if big else 3)
     if rank == 0 and world == 1 and not a.no_plugin:
         out["plugin_e2e"] = plugin_e2e(d_msg[:n].cpu().numpy(), table, C, N)
     if rank == 0 and world == 1:

@@ -296,13 +296,13 @@ int ilans_decode_chunks_adler32_dev(const uint16_t *d_payload, const uint64_t *d
 
 /* Chunked BYTE8 (8-bit digits, L = 2^23; ICH1 variant 0): chunk k is the
  * reference's encode_interleaved(msg[kC:(k+1)C], table, N, BYTE8)
- * (interleave.py:155-179), one warp per chunk, N in [1, 32].
- * Encode: d_scratch holds 3 bytes per message byte + 8 (chunk k's digits end
+ * (interleave.py:155-179), one warp per chunk, N in [1, 32], chunk_len <= 2^29.
+ * Encode: d_scratch holds 3 bytes per message byte + 16 (chunk k's digits end
  * at 3kC + 3 len_k); d_chunk_bytes[k] = its digit count. Frame: exclusive
  * scan into d_byte_offsets[K + 1] and byte compaction into d_payload (both
- * 4-byte aligned). Decode: d_payload must be 4-byte aligned (ILANS_ERR_VALUE
- * otherwise) and readable for 8 bytes past its last payload byte (the
- * refill loads two aligned words); one launch for all chunks, d_consumed[k] = bytes
+ * 4-byte aligned). Decode: d_payload must be 16-byte aligned (ILANS_ERR_VALUE
+ * otherwise; it streams into shared rings by 16-byte async copies, which
+ * never read past a chunk's last byte); one launch for all chunks, d_consumed[k] = bytes
  * read; errors land in the device status (zero-frequency symbol, exhausted
  * chunk, runaway refill = FormatError). */
 int ilans_encode_chunks_u8_dev(const uint8_t *d_msg, int64_t n, int64_t chunk_len,

@@ -1157,6 +1157,7 @@ extern "C" int ilans_encode_chunks_u8_dev(const uint8_t *d_msg, int64_t n, int64
                                           uint8_t *d_scratch, uint32_t *d_chunk_bytes,
                                           uint32_t *d_states, void *d_status, void *stream) {
     if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
+    if (chunk_len > (int64_t(1) << 29)) return ILANS_ERR_VALUE;  // 32-bit chunk cursors
     return launch_encode_chunks_u8(d_msg, n, chunk_len, n_lanes,
                                    static_cast<const TableDev *>(d_table), d_scratch,
                                    d_chunk_bytes, d_states, static_cast<DStatus *>(d_status),
@@ -1178,8 +1179,9 @@ extern "C" int ilans_decode_chunks_u8_dev(const uint8_t *d_payload, const uint64
                                           int32_t n_lanes, const void *d_table, uint8_t *d_out,
                                           uint64_t *d_consumed, void *d_status, void *stream) {
     if (n_lanes < 1 || n_lanes > 32 || chunk_len <= 0 || (chunk_len & 15)) return ILANS_ERR_VALUE;
-    // the refill reads two aligned u32 words of the payload (byte8.cu)
-    if (reinterpret_cast<uintptr_t>(d_payload) & 3) return ILANS_ERR_VALUE;
+    if (chunk_len > (int64_t(1) << 29)) return ILANS_ERR_VALUE;  // 32-bit chunk cursors
+    // the payload streams into shared rings by 16-byte cp.async (byte8.cu)
+    if (reinterpret_cast<uintptr_t>(d_payload) & 15) return ILANS_ERR_VALUE;
     return launch_decode_chunks_u8(d_payload, d_byte_offsets, d_states, n, chunk_len, n_lanes,
                                    static_cast<const TableDev *>(d_table), d_out, d_consumed,
                                    static_cast<DStatus *>(d_status), ST(stream)) == cudaSuccess
