@@ -28,7 +28,7 @@ namespace ilans {
 // offset, so the PRMT that assembles the address still does all of it.
 constexpr int kHistGroups = 3;
 constexpr int kHistThreads = 128 * kHistGroups;
-constexpr int kHistBatch = 12;                // 16-byte loads in flight per thread
+constexpr int kHistBatch = 8;                 // 16-byte loads per batch (two batches in flight)
 constexpr int64_t kHistVecPerRound = 4088;    // <= 65535 / 16 vectors between flushes
 
 __device__ __forceinline__ uint32_t hist_word(uint32_t bin, uint32_t tid) {
@@ -108,12 +108,25 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
     const int64_t per_round = stride * kHistVecPerRound;
     for (int64_t round_base = 0; round_base < nvec; round_base += per_round) {
         const int64_t round_end = min(nvec, round_base + per_round);
-        for (int64_t j0 = round_base + first; j0 < round_end; j0 += stride * kHistBatch) {
+        // software-pipelined: the next batch's loads are in flight while this
+        // batch's bytes are counted (a load-then-count loop left the HBM
+        // queue empty during every counting phase: long_scoreboard stalls)
+        uint4 nx[kHistBatch];
+        int64_t j0 = round_base + first;
+#pragma unroll
+        for (int r = 0; r < kHistBatch; ++r) {
+            const int64_t j = j0 + r * stride;
+            nx[r] = j < round_end ? __ldcs(vec + j) : make_uint4(0, 0, 0, 0);
+        }
+        for (; j0 < round_end; j0 += stride * kHistBatch) {
             uint4 v[kHistBatch];
 #pragma unroll
+            for (int r = 0; r < kHistBatch; ++r) v[r] = nx[r];
+            const int64_t j1 = j0 + stride * kHistBatch;
+#pragma unroll
             for (int r = 0; r < kHistBatch; ++r) {
-                const int64_t j = j0 + r * stride;
-                v[r] = j < round_end ? __ldcs(vec + j) : make_uint4(0, 0, 0, 0);
+                const int64_t j = j1 + r * stride;
+                nx[r] = j < round_end ? __ldcs(vec + j) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int r = 0; r < kHistBatch; ++r)

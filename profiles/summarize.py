@@ -85,7 +85,9 @@ def main(rep: str, launches: str, tag: str, config: str = "mib=256,chunk=65536,l
         wf = float(r[col["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]])
         inst = float(r[col["smsp__inst_executed.sum"]])
         for key in ("decode", "encode", "histogram", "compact"):
-            if key in short:
+            # the first launch of each: the bench step's (decode: from the
+            # encoder's slot layout; the packed-stream decode comes later)
+            if key in short and key not in traffic.get("dram_bytes", {}):
                 traffic.setdefault("dram_bytes", {})[key] = rd + wr
                 traffic.setdefault("smem_wavefronts", {})[key] = wf
                 traffic.setdefault("warp_instructions", {})[key] = inst
