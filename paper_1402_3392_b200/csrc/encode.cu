@@ -60,6 +60,12 @@ __host__ __device__ constexpr size_t encode_smem_bytes(int warps) {
            kOutRingBytes + size_t(warps) * kOutRingBytes;
 }
 
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<uint16_t>(v)));
 }
@@ -330,7 +336,63 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         // the lane's 32-bit shared slot address (no per-batch conversions)
         const uint8_t *seg_src = g + (issued_lo - 1) * kInSeg + lane * 16;
         const uint32_t ring_sa = smem_addr(ring) + lane * 16;
-        for (Idx b = full - 1; !bad && b >= 0; --b) {
+        Idx b = full - 1;
+        if (MODE == 0 && fast) {
+            // Pairs of blocks (32 groups) per iteration: one prefetch point
+            // and one wait per 1 KB of message, records loaded one group
+            // ahead straight across the two blocks; the spill ring is still
+            // drained between the halves (a half adds <= 512 words).
+            const uint32_t blk_sa = smem_addr(ring) + lane;
+            for (; b >= 1; b -= 2) {
+#pragma unroll
+                for (int q = 2; q <= 3; ++q) {
+                    const Idx sg = b - q;
+                    if (sg < issued_lo) {
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                                         ring_sa + ((static_cast<uint32_t>(sg) & 3u) << 9)),
+                                     "l"(sg >= 0 ? seg_src : g), "r"(sg >= 0 ? 16u : 0u)
+                                     : "memory");
+                        seg_src -= kInSeg;
+                        cp_async_commit();
+                        issued_lo = sg;
+                    }
+                }
+                cp_async_wait<2>();  // blocks b and b - 1 landed
+                __syncwarp();
+                const uint32_t hi_sa = blk_sa + ((static_cast<uint32_t>(b) & 3u) << 9);
+                const uint32_t lo_sa = blk_sa + ((static_cast<uint32_t>(b - 1) & 3u) << 9);
+                uint32_t topb = static_cast<uint32_t>(top) << 1;
+                uint32_t topb0 = topb;
+                uint32_t sym_n = lds_u8(hi_sa + (kInSeg / 32 - 1) * 32);
+                uint2 a_n = encf[sym_n];
+                sym_n = lds_u8(hi_sa + (kInSeg / 32 - 2) * 32);
+#pragma unroll
+                for (int gg = 2 * (kInSeg / 32) - 1; gg >= 0; --gg) {
+                    const uint2 a = a_n;  // {M, Z}
+                    if (gg > 0) {
+                        a_n = encf[sym_n];
+                        if (gg > 1) {
+                            const int nx = gg - 2;  // group two ahead
+                            sym_n = lds_u8((nx >= kInSeg / 32 ? hi_sa : lo_sa) +
+                                           (nx % (kInSeg / 32)) * 32);
+                        }
+                    }
+                    if (!COVERED) macc &= a.x;
+                    spill_group<0, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2, two);
+                    uint32_t q = __umulhi(x, a.x);
+                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
+                    x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
+                    if (gg == kInSeg / 32) {  // first half done: keep the spill ring < 512
+                        top -= static_cast<Idx>((topb0 - topb) >> 1);
+                        topb0 = topb;
+                        st.drain(top, lane);
+                    }
+                }
+                top -= static_cast<Idx>((topb0 - topb) >> 1);
+                st.drain(top, lane);
+            }
+        }
+        for (; !bad && b >= 0; --b) {
             if (b - 3 < issued_lo) {  // segments below `full` are whole 512-byte blocks
                 // (no __syncwarp: every lane's reads of this slot -- segment
                 // b + 1 -- were consumed before the previous batch's ballots;
