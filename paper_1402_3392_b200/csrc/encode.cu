@@ -337,7 +337,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         const uint8_t *seg_src = g + (issued_lo - 1) * kInSeg + lane * 16;
         const uint32_t ring_sa = smem_addr(ring) + lane * 16;
         Idx b = full - 1;
-        if (MODE == 0 && fast) {
+        if (MODE == 0 && (fast || fast12)) {
             // Pairs of blocks (32 groups) per iteration: one prefetch point
             // and one wait per 1 KB of message, records loaded one group
             // ahead straight across the two blocks; the spill ring is still
@@ -365,12 +365,15 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 uint32_t topb0 = topb;
                 uint32_t sym_n = lds_u8(hi_sa + (kInSeg / 32 - 1) * 32);
                 uint2 a_n = encf[sym_n];
+                uint32_t z_n = F12 ? encz[sym_n] : 0u;
                 sym_n = lds_u8(hi_sa + (kInSeg / 32 - 2) * 32);
 #pragma unroll
                 for (int gg = 2 * (kInSeg / 32) - 1; gg >= 0; --gg) {
-                    const uint2 a = a_n;  // {M, Z}
+                    const uint2 a = a_n;  // {M, Z} (F12: {M, Y})
+                    const uint32_t z = z_n;
                     if (gg > 0) {
                         a_n = encf[sym_n];
+                        if (F12) z_n = encz[sym_n];
                         if (gg > 1) {
                             const int nx = gg - 2;  // group two ahead
                             sym_n = lds_u8((nx >= kInSeg / 32 ? hi_sa : lo_sa) +
@@ -378,10 +381,20 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         }
                     }
                     if (!COVERED) macc &= a.x;
-                    spill_group<0, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2, two);
-                    uint32_t q = __umulhi(x, a.x);
-                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
-                    x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
+                    uint32_t q;
+                    if (!F12) {
+                        spill_group<0, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2,
+                                              two);
+                        q = __umulhi(x, a.x);
+                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
+                        x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
+                    } else {
+                        spill_group<1, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2,
+                                              two);
+                        q = __umulhi(x, a.x);
+                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
+                        x = q * (a.y & lowm) + (x + (z >> 17));
+                    }
                     if (gg == kInSeg / 32) {  // first half done: keep the spill ring < 512
                         top -= static_cast<Idx>((topb0 - topb) >> 1);
                         topb0 = topb;
