@@ -344,6 +344,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             // drained between the halves (a half adds <= 512 words).
             const uint32_t blk_sa = smem_addr(ring) + lane;
             for (; b >= 1; b -= 2) {
+                __syncwarp();  // every lane is done reading blocks b + 1, b + 2
 #pragma unroll
                 for (int q = 2; q <= 3; ++q) {
                     const Idx sg = b - q;
@@ -404,12 +405,16 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 top -= static_cast<Idx>((topb0 - topb) >> 1);
                 st.drain(top, lane);
             }
+            // an odd last block (b == 0) is read by the one-block loop below,
+            // whose wait counts one segment per block: land everything first
+            cp_async_wait<0>();
+            __syncwarp();
         }
         for (; !bad && b >= 0; --b) {
             if (b - 3 < issued_lo) {  // segments below `full` are whole 512-byte blocks
-                // (no __syncwarp: every lane's reads of this slot -- segment
-                // b + 1 -- were consumed before the previous batch's ballots;
-                // below segment 0 the copy reads nothing and zero-fills)
+                // every lane is done reading this slot (segment b + 1); below
+                // segment 0 the copy reads nothing and zero-fills
+                __syncwarp();
                 const Idx sg = b - 3;
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
                                  ring_sa + ((static_cast<uint32_t>(sg) & 3u) << 9)),
@@ -958,8 +963,10 @@ cudaError_t launch_frame(const uint16_t *d_scratch, int64_t n, int64_t chunk_len
                          const uint32_t *d_chunk_words, uint64_t *d_word_offsets,
                          uint16_t *d_payload, int carry_in, cudaStream_t stream) {
     const int64_t n_chunks = n <= 0 ? 0 : (n + chunk_len - 1) / chunk_len;
-    chunk_offsets_kernel<<<1, 1024, 0, stream>>>(d_chunk_words, n_chunks, d_word_offsets,
-                                                  carry_in);
+    // directory only (no packing): a 256-thread CTA, small enough to share
+    // an SM with the decoder it runs beside
+    chunk_offsets_kernel<<<1, d_payload ? 1024 : 256, 0, stream>>>(d_chunk_words, n_chunks,
+                                                                   d_word_offsets, carry_in);
     ilans_note_launch();
     if (n_chunks > 0 && d_payload) {  // d_payload == nullptr: the directory only
         compact_kernel<<<static_cast<unsigned>(n_chunks), 256, 0, stream>>>(

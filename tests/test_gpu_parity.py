@@ -501,3 +501,69 @@ def test_decode_from_slot_layout_matches_packed_decode():
         ad = codec.decode_adler32(n, slots=True).cpu().numpy().view(np.uint32)
         ref = [zlib.adler32(msg[i * C:(i + 1) * C].tobytes()) for i in range(k)]
         assert ad.tolist() == ref
+
+
+def test_chunked_covered_encode_equals_checked_encode_and_user_tables_still_check():
+    """The covered entry (table quantized from this message's own histogram,
+    no zero-frequency check) writes exactly what the checking entry writes;
+    a user table (build_table_from_freq) keeps the check and reports the
+    highest zero-frequency index like the reference."""
+    import torch
+
+    from paper_1402_3392_b200.chunked import DeviceCodec
+    from paper_1402_3392_b200.synth import synth_host
+
+    for sb in (12, 14):
+        n, C = 2_000_003, 65536
+        msg = synth_host(n, 1.1, seed=sb)
+        d = torch.from_numpy(msg).cuda()
+        codec = DeviceCodec(n, C, 32, sb)
+        codec.histogram(d, n)
+        codec.build_table_from_counts()
+        assert codec._covers == (d.data_ptr(), n)
+        codec.reset_status()
+        codec.encode(d, n)  # covered entry
+        codec.check_status()
+        covered = codec.encoded_host(n, codec.read_table())
+        k = covered.n_chunks
+        codec.reset_status()
+        codec.encode_range(d.data_ptr(), n, 0, k, covered=False)  # checking entry
+        codec.frame_range(n, 0, k, codec.payload.data_ptr())
+        codec.check_status()
+        checked = codec.encoded_host(n, covered.table)
+        assert covered.to_bytes() == checked.to_bytes()
+        # a user table without symbol 200 while the message holds it
+        freqs = list(covered.table.freq)
+        msg2 = msg.copy()
+        msg2[1_500_000] = 200
+        msg2[10] = 200
+        if 200 < len(freqs) and freqs[200]:
+            moved = freqs[200]
+            freqs[200] = 0
+            freqs[0] += moved
+        t = SymbolTable(freqs, sb)
+        d2 = torch.from_numpy(msg2).cuda()
+        codec.build_table_from_freq(t)
+        assert codec._covers is None
+        codec.reset_status()
+        codec.encode(d2, n)
+        want = int(np.nonzero(msg2 == 200)[0].max())  # the highest offending index
+        with pytest.raises(UnencodableSymbolError, match=f"index {want}$"):
+            codec.check_status()
+
+
+@pytest.mark.parametrize("C, sb", [(1536, 12), (2560 + 96, 12), (1536, 14), (512 * 7, 13)])
+def test_chunked_odd_block_counts_match_oracle(C, sb):
+    """Chunks whose 512-byte block count is odd (with and without a tail):
+    the encoder's pair-of-blocks loop hands the last block to the one-block
+    loop; every chunk equals the oracle's."""
+    from paper_1402_3392_b200.chunked import decode_chunked, encode_chunked
+    from paper_1402_3392_b200.synth import synth_host
+
+    msg = synth_host(C * 300 + 777, 1.15, seed=C + sb)
+    cc = encode_chunked(msg, None, 32, C, sb)
+    t = cc.table
+    p, o, st = oracle.encode_chunks_u16(msg, C, t.freq_u32, t.cum_u32, sb, 32)
+    assert np.array_equal(cc.payload, p) and np.array_equal(cc.word_offsets, o)
+    assert np.array_equal(cc.states, st)
+    assert np.array_equal(decode_chunked(cc), msg)
