@@ -480,7 +480,8 @@ def e2e(a, n, k_chunks, C, N, sb, dev, d_msg, allreduce, world, global_bytes, sl
 
     from paper_1402_3392_b200.chunked import HostCodec
 
-    hc = HostCodec(n, C, N, sb, dev, counts_allreduce=allreduce, slots=slots)
+    hc = HostCodec(n, C, N, sb, dev, counts_allreduce=allreduce, slots=slots,
+                   batch_bytes=64 << 20)
     h_msg = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     h_msg.copy_(d_msg[:n])
     h_outs = [torch.empty(n, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
