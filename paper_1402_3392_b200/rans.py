@@ -10,6 +10,7 @@ its own tables from the same frequencies.
 
 from __future__ import annotations
 
+import math
 import struct
 from dataclasses import dataclass
 from functools import cached_property
@@ -300,6 +301,12 @@ class Coder:
 
     def in_interval(self, state: int) -> bool:
         return self.lower_bound <= state < self.radix * self.lower_bound
+
+    @property
+    def max_digits_per_symbol(self) -> int:
+        # a normalised state reaches 0 after this many divisions by radix
+        # (ans.py:64-67), so no symbol can need more spills
+        return math.ceil(math.log(self.radix * self.lower_bound, self.radix)) + 1
 
 
 def rans_coder(table: SymbolTable, variant: RenormVariant) -> Coder:

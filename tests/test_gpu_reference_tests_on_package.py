@@ -1,0 +1,58 @@
+"""The reference's own test files (pkg/tests, 164 tests) run against THIS
+package: `ilans` is aliased to paper_1402_3392_b200 (rans, interleave,
+lanes, mux, backend, errors), with the reference's out-of-scope teaching
+modules (ans, bench, cli, the lane-simulation helpers) loaded inside that
+alias so they call this package (integration/reference_tests_on_package.py).
+
+Everything passes except tests of two deliberate differences
+(INTEGRATION.md section 3), listed here exactly so any other failure fails
+this test:
+* the pure-Python backend is not shipped (`backend.get("pure")` raises);
+* custom RenormVariants (e.g. the 1-bit "toy" digits) are not coded by the
+  interleaved B200 codec (UnsupportedVariantError)."""
+
+import re
+import sys
+from pathlib import Path
+
+import pytest
+
+from paper_1402_3392_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT / "integration"))
+
+EXPECTED_FAILURES = {
+    # no pure-Python backend (never a runtime fallback)
+    "tests/test_backend.py::TestSelection::test_pure_always_available",
+    "tests/test_backend.py::TestSelection::test_ext_resolves",
+    "tests/test_backend.py::TestSelection::test_env_override_pure",
+    "tests/test_backend.py::TestSelection::test_env_override_unknown_warns_and_falls_back",
+    "tests/test_backend.py::TestKernelEquivalence::test_encode_identical",
+    "tests/test_backend.py::TestKernelEquivalence::test_decode_identical",
+    "tests/test_backend.py::TestKernelEquivalence::test_lane_decode_identical",
+    "tests/test_backend.py::TestKernelEquivalence::test_same_errors_on_truncation",
+    "tests/test_backend.py::TestKernelEquivalence::test_same_errors_on_bad_symbol",
+    "tests/test_cli.py::TestBench::test_bench_pure_backend",
+    # custom (non word16 / byte8) variants in the interleaved coders
+    "tests/test_interleave.py::TestGolden::test_single_lane_recast_toy",
+    "tests/test_interleave.py::TestNegatives::test_unserializable_custom_variant",
+}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device: the -m gpu suite must run on a B200")
+
+
+def test_reference_test_files_against_this_package(tmp_path):
+    from reference_tests_on_package import build, run
+
+    dest = build(tmp_path / "pkg")
+    r = run(dest, "tests", "-rf")
+    failed = set(re.findall(r"^FAILED (\S+?)(?: - .*)?$", r.stdout, re.M))
+    assert failed == EXPECTED_FAILURES, r.stdout[-6000:]
+    m = re.search(r"(\d+) passed", r.stdout)
+    assert m and int(m.group(1)) == 164 - len(EXPECTED_FAILURES), r.stdout[-2000:]
