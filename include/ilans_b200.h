@@ -127,6 +127,28 @@ int ilans_decode_interleaved_u16_stats(const uint16_t *payload, int64_t pay_len,
                                        int32_t n_lanes, uint8_t *out, int64_t *consumed,
                                        ilans_status *st);
 
+/* Any RenormVariant (digit_bits in [1, 16], lower_bound L with L % 2^sb == 0
+ * and L << digit_bits <= 2^32): the reference's scalar path for variants
+ * other than word16 / byte8 (interleave.py:155-179, rans.py:266-314), e.g.
+ * 1-bit digits. One digit per u16 element, in decoder read order. Encode:
+ * digits_cap >= n * (ceil(sb / digit_bits) + 1). Decode: optional trace
+ * (all three trace pointers, as ilans_decode_trace_u16), FormatError after
+ * more than ceil(bits(L) / digit_bits) + 2 refills for one symbol. N in
+ * [1, 1024] (ILANS_ERR_UNSUPPORTED beyond). st->max_digits: the most
+ * digits one symbol moved. */
+int ilans_encode_interleaved_var(const uint8_t *msg, int64_t n, const uint32_t *freq,
+                                 int32_t n_freq, const uint32_t *cum, int32_t scale_bits,
+                                 int32_t n_lanes, int32_t digit_bits, uint32_t lower_bound,
+                                 uint16_t *digits_out, int64_t digits_cap, int64_t *n_digits,
+                                 uint32_t *states_out, ilans_status *st);
+int ilans_decode_interleaved_var(const uint16_t *payload, int64_t pay_len,
+                                 const uint32_t *states, const uint8_t *slot_sym,
+                                 int64_t n_slots, const uint32_t *freq, const uint32_t *cum,
+                                 int32_t n_freq, int32_t scale_bits, int64_t msg_len,
+                                 int32_t n_lanes, int32_t digit_bits, uint32_t lower_bound,
+                                 uint8_t *out, int64_t *consumed, uint32_t *trace_states,
+                                 uint64_t *trace_pos, int64_t *groups_done, ilans_status *st);
+
 /* Instrumented decode: the device form of interleave.decode_interleaved_steps
  * (interleave.py:251-268) and lanes.decode_lanes_steps (lanes.py:221-232).
  * Same arguments as ilans_decode_interleaved_u16 plus, per completed group g

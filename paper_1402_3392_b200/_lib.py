@@ -92,6 +92,11 @@ PROTOTYPES = [
      [_vp, _i64, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _st]),
     ("ilans_decode_interleaved_u16_stats", ctypes.c_int,
      [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _st]),
+    ("ilans_encode_interleaved_var", ctypes.c_int,
+     [_vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32, ctypes.c_uint32, _vp, _i64, _vp, _vp, _st]),
+    ("ilans_decode_interleaved_var", ctypes.c_int,
+     [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _i32, ctypes.c_uint32, _vp,
+      _vp, _vp, _vp, _vp, _st]),
     ("ilans_decode_trace_u16", ctypes.c_int,
      [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp,
       _st]),

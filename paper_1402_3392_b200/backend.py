@@ -238,3 +238,74 @@ def get(name: str | None = None) -> Backend:
 
 def available() -> list[str]:
     return ["b200"]
+
+
+# ---------------------------------------------------------------------------
+# Any RenormVariant (the reference's scalar path for variants other than
+# word16 / byte8, interleave.py:155-179): digits as one array element each.
+# ---------------------------------------------------------------------------
+def _digit_dtype(variant):
+    return np.uint16 if variant.digit_bits > 8 else np.uint8
+
+
+def encode_interleaved_var(msg, table, n_lanes: int, variant):
+    """Backward encode with ``variant``'s digits on the B200 -> (payload in
+    read order (u8 for digits <= 8 bits, else u16), states, max digits)."""
+    m = np.ascontiguousarray(msg, dtype=np.uint8)
+    f, c = table.freq_u32, table.cum_u32
+    kmax = -(-table.scale_bits // variant.digit_bits) + 1
+    digits = np.empty(max(1, len(m) * kmax), dtype=np.uint16)
+    states = np.empty(n_lanes, dtype=np.uint32)
+    count = ctypes.c_int64(0)
+    st = _lib.Status()
+    rc = _lib.lib.ilans_encode_interleaved_var(
+        _lib.ptr(m), len(m), _lib.ptr(f), len(f), _lib.ptr(c), int(table.scale_bits),
+        int(n_lanes), int(variant.digit_bits), int(variant.lower_bound), _lib.ptr(digits),
+        len(digits), ctypes.byref(count), _lib.ptr(states), ctypes.byref(st))
+    if rc == _lib.ERR_UNSUPPORTED:
+        from .errors import UnsupportedVariantError
+
+        raise UnsupportedVariantError(st.message.decode(errors="replace"))
+    _lib.raise_for(rc, st, "encode_interleaved_var")
+    return digits[: count.value].astype(_digit_dtype(variant)), states, int(st.max_digits)
+
+
+def decode_interleaved_var(payload, states, table, msg_len: int, n_lanes: int, variant,
+                           trace: bool = False):
+    """Forward decode with ``variant``'s digits on the B200 -> (message,
+    digits read, max digits); trace=True -> (message, trace states [groups,
+    N], read position per group, groups done, digits read, error or None)
+    for the step generator."""
+    pay = np.ascontiguousarray(payload, dtype=np.uint16)
+    xs = np.array(states, dtype=np.uint32)
+    f, c, slot = table.freq_u32, table.cum_u32, table.slot_u8
+    out = np.zeros(max(1, msg_len), dtype=np.uint8)
+    consumed = ctypes.c_int64(0)
+    st = _lib.Status()
+    groups = -(-msg_len // n_lanes) if msg_len else 0
+    tstates = np.zeros((max(1, groups), n_lanes), dtype=np.uint32) if trace else None
+    tpos = np.zeros(max(1, groups), dtype=np.uint64) if trace else None
+    done = ctypes.c_int64(0)
+    rc = _lib.lib.ilans_decode_interleaved_var(
+        _lib.ptr(pay), len(pay), _lib.ptr(xs), _lib.ptr(slot), len(slot), _lib.ptr(f), _lib.ptr(c),
+        len(f), int(table.scale_bits), int(msg_len), int(n_lanes), int(variant.digit_bits),
+        int(variant.lower_bound), _lib.ptr(out), ctypes.byref(consumed),
+        _lib.ptr(tstates) if trace else None, _lib.ptr(tpos) if trace else None,
+        ctypes.byref(done) if trace else None, ctypes.byref(st))
+    if rc == _lib.ERR_UNSUPPORTED:
+        from .errors import UnsupportedVariantError
+
+        raise UnsupportedVariantError(st.message.decode(errors="replace"))
+    if trace:
+        err = None
+        if rc in (_lib.ERR_TRUNCATED, _lib.ERR_FORMAT):
+            try:
+                _lib.raise_for(rc, st, "decode")
+            except Exception as exc:  # noqa: BLE001 -- handed back to the generator
+                err = exc
+        else:
+            _lib.raise_for(rc, st, "decode")
+        return out[:msg_len], tstates, tpos, int(done.value), int(st.consumed), err
+    _lib.raise_for(rc, st, "decode_interleaved_var")
+    return out[:msg_len], int(consumed.value), int(st.max_digits)
+

@@ -17,7 +17,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libilans_b200.so"
-SOURCES = ["capi.cu", "table.cu", "encode.cu", "decode.cu", "byte8.cu", "synth.cu", "mux.cu"]
+SOURCES = ["capi.cu", "table.cu", "encode.cu", "decode.cu", "byte8.cu", "variant.cu", "synth.cu",
+           "mux.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",

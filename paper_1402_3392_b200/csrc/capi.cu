@@ -883,6 +883,169 @@ extern "C" int ilans_decode_trace_u8(const uint8_t *payload, int64_t pay_len,
                             HostTrace{trace_states, trace_pos, groups_done});
 }
 
+// ---------------------------------------------------------------------------
+// any RenormVariant (variant.cu): the reference's scalar path for variants
+// other than word16 / byte8, digits as u16 (one per element)
+// ---------------------------------------------------------------------------
+static int check_variant(int32_t digit_bits, uint32_t lower_bound, int32_t scale_bits,
+                         int32_t n_lanes, ilans_status *st) {
+    if (digit_bits < 1 || digit_bits > 16)
+        return st_fail(st, ILANS_ERR_VALUE, "digit_bits must be in [1, 16]");
+    if (lower_bound < 1 || (uint64_t(lower_bound) << digit_bits) > (uint64_t(1) << 32))
+        return st_fail(st, ILANS_ERR_VALUE, "radix * lower_bound must fit in 32 bits");
+    if (scale_bits < 1 || scale_bits > kMaxScaleBits)
+        return st_fail(st, ILANS_ERR_VALUE, "scale_bits must be in [1, 16]");
+    if (lower_bound % (uint32_t(1) << scale_bits))
+        return st_fail(st, ILANS_ERR_VALUE, "lower_bound is not a multiple of the table total");
+    if (n_lanes < 1 || n_lanes > kVarMaxLanes)
+        return st_fail(st, ILANS_ERR_UNSUPPORTED, "custom variants take 1..%d lanes", kVarMaxLanes);
+    return ILANS_OK;
+}
+
+extern "C" int ilans_encode_interleaved_var(const uint8_t *msg, int64_t n, const uint32_t *freq,
+                                            int32_t n_freq, const uint32_t *cum,
+                                            int32_t scale_bits, int32_t n_lanes,
+                                            int32_t digit_bits, uint32_t lower_bound,
+                                            uint16_t *digits_out, int64_t digits_cap,
+                                            int64_t *n_digits, uint32_t *states_out,
+                                            ilans_status *st) {
+    st_clear(st);
+    if (n < 0 || digits_cap < 0) return st_fail(st, ILANS_ERR_VALUE, "negative length");
+    if (int rc = check_variant(digit_bits, lower_bound, scale_bits, n_lanes, st)) return rc;
+    if (n_freq < 0 || n_freq > kMaxSym)
+        return st_fail(st, ILANS_ERR_VALUE, "alphabet size must be in [1, 256]");
+    // a symbol spills at most ceil(sb / digit_bits) digits (x < L 2^b, T >= (L / m) 2^b)
+    const int64_t kmax = (scale_bits + digit_bits - 1) / digit_bits + 1;
+    if (digits_cap < n * kmax) return st_fail(st, ILANS_ERR_VALUE, "digit buffer too small");
+    Ctx *cp = nullptr;
+    if (int rc = current_device(st, &cp)) return rc;
+    Ctx &c = *cp;
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (int rc = ctx_init(c, st)) return rc;
+    if (n == 0) {
+        for (int l = 0; l < n_lanes; ++l) states_out[l] = lower_bound;
+        *n_digits = 0;
+        return ILANS_OK;
+    }
+    cudaStream_t s = c.stream;
+    const int64_t cap = n * kmax;
+    CK(c.msg.ensure(size_t(n)));
+    CK(c.scratch.ensure(size_t(cap) * 2));
+    CK(c.states.ensure(size_t(n_lanes) * 4));
+    CK(c.words.ensure(8));
+    CK(cudaMemcpyAsync(c.msg.p, msg, size_t(n), cudaMemcpyHostToDevice, s));
+    if (int rc = ensure_table(c, freq, n_freq, cum, nullptr, scale_bits, s, st)) return rc;
+    dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
+    ilans_note_launch();
+    CK(launch_encode_var(c.msg.as<uint8_t>(), n, n_lanes, c.table.as<TableDev>(), digit_bits,
+                         lower_bound, c.scratch.as<uint16_t>(), cap, c.words.as<uint64_t>(),
+                         c.states.as<uint32_t>(), c.status.as<DStatus>(), s));
+    DStatus hs;
+    if (int rc = read_dstatus(c.status.as<DStatus>(), s, &hs, st)) return rc;
+    st->max_digits = int32_t(hs.max_digits);
+    if (hs.unenc_index >= 0) {
+        st->index = hs.unenc_index;
+        st->symbol = msg[hs.unenc_index];
+        return st_fail(st, ILANS_ERR_UNENCODABLE, "symbol %d has frequency 0", st->symbol);
+    }
+    uint64_t w = 0;
+    CK(cudaMemcpyAsync(&w, c.words.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (w)
+        CK(cudaMemcpyAsync(digits_out, c.scratch.as<uint16_t>() + (cap - int64_t(w)),
+                           size_t(w) * 2, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(states_out, c.states.p, size_t(n_lanes) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *n_digits = int64_t(w);
+    return ILANS_OK;
+}
+
+extern "C" int ilans_decode_interleaved_var(const uint16_t *payload, int64_t pay_len,
+                                            const uint32_t *states, const uint8_t *slot_sym,
+                                            int64_t n_slots, const uint32_t *freq,
+                                            const uint32_t *cum, int32_t n_freq,
+                                            int32_t scale_bits, int64_t msg_len, int32_t n_lanes,
+                                            int32_t digit_bits, uint32_t lower_bound,
+                                            uint8_t *out, int64_t *consumed,
+                                            uint32_t *trace_states, uint64_t *trace_pos,
+                                            int64_t *groups_done, ilans_status *st) {
+    st_clear(st);
+    if (msg_len < 0 || pay_len < 0) return st_fail(st, ILANS_ERR_VALUE, "negative length");
+    if (int rc = check_variant(digit_bits, lower_bound, scale_bits, n_lanes, st)) return rc;
+    if (n_freq < 0 || n_freq > kMaxSym)
+        return st_fail(st, ILANS_ERR_VALUE, "alphabet size must be in [1, 256]");
+    const int64_t m = int64_t(1) << scale_bits;
+    if (n_slots < m) return st_fail(st, ILANS_ERR_VALUE, "slot table shorter than 2^scale_bits");
+    const bool traced = trace_states && trace_pos && groups_done;
+    Ctx *cp = nullptr;
+    if (int rc = current_device(st, &cp)) return rc;
+    Ctx &c = *cp;
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (int rc = ctx_init(c, st)) return rc;
+    if (msg_len == 0) {
+        *consumed = 0;
+        st->consumed = 0;
+        if (groups_done) *groups_done = 0;
+        return ILANS_OK;
+    }
+    cudaStream_t s = c.stream;
+    const int64_t n_groups = (msg_len + n_lanes - 1) / n_lanes;
+    DecodeTrace dt{nullptr, nullptr, nullptr, 0};
+    if (traced) {
+        CK(c.trace.ensure(size_t(n_groups) * n_lanes * 4 + size_t(n_groups) * 8 + 16));
+        dt.states = c.trace.as<uint32_t>();
+        dt.pos = reinterpret_cast<uint64_t *>(
+            c.trace.as<uint8_t>() + ((size_t(n_groups) * n_lanes * 4 + 7) & ~size_t(7)));
+        CK(c.words.ensure(8));
+        dt.groups = reinterpret_cast<uint64_t *>(c.words.p);
+    }
+    CK(c.payload.ensure(size_t(pay_len) * 2 + 16));
+    CK(c.states.ensure(size_t(n_lanes) * 4));
+    CK(c.out.ensure(size_t(msg_len)));
+    CK(c.consumed.ensure(8));
+    if (pay_len)
+        CK(cudaMemcpyAsync(c.payload.p, payload, size_t(pay_len) * 2, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c.states.p, states, size_t(n_lanes) * 4, cudaMemcpyHostToDevice, s));
+    if (int rc = ensure_table(c, freq, n_freq, cum, slot_sym, scale_bits, s, st)) return rc;
+    dstatus_reset_kernel<<<1, 1, 0, s>>>(c.status.as<DStatus>());
+    ilans_note_launch();
+    CK(launch_decode_var(c.payload.as<uint16_t>(), pay_len, c.states.as<uint32_t>(), msg_len,
+                         n_lanes, c.table.as<TableDev>(), digit_bits, lower_bound,
+                         c.out.as<uint8_t>(), c.consumed.as<uint64_t>(), c.status.as<DStatus>(),
+                         s, dt));
+    DStatus hs;
+    if (int rc = read_dstatus(c.status.as<DStatus>(), s, &hs, st)) return rc;
+    uint64_t used = 0;
+    CK(cudaMemcpyAsync(&used, c.consumed.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (traced) {
+        uint64_t g = 0;
+        CK(cudaMemcpyAsync(&g, dt.groups, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *groups_done = int64_t(g);
+        if (g) {
+            CK(cudaMemcpyAsync(trace_states, dt.states, size_t(g) * n_lanes * 4,
+                               cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(trace_pos, dt.pos, size_t(g) * 8, cudaMemcpyDeviceToHost, s));
+            const int64_t done = int64_t(g) * n_lanes < msg_len ? int64_t(g) * n_lanes : msg_len;
+            CK(cudaMemcpyAsync(out, c.out.p, size_t(done), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+    }
+    st->consumed = int64_t(used);
+    st->max_digits = int32_t(hs.max_digits);
+    if (hs.value_error == ILANS_ERR_FORMAT)
+        return st_fail(st, ILANS_ERR_FORMAT, "renormalization does not terminate; corrupt stream");
+    if (hs.trunc_stream != ~0ull) {
+        st->stream = int64_t(hs.trunc_stream);
+        return st_fail(st, ILANS_ERR_TRUNCATED, "digit stream exhausted mid-decode");
+    }
+    CK(cudaMemcpyAsync(out, c.out.p, size_t(msg_len), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *consumed = int64_t(used);
+    return ILANS_OK;
+}
+
 extern "C" int ilans_quantize(const uint64_t *counts, int32_t n, int32_t scale_bits,
                               uint32_t *freq_out, ilans_status *st) {
     st_clear(st);

@@ -86,4 +86,17 @@ __global__ void chunk_offsets_kernel(const uint32_t *__restrict__ words, int64_t
 
 int sm_count();
 
+
+// variant.cu -- any RenormVariant (the reference's scalar path), one warp
+// per stream, N <= kVarMaxLanes.
+constexpr int kVarMaxLanes = 1024;
+cudaError_t launch_encode_var(const uint8_t *d_msg, int64_t n, int n_lanes,
+                              const TableDev *d_table, int bits, uint32_t lbound,
+                              uint16_t *d_stack, int64_t cap, uint64_t *d_digits,
+                              uint32_t *d_states, DStatus *d_status, cudaStream_t stream);
+cudaError_t launch_decode_var(const uint16_t *d_payload, int64_t plen, const uint32_t *d_states,
+                              int64_t n, int n_lanes, const TableDev *d_table, int bits,
+                              uint32_t lbound, uint8_t *d_out, uint64_t *d_consumed,
+                              DStatus *d_status, cudaStream_t stream, DecodeTrace trace);
+
 }  // namespace ilans

@@ -4,12 +4,10 @@ lanes, mux, backend, errors), with the reference's out-of-scope teaching
 modules (ans, bench, cli, the lane-simulation helpers) loaded inside that
 alias so they call this package (integration/reference_tests_on_package.py).
 
-Everything passes except tests of two deliberate differences
+Everything passes except the tests of one deliberate difference
 (INTEGRATION.md section 3), listed here exactly so any other failure fails
-this test:
-* the pure-Python backend is not shipped (`backend.get("pure")` raises);
-* custom RenormVariants (e.g. the 1-bit "toy" digits) are not coded by the
-  interleaved B200 codec (UnsupportedVariantError)."""
+this test: the pure-Python backend is not shipped (`backend.get("pure")`
+raises; it is the test oracle, never a runtime fallback)."""
 
 import re
 import sys
@@ -35,9 +33,6 @@ EXPECTED_FAILURES = {
     "tests/test_backend.py::TestKernelEquivalence::test_same_errors_on_truncation",
     "tests/test_backend.py::TestKernelEquivalence::test_same_errors_on_bad_symbol",
     "tests/test_cli.py::TestBench::test_bench_pure_backend",
-    # custom (non word16 / byte8) variants in the interleaved coders
-    "tests/test_interleave.py::TestGolden::test_single_lane_recast_toy",
-    "tests/test_interleave.py::TestNegatives::test_unserializable_custom_variant",
 }
 
 

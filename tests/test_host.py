@@ -152,9 +152,11 @@ def test_api_argument_checks_before_device():
         ilb.encode_interleaved([1], t, 1 << 16)
     with pytest.raises(UnencodableSymbolError):
         ilb.encode_interleaved([5], t, 1)
-    toy = rans.RenormVariant("toy-bit", 1, 16)  # custom variants: teaching path, not built
-    with pytest.raises(UnsupportedVariantError):
-        ilb.encode_interleaved([1], t, 1, toy)
+    toy = rans.RenormVariant("toy-bit", 1, 16)  # custom variants: argument checks on the host
+    with pytest.raises(ValueError, match="not a multiple"):
+        ilb.encode_interleaved([1], t, 1, rans.RenormVariant("odd", 1, 10))
+    with pytest.raises(UnencodableSymbolError):
+        ilb.encode_interleaved([7], t, 1, toy)
     c = Container(BYTE8, 2, 1, t, (1 << 23, 1 << 23), np.zeros(0, np.uint8))
     with pytest.raises(UnsupportedVariantError, match="unsupported by lane decoder"):
         ilb.decode_lanes_full(c)
