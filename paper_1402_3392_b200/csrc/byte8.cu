@@ -228,7 +228,67 @@ decode_u8_ring_body(const uint8_t *__restrict__ payload, const uint64_t *__restr
         uint32_t most = 0;
         uint32_t base = 0;
         const uint32_t obuf_sa = smem_addr(obuf);
-        for (; base < len; base += n_lanes) {
+        // Fast path: N = 32, full groups, every initial state in [L, 2^31).
+        // From such a state a pop gives x' >= f (x >> sb) >= 2^(23 - sb) >=
+        // 2^7, so a lane refills 0, 1 or 2 digits ([x' < 2^23] + [x' <
+        // 2^15]: two ballots, no zero-state check) and the refills keep
+        // every state valid.
+        if (n_lanes == 32 && __all_sync(0xffffffffu, x >= kLow8)) {
+            const uint32_t full = len & ~31u;
+            const uint32_t st_sa = obuf_sa + lane;
+#pragma unroll 4
+            for (; base < full; base += 32) {
+                uint32_t s;
+                {
+                    const uint32_t slot = x & mask;
+                    if (PACKED) {
+                        const uint32_t e = packed[slot];
+                        x = (e >> 20) * ((x >> sb) - 4096u) + (e >> 8);
+                        s = e;
+                    } else {
+                        s = slot_sym[slot];
+                        const uint2 d = dec[s];
+                        x = d.x * (x >> sb) + slot - d.y;
+                    }
+                }
+                const bool r1 = x < kLow8, r2 = x < (1u << 15);
+                const uint32_t b1 = __ballot_sync(0xffffffffu, r1);
+                const uint32_t b2 = __ballot_sync(0xffffffffu, r2);
+                const uint32_t tot = __popc(b1) + __popc(b2);
+                if (pos + tot > pend) {
+                    err = ILANS_ERR_TRUNCATED;
+                    break;
+                }
+                const uint32_t q = pos + __popc(b1 & lt) + __popc(b2 & lt);
+                pos += tot;
+                // the lane's digits, most significant first: bytes q, q + 1
+                const uint32_t w0 = lds32(ring_sa + (q & (kRing8 - 4)));
+                const uint32_t w1 = lds32(ring_sa + ((q + 4u) & (kRing8 - 4)));
+                const uint32_t v = __byte_perm(__funnelshift_r(w0, w1, (q & 3u) * 8u), 0u, 0x0123u);
+                const uint32_t sh = r2 ? 16u : 8u;
+                x = r1 ? (x << sh) | (v >> (32u - sh)) : x;
+                most = max(most, r2 ? 2u : (r1 ? 1u : 0u));
+                sts8(st_sa + (base & (kObuf8 - 1)), s);
+                if ((base & 255u) == 224u) {  // a 256-byte half is complete
+                    __syncwarp();
+                    const uint32_t blk = base >> 8;
+                    const uint2 o = reinterpret_cast<const uint2 *>(obuf + (blk & 1) * 256)[lane];
+                    *reinterpret_cast<uint2 *>(outk + (blk << 8) + 8 * lane) = o;
+                    __syncwarp();
+                }
+                if ((pos >> 9) != cur) {  // segments below the cursor are read
+                    __syncwarp();
+                    while (cur < (pos >> 9)) {
+                        ++cur;
+                        issue_seg8(ring_sa, gbase, avail, cur + 3, lane);
+                        cp_async_commit();
+                    }
+                    cp_async_wait<2>();
+                    __syncwarp();
+                }
+            }
+        }
+        for (; !err && base < len; base += n_lanes) {
             const uint32_t left = len - base;
             const bool on = static_cast<uint32_t>(lane) < left && lane < n_lanes;
             uint32_t s = 0;
@@ -401,7 +461,10 @@ encode_u8_ring_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_
         uint32_t most = 0;
         const int groups = (len + n_lanes - 1) / n_lanes;
         int base = (groups - 1) * n_lanes;
-        for (; base >= 0; base -= n_lanes) {
+        // N = 32: the full groups below fast_top take the fast loop after
+        // this one has coded the partial top group (if any)
+        const int fast_top = n_lanes == 32 ? (len & ~31) : 0;
+        for (; base >= fast_top; base -= n_lanes) {
             const int left = len - base;
             const bool on = lane < left && lane < n_lanes;
             const int hs = (base + (left < n_lanes ? left : n_lanes) - 1) >> 9;
@@ -444,6 +507,58 @@ encode_u8_ring_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_
             if (sp >= 2u) sts8(out_sa + ((pe - out_sa - 1u) & (kRing8 - 1)), x >> 8);
             if (sp >= 3u) sts8(out_sa + ((pe - out_sa - 2u) & (kRing8 - 1)), x >> 16);
             if (on) x = enc_push(ctx, x >> (8u * sp), e);
+            most = max(most, sp);
+            if (flushed - top >= 512) {  // drain 512 bytes: 16 per lane
+                __syncwarp();
+                const uint32_t ro = static_cast<uint32_t>(flushed - 512) + lane * 16;
+                uint4 v;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                             : "r"(out_sa + (ro & (kRing8 - 1))));
+                *reinterpret_cast<uint4 *>(o + (flushed - 512) + lane * 16) = v;
+                flushed -= 512;
+                __syncwarp();
+            }
+        }
+        // Fast loop (N = 32, full groups): a state below 2^31 spills at most
+        // two digits (x >> 16 < 2^15 <= f 2^(31 - sb)), so two ballots give
+        // each lane its read-order offset; digits most significant first.
+        for (; !bad && base >= 0; base -= 32) {
+            const int hs = (base + 31) >> 9;
+            if (hs != cur) {  // segment cur consumed: prefetch cur - 4 into its slot
+                __syncwarp();
+                while (cur > hs) {
+                    const int sg = cur - 4;
+                    const bool ok = sg >= 0;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                                     in_sa + static_cast<uint32_t>(sg & 3) * kSeg8 + lane * 16),
+                                 "l"(ok ? g + sg * kSeg8 + lane * 16 : g), "r"(ok ? 16u : 0u)
+                                 : "memory");
+                    cp_async_commit();
+                    --cur;
+                }
+                cp_async_wait<2>();
+                __syncwarp();
+            }
+            const uint2 e = enc[lds8(in_sa + ((base + lane) & (kRing8 - 1)))];
+            if (__any_sync(0xffffffffu, e.x == 0u)) {
+                const uint32_t badmask = __ballot_sync(0xffffffffu, e.x == 0u);
+                if (lane == 0)
+                    atomicMax(&status->unenc_index,
+                              static_cast<long long>(cbase + base + 31 - __clz(badmask)));
+                bad = true;
+                break;
+            }
+            const uint32_t fm1 = e.y & 0xFFFFu;
+            const bool s1 = (x >> thr8) > fm1, s2 = ((x >> 8) >> thr8) > fm1;
+            const uint32_t b1 = __ballot_sync(0xffffffffu, s1);
+            const uint32_t b2 = __ballot_sync(0xffffffffu, s2);
+            top -= __popc(b1) + __popc(b2);
+            const uint32_t p = static_cast<uint32_t>(top) + __popc(b1 & lt) + __popc(b2 & lt);
+            if (s1) sts8(out_sa + (p & (kRing8 - 1)), s2 ? x >> 8 : x);
+            if (s2) sts8(out_sa + ((p + 1u) & (kRing8 - 1)), x);
+            const uint32_t sp = static_cast<uint32_t>(s1) + static_cast<uint32_t>(s2);
+            x = enc_push(ctx, x >> (8u * sp), e);
             most = max(most, sp);
             if (flushed - top >= 512) {  // drain 512 bytes: 16 per lane
                 __syncwarp();
