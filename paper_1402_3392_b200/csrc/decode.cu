@@ -909,7 +909,8 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                    int n_lanes, const TableDev *__restrict__ tab, uint8_t *__restrict__ out,
                    uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
                    DStatus *__restrict__ status) {
-    extern __shared__ __align__(16) uint8_t wsm[];  // dec[256] | slot [2^sb] | ws [N]
+    // dec[256] | slot [2^sb] | ws [N] | payload ring (as the warp kernel's)
+    extern __shared__ __align__(16) uint8_t wsm[];
     const int lane = threadIdx.x;
     const uint32_t lt = lanemask_lt();
     const int sb = static_cast<int>(tab->scale_bits);
@@ -917,6 +918,9 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
     uint2 *dec = reinterpret_cast<uint2 *>(wsm);
     uint8_t *slot_sym = wsm + kMaxSym * sizeof(uint2);
     uint32_t *ws = reinterpret_cast<uint32_t *>(slot_sym + (((size_t(1) << sb) + 15) & ~size_t(15)));
+    uint16_t *ring = reinterpret_cast<uint16_t *>(
+        reinterpret_cast<uint8_t *>(ws) + ((size_t(n_lanes) * 4 + 15) & ~size_t(15)));
+    const uint32_t ring_addr = smem_addr(ring);
     for (int i = lane; i < kMaxSym; i += 32) dec[i] = tab->dec[i];
     for (uint32_t i = lane; i < (1u << sb); i += 32) slot_sym[i] = tab->slot_sym[i];
     const int64_t k = blockIdx.x;
@@ -924,10 +928,20 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
     const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
     const uint64_t woff = offsets[k];
     const uint64_t wlen = offsets[k + 1] - woff;
-    const uint16_t *pay = payload + woff;
+    const uint32_t delta = static_cast<uint32_t>(woff & 7u);
+    // the payload streams through the shared ring (a refill read from global
+    // memory per 32-lane sub-group cost a full memory latency each)
+    SegSrc src{payload + (woff & ~7ull), wlen + delta};
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+        issue_segment(ring, src, q, lane);
+        cp_async_commit();
+    }
     for (int l = lane; l < n_lanes; l += 32) ws[l] = states[k * n_lanes + l];
+    cp_async_wait<2>();
     __syncwarp();
     uint64_t pos = 0;
+    uint64_t cur = 0;  // ring segment holding the cursor (delta + pos)
     bool truncated = false;
     for (int64_t base = 0; base < len && !truncated; base += n_lanes) {
         const int active = (len - base) < n_lanes ? static_cast<int>(len - base) : n_lanes;
@@ -948,14 +962,26 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                 truncated = true;
                 break;
             }
-            if (need) x = (x << 16) | pay[pos + __popc(mk & lt)];
+            if (need)
+                x = (x << 16) |
+                    ring_load(ring_addr, static_cast<uint32_t>(delta + pos + __popc(mk & lt)) << 1);
             pos += cnt;
             if (on) {
                 ws[l] = x;
                 out[cbase + base + l] = static_cast<uint8_t>(s);
             }
+            const uint64_t seg = (delta + pos) / kSegWords;
+            if (seg != cur) {  // segment cur fully read: refill its slot
+                cur = seg;
+                __syncwarp();
+                issue_segment(ring, src, static_cast<uint32_t>(cur + 3), lane);
+                cp_async_commit();
+                cp_async_wait<2>();
+                __syncwarp();
+            }
         }
     }
+    cp_async_wait<0>();
     __syncwarp();
     if (lane == 0) {
         if (truncated) atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
@@ -1067,7 +1093,7 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
     if (n_lanes > 32 && n_lanes <= kWideMax && !trace.states && !trace.stats) {
         const size_t smem = kMaxSym * sizeof(uint2) +
                             (((size_t(1) << scale_bits) + 15) & ~size_t(15)) +
-                            size_t(n_lanes) * 4;
+                            ((size_t(n_lanes) * 4 + 15) & ~size_t(15)) + kRingAllocBytes;
         smem_limit(reinterpret_cast<const void *>(decode_wide_kernel), int(smem));
         decode_wide_kernel<<<static_cast<unsigned>(n_chunks), 32, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table, d_out,

@@ -742,13 +742,26 @@ encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     int64_t top = len;
     bool bad = false;
     uint32_t most = 0;
-    for (int64_t gi = (len + n_lanes - 1) / n_lanes - 1; gi >= 0 && !bad; --gi) {
+    // the symbols of the group below are loaded one group ahead (a load
+    // from global memory per sub-group cost a full memory latency each);
+    // N <= 64: at most two 32-lane sub-groups, sym0 / sym1
+    const int64_t g_top = (len + n_lanes - 1) / n_lanes - 1;
+    auto load_syms = [&](int64_t gi, uint32_t &a, uint32_t &b) {
+        const int64_t base = gi * n_lanes;
+        a = (base + lane < len && lane < n_lanes) ? g[base + lane] : 0u;
+        b = (base + 32 + lane < len && 32 + lane < n_lanes) ? g[base + 32 + lane] : 0u;
+    };
+    uint32_t sym0 = 0, sym1 = 0;
+    if (g_top >= 0) load_syms(g_top, sym0, sym1);
+    for (int64_t gi = g_top; gi >= 0 && !bad; --gi) {
         const int64_t base = gi * n_lanes;
         const int active = (len - base) < n_lanes ? static_cast<int>(len - base) : n_lanes;
+        uint32_t nx0 = 0, nx1 = 0;
+        if (gi > 0) load_syms(gi - 1, nx0, nx1);
         for (int j0 = ((active - 1) >> 5) << 5; j0 >= 0; j0 -= 32) {
             const int l = j0 + lane;
             const bool on = l < active;
-            const uint2 e = enc[on ? g[base + l] : 0u];
+            const uint2 e = enc[on ? (j0 ? sym1 : sym0) : 0u];
             const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.x == 0u);
             if (badmask) {  // the highest offending index (the reference walks down)
                 if (lane == 0)
@@ -770,6 +783,8 @@ encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             if (stats && spill) most = max(most, enc_spill(ctx, x, e) ? 2u : 1u);
             if (on) wws[l] = enc_push(ctx, x, e);
         }
+        sym0 = nx0;
+        sym1 = nx1;
     }
     __syncwarp();
     if (stats) {
