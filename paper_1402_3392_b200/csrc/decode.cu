@@ -898,10 +898,11 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
         for (int l = lo; l < lo + per && l < n_lanes; ++l) final_states[k * n_lanes + l] = ws[l];
 }
 
-// 32 < N <= kWideMax, no trace: one warp per stream walks each group in
-// sub-groups of 32 lanes (lanes ascending, so the refill order is the
-// reference's), the lane states in shared memory. A sub-group costs about
-// what an N = 32 group does, with no CTA-wide scan per group.
+// 32 < N <= kWideMax, no trace: one warp per stream, each thread holds the
+// states of lanes `lane` and `32 + lane` in registers. Both halves of a group
+// look up their symbols together; the second half's refill positions start
+// after the first half's count (lanes ascending: the reference's order), so
+// a group costs about one N = 32 group plus a second popc.
 constexpr int kWideMax = 64;  // beyond this the CTA kernel wins (measured)
 __global__ void __launch_bounds__(32)
 decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
@@ -909,7 +910,7 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
                    int n_lanes, const TableDev *__restrict__ tab, uint8_t *__restrict__ out,
                    uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
                    DStatus *__restrict__ status) {
-    // dec[256] | slot [2^sb] | ws [N] | payload ring (as the warp kernel's)
+    // dec[256] | slot [2^sb] | payload ring (as the warp kernel's)
     extern __shared__ __align__(16) uint8_t wsm[];
     const int lane = threadIdx.x;
     const uint32_t lt = lanemask_lt();
@@ -917,9 +918,7 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
     const uint32_t mask = (1u << sb) - 1u;
     uint2 *dec = reinterpret_cast<uint2 *>(wsm);
     uint8_t *slot_sym = wsm + kMaxSym * sizeof(uint2);
-    uint32_t *ws = reinterpret_cast<uint32_t *>(slot_sym + (((size_t(1) << sb) + 15) & ~size_t(15)));
-    uint16_t *ring = reinterpret_cast<uint16_t *>(
-        reinterpret_cast<uint8_t *>(ws) + ((size_t(n_lanes) * 4 + 15) & ~size_t(15)));
+    uint16_t *ring = reinterpret_cast<uint16_t *>(slot_sym + (((size_t(1) << sb) + 15) & ~size_t(15)));
     const uint32_t ring_addr = smem_addr(ring);
     for (int i = lane; i < kMaxSym; i += 32) dec[i] = tab->dec[i];
     for (uint32_t i = lane; i < (1u << sb); i += 32) slot_sym[i] = tab->slot_sym[i];
@@ -929,56 +928,56 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
     const uint64_t woff = offsets[k];
     const uint64_t wlen = offsets[k + 1] - woff;
     const uint32_t delta = static_cast<uint32_t>(woff & 7u);
-    // the payload streams through the shared ring (a refill read from global
-    // memory per 32-lane sub-group cost a full memory latency each)
+    // the payload streams through the shared ring
     SegSrc src{payload + (woff & ~7ull), wlen + delta};
 #pragma unroll
     for (uint32_t q = 0; q < 4; ++q) {
         issue_segment(ring, src, q, lane);
         cp_async_commit();
     }
-    for (int l = lane; l < n_lanes; l += 32) ws[l] = states[k * n_lanes + l];
+    const int hi_lane = 32 + lane;
+    uint32_t x0 = states[k * n_lanes + lane];
+    uint32_t x1 = hi_lane < n_lanes ? states[k * n_lanes + hi_lane] : 0u;
     cp_async_wait<2>();
     __syncwarp();
     uint64_t pos = 0;
     uint64_t cur = 0;  // ring segment holding the cursor (delta + pos)
     bool truncated = false;
-    for (int64_t base = 0; base < len && !truncated; base += n_lanes) {
+    uint8_t *o = out + cbase;
+    for (int64_t base = 0; base < len; base += n_lanes) {
         const int active = (len - base) < n_lanes ? static_cast<int>(len - base) : n_lanes;
-        for (int j0 = 0; j0 < active; j0 += 32) {
-            const int l = j0 + lane;
-            const bool on = l < active;
-            uint32_t x = on ? ws[l] : 0u, s = 0;
-            if (on) {
-                const uint32_t slot = x & mask;
-                s = slot_sym[slot];
-                const uint2 d = dec[s];
-                x = d.x * (x >> sb) + slot - d.y;
-            }
-            const bool need = on && x < kLow;
-            const uint32_t mk = __ballot_sync(0xffffffffu, need);
-            const uint32_t cnt = __popc(mk);
-            if (pos + cnt > wlen) {
-                truncated = true;
-                break;
-            }
-            if (need)
-                x = (x << 16) |
-                    ring_load(ring_addr, static_cast<uint32_t>(delta + pos + __popc(mk & lt)) << 1);
-            pos += cnt;
-            if (on) {
-                ws[l] = x;
-                out[cbase + base + l] = static_cast<uint8_t>(s);
-            }
-            const uint64_t seg = (delta + pos) / kSegWords;
-            if (seg != cur) {  // segment cur fully read: refill its slot
-                cur = seg;
-                __syncwarp();
-                issue_segment(ring, src, static_cast<uint32_t>(cur + 3), lane);
-                cp_async_commit();
-                cp_async_wait<2>();
-                __syncwarp();
-            }
+        const bool on0 = lane < active, on1 = hi_lane < active;
+        // both lookups unconditional (lanes past the group decode their
+        // stale state and are masked below), so the two chains overlap
+        const uint32_t slot0 = x0 & mask, slot1 = x1 & mask;
+        const uint32_t s0 = slot_sym[slot0], s1 = slot_sym[slot1];
+        const uint2 d0 = dec[s0], d1 = dec[s1];
+        uint32_t y0 = d0.x * (x0 >> sb) + slot0 - d0.y;
+        uint32_t y1 = d1.x * (x1 >> sb) + slot1 - d1.y;
+        const bool need0 = on0 && y0 < kLow, need1 = on1 && y1 < kLow;
+        const uint32_t mk0 = __ballot_sync(0xffffffffu, need0);
+        const uint32_t mk1 = __ballot_sync(0xffffffffu, need1);
+        const uint32_t cnt0 = __popc(mk0), cnt = cnt0 + __popc(mk1);
+        if (pos + cnt > wlen) {
+            truncated = true;
+            break;
+        }
+        const uint32_t c0 = static_cast<uint32_t>(delta + pos);
+        if (need0) y0 = (y0 << 16) | ring_load(ring_addr, (c0 + __popc(mk0 & lt)) << 1);
+        if (need1) y1 = (y1 << 16) | ring_load(ring_addr, (c0 + cnt0 + __popc(mk1 & lt)) << 1);
+        x0 = on0 ? y0 : x0;
+        x1 = on1 ? y1 : x1;
+        if (on0) o[base + lane] = static_cast<uint8_t>(s0);
+        if (on1) o[base + hi_lane] = static_cast<uint8_t>(s1);
+        pos += cnt;
+        const uint64_t seg = (delta + pos) / kSegWords;
+        if (seg != cur) {  // segment cur fully read: refill its slot
+            cur = seg;
+            __syncwarp();
+            issue_segment(ring, src, static_cast<uint32_t>(cur + 3), lane);
+            cp_async_commit();
+            cp_async_wait<2>();
+            __syncwarp();
         }
     }
     cp_async_wait<0>();
@@ -987,8 +986,10 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         if (truncated) atomicMin(&status->trunc_stream, static_cast<unsigned long long>(k));
         if (consumed) consumed[k] = pos;
     }
-    if (final_states)
-        for (int l = lane; l < n_lanes; l += 32) final_states[k * n_lanes + l] = ws[l];
+    if (final_states) {
+        final_states[k * n_lanes + lane] = x0;
+        if (hi_lane < n_lanes) final_states[k * n_lanes + hi_lane] = x1;
+    }
 }
 
 static size_t decode_lut_bytes(int scale_bits, int kind) {
@@ -1092,8 +1093,7 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
     if (d_slot_words && n_lanes > 32) return cudaErrorInvalidValue;  // chunked streams: N <= 32
     if (n_lanes > 32 && n_lanes <= kWideMax && !trace.states && !trace.stats) {
         const size_t smem = kMaxSym * sizeof(uint2) +
-                            (((size_t(1) << scale_bits) + 15) & ~size_t(15)) +
-                            ((size_t(n_lanes) * 4 + 15) & ~size_t(15)) + kRingAllocBytes;
+                            (((size_t(1) << scale_bits) + 15) & ~size_t(15)) + kRingAllocBytes;
         smem_limit(reinterpret_cast<const void *>(decode_wide_kernel), int(smem));
         decode_wide_kernel<<<static_cast<unsigned>(n_chunks), 32, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table, d_out,

@@ -717,83 +717,137 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
     }
 }
 
-// 32 < N <= kWideMaxE: one warp per stream walks each group backwards in
-// sub-groups of 32 lanes (highest first; inside one, the packed store puts
-// the spills in ascending lane order), the lane states in shared memory.
+// 32 < N <= kWideMaxE (and the instrumented N <= 32 calls): one warp per
+// stream, each thread holds the states of lanes `lane` and `32 + lane` in
+// registers. A group is walked backwards: the upper half's spills are stored
+// above the lower half's, each half in ascending lane order (the reference's
+// payload order), both halves' records looked up together. The message
+// streams downwards through an 8 x 512 B shared ring (cp.async, issued six
+// segments ahead; a symbol read from global memory one group ahead left the
+// warp waiting a full memory latency per group), RING = the chunk bases are
+// reachable 16-byte aligned (the message pointer is).
 constexpr int kWideMaxE = 64;  // beyond this the CTA kernel wins (measured)
+constexpr int kWideSegs = 8;
+template <bool RING>
 __global__ void __launch_bounds__(32)
 encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len, int n_lanes,
                    const TableDev *__restrict__ tab, uint16_t *__restrict__ scratch,
                    uint32_t *__restrict__ chunk_words, uint32_t *__restrict__ states_out,
                    DStatus *__restrict__ status, int stats) {
     __shared__ uint2 enc[kMaxSym];
-    extern __shared__ __align__(16) uint32_t wws[];  // lane states [N]
+    __shared__ __align__(16) uint8_t mring[RING ? kWideSegs * kInSeg : 16];
     const int lane = threadIdx.x;
+    const int hi_lane = 32 + lane;
     const uint32_t lt = lanemask_lt();
-    for (int i = lane; i < kMaxSym; i += 32) enc[i] = tab->enc[i];
-    const EncCtx ctx(tab->scale_bits);
     const int64_t k = blockIdx.x;
     const int64_t cbase = k * chunk_len;
     const int64_t len = (n - cbase) < chunk_len ? (n - cbase) : chunk_len;
     const uint8_t *g = msg + cbase;
     uint16_t *out = scratch + cbase;
-    for (int l = lane; l < n_lanes; l += 32) wws[l] = kLow;
-    __syncwarp();
+    // ring: byte i of the chunk sits at (delta + i) mod the ring
+    const uint32_t delta = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(g) & 15u);
+    const uint8_t *ga = g - delta;
+    const int64_t avail = len + delta;
+    const uint32_t mring_sa = smem_addr(mring);
+    auto issue = [&](int64_t seg) {
+        if (RING) {
+            const int64_t b0 = seg * kInSeg + lane * 16;
+            uint32_t bytes = 0;
+            if (seg >= 0 && b0 < avail) bytes = (avail - b0) >= 16 ? 16u : static_cast<uint32_t>(avail - b0);
+            cp_async16(mring + (static_cast<uint32_t>(seg) & (kWideSegs - 1)) * kInSeg + lane * 16,
+                       bytes ? ga + b0 : ga, bytes);
+            cp_async_commit();
+        }
+    };
+    const int64_t g_top = (len + n_lanes - 1) / n_lanes - 1;
+    int64_t cur = g_top >= 0 ? (delta + g_top * n_lanes) / kInSeg : 0;  // segment of the group's low byte
+    if (RING) {
+        for (int q = 1; q >= 2 - kWideSegs; --q) issue(cur + q);
+    }
+    for (int i = lane; i < kMaxSym; i += 32) enc[i] = tab->enc[i];
+    const EncCtx ctx(tab->scale_bits);
+    uint32_t x0 = kLow, x1 = kLow;
     int64_t top = len;
     bool bad = false;
     uint32_t most = 0;
-    // the symbols of the group below are loaded one group ahead (a load
-    // from global memory per sub-group cost a full memory latency each);
-    // N <= 64: at most two 32-lane sub-groups, sym0 / sym1
-    const int64_t g_top = (len + n_lanes - 1) / n_lanes - 1;
+    if (RING) cp_async_wait<kWideSegs - 3>();  // segments cur + 1, cur, cur - 1
+    __syncwarp();
+    // the symbols of the group below are read one group ahead
     auto load_syms = [&](int64_t gi, uint32_t &a, uint32_t &b) {
         const int64_t base = gi * n_lanes;
-        a = (base + lane < len && lane < n_lanes) ? g[base + lane] : 0u;
-        b = (base + 32 + lane < len && 32 + lane < n_lanes) ? g[base + 32 + lane] : 0u;
+        if (RING) {
+            const uint32_t o = static_cast<uint32_t>(delta + base);
+            a = (base + lane < len && lane < n_lanes)
+                    ? lds_u8(mring_sa + ((o + lane) & (kWideSegs * kInSeg - 1))) : 0u;
+            b = (base + hi_lane < len && hi_lane < n_lanes)
+                    ? lds_u8(mring_sa + ((o + hi_lane) & (kWideSegs * kInSeg - 1))) : 0u;
+        } else {
+            a = (base + lane < len && lane < n_lanes) ? g[base + lane] : 0u;
+            b = (base + hi_lane < len && hi_lane < n_lanes) ? g[base + hi_lane] : 0u;
+        }
     };
     uint32_t sym0 = 0, sym1 = 0;
     if (g_top >= 0) load_syms(g_top, sym0, sym1);
-    for (int64_t gi = g_top; gi >= 0 && !bad; --gi) {
+    for (int64_t gi = g_top; gi >= 0; --gi) {
         const int64_t base = gi * n_lanes;
         const int active = (len - base) < n_lanes ? static_cast<int>(len - base) : n_lanes;
+        if (RING) {
+            const int64_t seg = (delta + base) / kInSeg;
+            if (seg != cur) {  // one segment lower: its slot's old segment (cur + 2) is done
+                cur = seg;
+                __syncwarp();
+                issue(cur + 2 - kWideSegs);
+                cp_async_wait<kWideSegs - 3>();  // segment cur - 1 (the next group's) landed
+                __syncwarp();
+            }
+        }
         uint32_t nx0 = 0, nx1 = 0;
         if (gi > 0) load_syms(gi - 1, nx0, nx1);
-        for (int j0 = ((active - 1) >> 5) << 5; j0 >= 0; j0 -= 32) {
-            const int l = j0 + lane;
-            const bool on = l < active;
-            const uint2 e = enc[on ? (j0 ? sym1 : sym0) : 0u];
-            const uint32_t badmask = __ballot_sync(0xffffffffu, on && e.x == 0u);
-            if (badmask) {  // the highest offending index (the reference walks down)
-                if (lane == 0)
-                    atomicMax(&status->unenc_index,
-                              static_cast<long long>(cbase + base + j0 + 31 - __clz(badmask)));
-                bad = true;
-                break;
-            }
-            uint32_t x = on ? wws[l] : 0u;
-            const bool spill = on && enc_spill(ctx, x, e);
-            const uint32_t mk = __ballot_sync(0xffffffffu, spill);
-            top -= __popc(mk);
-            if (spill) {
-                out[top + __popc(mk & lt)] = static_cast<uint16_t>(x & 0xFFFFu);
-                x >>= 16;
-            }
-            // stats: digits this symbol moves under the reference's spill
-            // loop (rans.py:284-287): one per pass while x >= threshold
-            if (stats && spill) most = max(most, enc_spill(ctx, x, e) ? 2u : 1u);
-            if (on) wws[l] = enc_push(ctx, x, e);
+        const bool on0 = lane < active, on1 = hi_lane < active;
+        const uint2 e0 = enc[sym0];
+        const uint2 e1 = enc[sym1];
+        const uint32_t bad1 = __ballot_sync(0xffffffffu, on1 && e1.x == 0u);
+        const uint32_t bad0 = __ballot_sync(0xffffffffu, on0 && e0.x == 0u);
+        if (bad0 | bad1) {  // the highest offending index (the reference walks down)
+            if (lane == 0)
+                atomicMax(&status->unenc_index,
+                          static_cast<long long>(cbase + base + (bad1 ? 63 - __clz(bad1)
+                                                                      : 31 - __clz(bad0))));
+            bad = true;
+            break;
         }
+        const bool sp1 = on1 && enc_spill(ctx, x1, e1);
+        const bool sp0 = on0 && enc_spill(ctx, x0, e0);
+        const uint32_t mk1 = __ballot_sync(0xffffffffu, sp1);
+        const uint32_t mk0 = __ballot_sync(0xffffffffu, sp0);
+        const int64_t top1 = top - __popc(mk1);
+        top = top1 - __popc(mk0);
+        if (sp1) out[top1 + __popc(mk1 & lt)] = static_cast<uint16_t>(x1 & 0xFFFFu);
+        if (sp0) out[top + __popc(mk0 & lt)] = static_cast<uint16_t>(x0 & 0xFFFFu);
+        const uint32_t z1 = sp1 ? x1 >> 16 : x1;
+        const uint32_t z0 = sp0 ? x0 >> 16 : x0;
+        // stats: digits this symbol moves under the reference's spill loop
+        // (rans.py:284-287): one per pass while x >= threshold
+        if (stats) {
+            if (sp1) most = max(most, enc_spill(ctx, z1, e1) ? 2u : 1u);
+            if (sp0) most = max(most, enc_spill(ctx, z0, e0) ? 2u : 1u);
+        }
+        const uint32_t p1 = enc_push(ctx, z1, e1);
+        const uint32_t p0 = enc_push(ctx, z0, e0);
+        x1 = on1 ? p1 : x1;
+        x0 = on0 ? p0 : x0;
         sym0 = nx0;
         sym1 = nx1;
     }
-    __syncwarp();
+    if (RING) cp_async_wait<0>();
     if (stats) {
         most = __reduce_max_sync(0xffffffffu, most);
         if (lane == 0 && most) atomicMax(&status->max_digits, most);
     }
     if (!bad) {
         if (lane == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
-        for (int l = lane; l < n_lanes; l += 32) states_out[k * n_lanes + l] = wws[l];
+        if (lane < n_lanes) states_out[k * n_lanes + lane] = x0;
+        if (hi_lane < n_lanes) states_out[k * n_lanes + hi_lane] = x1;
     }
 }
 
@@ -806,7 +860,11 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
     // stats (instrumented calls): the one-warp sub-group walk measures the
     // digits per symbol for every N <= 64, the CTA kernel beyond
     if ((n_lanes > 32 || stats) && n_lanes <= kWideMaxE) {
-        encode_wide_kernel<<<static_cast<unsigned>(n_chunks), 32, size_t(n_lanes) * 4, stream>>>(
+        // the shared message ring reads each chunk from its 16-byte aligned
+        // base below it: only when that stays inside the message
+        auto kernel = (reinterpret_cast<uintptr_t>(d_msg) & 15u) == 0 ? encode_wide_kernel<true>
+                                                                        : encode_wide_kernel<false>;
+        kernel<<<static_cast<unsigned>(n_chunks), 32, 0, stream>>>(
             d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states, d_status,
             stats ? 1 : 0);
     } else if (n_lanes > 32) {
