@@ -899,11 +899,13 @@ decode_block_kernel(const uint16_t *__restrict__ payload, const uint64_t *__rest
 }
 
 // 32 < N <= kWideMax, no trace: one warp per stream, each thread holds the
-// states of lanes `lane` and `32 + lane` in registers. Both halves of a group
-// look up their symbols together; the second half's refill positions start
-// after the first half's count (lanes ascending: the reference's order), so
-// a group costs about one N = 32 group plus a second popc.
-constexpr int kWideMax = 64;  // beyond this the CTA kernel wins (measured)
+// states of lanes lane, 32 + lane, ... (S sub-groups of 32) in registers. All
+// sub-groups of a group look up their symbols together; sub-group j's refill
+// positions start after the counts of sub-groups 0..j-1 (lanes ascending: the
+// reference's order), so a group costs about one N = 32 group plus S - 1
+// more ballots / popcs.
+constexpr int kWideMax = 256;  // beyond this the CTA kernel wins (measured)
+template <int S>
 __global__ void __launch_bounds__(32)
 decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restrict__ offsets,
                    const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -928,16 +930,18 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
     const uint64_t woff = offsets[k];
     const uint64_t wlen = offsets[k + 1] - woff;
     const uint32_t delta = static_cast<uint32_t>(woff & 7u);
-    // the payload streams through the shared ring
+    // the payload streams through the shared ring (<= 256 words per group:
+    // at most one segment per group)
     SegSrc src{payload + (woff & ~7ull), wlen + delta};
 #pragma unroll
     for (uint32_t q = 0; q < 4; ++q) {
         issue_segment(ring, src, q, lane);
         cp_async_commit();
     }
-    const int hi_lane = 32 + lane;
-    uint32_t x0 = states[k * n_lanes + lane];
-    uint32_t x1 = hi_lane < n_lanes ? states[k * n_lanes + hi_lane] : 0u;
+    uint32_t x[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+        x[j] = 32 * j + lane < n_lanes ? states[k * n_lanes + 32 * j + lane] : 0u;
     cp_async_wait<2>();
     __syncwarp();
     uint64_t pos = 0;
@@ -946,29 +950,36 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
     uint8_t *o = out + cbase;
     for (int64_t base = 0; base < len; base += n_lanes) {
         const int active = (len - base) < n_lanes ? static_cast<int>(len - base) : n_lanes;
-        const bool on0 = lane < active, on1 = hi_lane < active;
-        // both lookups unconditional (lanes past the group decode their
-        // stale state and are masked below), so the two chains overlap
-        const uint32_t slot0 = x0 & mask, slot1 = x1 & mask;
-        const uint32_t s0 = slot_sym[slot0], s1 = slot_sym[slot1];
-        const uint2 d0 = dec[s0], d1 = dec[s1];
-        uint32_t y0 = d0.x * (x0 >> sb) + slot0 - d0.y;
-        uint32_t y1 = d1.x * (x1 >> sb) + slot1 - d1.y;
-        const bool need0 = on0 && y0 < kLow, need1 = on1 && y1 < kLow;
-        const uint32_t mk0 = __ballot_sync(0xffffffffu, need0);
-        const uint32_t mk1 = __ballot_sync(0xffffffffu, need1);
-        const uint32_t cnt0 = __popc(mk0), cnt = cnt0 + __popc(mk1);
+        // lookups unconditional (lanes past the group decode their stale
+        // state and are masked below), so the S chains overlap
+        uint32_t sy[S], y[S], mk[S];
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            const uint32_t slot = x[j] & mask;
+            sy[j] = slot_sym[slot];
+            const uint2 d = dec[sy[j]];
+            y[j] = d.x * (x[j] >> sb) + slot - d.y;
+        }
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            mk[j] = __ballot_sync(0xffffffffu, 32 * j + lane < active && y[j] < kLow);
+            cnt += __popc(mk[j]);
+        }
         if (pos + cnt > wlen) {
             truncated = true;
             break;
         }
-        const uint32_t c0 = static_cast<uint32_t>(delta + pos);
-        if (need0) y0 = (y0 << 16) | ring_load(ring_addr, (c0 + __popc(mk0 & lt)) << 1);
-        if (need1) y1 = (y1 << 16) | ring_load(ring_addr, (c0 + cnt0 + __popc(mk1 & lt)) << 1);
-        x0 = on0 ? y0 : x0;
-        x1 = on1 ? y1 : x1;
-        if (on0) o[base + lane] = static_cast<uint8_t>(s0);
-        if (on1) o[base + hi_lane] = static_cast<uint8_t>(s1);
+        uint32_t c = static_cast<uint32_t>(delta + pos);
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            if ((mk[j] >> lane) & 1u)
+                y[j] = (y[j] << 16) | ring_load(ring_addr, (c + __popc(mk[j] & lt)) << 1);
+            c += __popc(mk[j]);
+            const bool on = 32 * j + lane < active;
+            x[j] = on ? y[j] : x[j];
+            if (on) o[base + 32 * j + lane] = static_cast<uint8_t>(sy[j]);
+        }
         pos += cnt;
         const uint64_t seg = (delta + pos) / kSegWords;
         if (seg != cur) {  // segment cur fully read: refill its slot
@@ -987,8 +998,9 @@ decode_wide_kernel(const uint16_t *__restrict__ payload, const uint64_t *__restr
         if (consumed) consumed[k] = pos;
     }
     if (final_states) {
-        final_states[k * n_lanes + lane] = x0;
-        if (hi_lane < n_lanes) final_states[k * n_lanes + hi_lane] = x1;
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+            if (32 * j + lane < n_lanes) final_states[k * n_lanes + 32 * j + lane] = x[j];
     }
 }
 
@@ -1094,8 +1106,10 @@ cudaError_t launch_decode(const uint16_t *d_payload, const uint64_t *d_word_offs
     if (n_lanes > 32 && n_lanes <= kWideMax && !trace.states && !trace.stats) {
         const size_t smem = kMaxSym * sizeof(uint2) +
                             (((size_t(1) << scale_bits) + 15) & ~size_t(15)) + kRingAllocBytes;
-        smem_limit(reinterpret_cast<const void *>(decode_wide_kernel), int(smem));
-        decode_wide_kernel<<<static_cast<unsigned>(n_chunks), 32, smem, stream>>>(
+        auto kernel = n_lanes <= 64 ? decode_wide_kernel<2>
+                    : n_lanes <= 128 ? decode_wide_kernel<4> : decode_wide_kernel<8>;
+        smem_limit(reinterpret_cast<const void *>(kernel), int(smem));
+        kernel<<<static_cast<unsigned>(n_chunks), 32, smem, stream>>>(
             d_payload, d_word_offsets, d_states, n, chunk_len, n_lanes, d_table, d_out,
             d_consumed, d_final_states, d_status);
         ilans_note_launch();

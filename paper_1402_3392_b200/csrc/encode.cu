@@ -718,26 +718,26 @@ encode_block_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_le
 }
 
 // 32 < N <= kWideMaxE (and the instrumented N <= 32 calls): one warp per
-// stream, each thread holds the states of lanes `lane` and `32 + lane` in
-// registers. A group is walked backwards: the upper half's spills are stored
-// above the lower half's, each half in ascending lane order (the reference's
-// payload order), both halves' records looked up together. The message
-// streams downwards through an 8 x 512 B shared ring (cp.async, issued six
-// segments ahead; a symbol read from global memory one group ahead left the
-// warp waiting a full memory latency per group), RING = the chunk bases are
-// reachable 16-byte aligned (the message pointer is).
-constexpr int kWideMaxE = 64;  // beyond this the CTA kernel wins (measured)
+// stream, each thread holds the states of lanes lane, 32 + lane, ... (S
+// sub-groups of 32) in registers. A group is walked backwards: a higher
+// sub-group's spills are stored above a lower one's, each sub-group in
+// ascending lane order (the reference's payload order), all records looked
+// up together. The message streams downwards through an 8 x 512 B shared
+// ring (cp.async, issued six segments ahead; a symbol read from global
+// memory one group ahead left the warp waiting a full memory latency per
+// group). The message pointer is 16-byte aligned (both callers' buffers
+// are), so each chunk's aligned base below it lies inside the message.
+constexpr int kWideMaxE = 256;  // beyond this the CTA kernel wins (measured)
 constexpr int kWideSegs = 8;
-template <bool RING>
+template <int S>
 __global__ void __launch_bounds__(32)
 encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len, int n_lanes,
                    const TableDev *__restrict__ tab, uint16_t *__restrict__ scratch,
                    uint32_t *__restrict__ chunk_words, uint32_t *__restrict__ states_out,
                    DStatus *__restrict__ status, int stats) {
     __shared__ uint2 enc[kMaxSym];
-    __shared__ __align__(16) uint8_t mring[RING ? kWideSegs * kInSeg : 16];
+    __shared__ __align__(16) uint8_t mring[kWideSegs * kInSeg];
     const int lane = threadIdx.x;
-    const int hi_lane = 32 + lane;
     const uint32_t lt = lanemask_lt();
     const int64_t k = blockIdx.x;
     const int64_t cbase = k * chunk_len;
@@ -750,104 +750,104 @@ encode_wide_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     const int64_t avail = len + delta;
     const uint32_t mring_sa = smem_addr(mring);
     auto issue = [&](int64_t seg) {
-        if (RING) {
-            const int64_t b0 = seg * kInSeg + lane * 16;
-            uint32_t bytes = 0;
-            if (seg >= 0 && b0 < avail) bytes = (avail - b0) >= 16 ? 16u : static_cast<uint32_t>(avail - b0);
-            cp_async16(mring + (static_cast<uint32_t>(seg) & (kWideSegs - 1)) * kInSeg + lane * 16,
-                       bytes ? ga + b0 : ga, bytes);
-            cp_async_commit();
-        }
+        const int64_t b0 = seg * kInSeg + lane * 16;
+        uint32_t bytes = 0;
+        if (seg >= 0 && b0 < avail) bytes = (avail - b0) >= 16 ? 16u : static_cast<uint32_t>(avail - b0);
+        cp_async16(mring + (static_cast<uint32_t>(seg) & (kWideSegs - 1)) * kInSeg + lane * 16,
+                   bytes ? ga + b0 : ga, bytes);
+        cp_async_commit();
     };
+    // groups <= 256 bytes < a segment: the low byte's segment steps down by
+    // at most one per group, a group spans at most two segments
     const int64_t g_top = (len + n_lanes - 1) / n_lanes - 1;
     int64_t cur = g_top >= 0 ? (delta + g_top * n_lanes) / kInSeg : 0;  // segment of the group's low byte
-    if (RING) {
-        for (int q = 1; q >= 2 - kWideSegs; --q) issue(cur + q);
-    }
+    for (int q = 1; q >= 2 - kWideSegs; --q) issue(cur + q);
     for (int i = lane; i < kMaxSym; i += 32) enc[i] = tab->enc[i];
     const EncCtx ctx(tab->scale_bits);
-    uint32_t x0 = kLow, x1 = kLow;
+    uint32_t x[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) x[j] = kLow;
     int64_t top = len;
     bool bad = false;
     uint32_t most = 0;
-    if (RING) cp_async_wait<kWideSegs - 3>();  // segments cur + 1, cur, cur - 1
+    cp_async_wait<kWideSegs - 3>();  // segments cur + 1, cur, cur - 1
     __syncwarp();
     // the symbols of the group below are read one group ahead
-    auto load_syms = [&](int64_t gi, uint32_t &a, uint32_t &b) {
+    auto load_syms = [&](int64_t gi, uint32_t *sy) {
         const int64_t base = gi * n_lanes;
-        if (RING) {
-            const uint32_t o = static_cast<uint32_t>(delta + base);
-            a = (base + lane < len && lane < n_lanes)
-                    ? lds_u8(mring_sa + ((o + lane) & (kWideSegs * kInSeg - 1))) : 0u;
-            b = (base + hi_lane < len && hi_lane < n_lanes)
-                    ? lds_u8(mring_sa + ((o + hi_lane) & (kWideSegs * kInSeg - 1))) : 0u;
-        } else {
-            a = (base + lane < len && lane < n_lanes) ? g[base + lane] : 0u;
-            b = (base + hi_lane < len && hi_lane < n_lanes) ? g[base + hi_lane] : 0u;
+        const uint32_t o = static_cast<uint32_t>(delta + base);
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            const int l = 32 * j + lane;
+            const bool in = base + l < len && l < n_lanes;
+            sy[j] = in ? lds_u8(mring_sa + ((o + l) & (kWideSegs * kInSeg - 1))) : 0u;
         }
     };
-    uint32_t sym0 = 0, sym1 = 0;
-    if (g_top >= 0) load_syms(g_top, sym0, sym1);
+    uint32_t sym[S], nx[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) sym[j] = nx[j] = 0;
+    if (g_top >= 0) load_syms(g_top, sym);
     for (int64_t gi = g_top; gi >= 0; --gi) {
         const int64_t base = gi * n_lanes;
         const int active = (len - base) < n_lanes ? static_cast<int>(len - base) : n_lanes;
-        if (RING) {
-            const int64_t seg = (delta + base) / kInSeg;
-            if (seg != cur) {  // one segment lower: its slot's old segment (cur + 2) is done
-                cur = seg;
-                __syncwarp();
-                issue(cur + 2 - kWideSegs);
-                cp_async_wait<kWideSegs - 3>();  // segment cur - 1 (the next group's) landed
-                __syncwarp();
-            }
+        const int64_t seg = (delta + base) / kInSeg;
+        if (seg != cur) {  // one segment lower: its slot's old segment (cur + 2) is done
+            cur = seg;
+            __syncwarp();
+            issue(cur + 2 - kWideSegs);
+            cp_async_wait<kWideSegs - 3>();  // segment cur - 1 (the next group's) landed
+            __syncwarp();
         }
-        uint32_t nx0 = 0, nx1 = 0;
-        if (gi > 0) load_syms(gi - 1, nx0, nx1);
-        const bool on0 = lane < active, on1 = hi_lane < active;
-        const uint2 e0 = enc[sym0];
-        const uint2 e1 = enc[sym1];
-        const uint32_t bad1 = __ballot_sync(0xffffffffu, on1 && e1.x == 0u);
-        const uint32_t bad0 = __ballot_sync(0xffffffffu, on0 && e0.x == 0u);
-        if (bad0 | bad1) {  // the highest offending index (the reference walks down)
-            if (lane == 0)
-                atomicMax(&status->unenc_index,
-                          static_cast<long long>(cbase + base + (bad1 ? 63 - __clz(bad1)
-                                                                      : 31 - __clz(bad0))));
+        if (gi > 0) load_syms(gi - 1, nx);
+        uint2 e[S];
+        uint32_t badm[S];
+        bool anybad = false;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            e[j] = enc[sym[j]];
+            badm[j] = __ballot_sync(0xffffffffu, 32 * j + lane < active && e[j].x == 0u);
+            anybad |= badm[j] != 0u;
+        }
+        if (anybad) {  // the highest offending index (the reference walks down)
+            int hi = -1;
+#pragma unroll
+            for (int j = 0; j < S; ++j)
+                if (badm[j]) hi = 32 * j + 31 - __clz(badm[j]);
+            if (lane == 0) atomicMax(&status->unenc_index, static_cast<long long>(cbase + base + hi));
             bad = true;
             break;
         }
-        const bool sp1 = on1 && enc_spill(ctx, x1, e1);
-        const bool sp0 = on0 && enc_spill(ctx, x0, e0);
-        const uint32_t mk1 = __ballot_sync(0xffffffffu, sp1);
-        const uint32_t mk0 = __ballot_sync(0xffffffffu, sp0);
-        const int64_t top1 = top - __popc(mk1);
-        top = top1 - __popc(mk0);
-        if (sp1) out[top1 + __popc(mk1 & lt)] = static_cast<uint16_t>(x1 & 0xFFFFu);
-        if (sp0) out[top + __popc(mk0 & lt)] = static_cast<uint16_t>(x0 & 0xFFFFu);
-        const uint32_t z1 = sp1 ? x1 >> 16 : x1;
-        const uint32_t z0 = sp0 ? x0 >> 16 : x0;
-        // stats: digits this symbol moves under the reference's spill loop
-        // (rans.py:284-287): one per pass while x >= threshold
-        if (stats) {
-            if (sp1) most = max(most, enc_spill(ctx, z1, e1) ? 2u : 1u);
-            if (sp0) most = max(most, enc_spill(ctx, z0, e0) ? 2u : 1u);
+        bool sp[S];
+        uint32_t mk[S];
+#pragma unroll
+        for (int j = S - 1; j >= 0; --j) {
+            sp[j] = 32 * j + lane < active && enc_spill(ctx, x[j], e[j]);
+            mk[j] = __ballot_sync(0xffffffffu, sp[j]);
         }
-        const uint32_t p1 = enc_push(ctx, z1, e1);
-        const uint32_t p0 = enc_push(ctx, z0, e0);
-        x1 = on1 ? p1 : x1;
-        x0 = on0 ? p0 : x0;
-        sym0 = nx0;
-        sym1 = nx1;
+#pragma unroll
+        for (int j = S - 1; j >= 0; --j) {
+            top -= __popc(mk[j]);
+            if (sp[j]) out[top + __popc(mk[j] & lt)] = static_cast<uint16_t>(x[j] & 0xFFFFu);
+            const uint32_t z = sp[j] ? x[j] >> 16 : x[j];
+            // stats: digits this symbol moves under the reference's spill
+            // loop (rans.py:284-287): one per pass while x >= threshold
+            if (stats && sp[j]) most = max(most, enc_spill(ctx, z, e[j]) ? 2u : 1u);
+            const uint32_t p = enc_push(ctx, z, e[j]);
+            x[j] = 32 * j + lane < active ? p : x[j];
+        }
+#pragma unroll
+        for (int j = 0; j < S; ++j) sym[j] = nx[j];
     }
-    if (RING) cp_async_wait<0>();
+    cp_async_wait<0>();
     if (stats) {
         most = __reduce_max_sync(0xffffffffu, most);
         if (lane == 0 && most) atomicMax(&status->max_digits, most);
     }
     if (!bad) {
         if (lane == 0) chunk_words[k] = static_cast<uint32_t>(len - top);
-        if (lane < n_lanes) states_out[k * n_lanes + lane] = x0;
-        if (hi_lane < n_lanes) states_out[k * n_lanes + hi_lane] = x1;
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+            if (32 * j + lane < n_lanes) states_out[k * n_lanes + 32 * j + lane] = x[j];
     }
 }
 
@@ -858,12 +858,13 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
     if (n <= 0) return cudaSuccess;
     const int64_t n_chunks = (n + chunk_len - 1) / chunk_len;
     // stats (instrumented calls): the one-warp sub-group walk measures the
-    // digits per symbol for every N <= 64, the CTA kernel beyond
+    // digits per symbol for every N <= 256, the CTA kernel beyond
     if ((n_lanes > 32 || stats) && n_lanes <= kWideMaxE) {
         // the shared message ring reads each chunk from its 16-byte aligned
-        // base below it: only when that stays inside the message
-        auto kernel = (reinterpret_cast<uintptr_t>(d_msg) & 15u) == 0 ? encode_wide_kernel<true>
-                                                                        : encode_wide_kernel<false>;
+        // base below it
+        if (reinterpret_cast<uintptr_t>(d_msg) & 15u) return cudaErrorMisalignedAddress;
+        auto kernel = n_lanes <= 64 ? encode_wide_kernel<2>
+                    : n_lanes <= 128 ? encode_wide_kernel<4> : encode_wide_kernel<8>;
         kernel<<<static_cast<unsigned>(n_chunks), 32, 0, stream>>>(
             d_msg, n, chunk_len, n_lanes, d_table, d_scratch, d_chunk_words, d_states, d_status,
             stats ? 1 : 0);

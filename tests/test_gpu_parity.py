@@ -141,7 +141,8 @@ def test_histogram_matches_bincount():
 # ------------------------------------------------------- API behaviour ---
 def test_round_trips_many_shapes():
     rng = np.random.default_rng(2026)
-    for lanes in (1, 2, 3, 5, 8, 16, 17, 31, 32, 33, 64, 100, 1024, 1500):
+    for lanes in (1, 2, 3, 5, 8, 16, 17, 31, 32, 33, 64, 65, 100, 128, 129, 200, 256, 257,
+                  1024, 1500):
         t = random_table(rng)
         for n in sorted({0, 1, lanes - 1, lanes, lanes + 1, 2 * lanes + 1, 513, 4097,
                          int(rng.integers(1000, 20000))}):
@@ -169,7 +170,7 @@ def test_max_lanes_65535():
 def test_truncation_raises_like_reference():
     rng = np.random.default_rng(63)
     t = random_table(rng)
-    for lanes in (1, 2, 4, 8, 16, 32, 40):
+    for lanes in (1, 2, 4, 8, 16, 32, 40, 100, 200):
         msg = random_message(rng, t, 1500)
         c = ilb.encode_interleaved(msg, t, lanes, WORD16)
         if len(c.payload) == 0:
@@ -230,7 +231,7 @@ def test_unencodable_symbol_in_fast_batches():
     names the symbol at the highest offending index (the reference's
     backward walk meets it first, _core.pyx:33-34)."""
     t = SymbolTable([2048, 2047, 0, 0, 1], 12)
-    for lanes in (32, 8, 1, 7, 3):
+    for lanes in (32, 8, 1, 7, 3, 40, 64, 100, 200, 256):
         msg = np.zeros(70_000, dtype=np.uint8)
         msg[100], msg[60_000] = 2, 3
         with pytest.raises(UnencodableSymbolError, match="symbol 3"):
@@ -238,6 +239,13 @@ def test_unencodable_symbol_in_fast_batches():
         msg[60_000] = 1
         msg[40_000] = 2
         with pytest.raises(UnencodableSymbolError, match="symbol 2"):
+            ilb.encode_interleaved(msg, t, lanes, WORD16)
+    # two in one group, lower sub-group first (the wide coders' S x 32 lanes)
+    for lanes in (64, 100, 200, 256):
+        msg = np.zeros(70_000, dtype=np.uint8)
+        base = (50_000 // lanes) * lanes
+        msg[base + 3], msg[base + lanes - 2] = 2, 3
+        with pytest.raises(UnencodableSymbolError, match="symbol 3"):
             ilb.encode_interleaved(msg, t, lanes, WORD16)
 
 
