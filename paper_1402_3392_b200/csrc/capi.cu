@@ -61,28 +61,6 @@ int sm_count() {
     return cached[dev];
 }
 
-cudaError_t launch_histogram(const uint8_t *d_msg, int64_t n, unsigned long long *d_counts,
-                             cudaStream_t stream) {
-    if (n <= 0) return cudaSuccess;
-    static bool attr_set[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int smem = 256 * 256 * 3;  // kHistGroups counter blocks of 64 KB
-    if (!attr_set[dev & 63]) {
-        cudaFuncSetAttribute(histogram_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem);
-        attr_set[dev & 63] = true;
-    }
-    // one CTA per SM: 3 x 128 threads, 3 x 64 KB of counters; small inputs
-    // get fewer CTAs
-    int64_t blocks = int64_t(sm_count());
-    const int64_t want = (n + 384 * 16 * 8 - 1) / (384 * 16 * 8);
-    if (blocks > want) blocks = want < 1 ? 1 : want;
-    histogram_u8_kernel<<<static_cast<unsigned>(blocks), 384, smem, stream>>>(d_msg, n, d_counts);
-    ilans_note_launch();
-    return cudaGetLastError();
-}
-
 cudaError_t launch_build_table(const unsigned long long *d_counts, const uint32_t *d_freq,
                                int n_freq, const uint32_t *d_cum, const uint8_t *d_slot,
                                int scale_bits, TableDev *d_table, cudaStream_t stream) {

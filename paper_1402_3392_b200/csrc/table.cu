@@ -19,17 +19,32 @@ namespace ilans {
 // the same as a uniform one. Each increment is one fire-and-forget shared
 // add (red.shared of 1 << 16*(w & 1)) -- no per-thread read-modify-write
 // chain, one shared-memory wavefront per 32 bytes. A counter can only carry
-// into its neighbour after 65536 bytes of one thread, so the block flushes
-// every 4095 vectors per thread (once per launch at every realistic size):
-// thread t sums bins t and t+128 over all 128 columns and zeroes them.
+// into its neighbour after 65536 bytes of one thread, so the counting threads
+// flush every kHistFlushStages ring slots (64 bytes per thread per slot; once
+// per launch below ~2.4 GB per SM): thread t sums bins t and t+128 over all
+// 128 columns and zeroes them.
 // ---------------------------------------------------------------------------
-// Three independent 128-thread counter blocks (64 KB each) per CTA, one CTA
-// per SM: the sub-block index sits in byte 2 of each thread's column
-// offset, so the PRMT that assembles the address still does all of it.
-constexpr int kHistGroups = 3;
-constexpr int kHistThreads = 128 * kHistGroups;
-constexpr int kHistBatch = 8;                 // 16-byte loads per batch (two batches in flight)
-constexpr int64_t kHistVecPerRound = 4088;    // <= 65535 / 16 vectors between flushes
+// Two independent 128-thread counter blocks (64 KB each) per CTA, one CTA per
+// SM, fed by the bulk-copy engine: each CTA streams its contiguous share of
+// the message through a 3 x 32 KB shared ring (cp.async.bulk completing on
+// an mbarrier per slot; a producer warp refills a slot once the 8 counting
+// warps have released it). 96 KB in flight per SM keeps HBM busy without the
+// register double-buffering of a load-and-count loop (66 us at config 2,
+// ~0.6 of HBM: 12 warps/SM, long_scoreboard); measured at 256 MiB: 3 x 32 KB
+// 48.6 us, 4 x 24 KB 49.3, 6 x 16 KB 50.0, 12 x 8 KB 58.6, and one counter
+// block with 10 x 16 KB 55.0 (the shared atomics then lack issuing warps).
+// The shared-memory pipe is the co-bound: one wavefront per 32 counted bytes
+// plus four per 512-byte LDS.128 (~0.8 of one wavefront per SM clock).
+constexpr int kHistGroups = 2;
+constexpr int kHistCounters = 128 * kHistGroups;        // counting threads
+constexpr int kHistThreads = kHistCounters + 32;        // + the producer warp
+constexpr uint32_t kHistStage = 32768;                  // bytes per ring slot
+constexpr int kHistStages = 3;
+// slots between counter flushes: < 65536 bytes per thread
+constexpr int kHistFlushStages = 64000 / (kHistStage / kHistCounters);
+constexpr size_t kHistCounterBytes = size_t(256) * 64 * 4 * kHistGroups;
+constexpr size_t kHistSmem = kHistCounterBytes + size_t(kHistStages) * kHistStage +
+                             2 * kHistStages * 8;
 
 __device__ __forceinline__ uint32_t hist_word(uint32_t bin, uint32_t tid) {
     return bin * 64u + ((tid >> 6) << 5) + (tid & 31u);  // 64 words per bin
@@ -76,72 +91,156 @@ __device__ __forceinline__ void hist_flush(uint32_t *h, uint32_t tid, unsigned l
     }
 }
 
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(addr),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t addr) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(addr), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void counters_sync() {  // the 256 counting threads only
+    asm volatile("bar.sync 1, %0;" ::"n"(kHistCounters) : "memory");
+}
+
 __global__ void __launch_bounds__(kHistThreads, 1)
 histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
                     unsigned long long *__restrict__ counts) {
-    extern __shared__ __align__(16) uint32_t hist_smem[];
+    extern __shared__ __align__(128) uint32_t hist_smem[];
     const uint32_t gtid = threadIdx.x;
-    const uint32_t sub = gtid >> 7;   // counter block of this thread
-    const uint32_t tid = gtid & 127u;  // column within the block
     const uint32_t base_addr = smem_addr(hist_smem);
-    for (uint32_t i = gtid; i < 256u * 64u * kHistGroups; i += kHistThreads) hist_smem[i] = 0;
+    const uint32_t ring_addr = base_addr + static_cast<uint32_t>(kHistCounterBytes);
+    const uint32_t full_addr = ring_addr + kHistStages * kHistStage;  // full[s], empty[s]
+    const uint32_t empty_addr = full_addr + kHistStages * 8;
+    for (uint32_t i = gtid; i < kHistCounterBytes / 4; i += kHistThreads) hist_smem[i] = 0;
+    if (gtid == 0) {
+        for (int q = 0; q < kHistStages; ++q) {
+            mbar_init(full_addr + 8 * q, 1);
+            mbar_init(empty_addr + 8 * q, kHistCounters / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
 
-    // unaligned head / tail bytes: block 0, thread 0 (its own counters)
+    // 16-byte aligned body, split into contiguous per-CTA ranges; unaligned
+    // head / tail bytes: block 0, thread 0 (its own counters)
     const uintptr_t addr = reinterpret_cast<uintptr_t>(msg);
     int64_t head = static_cast<int64_t>((16 - (addr & 15)) & 15);
     if (head > n) head = n;
-    const int64_t nvec = (n - head) >> 4;
-    const int64_t tail_start = head + (nvec << 4);
-    if (blockIdx.x == 0 && gtid == 0) {
-        for (int64_t i = 0; i < head; ++i) hist_red(base_addr, 0, msg[i]);
-        for (int64_t i = tail_start; i < n; ++i) hist_red(base_addr, 0, msg[i]);
+    const int64_t body = ((n - head) >> 4) << 4;
+    const int64_t per_cta = (((body + gridDim.x - 1) / gridDim.x) + 15) & ~int64_t(15);
+    const int64_t lo = per_cta * blockIdx.x < body ? per_cta * blockIdx.x : body;
+    const int64_t hi = lo + per_cta < body ? lo + per_cta : body;
+    // < 2^31 slots per CTA (the message is < 2^31 * 16 KB * gridDim)
+    const uint32_t n_stages = static_cast<uint32_t>((hi - lo + kHistStage - 1) / kHistStage);
+    const uint32_t last_bytes =
+        n_stages ? static_cast<uint32_t>(hi - lo - int64_t(n_stages - 1) * kHistStage) : 0u;
+    const uint8_t *src = msg + head + lo;
+
+    if (gtid >= kHistCounters) {  // producer warp: one elected lane issues
+        if (gtid == kHistCounters) {
+            uint32_t q = 0, ph = 0;
+            for (uint32_t i = 0; i < n_stages; ++i) {
+                if (i >= kHistStages) mbar_wait(empty_addr + 8 * q, ph ^ 1u);
+                const uint32_t bytes = i + 1 < n_stages ? kHistStage : last_bytes;
+                mbar_expect_tx(full_addr + 8 * q, bytes);
+                bulk_g2s(ring_addr + q * kHistStage, src + size_t(i) * kHistStage, bytes,
+                         full_addr + 8 * q);
+                if (++q == kHistStages) {
+                    q = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        return;
     }
 
+    const uint32_t sub = gtid >> 7;   // counter block of this thread
+    const uint32_t tid = gtid & 127u;  // column within the block
+    if (blockIdx.x == 0 && gtid == 0) {
+        for (int64_t i = 0; i < head; ++i) hist_red(base_addr, 0, msg[i]);
+        for (int64_t i = head + body; i < n; ++i) hist_red(base_addr, 0, msg[i]);
+    }
     unsigned long long acc[2] = {0, 0};
     // byte 0: column (< 256), byte 1: bin (PRMT), byte 2: counter block
     const uint32_t col = 4u * hist_word(0, tid) | sub << 16;
     const uint32_t inc = 1u << (((tid >> 5) & 1u) * 16);
-    const uint4 *vec = reinterpret_cast<const uint4 *>(msg + head);
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * kHistThreads;
-    const int64_t first = static_cast<int64_t>(blockIdx.x) * kHistThreads + gtid;
-    const int64_t per_round = stride * kHistVecPerRound;
-    for (int64_t round_base = 0; round_base < nvec; round_base += per_round) {
-        const int64_t round_end = min(nvec, round_base + per_round);
-        // software-pipelined: the next batch's loads are in flight while this
-        // batch's bytes are counted (a load-then-count loop left the HBM
-        // queue empty during every counting phase: long_scoreboard stalls)
-        uint4 nx[kHistBatch];
-        int64_t j0 = round_base + first;
+    constexpr int kVecs = kHistStage / 16 / kHistCounters;  // 16-byte vectors per thread per slot
+    uint32_t q = 0, ph = 0, flush_left = kHistFlushStages;
+    for (uint32_t i = 0; i < n_stages; ++i) {
+        mbar_wait(full_addr + 8 * q, ph);
+        const uint32_t slot = ring_addr + q * kHistStage + 16 * gtid;
+        uint4 v[kVecs];
+        if (i + 1 < n_stages || last_bytes == kHistStage) {  // full slot
 #pragma unroll
-        for (int r = 0; r < kHistBatch; ++r) {
-            const int64_t j = j0 + r * stride;
-            nx[r] = j < round_end ? __ldcs(vec + j) : make_uint4(0, 0, 0, 0);
-        }
-        for (; j0 < round_end; j0 += stride * kHistBatch) {
-            uint4 v[kHistBatch];
+            for (int r = 0; r < kVecs; ++r)
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v[r].x), "=r"(v[r].y), "=r"(v[r].z), "=r"(v[r].w)
+                             : "r"(slot + 16 * kHistCounters * r));
+            __syncwarp();
+            if ((gtid & 31) == 0) mbar_arrive(empty_addr + 8 * q);  // slot read: release it
 #pragma unroll
-            for (int r = 0; r < kHistBatch; ++r) v[r] = nx[r];
-            const int64_t j1 = j0 + stride * kHistBatch;
+            for (int r = 0; r < kVecs; ++r) hist_bump16(base_addr, col, inc, v[r]);
+        } else {  // the CTA's last, partial slot
+            const uint32_t nvec = last_bytes >> 4;
 #pragma unroll
-            for (int r = 0; r < kHistBatch; ++r) {
-                const int64_t j = j1 + r * stride;
-                nx[r] = j < round_end ? __ldcs(vec + j) : make_uint4(0, 0, 0, 0);
+            for (int r = 0; r < kVecs; ++r) {
+                v[r] = make_uint4(0, 0, 0, 0);
+                if (gtid + r * kHistCounters < nvec)
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v[r].x), "=r"(v[r].y), "=r"(v[r].z), "=r"(v[r].w)
+                                 : "r"(slot + 16 * kHistCounters * r));
             }
+            __syncwarp();
+            if ((gtid & 31) == 0) mbar_arrive(empty_addr + 8 * q);
 #pragma unroll
-            for (int r = 0; r < kHistBatch; ++r)
-                if (j0 + r * stride < round_end) hist_bump16(base_addr, col, inc, v[r]);
+            for (int r = 0; r < kVecs; ++r)
+                if (gtid + r * kHistCounters < nvec) hist_bump16(base_addr, col, inc, v[r]);
         }
-        __syncthreads();
-        hist_flush(hist_smem + sub * (256u * 64u), tid, acc);
-        __syncthreads();
+        if (--flush_left == 0) {
+            flush_left = kHistFlushStages;
+            counters_sync();
+            hist_flush(hist_smem + sub * (256u * 64u), tid, acc);
+            counters_sync();
+        }
+        if (++q == kHistStages) {
+            q = 0;
+            ph ^= 1u;
+        }
     }
-    if (nvec == 0) {  // head / tail only
-        __syncthreads();
-        hist_flush(hist_smem + sub * (256u * 64u), tid, acc);
-    }
+    counters_sync();
+    hist_flush(hist_smem + sub * (256u * 64u), tid, acc);
     if (acc[0]) atomicAdd(counts + tid, acc[0]);
     if (acc[1]) atomicAdd(counts + tid + 128, acc[1]);
+}
+
+cudaError_t launch_histogram(const uint8_t *d_msg, int64_t n, unsigned long long *d_counts,
+                             cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    smem_limit(reinterpret_cast<const void *>(histogram_u8_kernel), int(kHistSmem));
+    // one CTA per SM; small inputs get fewer CTAs (>= 4 ring slots each)
+    int64_t blocks = int64_t(sm_count());
+    const int64_t want = (n + 4 * kHistStage - 1) / (4 * kHistStage);
+    if (blocks > want) blocks = want < 1 ? 1 : want;
+    histogram_u8_kernel<<<static_cast<unsigned>(blocks), kHistThreads, kHistSmem, stream>>>(
+        d_msg, n, d_counts);
+    ilans_note_launch();
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

@@ -138,6 +138,41 @@ def test_histogram_matches_bincount():
             assert np.array_equal(counts, ref) and alpha.value == ref_alpha
 
 
+def test_histogram_device_pointers_and_flush():
+    """ilans_histogram_u8_dev on offset device pointers (unaligned head and
+    tail bytes around the bulk-copied body), and a 1-symbol source large
+    enough that every CTA flushes its 16-bit counters mid-stream (> 1000
+    ring slots per CTA)."""
+    import ctypes
+
+    import torch
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(11)
+    host = rng.integers(0, 256, size=5_000_011).astype(np.uint8)
+    d = torch.from_numpy(host).to(dev)
+    counts = torch.zeros(256, dtype=torch.int64, device=dev)
+    for off, n in ((0, len(host)), (1, 100_000), (7, 4_999_999), (13, 17), (3, 65_549)):
+        counts.zero_()
+        rc = _lib.lib.ilans_histogram_u8_dev(d.data_ptr() + off, n, counts.data_ptr(), None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        ref = np.bincount(host[off:off + n], minlength=256)
+        assert np.array_equal(counts.cpu().numpy(), ref), (off, n)
+    del d
+    n = 148 * 17 * (1 << 20) + 12_345  # ~2.5 GB: > 1000 x 16 KB slots per CTA
+    big = torch.full((n + 1,), 200, dtype=torch.uint8, device=dev)
+    big[0] = 3
+    counts.zero_()
+    rc = _lib.lib.ilans_histogram_u8_dev(big.data_ptr() + 1, n, counts.data_ptr(), None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    c = counts.cpu().numpy()
+    assert c[200] == n and c.sum() == n
+    del big
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------- API behaviour ---
 def test_round_trips_many_shapes():
     rng = np.random.default_rng(2026)
