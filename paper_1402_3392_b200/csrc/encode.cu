@@ -53,10 +53,18 @@ constexpr int kEncMaxWarps = 28;
 constexpr int kOutRing = 1024;   // per-warp staging ring for spilled words (2 KB)
 constexpr uint32_t kOutRingBytes = kOutRing * 2;
 
-// dynamic shared memory: enc[256] | encf[256] | encz[256] | W message rings |
+// dynamic shared memory: enc[256] | encf x 16 | encz x 32 | W message rings |
 // pad | W spill rings
+// Bank-private copies of the fast records: entry e of copy c sits at
+// e * copies + c, and lane l reads copy l % copies, so a warp's record loads
+// never conflict whatever the symbols (one LDS.64 = 2 wavefronts, one LDS.32
+// = 1; a single copy cost ~2.6 extra wavefronts per group at config 2, the
+// encoder's shared-memory pipe then ~0.9 busy).
+constexpr int kEncfCopies = 16;  // 8-byte records: a half-warp per wavefront
+constexpr int kEnczCopies = 32;
 __host__ __device__ constexpr size_t encode_smem_bytes(int warps) {
-    return 2 * kMaxSym * sizeof(uint2) + kMaxSym * sizeof(uint32_t) + size_t(warps) * kInRing +
+    return kMaxSym * sizeof(uint2) + size_t(kEncfCopies) * kMaxSym * sizeof(uint2) +
+           size_t(kEnczCopies) * kMaxSym * sizeof(uint32_t) + size_t(warps) * kInRing +
            kOutRingBytes + size_t(warps) * kOutRingBytes;
 }
 
@@ -229,18 +237,21 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     constexpr bool SMALL = MODE == 1;
     const int nw = blockDim.x >> 5;
     uint2 *enc = reinterpret_cast<uint2 *>(esmem);
-    uint2 *encf = enc + kMaxSym;  // EncFast {M, Z} / EncFast12 {M, Y}
-    uint32_t *encz = reinterpret_cast<uint32_t *>(encf + kMaxSym);  // EncFast12 Z
-    uint8_t *rings = reinterpret_cast<uint8_t *>(encz + kMaxSym);
+    uint2 *encf_rep = enc + kMaxSym;  // EncFast {M, Z} / EncFast12 {M, Y}, x 16
+    uint32_t *encz_rep = reinterpret_cast<uint32_t *>(encf_rep + kEncfCopies * kMaxSym);
+    uint8_t *rings = reinterpret_cast<uint8_t *>(encz_rep + kEnczCopies * kMaxSym);
     uint16_t *oring_raw = reinterpret_cast<uint16_t *>(rings + nw * kInRing);
     const bool fast = !F12 && (tab->flags & kTabEncFast) != 0u;
     const bool fast12 = F12 && (tab->flags & kTabEncFast12) != 0u;
-    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) {
-        enc[i] = tab->enc[i];
-        encf[i] = tab->encf[i];
-        encz[i] = tab->encz[i];
-    }
+    for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
+    for (int i = threadIdx.x; i < kEncfCopies * kMaxSym; i += blockDim.x)
+        encf_rep[i] = tab->encf[i / kEncfCopies];
+    for (int i = threadIdx.x; i < kEnczCopies * kMaxSym; i += blockDim.x)
+        encz_rep[i] = tab->encz[i / kEnczCopies];
     __syncthreads();
+    // this lane's copies: record of symbol s at encf[s * kEncfCopies]
+    const uint2 *encf = encf_rep + (threadIdx.x & (kEncfCopies - 1));
+    const uint32_t *encz = encz_rep + (threadIdx.x & (kEnczCopies - 1));
     const EncCtx ctx(tab->scale_bits);
     const uint32_t lowm = ~0u >> tab->scale_bits;  // 2^t - 1, t = 32 - sb
     const uint32_t t_shift = 32u - tab->scale_bits;
@@ -365,16 +376,16 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 uint32_t topb = static_cast<uint32_t>(top) << 1;
                 uint32_t topb0 = topb;
                 uint32_t sym_n = lds_u8(hi_sa + (kInSeg / 32 - 1) * 32);
-                uint2 a_n = encf[sym_n];
-                uint32_t z_n = F12 ? encz[sym_n] : 0u;
+                uint2 a_n = encf[sym_n * kEncfCopies];
+                uint32_t z_n = F12 ? encz[sym_n * kEnczCopies] : 0u;
                 sym_n = lds_u8(hi_sa + (kInSeg / 32 - 2) * 32);
 #pragma unroll
                 for (int gg = 2 * (kInSeg / 32) - 1; gg >= 0; --gg) {
                     const uint2 a = a_n;  // {M, Z} (F12: {M, Y})
                     const uint32_t z = z_n;
                     if (gg > 0) {
-                        a_n = encf[sym_n];
-                        if (F12) z_n = encz[sym_n];
+                        a_n = encf[sym_n * kEncfCopies];
+                        if (F12) z_n = encz[sym_n * kEnczCopies];
                         if (gg > 1) {
                             const int nx = gg - 2;  // group two ahead
                             sym_n = lds_u8((nx >= kInSeg / 32 ? hi_sa : lo_sa) +
@@ -445,14 +456,14 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         bp -= n_lanes;
                         const uint32_t sym = sym_n;
                         if (j < 15 || gb > 15) sym_n = *bp;
-                        const uint2 a = encf[sym];
+                        const uint2 a = encf[sym * kEncfCopies];
                         if (!COVERED) macc &= a.x;
                         uint32_t z = 0;
                         if (!F12) {
                             spill_group<0, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr,
                                                  neg2, two);
                         } else {
-                            z = encz[sym];
+                            z = encz[sym * kEnczCopies];
                             spill_group<1, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr,
                                                  neg2, two);
                         }
@@ -471,13 +482,13 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 // stores go to shared memory too, so the compiler cannot
                 // hoist a later group's loads above them by itself.
                 uint32_t sym_n = blk[(kInSeg / 32 - 1) * 32 + lane];
-                uint2 a_n = encf[sym_n];
+                uint2 a_n = encf[sym_n * kEncfCopies];
                 sym_n = blk[(kInSeg / 32 - 2) * 32 + lane];
 #pragma unroll
                 for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
                     const uint2 a = a_n;  // {M, Z}
                     if (gg > 0) {
-                        a_n = encf[sym_n];
+                        a_n = encf[sym_n * kEncfCopies];
                         if (gg > 1) sym_n = blk[(gg - 2) * 32 + lane];
                     }
                     if (!COVERED) macc &= a.x;
@@ -489,16 +500,16 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 }
             } else if (fast12) {
                 uint32_t sym_n = blk[(kInSeg / 32 - 1) * 32 + lane];
-                uint2 a_n = encf[sym_n];
-                uint32_t z_n = encz[sym_n];
+                uint2 a_n = encf[sym_n * kEncfCopies];
+                uint32_t z_n = encz[sym_n * kEnczCopies];
                 sym_n = blk[(kInSeg / 32 - 2) * 32 + lane];
 #pragma unroll
                 for (int gg = kInSeg / 32 - 1; gg >= 0; --gg) {
                     const uint2 a = a_n;  // {M, Y}
                     const uint32_t z = z_n;
                     if (gg > 0) {
-                        a_n = encf[sym_n];
-                        z_n = encz[sym_n];
+                        a_n = encf[sym_n * kEncfCopies];
+                        z_n = encz[sym_n * kEnczCopies];
                         if (gg > 1) sym_n = blk[(gg - 2) * 32 + lane];
                     }
                     if (!COVERED) macc &= a.x;
@@ -565,14 +576,14 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                     const uint32_t sym = sym_n;
                     ri -= n_lanes;
                     if (j + 1 < G) sym_n = ring[ri & (kInRing - 1)];
-                    const uint2 a = encf[sym];
+                    const uint2 a = encf[sym * kEncfCopies];
                     if (!COVERED) macc &= a.x;
                     uint32_t z = 0;
                     if (!F12) {
                         spill_group<0, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr, neg2,
                                              two);
                     } else {
-                        z = encz[sym];
+                        z = encz[sym * kEnczCopies];
                         spill_group<1, true>(x, topb, lowm, a.y, on, lt_mul, oring_addr, neg2,
                                              two);
                     }
