@@ -2,7 +2,7 @@
 encode (one warp per chunk) + byte framing, and decode, at 256 MiB of the
 config-2 Zipf source, for N = 2 (config 1's lane count) and N = 32.
 
-    python tools/byte8_chunked_probe.py [mib]
+    python tools/byte8_chunked_probe.py [mib] [lanes:chunk,...]
 """
 import ctypes
 import sys
@@ -22,7 +22,10 @@ d_msg = synth_device(n, 1.1, 1234)
 m = _Model(torch, dev)
 table = m.from_message(d_msg, n, 12)
 p = lambda t: int(t.data_ptr())  # noqa: E731
-for lanes, C in ((2, 65536), (32, 65536), (32, 16384)):
+cases = ((2, 65536), (32, 65536), (32, 16384))
+if len(sys.argv) > 2:
+    cases = [tuple(int(v) for v in c.split(":")) for c in sys.argv[2].split(",")]
+for lanes, C in cases:
     k = n_chunks_for(n, C)
     scratch = torch.empty(3 * n + 16, dtype=torch.uint8, device=dev)
     payload = torch.empty(3 * n + 16, dtype=torch.uint8, device=dev)
