@@ -140,16 +140,29 @@ constexpr int kRing8 = 4 * kSeg8;          // per-warp ring
 constexpr int kObuf8 = 512;                // decoded-byte staging per warp
 constexpr int kMaxWarps8 = 28;
 constexpr int64_t kRingMaxChunk8 = int64_t(1) << 29;  // 32-bit chunk cursors (3 len < 2^31)
+// bank-private copies of the 16-byte fast encode records (a quarter-warp per
+// wavefront: lane l reads copy l % 8, conflict-free whatever the symbols)
+constexpr int kRec8Copies = 8;
 
+constexpr int kRing8Alloc = kRing8 + 16;   // decode ring + a copy of its first 16 bytes
+
+// Segment seg of the payload into ring slot seg % 4; slot 0's first 16 bytes
+// are also copied past the ring's end, so a 2-byte read at the last ring
+// byte needs no wrap.
 __device__ __forceinline__ void issue_seg8(uint32_t ring_sa, const uint8_t *gbase, uint64_t avail,
                                            uint64_t seg, int lane) {
     const uint64_t b0 = seg * kSeg8 + lane * 16;
     uint32_t bytes = 0;
     if (avail > b0) bytes = (avail - b0) >= 16 ? 16u : static_cast<uint32_t>(avail - b0);
+    const uint8_t *src = bytes ? gbase + b0 : gbase;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
                      ring_sa + static_cast<uint32_t>(seg & 3u) * kSeg8 + lane * 16),
-                 "l"(bytes ? gbase + b0 : gbase), "r"(bytes)
+                 "l"(src), "r"(bytes)
                  : "memory");
+    if ((seg & 3u) == 0 && lane == 0)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(ring_sa + kRing8),
+                     "l"(src), "r"(bytes)
+                     : "memory");
 }
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
@@ -178,7 +191,7 @@ decode_u8_ring_body(const uint8_t *__restrict__ payload, const uint64_t *__restr
     const int nw = blockDim.x >> 5;
     const int sb = static_cast<int>(tab->scale_bits);
     const uint32_t m = 1u << sb, mask = m - 1u;
-    uint8_t *lut = sm8 + nw * (kRing8 + kObuf8);
+    uint8_t *lut = sm8 + nw * (kRing8Alloc + kObuf8);
     if (PACKED) {
         uint32_t *p = reinterpret_cast<uint32_t *>(lut);
         for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) p[i] = tab->packed[i];
@@ -197,8 +210,8 @@ decode_u8_ring_body(const uint8_t *__restrict__ payload, const uint64_t *__restr
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const uint32_t lt = lanemask_lt();
-    const uint32_t ring_sa = smem_addr(sm8 + wib * kRing8);
-    uint8_t *obuf = sm8 + nw * kRing8 + wib * kObuf8;
+    const uint32_t ring_sa = smem_addr(sm8 + wib * kRing8Alloc);
+    uint8_t *obuf = sm8 + nw * kRing8Alloc + wib * kObuf8;
     int64_t nwk = (n_chunks + gridDim.x - 1) / gridDim.x;
     if (nwk > nw) nwk = nw;
     if (wib >= nwk) return;
@@ -232,62 +245,74 @@ decode_u8_ring_body(const uint8_t *__restrict__ payload, const uint64_t *__restr
         // From such a state a pop gives x' >= f (x >> sb) >= 2^(23 - sb) >=
         // 2^7, so a lane refills 0, 1 or 2 digits ([x' < 2^23] + [x' <
         // 2^15]: two ballots, no zero-state check) and the refills keep
-        // every state valid.
+        // every state valid. Batches of 16 groups (512 symbols, <= 1024
+        // digits: the cursor's segment and the two above it, landed before
+        // the batch); the decoded bytes leave once per batch, the ring and
+        // the truncation check (reads past the payload only see the ring's
+        // zero fill) once per batch too.
+        uint32_t any2 = 0;  // a group of the fast region refilled two digits
+        const uint32_t pos_fast0 = pos;
         if (n_lanes == 32 && __all_sync(0xffffffffu, x >= kLow8)) {
-            const uint32_t full = len & ~31u;
+            const uint32_t nbatch = len >> 9;
+            const uint32_t lt_mul = lane ? 1u << (32 - lane) : 0u;  // popc(b & lt) = popc(b * lt_mul)
             const uint32_t st_sa = obuf_sa + lane;
-#pragma unroll 4
-            for (; base < full; base += 32) {
-                uint32_t s;
-                {
-                    const uint32_t slot = x & mask;
-                    if (PACKED) {
-                        const uint32_t e = packed[slot];
-                        x = (e >> 20) * ((x >> sb) - 4096u) + (e >> 8);
-                        s = e;
-                    } else {
-                        s = slot_sym[slot];
-                        const uint2 d = dec[s];
-                        x = d.x * (x >> sb) + slot - d.y;
+            cp_async_wait<1>();  // segments 0..2 landed
+            __syncwarp();
+            for (uint32_t bt = 0; bt < nbatch; ++bt) {
+#pragma unroll
+                for (int g = 0; g < 16; ++g) {
+                    uint32_t s;
+                    {
+                        const uint32_t slot = x & mask;
+                        if (PACKED) {
+                            const uint32_t e = packed[slot];
+                            x = (e >> 20) * ((x >> sb) - 4096u) + (e >> 8);
+                            s = e;
+                        } else {
+                            s = slot_sym[slot];
+                            const uint2 d = dec[s];
+                            x = d.x * (x >> sb) + slot - d.y;
+                        }
                     }
+                    const bool r1 = x < kLow8, r2 = x < (1u << 15);
+                    const uint32_t b1 = __ballot_sync(0xffffffffu, r1);
+                    const uint32_t b2 = __ballot_sync(0xffffffffu, r2);
+                    // the lane's digits, most significant first: bytes q, q + 1
+                    const uint32_t q = pos + __popc(b1 * lt_mul) + __popc(b2 * lt_mul);
+                    pos += __popc(b1) + __popc(b2);
+                    any2 |= b2;
+                    const uint32_t a = ring_sa + (q & (kRing8 - 1));
+                    const uint32_t d0 = lds8(a), d1 = lds8(a + 1u);
+                    const uint32_t y1 = x * 256u + d0;
+                    x = r2 ? y1 * 256u + d1 : (r1 ? y1 : x);
+                    sts8(st_sa + g * 32, s);
                 }
-                const bool r1 = x < kLow8, r2 = x < (1u << 15);
-                const uint32_t b1 = __ballot_sync(0xffffffffu, r1);
-                const uint32_t b2 = __ballot_sync(0xffffffffu, r2);
-                const uint32_t tot = __popc(b1) + __popc(b2);
-                if (pos + tot > pend) {
+                __syncwarp();
+                {   // 512 decoded bytes: 2 x 8 per lane
+                    const uint2 o0 = reinterpret_cast<const uint2 *>(obuf)[lane];
+                    const uint2 o1 = reinterpret_cast<const uint2 *>(obuf + 256)[lane];
+                    *reinterpret_cast<uint2 *>(outk + base + 8 * lane) = o0;
+                    *reinterpret_cast<uint2 *>(outk + base + 256 + 8 * lane) = o1;
+                }
+                base += 512;
+                if (pos > pend) {
                     err = ILANS_ERR_TRUNCATED;
                     break;
                 }
-                const uint32_t q = pos + __popc(b1 & lt) + __popc(b2 & lt);
-                pos += tot;
-                // the lane's digits, most significant first: bytes q, q + 1
-                const uint32_t w0 = lds32(ring_sa + (q & (kRing8 - 4)));
-                const uint32_t w1 = lds32(ring_sa + ((q + 4u) & (kRing8 - 4)));
-                const uint32_t v = __byte_perm(__funnelshift_r(w0, w1, (q & 3u) * 8u), 0u, 0x0123u);
-                const uint32_t sh = r2 ? 16u : 8u;
-                x = r1 ? (x << sh) | (v >> (32u - sh)) : x;
-                most = max(most, r2 ? 2u : (r1 ? 1u : 0u));
-                sts8(st_sa + (base & (kObuf8 - 1)), s);
-                if ((base & 255u) == 224u) {  // a 256-byte half is complete
-                    __syncwarp();
-                    const uint32_t blk = base >> 8;
-                    const uint2 o = reinterpret_cast<const uint2 *>(obuf + (blk & 1) * 256)[lane];
-                    *reinterpret_cast<uint2 *>(outk + (blk << 8) + 8 * lane) = o;
-                    __syncwarp();
-                }
                 if ((pos >> 9) != cur) {  // segments below the cursor are read
-                    __syncwarp();
                     while (cur < (pos >> 9)) {
                         ++cur;
                         issue_seg8(ring_sa, gbase, avail, cur + 3, lane);
                         cp_async_commit();
                     }
-                    cp_async_wait<2>();
-                    __syncwarp();
                 }
+                cp_async_wait<1>();  // the cursor's segment and the two above landed
+                __syncwarp();
             }
+            cp_async_wait<0>();
+            __syncwarp();
         }
+        most = any2 ? 2u : (pos != pos_fast0 ? 1u : 0u);
         for (; !err && base < len; base += n_lanes) {
             const uint32_t left = len - base;
             const bool on = static_cast<uint32_t>(lane) < left && lane < n_lanes;
@@ -416,18 +441,33 @@ encode_u8_ring_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_
     extern __shared__ __align__(16) uint8_t sm8[];
     const int nw = blockDim.x >> 5;
     uint2 *enc = reinterpret_cast<uint2 *>(sm8);
+    uint4 *rec8 = reinterpret_cast<uint4 *>(sm8 + kMaxSym * sizeof(uint2));
+    // fast batches (N = 32) take the 8-byte fast records (sb <= 13, every
+    // f <= m / 2: table flag kTabEncFast) plus the spill threshold f << (31 - sb)
+    const bool fast8 = n_lanes == 32 && (tab->flags & kTabEncFast) != 0u;
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
+    if (fast8) {
+        const uint32_t t1 = 31u - tab->scale_bits;
+        for (int i = threadIdx.x; i < kRec8Copies * kMaxSym; i += blockDim.x) {
+            const int sym = i / kRec8Copies;
+            const uint2 f = tab->encf[sym];
+            rec8[i] = make_uint4(f.x, f.y, tab->freq[sym] << t1, 0u);
+        }
+    }
     __syncthreads();
     const EncCtx ctx(tab->scale_bits);
     const uint32_t thr8 = 31u - tab->scale_bits;  // spill while x >= f << (31 - sb)
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const uint32_t lt = lanemask_lt();
-    // [enc 2 KB][W message rings][pad to 2 KB][W spill rings, 2 KB aligned]
-    const uint32_t in_sa = smem_addr(sm8 + kMaxSym * sizeof(uint2) + wib * kRing8);
-    const uint32_t raw = smem_addr(sm8 + kMaxSym * sizeof(uint2) + nw * kRing8);
+    // [enc 2 KB][rec8 32 KB][W message rings][pad to 2 KB][W spill rings, 2 KB aligned]
+    uint8_t *rings = sm8 + kMaxSym * sizeof(uint2) + size_t(kRec8Copies) * kMaxSym * sizeof(uint4);
+    const uint32_t in_sa = smem_addr(rings + wib * kRing8);
+    const uint32_t raw = smem_addr(rings + nw * kRing8);
     const uint32_t out_sa = ((raw + kRing8 - 1) & ~uint32_t(kRing8 - 1)) + wib * kRing8;
     const uint8_t *out_ring = sm8 + (out_sa - smem_addr(sm8));
+    // this lane's record copy: symbol s at rec_sa + s * 16 * kRec8Copies
+    const uint32_t rec_sa = smem_addr(rec8 + (lane & (kRec8Copies - 1)));
     int64_t nwk = (n_chunks + gridDim.x - 1) / gridDim.x;
     if (nwk > nw) nwk = nw;
     if (wib >= nwk) return;
@@ -463,7 +503,8 @@ encode_u8_ring_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_
         int base = (groups - 1) * n_lanes;
         // N = 32: the full groups below fast_top take the fast loop after
         // this one has coded the partial top group (if any)
-        const int fast_top = n_lanes == 32 ? (len & ~31) : 0;
+        // (fast8: the whole 512-symbol blocks below take the batched loop)
+        const int fast_top = n_lanes == 32 ? (fast8 ? (len & ~511) : (len & ~31)) : 0;
         for (; base >= fast_top; base -= n_lanes) {
             const int left = len - base;
             const bool on = lane < left && lane < n_lanes;
@@ -519,6 +560,89 @@ encode_u8_ring_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_
                 flushed -= 512;
                 __syncwarp();
             }
+        }
+        // Batched fast loop (fast8): blocks of 16 groups, backwards. A state
+        // below 2^31 spills at most two digits (x >> 16 < 2^15 <= f 2^(31 -
+        // sb)): s1 = x >= T1, s2 = x >> 8 >= T1 with T1 = f << (31 - sb); two
+        // ballots give each lane its read-order offset, digits most
+        // significant first. The push is the word16 fast record's (the
+        // state after the spills is below f 2^(31 - sb) <= 2^30). Records
+        // of frequency 0 clear bit 31 of the AND of every M, checked once
+        // per block (then the block is rescanned for the reference's
+        // highest offending index). The spill ring drains per block (a
+        // block adds <= 1024 digits to < 512 pending).
+        if (fast8) {
+            const uint32_t lt_mul = lane ? 1u << (32 - lane) : 0u;
+            const uint32_t t_shift = 32u - tab->scale_bits;
+            const uint32_t qoff = 1u << (27u - tab->scale_bits);
+            uint32_t any2 = 0;
+            const int top_fast0 = top;
+            for (int b = (base + 32) / 512 - 1; b >= 0 && !bad; --b) {
+                if (b != cur) {  // segment cur consumed: prefetch cur - 4 into its slot
+                    __syncwarp();
+                    while (cur > b) {
+                        const int sg = cur - 4;
+                        const bool ok = sg >= 0;
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                                         in_sa + static_cast<uint32_t>(sg & 3) * kSeg8 + lane * 16),
+                                     "l"(ok ? g + sg * kSeg8 + lane * 16 : g), "r"(ok ? 16u : 0u)
+                                     : "memory");
+                        cp_async_commit();
+                        --cur;
+                    }
+                    cp_async_wait<2>();
+                    __syncwarp();
+                }
+                const uint32_t blk_sa = in_sa + static_cast<uint32_t>(b & 3) * kSeg8 + lane;
+                uint32_t macc = ~0u;
+                uint32_t sym_n = lds8(blk_sa + 15 * 32);
+#pragma unroll
+                for (int gg = 15; gg >= 0; --gg) {
+                    uint4 e;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
+                                 : "r"(rec_sa + sym_n * (16u * kRec8Copies)));
+                    if (gg > 0) sym_n = lds8(blk_sa + (gg - 1) * 32);
+                    macc &= e.x;
+                    const bool s1 = x >= e.z, s2 = (x >> 8) >= e.z;
+                    const uint32_t b1 = __ballot_sync(0xffffffffu, s1);
+                    const uint32_t b2 = __ballot_sync(0xffffffffu, s2);
+                    top -= static_cast<int>(__popc(b1) + __popc(b2));
+                    any2 |= b2;
+                    const uint32_t p = static_cast<uint32_t>(top) + __popc(b1 * lt_mul) +
+                                       __popc(b2 * lt_mul);
+                    if (s1) sts8(out_sa + (p & (kRing8 - 1)), s2 ? x >> 8 : x);
+                    if (s2) sts8(out_sa + ((p + 1u) & (kRing8 - 1)), x);
+                    x = s2 ? x >> 16 : (s1 ? x >> 8 : x);
+                    uint32_t q = __umulhi(x, e.x);
+                    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(e.y));
+                    x = (e.y >> t_shift) * (q - qoff) + (x + (e.y >> 5));
+                }
+                if (__any_sync(0xffffffffu, !(macc >> 31))) {  // a symbol of frequency 0 here
+                    uint32_t hi = 0;
+                    for (int gg = 0; gg < 16; ++gg)
+                        if (enc[lds8(blk_sa + gg * 32)].x == 0u) hi = 32u * gg + lane + 1u;
+                    hi = __reduce_max_sync(0xffffffffu, hi);
+                    if (lane == 0)
+                        atomicMax(&status->unenc_index,
+                                  static_cast<long long>(cbase + b * 512 + int(hi) - 1));
+                    bad = true;
+                    break;
+                }
+                __syncwarp();
+                while (flushed - top >= 512) {  // drain 512 bytes: 16 per lane
+                    const uint32_t ro = static_cast<uint32_t>(flushed - 512) + lane * 16;
+                    uint4 v;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                 : "r"(out_sa + (ro & (kRing8 - 1))));
+                    *reinterpret_cast<uint4 *>(o + (flushed - 512) + lane * 16) = v;
+                    flushed -= 512;
+                }
+                __syncwarp();
+            }
+            base = -32;  // every group coded
+            most = max(most, any2 ? 2u : (top != top_fast0 ? 1u : 0u));
         }
         // Fast loop (N = 32, full groups): a state below 2^31 spills at most
         // two digits (x >> 16 < 2^15 <= f 2^(31 - sb)), so two ballots give
@@ -598,11 +722,12 @@ encode_u8_ring_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_
 static size_t ring8_decode_smem(int warps, int sb, bool packed) {
     const size_t m = size_t(1) << sb;
     const size_t lut = packed ? m * 4 : kMaxSym * sizeof(uint2) + (m < 16 ? 16 : m);
-    return size_t(warps) * (kRing8 + kObuf8) + ((lut + 15) & ~size_t(15));
+    return size_t(warps) * (kRing8Alloc + kObuf8) + ((lut + 15) & ~size_t(15));
 }
 
 static size_t ring8_encode_smem(int warps) {
-    return kMaxSym * sizeof(uint2) + size_t(warps) * kRing8 + kRing8 + size_t(warps) * kRing8;
+    return kMaxSym * sizeof(uint2) + size_t(kRec8Copies) * kMaxSym * sizeof(uint4) +
+           size_t(warps) * kRing8 + kRing8 + size_t(warps) * kRing8;
 }
 
 // one CTA per SM with the SM's share of the streams (as the word16 coders)

@@ -156,7 +156,12 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
         if (gtid == kHistCounters) {
             uint32_t q = 0, ph = 0;
             for (uint32_t i = 0; i < n_stages; ++i) {
-                if (i >= kHistStages) mbar_wait(empty_addr + 8 * q, ph ^ 1u);
+                if (i >= kHistStages) {
+                    mbar_wait(empty_addr + 8 * q, ph ^ 1u);
+                    // the counting warps' reads of this slot (generic proxy)
+                    // before the bulk copy's writes (async proxy)
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
                 const uint32_t bytes = i + 1 < n_stages ? kHistStage : last_bytes;
                 mbar_expect_tx(full_addr + 8 * q, bytes);
                 bulk_g2s(ring_addr + q * kHistStage, src + size_t(i) * kHistStage, bytes,

@@ -163,3 +163,66 @@ def test_chunked_byte8_device_model_and_errors():
     short.word_offsets[-1] -= 1  # last chunk one byte short
     with pytest.raises(TruncatedStreamError):
         decode_chunked(short)
+
+
+# --------------------------------------------- N = 32 batched fast loops ---
+@pytest.mark.parametrize("sb", [8, 12, 13])
+def test_byte8_n32_fast_batches_match_oracle(sb):
+    """N = 32 byte8 with a fast record table (sb <= 13, every f <= m/2):
+    the encoder's 16-group batches (16-byte records, two spill ballots) and
+    the decoder's 16-group batches, single stream and chunked, equal the
+    reference restatement; f = 1 symbols and a near-m/2 symbol included."""
+    from paper_1402_3392_b200.chunked import decode_chunked, encode_chunked
+
+    rng = np.random.default_rng(sb)
+    m = 1 << sb
+    n_sym = min(60, m // 4)
+    freq = [1] * n_sym
+    freq[0] = m // 2  # f = m/2: the fast record's bound
+    freq[1] += m - sum(freq)
+    t = SymbolTable(freq, sb)
+    for n in (512 * 37 + 5, 65536 * 3 + 1000):
+        msg = random_message(rng, t, n)
+        msg[::97] = rng.integers(2, n_sym, size=len(msg[::97]))  # the f = 1 symbols
+        c = ilb.encode_interleaved(msg, t, 32, BYTE8)
+        p, s = oracle.encode_interleaved_u8(msg, t.freq_u32, t.cum_u32, sb, 32)
+        assert np.array_equal(c.payload, p) and c.final_states == tuple(s.tolist())
+        assert np.array_equal(ilb.decode_interleaved(c), msg)
+        cc = encode_chunked(msg, t, 32, 16384, variant=BYTE8)
+        for j in (0, cc.n_chunks - 1):
+            chunk = msg[j * 16384:(j + 1) * 16384]
+            p, s = oracle.encode_interleaved_u8(chunk, t.freq_u32, t.cum_u32, sb, 32)
+            a, b = int(cc.word_offsets[j]), int(cc.word_offsets[j + 1])
+            assert np.array_equal(cc.payload[a:b], p) and np.array_equal(cc.states[j], s)
+        assert np.array_equal(decode_chunked(cc), msg)
+
+
+def test_byte8_n32_fast_errors_and_stats():
+    """The batched N = 32 loops: a zero-frequency symbol inside a batch names
+    the symbol at the highest offending index (the reference walks down);
+    a payload cut inside the batched region raises TruncatedStreamError;
+    the digit maxima agree between the encode and decode kernels (a
+    symbol's spills are its refills)."""
+    from paper_1402_3392_b200.errors import UnencodableSymbolError
+
+    t = SymbolTable([2048, 2047, 0, 0, 1], 12)
+    msg = np.zeros(70_000, dtype=np.uint8)
+    msg[100], msg[60_000] = 2, 3
+    with pytest.raises(UnencodableSymbolError, match="symbol 3"):
+        ilb.encode_interleaved(msg, t, 32, BYTE8)
+    msg[60_000] = 1
+    msg[40_000] = 2
+    with pytest.raises(UnencodableSymbolError, match="symbol 2"):
+        ilb.encode_interleaved(msg, t, 32, BYTE8)
+    msg = zipf_1mib()
+    counts, alpha = oracle.histogram(msg)
+    t = SymbolTable.from_counts(counts[:alpha].tolist(), 12)
+    stats = RenormStats()
+    c = ilb.encode_interleaved(msg, t, 32, BYTE8, stats=stats)
+    assert np.array_equal(ilb.decode_interleaved(c, stats=stats), msg)
+    assert stats.max_encode_digits == stats.max_decode_digits == 2
+    for cut in (len(c.payload) // 3, len(c.payload) - 1):
+        short = Container(c.variant, c.lane_count, c.message_length, c.table, c.final_states,
+                          c.payload[:cut])
+        with pytest.raises(TruncatedStreamError):
+            ilb.decode_interleaved(short)
