@@ -27,8 +27,10 @@ namespace ilans {
 // Two independent 128-thread counter blocks (64 KB each) per CTA, one CTA per
 // SM, fed by the bulk-copy engine: each CTA streams its contiguous share of
 // the message through a 3 x 32 KB shared ring (cp.async.bulk completing on
-// an mbarrier per slot; a producer warp refills a slot once the 8 counting
-// warps have released it). 96 KB in flight per SM keeps HBM busy without the
+// an mbarrier per slot; thread 0 refills a slot right after the CTA barrier
+// that ends every thread's reads of it -- a barrier, rather than a producer
+// warp waiting on an "empty" mbarrier, so compute-sanitizer racecheck can
+// see the read -> refill order; same speed). 96 KB in flight per SM keeps HBM busy without the
 // register double-buffering of a load-and-count loop (66 us at config 2,
 // ~0.6 of HBM: 12 warps/SM, long_scoreboard); measured at 256 MiB: 3 x 32 KB
 // 48.6 us, 4 x 24 KB 49.3, 6 x 16 KB 50.0, 12 x 8 KB 58.6, and one counter
@@ -37,14 +39,14 @@ namespace ilans {
 // plus four per 512-byte LDS.128 (~0.8 of one wavefront per SM clock).
 constexpr int kHistGroups = 2;
 constexpr int kHistCounters = 128 * kHistGroups;        // counting threads
-constexpr int kHistThreads = kHistCounters + 32;        // + the producer warp
+constexpr int kHistThreads = kHistCounters;             // thread 0 also issues the copies
 constexpr uint32_t kHistStage = 32768;                  // bytes per ring slot
 constexpr int kHistStages = 3;
 // slots between counter flushes: < 65536 bytes per thread
 constexpr int kHistFlushStages = 64000 / (kHistStage / kHistCounters);
 constexpr size_t kHistCounterBytes = size_t(256) * 64 * 4 * kHistGroups;
 constexpr size_t kHistSmem = kHistCounterBytes + size_t(kHistStages) * kHistStage +
-                             2 * kHistStages * 8;
+                             kHistStages * 8;
 
 __device__ __forceinline__ uint32_t hist_word(uint32_t bin, uint32_t tid) {
     return bin * 64u + ((tid >> 6) << 5) + (tid & 31u);  // 64 words per bin
@@ -125,14 +127,10 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
     const uint32_t gtid = threadIdx.x;
     const uint32_t base_addr = smem_addr(hist_smem);
     const uint32_t ring_addr = base_addr + static_cast<uint32_t>(kHistCounterBytes);
-    const uint32_t full_addr = ring_addr + kHistStages * kHistStage;  // full[s], empty[s]
-    const uint32_t empty_addr = full_addr + kHistStages * 8;
+    const uint32_t full_addr = ring_addr + kHistStages * kHistStage;  // full[s]
     for (uint32_t i = gtid; i < kHistCounterBytes / 4; i += kHistThreads) hist_smem[i] = 0;
     if (gtid == 0) {
-        for (int q = 0; q < kHistStages; ++q) {
-            mbar_init(full_addr + 8 * q, 1);
-            mbar_init(empty_addr + 8 * q, kHistCounters / 32);
-        }
+        for (int q = 0; q < kHistStages; ++q) mbar_init(full_addr + 8 * q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -152,28 +150,18 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
         n_stages ? static_cast<uint32_t>(hi - lo - int64_t(n_stages - 1) * kHistStage) : 0u;
     const uint8_t *src = msg + head + lo;
 
-    if (gtid >= kHistCounters) {  // producer warp: one elected lane issues
-        if (gtid == kHistCounters) {
-            uint32_t q = 0, ph = 0;
-            for (uint32_t i = 0; i < n_stages; ++i) {
-                if (i >= kHistStages) {
-                    mbar_wait(empty_addr + 8 * q, ph ^ 1u);
-                    // the counting warps' reads of this slot (generic proxy)
-                    // before the bulk copy's writes (async proxy)
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                }
-                const uint32_t bytes = i + 1 < n_stages ? kHistStage : last_bytes;
-                mbar_expect_tx(full_addr + 8 * q, bytes);
-                bulk_g2s(ring_addr + q * kHistStage, src + size_t(i) * kHistStage, bytes,
-                         full_addr + 8 * q);
-                if (++q == kHistStages) {
-                    q = 0;
-                    ph ^= 1u;
-                }
-            }
-        }
-        return;
-    }
+    // stage i -> ring slot i % kHistStages, completing on that slot's
+    // mbarrier; thread 0 issues (the first kHistStages here, each later one
+    // right after the barrier that ends every thread's reads of its slot)
+    auto issue = [&](uint32_t i) {
+        const uint32_t q = i % kHistStages;
+        const uint32_t bytes = i + 1 < n_stages ? kHistStage : last_bytes;
+        mbar_expect_tx(full_addr + 8 * q, bytes);
+        bulk_g2s(ring_addr + q * kHistStage, src + size_t(i) * kHistStage, bytes,
+                 full_addr + 8 * q);
+    };
+    if (gtid == 0)
+        for (uint32_t i = 0; i < kHistStages && i < n_stages; ++i) issue(i);
 
     const uint32_t sub = gtid >> 7;   // counter block of this thread
     const uint32_t tid = gtid & 127u;  // column within the block
@@ -197,8 +185,8 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(v[r].x), "=r"(v[r].y), "=r"(v[r].z), "=r"(v[r].w)
                              : "r"(slot + 16 * kHistCounters * r));
-            __syncwarp();
-            if ((gtid & 31) == 0) mbar_arrive(empty_addr + 8 * q);  // slot read: release it
+            counters_sync();  // every thread has read slot q: refill it
+            if (gtid == 0 && i + kHistStages < n_stages) issue(i + kHistStages);
 #pragma unroll
             for (int r = 0; r < kVecs; ++r) hist_bump16(base_addr, col, inc, v[r]);
         } else {  // the CTA's last, partial slot
@@ -211,8 +199,7 @@ histogram_u8_kernel(const uint8_t *__restrict__ msg, int64_t n,
                                  : "=r"(v[r].x), "=r"(v[r].y), "=r"(v[r].z), "=r"(v[r].w)
                                  : "r"(slot + 16 * kHistCounters * r));
             }
-            __syncwarp();
-            if ((gtid & 31) == 0) mbar_arrive(empty_addr + 8 * q);
+            counters_sync();  // (the last slot: nothing left to issue)
 #pragma unroll
             for (int r = 0; r < kVecs; ++r)
                 if (gtid + r * kHistCounters < nvec) hist_bump16(base_addr, col, inc, v[r]);
