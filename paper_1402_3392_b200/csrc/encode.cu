@@ -24,6 +24,8 @@
 // Framing: chunk k's payload sits at scratch[k*C + len_k - w_k, k*C + len_k);
 // an exclusive scan of w_k gives word offsets and a compaction kernel packs
 // the payloads back to back (SURVEY A12 chunk framing).
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -160,6 +162,51 @@ __device__ __forceinline__ void spill_group(uint32_t &x, uint32_t &topb, uint32_
             : "memory");
 }
 
+// The N = 32 fast loop's spill step with the words stored straight to HBM
+// (no staging ring, no drains). The chunk's scratch region never straddles
+// a 4 GiB boundary here (checked by the caller), so the address is
+// {topb, hi} with a constant high word: topb is the low word of the stack
+// top's byte address, moved down by 2 per spilled word; spilling lane i
+// stores at topb_new + 2 * (spilling lanes below it). A group's <= 32 words
+// are contiguous: one coalesced request per group.
+template <int TEST>
+__device__ __forceinline__ void spill_group_g(uint32_t &x, uint32_t &topb, uint32_t hi,
+                                              uint32_t lowm, uint32_t key, uint32_t lt_mul,
+                                              uint32_t neg2, uint32_t two) {
+    if (TEST == 0)
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t, mk, c, cl, al;\n\t.reg .b64 ad;\n\t"
+            "lop3.b32 t, %0, %3, 0, 0xcf;\n\t"
+            "setp.lt.u32 p, t, %4;\n\t"
+            "vote.sync.ballot.b32 mk, p, 0xffffffff;\n\t"
+            "popc.b32 c, mk;\n\t"
+            "mad.lo.u32 %1, c, %6, %1;\n\t"
+            "mul.lo.u32 cl, mk, %5;\n\t"
+            "popc.b32 cl, cl;\n\t"
+            "mad.lo.u32 al, cl, %7, %1;\n\t"
+            "mov.b64 ad, {al, %2};\n\t"
+            "@p st.global.u16 [ad], %0;\n\t"
+            "@p shr.b32 %0, %0, 16;\n\t}"
+            : "+r"(x), "+r"(topb)
+            : "r"(hi), "r"(lowm), "r"(key), "r"(lt_mul), "r"(neg2), "r"(two)
+            : "memory");
+    else
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t, mk, c, cl, al;\n\t.reg .b64 ad;\n\t"
+            "or.b32 t, %0, %3;\n\t"
+            "setp.ge.u32 p, t, %4;\n\t"
+            "vote.sync.ballot.b32 mk, p, 0xffffffff;\n\t"
+            "popc.b32 c, mk;\n\t"
+            "mad.lo.u32 %1, c, %6, %1;\n\t"
+            "mul.lo.u32 cl, mk, %5;\n\t"
+            "popc.b32 cl, cl;\n\t"
+            "mad.lo.u32 al, cl, %7, %1;\n\t"
+            "mov.b64 ad, {al, %2};\n\t"
+            "@p st.global.u16 [ad], %0;\n\t"
+            "@p shr.b32 %0, %0, 16;\n\t}"
+            : "+r"(x), "+r"(topb)
+            : "r"(hi), "r"(lowm), "r"(key), "r"(lt_mul), "r"(neg2), "r"(two)
+            : "memory");
+}
+
 // Spilled words are staged in a per-warp shared ring (2 KB aligned, so an
 // address is base | (byte_offset & mask)) indexed by their final scratch
 // position w & 1023, and written to HBM as aligned 16-byte blocks. `flushed`
@@ -259,8 +306,9 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     const int lane = threadIdx.x & 31;
     // popc(mk & lanemask_lt) == popc(mk * 2^(32 - lane)) (FMA pipe, not ALU)
     const uint32_t lt_mul = lane ? 1u << (32 - lane) : 0u;
-    uint32_t two;  // opaque 2: keeps the cursor arithmetic as IMADs
-    asm volatile("mov.u32 %0, 2;" : "=r"(two));
+    // opaque 2 (ptxas cannot fold it: n_chunks >= 0): keeps the cursor
+    // arithmetic as IMADs (a known 2 becomes LEA / LEA.HI.X pairs)
+    const uint32_t two = 2u + static_cast<uint32_t>(static_cast<unsigned long long>(n_chunks) >> 63);
     const uint32_t neg2 = 0u - two;
     const int wib = threadIdx.x >> 5;
     uint8_t *ring = rings + wib * kInRing;
@@ -348,12 +396,54 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         const uint8_t *seg_src = g + (issued_lo - 1) * kInSeg + lane * 16;
         const uint32_t ring_sa = smem_addr(ring) + lane * 16;
         Idx b = full - 1;
-        if (MODE == 0 && (fast || fast12)) {
+        if (MODE == 0 && (fast || fast12) &&
+            (reinterpret_cast<unsigned long long>(scratch + cbase) >> 32) ==
+                (reinterpret_cast<unsigned long long>(scratch + cbase + len) >> 32)) {
             // Pairs of blocks (32 groups) per iteration: one prefetch point
             // and one wait per 1 KB of message, records loaded one group
-            // ahead straight across the two blocks; the spill ring is still
-            // drained between the halves (a half adds <= 512 words).
+            // ahead straight across the two blocks, spilled words stored
+            // straight to the scratch (spill_group_g). The per-group loop's
+            // ring is written out first; an odd last block runs the same
+            // body for 16 groups.
+            st.finish(top, lane);
             const uint32_t blk_sa = smem_addr(ring) + lane;
+            const unsigned long long gbase = reinterpret_cast<unsigned long long>(scratch + cbase);
+            const uint32_t hi = static_cast<uint32_t>(gbase >> 32);
+            uint32_t topb = static_cast<uint32_t>(gbase) + 2u * static_cast<uint32_t>(top);
+            auto body = [&](auto ng, uint32_t hi_sa, uint32_t lo_sa) {
+                constexpr int NG = decltype(ng)::value;  // groups: 32 (hi, lo) or 16 (hi)
+                uint32_t sym_n = lds_u8(hi_sa + (kInSeg / 32 - 1) * 32);
+                uint2 a_n = encf[sym_n * kEncfCopies];
+                uint32_t z_n = F12 ? encz[sym_n * kEnczCopies] : 0u;
+                sym_n = lds_u8(hi_sa + (kInSeg / 32 - 2) * 32);
+#pragma unroll
+                for (int gg = NG - 1; gg >= 0; --gg) {
+                    const uint2 a = a_n;  // {M, Z} (F12: {M, Y})
+                    const uint32_t z = z_n;
+                    if (gg > 0) {
+                        a_n = encf[sym_n * kEncfCopies];
+                        if (F12) z_n = encz[sym_n * kEnczCopies];
+                        if (gg > 1) {
+                            const int nx = gg - 2;  // group two ahead
+                            sym_n = lds_u8((nx >= kInSeg / 32 ? hi_sa : lo_sa) +
+                                           (nx % (kInSeg / 32)) * 32);
+                        }
+                    }
+                    if (!COVERED) macc &= a.x;
+                    uint32_t q;
+                    if (!F12) {
+                        spill_group_g<0>(x, topb, hi, lowm, a.y, lt_mul, neg2, two);
+                        q = __umulhi(x, a.x);
+                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
+                        x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
+                    } else {
+                        spill_group_g<1>(x, topb, hi, lowm, a.y, lt_mul, neg2, two);
+                        q = __umulhi(x, a.x);
+                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
+                        x = q * (a.y & lowm) + (x + (z >> 17));
+                    }
+                }
+            };
             for (; b >= 1; b -= 2) {
                 __syncwarp();  // every lane is done reading blocks b + 1, b + 2
 #pragma unroll
@@ -371,55 +461,18 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 }
                 cp_async_wait<2>();  // blocks b and b - 1 landed
                 __syncwarp();
-                const uint32_t hi_sa = blk_sa + ((static_cast<uint32_t>(b) & 3u) << 9);
-                const uint32_t lo_sa = blk_sa + ((static_cast<uint32_t>(b - 1) & 3u) << 9);
-                uint32_t topb = static_cast<uint32_t>(top) << 1;
-                uint32_t topb0 = topb;
-                uint32_t sym_n = lds_u8(hi_sa + (kInSeg / 32 - 1) * 32);
-                uint2 a_n = encf[sym_n * kEncfCopies];
-                uint32_t z_n = F12 ? encz[sym_n * kEnczCopies] : 0u;
-                sym_n = lds_u8(hi_sa + (kInSeg / 32 - 2) * 32);
-#pragma unroll
-                for (int gg = 2 * (kInSeg / 32) - 1; gg >= 0; --gg) {
-                    const uint2 a = a_n;  // {M, Z} (F12: {M, Y})
-                    const uint32_t z = z_n;
-                    if (gg > 0) {
-                        a_n = encf[sym_n * kEncfCopies];
-                        if (F12) z_n = encz[sym_n * kEnczCopies];
-                        if (gg > 1) {
-                            const int nx = gg - 2;  // group two ahead
-                            sym_n = lds_u8((nx >= kInSeg / 32 ? hi_sa : lo_sa) +
-                                           (nx % (kInSeg / 32)) * 32);
-                        }
-                    }
-                    if (!COVERED) macc &= a.x;
-                    uint32_t q;
-                    if (!F12) {
-                        spill_group<0, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2,
-                                              two);
-                        q = __umulhi(x, a.x);
-                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
-                        x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
-                    } else {
-                        spill_group<1, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2,
-                                              two);
-                        q = __umulhi(x, a.x);
-                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
-                        x = q * (a.y & lowm) + (x + (z >> 17));
-                    }
-                    if (gg == kInSeg / 32) {  // first half done: keep the spill ring < 512
-                        top -= static_cast<Idx>((topb0 - topb) >> 1);
-                        topb0 = topb;
-                        st.drain(top, lane);
-                    }
-                }
-                top -= static_cast<Idx>((topb0 - topb) >> 1);
-                st.drain(top, lane);
+                body(std::integral_constant<int, 2 * (kInSeg / 32)>{},
+                     blk_sa + ((static_cast<uint32_t>(b) & 3u) << 9),
+                     blk_sa + ((static_cast<uint32_t>(b - 1) & 3u) << 9));
             }
-            // an odd last block (b == 0) is read by the one-block loop below,
-            // whose wait counts one segment per block: land everything first
             cp_async_wait<0>();
             __syncwarp();
+            if (b == 0) {  // an odd last block
+                body(std::integral_constant<int, kInSeg / 32>{}, blk_sa, blk_sa);
+                b = -1;
+            }
+            top = static_cast<Idx>((topb - static_cast<uint32_t>(gbase)) >> 1);
+            st.flushed = top;  // every word below the ring's is in HBM already
         }
         for (; !bad && b >= 0; --b) {
             if (b - 3 < issued_lo) {  // segments below `full` are whole 512-byte blocks
