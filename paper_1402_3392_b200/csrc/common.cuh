@@ -22,7 +22,7 @@ constexpr int kPackedMaxBits = 15;           // packed 32-bit slot entry: sym|bi
 constexpr uint32_t kTabPacked = 1u;          // packed[] valid (sb <= 15, every f < 4096, consistent)
 constexpr uint32_t kTabEncFast = 2u;         // encf valid (sb <= 13, every f <= m/2)
 constexpr uint32_t kTabPacked64 = 4u;        // packed64[] valid (13 <= sb <= 14)
-constexpr uint32_t kTabEncFast12 = 8u;       // encf = {M, Y} + encz valid (sb = 14, f <= m/2)
+constexpr uint32_t kTabEncFast12 = 8u;       // encf = {M, Y} + encz valid (sb = 14, 15, f <= m/2)
 constexpr int kPacked64MinBits = 13;
 constexpr int kPacked64MaxBits = 14;
 constexpr int kEncFastMaxBits = 13;             // bias < 2^(sb+1) fits Z's bits [5, 32-sb)
@@ -206,12 +206,13 @@ struct EncFast {
     }
 };
 
-// sb = 14 (every f <= m / 2): bias < 2^15 no longer fits beside m - f and s
-// in one word, so the record takes 12 bytes:
-//   .x = M (as EncFast),  .y = Y = f << t | (m - f)   (m - f < 2^t)
-//   Z  = s | bias << 17   (a separate 4-byte array)
+// sb = 14, 15 (every f <= m / 2): bias < 2^(sb+1) no longer fits beside
+// m - f and s in one word, so the record takes 12 bytes:
+//   .x = M (as EncFast),  .y = Y = f << t | (m - f)   (m - f < 2^sb <= 2^t)
+//   Z  = s | bias << 16   (a separate 4-byte array; bias < 2^16, s < 16)
 // spill: (x | (2^t - 1)) >= Y;  q = umulhi(x, M) >> s (s = Z & 31);
-// x' = q (Y & (2^t - 1)) + x + (Z >> 17).
+// x' = q (Y & (2^t - 1)) + x + (Z >> 16). q is exact for every post-spill
+// x < f 2^t <= 2^31 whatever sb (f <= m / 2, see EncFast).
 struct EncFast12 {
     __host__ __device__ static void make(uint32_t f, uint32_t cum, int sb, uint2 *a,
                                          uint32_t *z) {
@@ -232,7 +233,7 @@ struct EncFast12 {
             sh = c - 1u;
         }
         *a = make_uint2(M, f << t | (m - f));
-        *z = sh | bias << 17;
+        *z = sh | bias << 16;
     }
 };
 

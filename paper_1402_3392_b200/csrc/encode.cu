@@ -440,7 +440,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         spill_group_g<1>(x, topb, hi, lowm, a.y, lt_mul, neg2, two);
                         q = __umulhi(x, a.x);
                         asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
-                        x = q * (a.y & lowm) + (x + (z >> 17));
+                        x = q * (a.y & lowm) + (x + (z >> 16));
                     }
                 }
             };
@@ -526,7 +526,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                             x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
                         } else {
                             asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
-                            x = q * (a.y & lowm) + (x + (z >> 17));
+                            x = q * (a.y & lowm) + (x + (z >> 16));
                         }
                     }
                 }
@@ -569,7 +569,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                     spill_group<1, false>(x, topb, lowm, a.y, 1u, lt_mul, oring_addr, neg2, two);
                     uint32_t q = __umulhi(x, a.x);
                     asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
-                    x = q * (a.y & lowm) + (x + (z >> 17));
+                    x = q * (a.y & lowm) + (x + (z >> 16));
                 }
             } else {
 #pragma unroll
@@ -646,7 +646,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                         x = (a.y >> t_shift) * (q - qoff) + (x + (a.y >> 5));
                     } else {
                         asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(z));
-                        x = q * (a.y & lowm) + (x + (z >> 17));
+                        x = q * (a.y & lowm) + (x + (z >> 16));
                     }
                 }
                 top -= static_cast<Idx>((topb0 - topb) >> 1);
@@ -962,7 +962,7 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
         };
         // the table's scale_bits is on the device; the sb = 14 instantiation
         // is picked by the caller's scale_bits and re-checks the flag itself
-        const bool sb14 = scale_bits == 14;
+        const bool sb14 = scale_bits == 14 || scale_bits == 15;  // the 12-byte fast record
         // mode 1: power-of-two N < 32, mode 2: other N < 32, mode 0: N = 32
         const int mode = n_lanes >= 32 ? 0 : (n_lanes & (n_lanes - 1)) == 0 ? 1 : 2;
         auto pick = [&](auto idx) {

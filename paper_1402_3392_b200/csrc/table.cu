@@ -333,7 +333,7 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         t->freq[tid] = f;
         t->enc[tid] = EncSym::make(f, cum[tid], scale_bits);
         t->dec[tid] = make_uint2(f, cum[tid]);
-        if (scale_bits == 14) {
+        if (scale_bits == 14 || scale_bits == 15) {
             uint2 a;
             uint32_t z;
             EncFast12::make(f, cum[tid], scale_bits, &a, &z);
@@ -345,7 +345,7 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         }
     }
     // fast encoder records: sb <= 13 and no symbol above half the range
-    const int fast_ok = (scale_bits <= kEncFastMaxBits || scale_bits == 14) &&
+    const int fast_ok = (scale_bits <= kEncFastMaxBits || scale_bits == 14 || scale_bits == 15) &&
                         freq[tid] <= (m >> 1) ? 1 : 0;
     if (tid == 0) t->cum[kMaxSym] = cum[kMaxSym];
     t->cum[tid] = cum[tid];
@@ -419,7 +419,7 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
     const bool p64 = -block_max_256(-ok64, red) != 0;
     if (tid == 0)
         t->flags = (all_ok ? kTabPacked : 0u) |
-                   (all_fast ? (scale_bits == 14 ? kTabEncFast12 : kTabEncFast) : 0u) |
+                   (all_fast ? (scale_bits >= 14 ? kTabEncFast12 : kTabEncFast) : 0u) |
                    (p64 ? kTabPacked64 : 0u);
 }
 

@@ -260,29 +260,30 @@ def test_fast_encoder_record_exact():
             assert np.array_equal(xm + u(Z) >= u(1 << 32), xx >= u(X)), (sb, f)
 
 
-def test_fast_encoder_record12_exact():
-    """sb = 14 takes the 12-byte fast record (common.cuh EncFast12):
+@pytest.mark.parametrize("sb", [14, 15])
+def test_fast_encoder_record12_exact(sb):
+    """sb = 14 and 15 take the 12-byte fast record (common.cuh EncFast12):
     Y = f << t | (m - f) gives the spill test (x | (2^t - 1)) >= Y and the
-    complement, Z = s | bias << 17 the shift and the bias; checked for every
-    f <= m/2 on edge, top-of-range and random numerators."""
+    complement, Z = s | bias << 16 the shift and the bias; checked for every
+    f <= m/2 (cum at both ends of its range, so bias = cum + m - 1 of f = 1
+    reaches 2m - 2) on edge, top-of-range and random numerators."""
     rng = np.random.default_rng(2)
     u = np.uint64
-    sb = 14
     m, t = 1 << sb, 32 - sb
     for f in range(1, m // 2 + 1):
-        cum = (m - f) // 3
-        M, s, bias = _encfast(f, cum, sb)
-        Y, Z = (f << t) | (m - f), s | bias << 17
-        assert Z < (1 << 32) and (Z & 31) == s and (Y & ((1 << t) - 1)) == m - f
-        X = f << t
-        xs = np.concatenate([np.arange(max(1, X - 64), X, dtype=np.uint64),
-                             rng.integers(1, X, 64, dtype=np.uint64)])
-        q = ((xs * u(M)) >> u(32)) >> u(Z & 31)
-        x2 = (q * u(Y & ((1 << t) - 1)) + xs + u(Z >> 17)) & u(0xFFFFFFFF)
-        assert np.array_equal(x2, (xs // u(f)) * u(m) + xs % u(f) + u(cum)), f
+        for cum in (m - f, (m - f) // 3):
+            M, s, bias = _encfast(f, cum, sb)
+            Y, Z = (f << t) | (m - f), s | bias << 16
+            assert Z < (1 << 32) and (Z & 31) == s and (Y & ((1 << t) - 1)) == m - f
+            X = f << t
+            xs = np.concatenate([np.arange(max(1, X - 64), X, dtype=np.uint64),
+                                 rng.integers(1, X, 64, dtype=np.uint64)])
+            q = ((xs * u(M)) >> u(32)) >> u(Z & 31)
+            x2 = (q * u(Y & ((1 << t) - 1)) + xs + u(Z >> 16)) & u(0xFFFFFFFF)
+            assert np.array_equal(x2, (xs // u(f)) * u(m) + xs % u(f) + u(cum)), (sb, f)
         xx = np.concatenate([np.arange(max(0, X - 40), X + 40, dtype=np.uint64),
                              rng.integers(0, 1 << 32, 32, dtype=np.uint64)])
-        assert np.array_equal((xx | u((1 << t) - 1)) >= u(Y), xx >= u(X)), f
+        assert np.array_equal((xx | u((1 << t) - 1)) >= u(Y), xx >= u(X)), (sb, f)
 
 
 def test_synth_host_deterministic_and_zipf():
