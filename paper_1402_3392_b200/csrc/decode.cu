@@ -95,7 +95,10 @@ __host__ __device__ constexpr bool allows64(int maxkind) {
     return maxkind == kLutPacked64 || maxkind == kLutPacked3264;
 }
 
-template <int KIND>
+// SBC: scale bits known at compile time (0: the runtime value in sb). With
+// a constant, h = (x >> sb) - 4096 is one LEA.HI instead of SHF + IADD and
+// the slot mask is an immediate (the sb = 12 packed decoder).
+template <int KIND, int SBC = 0>
 struct Lut {
     const uint32_t *packed;  // kLutPacked32: sym | bias << 8 | f << 20
     const uint2 *packed64;   // kLutPacked64: {sym | bias << 8, f}
@@ -106,7 +109,8 @@ struct Lut {
 
     // returns the symbol in the low byte
     __device__ __forceinline__ uint32_t pop(uint32_t &x) const {
-        const uint32_t slot = x & mask;
+        const uint32_t sb = SBC ? static_cast<uint32_t>(SBC) : this->sb;
+        const uint32_t slot = x & (SBC ? (1u << SBC) - 1u : mask);
         if (KIND == kLutPacked32) {
             // h = (x >> sb) - 4096; e >> 8 = bias + f * 4096, so
             // f * h + (e >> 8) = f * (x >> sb) + bias with no field mask,
@@ -141,7 +145,18 @@ struct Lut {
 struct StoreSink {
     uint8_t *out;
     uint8_t *out_k;
-    __device__ __forceinline__ void begin(int64_t, int64_t cbase, int) { out_k = out + cbase; }
+    uint8_t *run;  // next512's lane pointer (running: no per-batch address math)
+    __device__ __forceinline__ void begin(int64_t, int64_t cbase, int lane) {
+        out_k = out + cbase;
+        run = out_k + 16 * lane;
+    }
+    // the fast path's consecutive 512-byte blocks from the chunk start
+    __device__ __forceinline__ void next512(const uint8_t *buf, int lane) {
+        const uint4 o = reinterpret_cast<const uint4 *>(buf)[lane];
+        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(run), "r"(o.x), "r"(o.y),
+                     "r"(o.z), "r"(o.w) : "memory");
+        run += 512;
+    }
     __device__ __forceinline__ void block512(const uint8_t *buf, int64_t pos, int lane) {
         const uint4 o = reinterpret_cast<const uint4 *>(buf)[lane];
         asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(out_k + pos + 16 * lane),
@@ -166,7 +181,11 @@ struct StoreSink {
 struct Adler32Sink {
     uint32_t *adler;
     unsigned long long s1, si;  // per-lane partial sums (exact for chunks <= 2^27 B: < 2^62)
-    __device__ __forceinline__ void begin(int64_t, int64_t, int) { s1 = si = 0; }
+    int64_t rpos;               // next512's lane position
+    __device__ __forceinline__ void begin(int64_t, int64_t, int lane) {
+        s1 = si = 0;
+        rpos = 16 * lane;
+    }
     __device__ __forceinline__ void words(const uint32_t *w, int nw, int64_t pos0) {
         uint32_t t1 = 0, tj = 0;
 #pragma unroll
@@ -184,6 +203,12 @@ struct Adler32Sink {
         const uint4 o = reinterpret_cast<const uint4 *>(buf)[lane];
         const uint32_t w[4] = {o.x, o.y, o.z, o.w};
         words(w, 4, pos + 16 * lane);
+    }
+    __device__ __forceinline__ void next512(const uint8_t *buf, int lane) {
+        const uint4 o = reinterpret_cast<const uint4 *>(buf)[lane];
+        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+        words(w, 4, rpos);
+        rpos += 512;
     }
     __device__ __forceinline__ void block256(const uint8_t *buf, int64_t pos, int lane) {
         const uint2 o = reinterpret_cast<const uint2 *>(buf)[lane];
@@ -221,7 +246,7 @@ __host__ __device__ constexpr size_t decode_warp_smem() { return kRingAllocBytes
 // body keeps its own register allocation.
 // SMALL: the instantiation for power-of-two N < 32 (512/N-group batches);
 // a separate body so the N = 32 batch loop keeps its own schedule.
-template <int KIND, class Sink, bool SMALL>
+template <int KIND, class Sink, bool SMALL, int SBC = 0>
 __device__ __noinline__ void
 decode_warp_body(const uint16_t *__restrict__ payload, ChunkDir dir,
                  const uint32_t *__restrict__ states, int64_t n, int64_t chunk_len,
@@ -234,7 +259,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, ChunkDir dir,
     uint8_t *lut_base = smem + nw * (kRingAllocBytes + kObufBytes);
 
     // ---- stage the lookup tables in shared memory ------------------------
-    Lut<KIND> lut;
+    Lut<KIND, SBC> lut;
     lut.mask = m - 1u;
     lut.sb = static_cast<uint32_t>(sb);
     if (KIND == kLutPacked32) {
@@ -320,7 +345,10 @@ decode_warp_body(const uint16_t *__restrict__ payload, ChunkDir dir,
             const uint16_t *seg_g = src.g + 4 * kSegWords + lane * 8;
             cp_async_wait<1>();
             __syncwarp();
-            for (int64_t b = 0; b < full; ++b) {
+            // 32-bit batch counter (full < 2^29 for any message that fits in
+            // HBM); the word cursor v is rebuilt after the loop from the
+            // segment count (v / kSegWords == next_seg - 4) and vb's low bits
+            for (uint32_t b = 0; b < static_cast<uint32_t>(full); ++b) {
                 const uint32_t vb0 = vb;
                 // shared address of the cursor; the batch reads < 512 words
                 // past it, which the mirrored slots keep contiguous
@@ -359,8 +387,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, ChunkDir dir,
                 }
                 vb = vb0 + (a - a0);
                 __syncwarp();
-                sink.block512(obuf, b * (32 * kBatch), lane);
-                v += (vb - vb0) >> 1;
+                sink.next512(obuf, lane);
                 const uint32_t seg = (vb >> 9) & 0x7FFFFFu;
                 if (seg != seg_cur) {  // one or two segments were finished
                     do {
@@ -381,6 +408,7 @@ decode_warp_body(const uint16_t *__restrict__ payload, ChunkDir dir,
                 __syncwarp();
             }
             cur = next_seg - 4;  // == v / kSegWords; cur + 1.. cur + 3 issued
+            v = cur * kSegWords + ((vb >> 1) & (kSegWords - 1));
             base = full * (32 * kBatch);
         }
         // ---------------- generic per-group loop (any N <= 32, tails) ------
@@ -455,7 +483,15 @@ decode_warp_dispatch(const uint16_t *__restrict__ payload, ChunkDir dir,
                      int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab, Sink out,
                      uint64_t *__restrict__ consumed, uint32_t *__restrict__ final_states,
                      DStatus *__restrict__ status, DecodeTrace trace, uint8_t *smem, int sb) {
-    if (allows32(MAXKIND) && (tab->flags & kTabPacked))
+    if (MAXKIND == kLutPacked32 && !SMALL && sb == 12 && (tab->flags & kTabPacked))
+        decode_warp_body<kLutPacked32, Sink, SMALL, 12>(payload, dir, states, n, chunk_len,
+                                                        n_chunks, n_lanes, tab, out, consumed,
+                                                        final_states, status, trace, smem, sb);
+    else if (MAXKIND == kLutPacked3264 && !SMALL && sb == 14 && (tab->flags & kTabPacked))
+        decode_warp_body<kLutPacked32, Sink, SMALL, 14>(payload, dir, states, n, chunk_len,
+                                                        n_chunks, n_lanes, tab, out, consumed,
+                                                        final_states, status, trace, smem, sb);
+    else if (allows32(MAXKIND) && (tab->flags & kTabPacked))
         decode_warp_body<kLutPacked32, Sink, SMALL>(payload, dir, states, n, chunk_len,
                                                     n_chunks, n_lanes, tab, out, consumed,
                                                     final_states, status, trace, smem, sb);
