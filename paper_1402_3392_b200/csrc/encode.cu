@@ -446,17 +446,32 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             };
             for (; b >= 1; b -= 2) {
                 __syncwarp();  // every lane is done reading blocks b + 1, b + 2
+                if (b >= 3 && issued_lo == b - 1) {
+                    // steady state: segments b - 2 and b - 3 exist and are
+                    // the next two to issue (no bounds or zero-fill selects)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                                     ring_sa + ((static_cast<uint32_t>(b - 2) & 3u) << 9)),
+                                 "l"(seg_src) : "memory");
+                    cp_async_commit();
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                                     ring_sa + ((static_cast<uint32_t>(b - 3) & 3u) << 9)),
+                                 "l"(seg_src - kInSeg) : "memory");
+                    cp_async_commit();
+                    seg_src -= 2 * kInSeg;
+                    issued_lo = b - 3;
+                } else {
 #pragma unroll
-                for (int q = 2; q <= 3; ++q) {
-                    const Idx sg = b - q;
-                    if (sg < issued_lo) {
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
-                                         ring_sa + ((static_cast<uint32_t>(sg) & 3u) << 9)),
-                                     "l"(sg >= 0 ? seg_src : g), "r"(sg >= 0 ? 16u : 0u)
-                                     : "memory");
-                        seg_src -= kInSeg;
-                        cp_async_commit();
-                        issued_lo = sg;
+                    for (int q = 2; q <= 3; ++q) {
+                        const Idx sg = b - q;
+                        if (sg < issued_lo) {
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                                             ring_sa + ((static_cast<uint32_t>(sg) & 3u) << 9)),
+                                         "l"(sg >= 0 ? seg_src : g), "r"(sg >= 0 ? 16u : 0u)
+                                         : "memory");
+                            seg_src -= kInSeg;
+                            cp_async_commit();
+                            issued_lo = sg;
+                        }
                     }
                 }
                 cp_async_wait<2>();  // blocks b and b - 1 landed
