@@ -23,6 +23,7 @@ constexpr uint32_t kTabPacked = 1u;          // packed[] valid (sb <= 15, every 
 constexpr uint32_t kTabEncFast = 2u;         // encf valid (sb <= 13, every f <= m/2)
 constexpr uint32_t kTabPacked64 = 4u;        // packed64[] valid (13 <= sb <= 14)
 constexpr uint32_t kTabEncFast12 = 8u;       // encf = {M, Y} + encz valid (sb = 14, 15, f <= m/2)
+constexpr uint32_t kTabEncQuad = 16u;        // encq valid (any sb, every f <= m/2)
 constexpr int kPacked64MinBits = 13;
 constexpr int kPacked64MaxBits = 14;
 constexpr int kEncFastMaxBits = 13;             // bias < 2^(sb+1) fits Z's bits [5, 32-sb)
@@ -42,6 +43,7 @@ struct alignas(16) TableDev {
     uint2 encf[kMaxSym];              // EncFast records {M, (m - f) << t | bias << 5 | s}
                                       // (sb = 14: EncFast12 {M, f << t | (m - f)})
     uint32_t encz[kMaxSym];           // EncFast12: s | bias << 17
+    uint4 encq[kMaxSym];              // EncQuad records {M, f << t | s, m - f, bias}
     uint32_t packed[1 << kPackedMaxBits];  // sym | bias << 8 | f << 20 (f < 4096)
     uint8_t slot_sym[1 << kMaxScaleBits];
     uint2 packed64[1 << 14];          // 13 <= sb <= 14: {sym | bias << 8, f}
@@ -234,6 +236,33 @@ struct EncFast12 {
         }
         *a = make_uint2(M, f << t | (m - f));
         *z = sh | bias << 16;
+    }
+};
+
+// 16-byte fast record (any sb <= 16 with every f <= m / 2, flag
+// kTabEncQuad): the N = 32 encoder's form. One LDS.128 (a quarter-warp per
+// wavefront) hands every field over ready to use, so the push is 4 ops:
+//   .x = M (as EncFast)      .y = Y = f << t | s   (s < 32 <= 2^t - 1)
+//   .z = m - f               .w = bias (as EncFast: cum, + m - 1 for f = 1)
+// spill:  (x | (2^t - 1)) >= Y   (<=> x >= f << t: the low t bits of the
+//         left side are all ones, and s < 2^t)
+// push:   q = umulhi(x, M) >> s  (shf.r.wrap reads s from Y's low 5 bits)
+//         x' = (m - f) q + (x + bias)
+struct EncQuad {
+    __host__ __device__ static uint4 make(uint32_t f, uint32_t cum, int sb) {
+        const uint32_t m = 1u << sb, t = 32u - static_cast<uint32_t>(sb);
+        if (f == 0 || f > m / 2) return make_uint4(0u, 0u, 0u, 0u);
+        uint32_t M, sh, bias = cum;
+        if (f == 1) {
+            M = 0xFFFFFFFFu;
+            sh = 0u;
+            bias = cum + m - 1u;
+        } else {
+            const uint32_t c = ceil_log2(f);
+            M = static_cast<uint32_t>(((1ull << (31 + c)) + f - 1) / f);
+            sh = c - 1u;
+        }
+        return make_uint4(M, f << t | sh, m - f, bias);
     }
 };
 

@@ -64,6 +64,9 @@ constexpr uint32_t kOutRingBytes = kOutRing * 2;
 // encoder's shared-memory pipe then ~0.9 busy).
 constexpr int kEncfCopies = 16;  // 8-byte records: a half-warp per wavefront
 constexpr int kEnczCopies = 32;
+constexpr int kEncqCopies = 8;   // 16-byte records (QUAD): a quarter-warp per wavefront
+static_assert(kEncqCopies * sizeof(uint4) == kEncfCopies * sizeof(uint2),
+              "the QUAD copies reuse the fast-record region");
 __host__ __device__ constexpr size_t encode_smem_bytes(int warps) {
     return kMaxSym * sizeof(uint2) + size_t(kEncfCopies) * kMaxSym * sizeof(uint2) +
            size_t(kEnczCopies) * kMaxSym * sizeof(uint32_t) + size_t(warps) * kInRing +
@@ -274,7 +277,9 @@ struct SpillStage {
 // COVERED: the table was quantized from this message's own histogram, so
 // every symbol in it has f >= 1 (rans.py:197-199) and the fast loops skip
 // the per-group zero-frequency check (the AND of every record's M).
-template <typename Idx, bool F12, int MODE, bool COVERED = false>
+// QUAD (N = 32, int chunks): the fast loop runs on the 16-byte EncQuad
+// records (8 bank-private copies in the fast-record region) whatever sb.
+template <typename Idx, bool F12, int MODE, bool COVERED = false, bool QUAD = false>
 __global__ void __launch_bounds__(kEncMaxWarps * 32, 1)
 encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len,
                    int64_t n_chunks, int n_lanes, const TableDev *__restrict__ tab,
@@ -288,17 +293,25 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     uint32_t *encz_rep = reinterpret_cast<uint32_t *>(encf_rep + kEncfCopies * kMaxSym);
     uint8_t *rings = reinterpret_cast<uint8_t *>(encz_rep + kEnczCopies * kMaxSym);
     uint16_t *oring_raw = reinterpret_cast<uint16_t *>(rings + nw * kInRing);
-    const bool fast = !F12 && (tab->flags & kTabEncFast) != 0u;
-    const bool fast12 = F12 && (tab->flags & kTabEncFast12) != 0u;
+    const bool fast = !QUAD && !F12 && (tab->flags & kTabEncFast) != 0u;
+    const bool fast12 = !QUAD && F12 && (tab->flags & kTabEncFast12) != 0u;
+    const bool quad = QUAD && (tab->flags & kTabEncQuad) != 0u;
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
-    for (int i = threadIdx.x; i < kEncfCopies * kMaxSym; i += blockDim.x)
-        encf_rep[i] = tab->encf[i / kEncfCopies];
-    for (int i = threadIdx.x; i < kEnczCopies * kMaxSym; i += blockDim.x)
-        encz_rep[i] = tab->encz[i / kEnczCopies];
+    if (QUAD) {
+        uint4 *q = reinterpret_cast<uint4 *>(encf_rep);
+        for (int i = threadIdx.x; i < kEncqCopies * kMaxSym; i += blockDim.x)
+            q[i] = tab->encq[i / kEncqCopies];
+    } else {
+        for (int i = threadIdx.x; i < kEncfCopies * kMaxSym; i += blockDim.x)
+            encf_rep[i] = tab->encf[i / kEncfCopies];
+        for (int i = threadIdx.x; i < kEnczCopies * kMaxSym; i += blockDim.x)
+            encz_rep[i] = tab->encz[i / kEnczCopies];
+    }
     __syncthreads();
     // this lane's copies: record of symbol s at encf[s * kEncfCopies]
     const uint2 *encf = encf_rep + (threadIdx.x & (kEncfCopies - 1));
     const uint32_t *encz = encz_rep + (threadIdx.x & (kEnczCopies - 1));
+    const uint4 *encq = reinterpret_cast<const uint4 *>(encf_rep) + (threadIdx.x & (kEncqCopies - 1));
     const EncCtx ctx(tab->scale_bits);
     const uint32_t lowm = ~0u >> tab->scale_bits;  // 2^t - 1, t = 32 - sb
     const uint32_t t_shift = 32u - tab->scale_bits;
@@ -396,7 +409,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         const uint8_t *seg_src = g + (issued_lo - 1) * kInSeg + lane * 16;
         const uint32_t ring_sa = smem_addr(ring) + lane * 16;
         Idx b = full - 1;
-        if (MODE == 0 && (fast || fast12) &&
+        if (MODE == 0 && (fast || fast12 || quad) &&
             (reinterpret_cast<unsigned long long>(scratch + cbase) >> 32) ==
                 (reinterpret_cast<unsigned long long>(scratch + cbase + len) >> 32)) {
             // Pairs of blocks (32 groups) per iteration: one prefetch point
@@ -412,6 +425,29 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             uint32_t topb = static_cast<uint32_t>(gbase) + 2u * static_cast<uint32_t>(top);
             auto body = [&](auto ng, uint32_t hi_sa, uint32_t lo_sa) {
                 constexpr int NG = decltype(ng)::value;  // groups: 32 (hi, lo) or 16 (hi)
+                if (QUAD) {
+                    uint32_t sym_n = lds_u8(hi_sa + (kInSeg / 32 - 1) * 32);
+                    uint4 a_n = encq[sym_n * kEncqCopies];
+                    sym_n = lds_u8(hi_sa + (kInSeg / 32 - 2) * 32);
+#pragma unroll
+                    for (int gg = NG - 1; gg >= 0; --gg) {
+                        const uint4 a = a_n;  // {M, Y, m - f, bias}
+                        if (gg > 0) {
+                            a_n = encq[sym_n * kEncqCopies];
+                            if (gg > 1) {
+                                const int nx = gg - 2;
+                                sym_n = lds_u8((nx >= kInSeg / 32 ? hi_sa : lo_sa) +
+                                               (nx % (kInSeg / 32)) * 32);
+                            }
+                        }
+                        if (!COVERED) macc &= a.x;
+                        spill_group_g<1>(x, topb, hi, lowm, a.y, lt_mul, neg2, two);
+                        uint32_t q = __umulhi(x, a.x);
+                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
+                        x = a.z * q + (x + a.w);
+                    }
+                    return;
+                }
                 uint32_t sym_n = lds_u8(hi_sa + (kInSeg / 32 - 1) * 32);
                 uint2 a_n = encf[sym_n * kEncfCopies];
                 uint32_t z_n = F12 ? encz[sym_n * kEnczCopies] : 0u;
@@ -668,7 +704,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 st.drain(top, lane);
             }
         }
-        if ((fast || fast12) && !bad && __ballot_sync(0xffffffffu, (macc >> 31) == 0u)) {
+        if ((fast || fast12 || quad) && !bad && __ballot_sync(0xffffffffu, (macc >> 31) == 0u)) {
             // rare: some symbol of the fast region has f = 0 (its scratch is
             // garbage but stayed inside the chunk: at most 32 spills per
             // group). The highest offending index, as the reference's
@@ -988,9 +1024,9 @@ cudaError_t launch_encode(const uint8_t *d_msg, int64_t n, int64_t chunk_len, in
             } else if (mode == 2) {
                 if (sb14) go(encode_warp_kernel<I, true, 2>);
                 else go(encode_warp_kernel<I, false, 2>);
-            } else if (covered && sizeof(I) == 4) {
-                if (sb14) go(encode_warp_kernel<int, true, 0, true>);
-                else go(encode_warp_kernel<int, false, 0, true>);
+            } else if (sizeof(I) == 4) {  // N = 32: the 16-byte records, any sb
+                if (covered) go(encode_warp_kernel<int, false, 0, true, true>);
+                else go(encode_warp_kernel<int, false, 0, false, true>);
             } else {
                 if (sb14) go(encode_warp_kernel<I, true, 0>);
                 else go(encode_warp_kernel<I, false, 0>);

@@ -343,7 +343,9 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
             t->encf[tid] = EncFast::make(f, cum[tid], scale_bits);
             t->encz[tid] = 0u;
         }
+        t->encq[tid] = EncQuad::make(f, cum[tid], scale_bits);
     }
+    const int quad_ok = freq[tid] <= (m >> 1) ? 1 : 0;
     // fast encoder records: sb <= 13 and no symbol above half the range
     const int fast_ok = (scale_bits <= kEncFastMaxBits || scale_bits == 14 || scale_bits == 15) &&
                         freq[tid] <= (m >> 1) ? 1 : 0;
@@ -416,11 +418,12 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
     __syncthreads();
     const int all_ok = -block_max_256(-ok, red);  // min over threads
     const int all_fast = -block_max_256(-fast_ok, red);
+    const int all_quad = -block_max_256(-quad_ok, red);
     const bool p64 = -block_max_256(-ok64, red) != 0;
     if (tid == 0)
         t->flags = (all_ok ? kTabPacked : 0u) |
                    (all_fast ? (scale_bits >= 14 ? kTabEncFast12 : kTabEncFast) : 0u) |
-                   (p64 ? kTabPacked64 : 0u);
+                   (p64 ? kTabPacked64 : 0u) | (all_quad ? kTabEncQuad : 0u);
 }
 
 // mode: counts != nullptr -> quantize(counts) first (alphabet = max+1).

@@ -286,6 +286,37 @@ def test_fast_encoder_record12_exact(sb):
         assert np.array_equal((xx | u((1 << t) - 1)) >= u(Y), xx >= u(X)), (sb, f)
 
 
+@pytest.mark.parametrize("sb", [1, 5, 11, 12, 13, 14, 15, 16])
+def test_quad_encoder_record_exact(sb):
+    """The 16-byte fast record of the N = 32 encoder (common.cuh EncQuad,
+    any sb, every f <= m/2): {M, Y = f << t | s, m - f, bias}. The spill test
+    (x | (2^t - 1)) >= Y is x >= f << t, q = umulhi(x, M) >> (Y & 31) is x // f
+    (x - 1 for f = 1) and (m - f) q + x + bias is the reference push
+    (_core.pyx:36-41) -- for every f at sb <= 13 and for the edges plus a
+    sample of f above, cum at both ends of its range, on edge, top-of-range
+    and random post-spill numerators."""
+    rng = np.random.default_rng(3)
+    u = np.uint64
+    m, t = 1 << sb, 32 - sb
+    fs = np.arange(1, max(1, m // 2) + 1)
+    if len(fs) > 4096:
+        fs = np.unique(np.concatenate([fs[:512], fs[-512:], rng.choice(fs, 2048, replace=False)]))
+    for f in map(int, fs):
+        X = f << t
+        for cum in (m - f, (m - f) // 3, 0):
+            M, s, bias = _encfast(f, cum, sb)
+            Y = (f << t) | s
+            assert Y < (1 << 32) and (Y & 31) == s and s < (1 << t) - 1
+            xs = np.concatenate([np.arange(max(1, X - 64), X, dtype=np.uint64),
+                                 rng.integers(1, X, 64, dtype=np.uint64)])
+            q = ((xs * u(M)) >> u(32)) >> u(Y & 31)
+            x2 = (u(m - f) * q + xs + u(bias)) & u(0xFFFFFFFF)
+            assert np.array_equal(x2, (xs // u(f)) * u(m) + xs % u(f) + u(cum)), (sb, f)
+        xx = np.concatenate([np.arange(max(0, X - 40), min(1 << 32, X + 40), dtype=np.uint64),
+                             rng.integers(0, 1 << 32, 32, dtype=np.uint64)])
+        assert np.array_equal((xx | u((1 << t) - 1)) >= u(Y), xx >= u(X)), (sb, f)
+
+
 def test_synth_host_deterministic_and_zipf():
     a = synth.synth_host(1 << 16, 1.1, seed=7)
     b = synth.synth_host(1 << 16, 1.1, seed=7)
