@@ -289,6 +289,19 @@ __device__ __forceinline__ int block_max_256(int v, int *red) {
     return s;
 }
 
+__device__ __forceinline__ uint32_t block_and_256(uint32_t v, uint32_t *red) {
+    const int tid = threadIdx.x;
+    v = __reduce_and_sync(0xffffffffu, v);
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    uint32_t s = red[0];
+#pragma unroll
+    for (int w = 1; w < kMaxSym / 32; ++w) s &= red[w];
+    __syncthreads();
+    return s;
+}
+
 // floor(c * m / T) for c*m < 2^81, result <= m <= 2^16: binary search on q.
 __device__ __forceinline__ uint32_t floor_cm_over_t(unsigned long long c, uint32_t m,
                                                     u128 total) {
@@ -416,10 +429,14 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
         }
     }
     __syncthreads();
-    const int all_ok = -block_max_256(-ok, red);  // min over threads
-    const int all_fast = -block_max_256(-fast_ok, red);
-    const int all_quad = -block_max_256(-quad_ok, red);
-    const bool p64 = -block_max_256(-ok64, red) != 0;
+    // the four "every thread" conditions in one CTA-wide AND
+    const uint32_t all = block_and_256(static_cast<uint32_t>((ok ? 1 : 0) | (fast_ok ? 2 : 0) |
+                                                             (ok64 ? 4 : 0) | (quad_ok ? 8 : 0)),
+                                       reinterpret_cast<uint32_t *>(red));
+    const int all_ok = (all & 1u) != 0u;
+    const int all_fast = (all & 2u) != 0u;
+    const bool p64 = (all & 4u) != 0u;
+    const int all_quad = (all & 8u) != 0u;
     if (tid == 0)
         t->flags = (all_ok ? kTabPacked : 0u) |
                    (all_fast ? (scale_bits >= 14 ? kTabEncFast12 : kTabEncFast) : 0u) |
@@ -451,19 +468,48 @@ build_table_kernel(const unsigned long long *__restrict__ counts, const uint32_t
     if (counts) {
         // ---- rans.quantize (rans.py:171-211), bit-exact ------------------
         unsigned long long c = counts[tid];
-        const int alpha = block_max_256(c ? tid + 1 : 0, red);
+        // alphabet (highest present symbol + 1), present symbols and the
+        // 128-bit total (as two 64-bit halves) in one CTA-wide reduction
+        int alpha, present;
+        u128 total;
+        {
+            __shared__ unsigned long long red_hi[8];
+            __shared__ int red_p[8];
+            int a = c ? tid + 1 : 0, p = c ? 1 : 0;
+            unsigned long long lo = c & 0xFFFFFFFFull, hi = c >> 32;
+            for (int o = 16; o > 0; o >>= 1) {
+                a = max(a, __shfl_xor_sync(0xffffffffu, a, o));
+                p += __shfl_xor_sync(0xffffffffu, p, o);
+                lo += __shfl_xor_sync(0xffffffffu, lo, o);
+                hi += __shfl_xor_sync(0xffffffffu, hi, o);
+            }
+            if ((tid & 31) == 0) {
+                red[tid >> 5] = a;
+                red_p[tid >> 5] = p;
+                red64[tid >> 5] = lo;
+                red_hi[tid >> 5] = hi;
+            }
+            __syncthreads();
+            alpha = red[0];
+            present = red_p[0];
+            lo = red64[0];
+            hi = red_hi[0];
+#pragma unroll
+            for (int w = 1; w < kMaxSym / 32; ++w) {
+                alpha = max(alpha, red[w]);
+                present += red_p[w];
+                lo += red64[w];
+                hi += red_hi[w];
+            }
+            __syncthreads();
+            total = ((u128)hi << 32) + lo;
+        }
         n_sym = alpha;
         if (alpha == 0) {  // empty message -> counts [1, 1] (cli.py:32-34)
             n_sym = 2;
             c = tid < 2 ? 1ull : 0ull;
-        }
-        const int present = block_sum_256<int>(c ? 1 : 0, red);
-        u128 total = 0;
-        {
-            // 128-bit sum as two 64-bit halves
-            const unsigned long long lo = block_sum_256<unsigned long long>(c & 0xFFFFFFFFull, red64);
-            const unsigned long long hi = block_sum_256<unsigned long long>(c >> 32, red64);
-            total = ((u128)hi << 32) + lo;
+            present = 2;
+            total = 2;
         }
         if (static_cast<uint32_t>(present) > m) {
             if (tid == 0) {
