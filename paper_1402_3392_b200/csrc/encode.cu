@@ -410,8 +410,8 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         const uint32_t ring_sa = smem_addr(ring) + lane * 16;
         Idx b = full - 1;
         if (MODE == 0 && (fast || fast12 || quad) &&
-            (reinterpret_cast<unsigned long long>(scratch + cbase) >> 32) ==
-                (reinterpret_cast<unsigned long long>(scratch + cbase + len) >> 32)) {
+            (QUAD || (reinterpret_cast<unsigned long long>(scratch + cbase) >> 32) ==
+                         (reinterpret_cast<unsigned long long>(scratch + cbase + len) >> 32))) {
             // Pairs of blocks (32 groups) per iteration: one prefetch point
             // and one wait per 1 KB of message, records loaded one group
             // ahead straight across the two blocks, spilled words stored
@@ -421,10 +421,42 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             st.finish(top, lane);
             const uint32_t blk_sa = smem_addr(ring) + lane;
             const unsigned long long gbase = reinterpret_cast<unsigned long long>(scratch + cbase);
-            const uint32_t hi = static_cast<uint32_t>(gbase >> 32);
-            uint32_t topb = static_cast<uint32_t>(gbase) + 2u * static_cast<uint32_t>(top);
-            auto body = [&](auto ng, uint32_t hi_sa, uint32_t lo_sa) {
+            // byte address of the stack top as {topb, hi}: the 32-bit low
+            // word moves, the high word is fixed while an iteration cannot
+            // borrow from it (QUAD: topb >= the iteration's 2 KB of spills;
+            // otherwise the WIDE body carries it -- a chunk whose slot
+            // crosses a 4 GiB boundary stays on the fast path)
+            const unsigned long long top0 = gbase + 2ull * static_cast<unsigned long long>(top);
+            uint32_t hi = static_cast<uint32_t>(top0 >> 32);
+            uint32_t topb = static_cast<uint32_t>(top0);
+            auto body = [&](auto ng, auto wide, uint32_t hi_sa, uint32_t lo_sa) {
                 constexpr int NG = decltype(ng)::value;  // groups: 32 (hi, lo) or 16 (hi)
+                constexpr bool WIDE = decltype(wide)::value;
+                if constexpr (QUAD && WIDE) {
+                    unsigned long long t64 = static_cast<unsigned long long>(hi) << 32 | topb;
+#pragma unroll 1
+                    for (int gg = NG - 1; gg >= 0; --gg) {
+                        const uint32_t sym = lds_u8((gg >= kInSeg / 32 ? hi_sa : lo_sa) +
+                                                    (gg % (kInSeg / 32)) * 32);
+                        const uint4 a = encq[sym * kEncqCopies];
+                        if (!COVERED) macc &= a.x;
+                        const bool p = (x | lowm) >= a.y;
+                        const uint32_t mk = __ballot_sync(0xffffffffu, p);
+                        t64 -= 2ull * static_cast<unsigned long long>(__popc(mk));
+                        if (p) {
+                            *reinterpret_cast<uint16_t *>(
+                                t64 + 2ull * static_cast<unsigned long long>(__popc(mk & lt))) =
+                                static_cast<uint16_t>(x);
+                            x >>= 16;
+                        }
+                        uint32_t q = __umulhi(x, a.x);
+                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
+                        x = a.z * q + (x + a.w);
+                    }
+                    topb = static_cast<uint32_t>(t64);
+                    hi = static_cast<uint32_t>(t64 >> 32);
+                    return;
+                }
                 if (QUAD) {
                     uint32_t sym_n = lds_u8(hi_sa + (kInSeg / 32 - 1) * 32);
                     uint4 a_n = encq[sym_n * kEncqCopies];
@@ -480,6 +512,11 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                     }
                 }
             };
+            // CHK: the chunk's slot crosses a 4 GiB boundary, so each
+            // iteration checks whether it could borrow from the high word
+            // (a separate copy of the loop: the others pay nothing for it)
+            auto pairs = [&](auto chk) {
+            constexpr bool CHK = decltype(chk)::value;
             for (; b >= 1; b -= 2) {
                 __syncwarp();  // every lane is done reading blocks b + 1, b + 2
                 if (b >= 3 && issued_lo == b - 1) {
@@ -512,17 +549,33 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 }
                 cp_async_wait<2>();  // blocks b and b - 1 landed
                 __syncwarp();
-                body(std::integral_constant<int, 2 * (kInSeg / 32)>{},
-                     blk_sa + ((static_cast<uint32_t>(b) & 3u) << 9),
-                     blk_sa + ((static_cast<uint32_t>(b - 1) & 3u) << 9));
+                const uint32_t sa_hi = blk_sa + ((static_cast<uint32_t>(b) & 3u) << 9);
+                const uint32_t sa_lo = blk_sa + ((static_cast<uint32_t>(b - 1) & 3u) << 9);
+                if (!CHK || topb >= 2u * 32u * 2u * (kInSeg / 32))
+                    body(std::integral_constant<int, 2 * (kInSeg / 32)>{}, std::false_type{},
+                         sa_hi, sa_lo);
+                else
+                    body(std::integral_constant<int, 2 * (kInSeg / 32)>{}, std::true_type{},
+                         sa_hi, sa_lo);
             }
+            };
+            if (QUAD && (gbase >> 32) != ((gbase + 2ull * static_cast<unsigned long long>(len)) >> 32))
+                pairs(std::true_type{});
+            else
+                pairs(std::false_type{});
             cp_async_wait<0>();
             __syncwarp();
             if (b == 0) {  // an odd last block
-                body(std::integral_constant<int, kInSeg / 32>{}, blk_sa, blk_sa);
+                if (!QUAD || topb >= 32u * 2u * (kInSeg / 32))
+                    body(std::integral_constant<int, kInSeg / 32>{}, std::false_type{}, blk_sa,
+                         blk_sa);
+                else
+                    body(std::integral_constant<int, kInSeg / 32>{}, std::true_type{}, blk_sa,
+                         blk_sa);
                 b = -1;
             }
-            top = static_cast<Idx>((topb - static_cast<uint32_t>(gbase)) >> 1);
+            top = static_cast<Idx>(
+                ((static_cast<unsigned long long>(hi) << 32 | topb) - gbase) >> 1);
             st.flushed = top;  // every word below the ring's is in HBM already
         }
         for (; !bad && b >= 0; --b) {
