@@ -922,7 +922,8 @@ def other_precision(a, dev, d_msg, n, sb, steps=10):
             "decode_roofline_frac": dec_bytes / (ph[3] * 1e-3) / 1e9 / hbm,
             "encode_roofline_frac": enc_bytes / (ph[1] * 1e-3) / 1e9 / hbm,
             "decode_lut": "packed32" if flags & 1 else "packed64" if flags & 4 else "two-lookup",
-            "encode_record": "fast12" if flags & 8 else "fast" if flags & 2 else "generic",
+            "encode_record": ("quad16" if flags & 16 else "fast12" if flags & 8 else "fast" if flags & 2
+                              else "generic"),
             "payload_bits_per_byte": 16 * words / n}
 
 
