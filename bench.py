@@ -372,14 +372,17 @@ def _plugin_range(job):
 
     lo, hi = job
     msg, table, C, lanes = _PLUGIN
-    ok = True
+    outs = []
     t0 = time.perf_counter()
     for k in range(lo, hi):
         chunk = msg[k * C:(k + 1) * C]
         c = encode_interleaved(chunk, table, lanes, WORD16, backend="b200")
-        out = decode_interleaved(c, backend="b200")
-        ok &= bool(np.array_equal(out, chunk))
-    return time.perf_counter() - t0, ok
+        outs.append(decode_interleaved(c, backend="b200"))
+    el = time.perf_counter() - t0
+    # round-trip check after the clock (the reference bench verifies
+    # outside its timed region too, reference bench.py:86-93)
+    ok = all(np.array_equal(o, msg[k * C:(k + 1) * C]) for k, o in zip(range(lo, hi), outs))
+    return el, ok
 
 
 CONFIG1_DIGEST = "1ea63c4d860a4650"  # byte8 N=2 sb=12 container
@@ -1103,6 +1106,12 @@ def main():
         sys.exit(launch_ranks(a))
     else:
         run_b200(a)
+    # the line is printed: leave without the interpreter's teardown (one
+    # --plugin-only run of many died with SIGSEGV after printing, during
+    # CUDA / thread teardown at exit; the result is already out)
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(0)
 
 
 if __name__ == "__main__":

@@ -66,6 +66,11 @@ int ilans_set_device(int device, ilans_status *st);
 /* Number of kernel launches issued by this library since load (counter used
  * by bench.py's gpu_launches evidence). */
 uint64_t ilans_launch_count(void);
+/* The process is exiting: per-thread contexts destroyed after this (the
+ * main thread's, after the host language's own shutdown) release nothing
+ * through the CUDA runtime, whose teardown may already have run; the OS
+ * reclaims their memory. Bindings call it from their exit hook. */
+void ilans_process_exiting(void);
 
 /* -------------------------------------------------------------------------
  * 1. Host-buffer drop-ins (reference: pkg/src/ilans/_core.pyx)

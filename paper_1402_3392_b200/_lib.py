@@ -9,6 +9,7 @@ RuntimeError (ILANS_ERR_CUDA).
 
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 from pathlib import Path
@@ -82,6 +83,7 @@ PROTOTYPES = [
     ("ilans_device_count", ctypes.c_int, []),
     ("ilans_set_device", ctypes.c_int, [ctypes.c_int, _st]),
     ("ilans_launch_count", ctypes.c_uint64, []),
+    ("ilans_process_exiting", None, []),
     ("ilans_encode_interleaved_u16", ctypes.c_int,
      [_vp, _i64, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _st]),
     ("ilans_decode_interleaved_u16", ctypes.c_int,
@@ -156,6 +158,10 @@ for _name, _res, _args in PROTOTYPES:
     _fn.argtypes = _args
 
 EXPORTED = [p[0] for p in PROTOTYPES]
+
+# per-thread contexts outliving the interpreter must not call into a
+# CUDA runtime that is being torn down (see ilans_process_exiting)
+atexit.register(lib.ilans_process_exiting)
 
 
 def raise_for(rc: int, st: Status, what: str = "") -> None:

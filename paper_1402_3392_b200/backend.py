@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes
 import os
 import warnings
+import weakref
 from dataclasses import dataclass
 from typing import Callable
 
@@ -35,6 +36,28 @@ def _u32(a):
     return np.ascontiguousarray(a, dtype=np.uint32)
 
 
+# Host addresses of the model arrays: drop-in callers pass the same table
+# views (SymbolTable's cached freq_u32 / cum_u32 / slot_u8) on every call,
+# and a.ctypes.data costs ~1 us per array per call under the GIL.
+_ptr_cache: dict[int, tuple] = {}
+
+
+def _tptr(a: np.ndarray) -> int:
+    # keyed by identity (a weak reference guards against a reused id) and
+    # size (an in-place resize that moves the buffer changes it)
+    hit = _ptr_cache.get(id(a))
+    if hit is not None and hit[0]() is a and hit[2] == a.size:
+        return hit[1]
+    p = a.ctypes.data
+    if len(_ptr_cache) > 64:
+        _ptr_cache.clear()
+    try:
+        _ptr_cache[id(a)] = (weakref.ref(a), p, a.size)
+    except TypeError:  # not weak-referenceable: no caching
+        pass
+    return p
+
+
 def encode_interleaved_u16(msg, freq, cum, scale_bits: int, n_lanes: int):
     """Backward interleaved encode on the B200. Returns (payload u16 array in
     decoder read order, final lane states u32 array) -- contract of
@@ -49,7 +72,7 @@ def encode_interleaved_u16(msg, freq, cum, scale_bits: int, n_lanes: int):
     words = ctypes.c_int64(0)
     st = _lib.Status()
     rc = _lib.lib.ilans_encode_interleaved_u16(
-        _lib.ptr(m), len(m), _lib.ptr(f), len(f), _lib.ptr(c), int(scale_bits), int(n_lanes),
+        _lib.ptr(m), len(m), _tptr(f), len(f), _tptr(c), int(scale_bits), int(n_lanes),
         _lib.ptr(payload), ctypes.byref(words), _lib.ptr(states), ctypes.byref(st))
     _lib.raise_for(rc, st, "encode_interleaved_u16")
     return payload[: words.value].copy(), states
@@ -88,8 +111,8 @@ def _decode(fn, payload, states, slot_sym, freq, cum, scale_bits, msg_len, n_lan
     out = np.empty(max(1, msg_len), dtype=np.uint8)
     consumed = ctypes.c_int64(0)
     st = _lib.Status()
-    rc = fn(_lib.ptr(pay), len(pay), _lib.ptr(xs), _lib.ptr(slot), len(slot), _lib.ptr(f),
-            _lib.ptr(c), len(f), int(scale_bits), int(msg_len), int(n_lanes), _lib.ptr(out),
+    rc = fn(_lib.ptr(pay), len(pay), _lib.ptr(xs), _tptr(slot), len(slot), _tptr(f),
+            _tptr(c), len(f), int(scale_bits), int(msg_len), int(n_lanes), _lib.ptr(out),
             ctypes.byref(consumed), ctypes.byref(st))
     _lib.raise_for(rc, st, "decode")
     if with_stats:

@@ -79,7 +79,7 @@ class ChunkedContainer:
         """Chunk k as a standalone IEC1 container (reference-decodable)."""
         a, b = int(self.word_offsets[k]), int(self.word_offsets[k + 1])
         return Container(self.variant, self.lane_count, self.chunk_length(k), self.table,
-                         tuple(int(x) for x in self.states[k]), self.payload[a:b].copy())
+                         tuple(self.states[k].tolist()), self.payload[a:b].copy())
 
     def to_bytes(self) -> bytes:
         byte8 = self.variant == BYTE8

@@ -10,6 +10,8 @@
 #include <cstring>
 #include <mutex>
 #include <sched.h>
+#include <time.h>
+#include <unistd.h>
 #include <unordered_map>
 #include <vector>
 
@@ -81,6 +83,8 @@ using namespace ilans;
 // ---------------------------------------------------------------------------
 namespace {
 
+std::atomic<bool> g_exiting{false};  // ilans_process_exiting()
+
 struct DevBuf {
     void *p = nullptr;
     size_t cap = 0;
@@ -143,7 +147,10 @@ struct Ctx {
     uint32_t tab_f[kMaxSym] = {0}, tab_c[kMaxSym + 1] = {0};
     std::vector<uint8_t> tab_slot;
     ~Ctx() {
-        if (!init || cudaSetDevice(dev) != cudaSuccess) return;
+        // at process exit the runtime may be torn down already (the main
+        // thread's thread_local contexts die after the interpreter's exit
+        // hooks): leave the memory to the OS
+        if (!init || g_exiting.load() || cudaSetDevice(dev) != cudaSuccess) return;
         for (DevBuf *b : {&msg, &scratch, &payload, &out, &states, &ws, &slot, &freq, &cum, &table,
                           &status, &counts, &offsets, &consumed, &words, &trace, &io})
             if (b->p) cudaFree(b->p);
@@ -243,6 +250,8 @@ extern "C" int ilans_set_device(int device, ilans_status *st) {
 
 extern "C" uint64_t ilans_launch_count(void) { return g_launches.load(); }
 
+extern "C" void ilans_process_exiting(void) { g_exiting.store(true); }
+
 extern "C" size_t ilans_table_bytes(void) { return sizeof(TableDev); }
 extern "C" size_t ilans_dstatus_bytes(void) { return sizeof(DStatus); }
 
@@ -329,12 +338,27 @@ static bool encode_table_fits(const uint32_t *freq, const uint32_t *cum, int n_f
 // last copy, and the host polls that word, yielding its core between polls
 // (no driver lock, no spinning thread starving the Python threads). The
 // stream is queried now and then so a failed launch cannot hang the wait.
+// Waiting threads beyond half the host's cores sleep 20 us between polls
+// instead of yielding: with more pollers than cores the yielding threads
+// took the cores from the one thread holding the GIL (plugin throughput
+// fell from 8 to 16 to 32 threads). One or a few waiters keep yielding
+// (no added latency).
+static std::atomic<int> g_waiters{0};
+static const int g_spin_waiters = [] {
+    const long n = sysconf(_SC_NPROCESSORS_ONLN);
+    return n > 1 ? static_cast<int>(n / 2) : 1;
+}();
+
 static cudaError_t ctx_wait(Ctx &c) {
     const uint32_t want = ++c.seq;
     flag_kernel<<<1, 1, 0, c.stream>>>(c.dflag, want);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     ilans_note_launch();
+    struct Waiter {
+        Waiter() { g_waiters.fetch_add(1, std::memory_order_relaxed); }
+        ~Waiter() { g_waiters.fetch_sub(1, std::memory_order_relaxed); }
+    } waiter;
     for (uint32_t i = 1;; ++i) {
         if (__atomic_load_n(c.hflag, __ATOMIC_ACQUIRE) == want) return cudaSuccess;
         if ((i & 1023u) == 0) {
@@ -343,7 +367,12 @@ static cudaError_t ctx_wait(Ctx &c) {
             if (e == cudaSuccess && __atomic_load_n(c.hflag, __ATOMIC_ACQUIRE) != want)
                 return cudaStreamSynchronize(c.stream);  // (flag store not yet visible)
         }
-        sched_yield();
+        if (g_waiters.load(std::memory_order_relaxed) > g_spin_waiters) {
+            const timespec ts{0, 20000};
+            nanosleep(&ts, nullptr);
+        } else {
+            sched_yield();
+        }
     }
 }
 
