@@ -9,6 +9,7 @@ ilans_decode_interleaved_u16, ilans_decode_lanes_u16). Same signatures,
 same return values, same exception types. ``integration/install_into_reference.py``
 installs it into a copy of the reference and registers ``Backend("b200")``.
 """
+import atexit
 import ctypes
 import os
 
@@ -17,6 +18,8 @@ import numpy as np
 from .errors import TruncatedStreamError, UnencodableSymbolError
 
 _lib = ctypes.CDLL(os.environ.get("ILANS_B200_LIB", "libilans_b200.so"))
+# the library's per-thread contexts skip CUDA teardown once the process exits
+atexit.register(_lib.ilans_process_exiting)
 
 
 class _Status(ctypes.Structure):  # ilans_status (include/ilans_b200.h)
