@@ -24,6 +24,7 @@ constexpr uint32_t kTabEncFast = 2u;         // encf valid (sb <= 13, every f <=
 constexpr uint32_t kTabPacked64 = 4u;        // packed64[] valid (13 <= sb <= 14)
 constexpr uint32_t kTabEncFast12 = 8u;       // encf = {M, Y} + encz valid (sb = 14, 15, f <= m/2)
 constexpr uint32_t kTabEncQuad = 16u;        // encq valid (any sb, every f <= m/2)
+constexpr uint32_t kTabEncQuadX = 32u;       // encqx valid (any sb, every f < m)
 constexpr int kPacked64MinBits = 13;
 constexpr int kPacked64MaxBits = 14;
 constexpr int kEncFastMaxBits = 13;             // bias < 2^(sb+1) fits Z's bits [5, 32-sb)
@@ -44,6 +45,7 @@ struct alignas(16) TableDev {
                                       // (sb = 14: EncFast12 {M, f << t | (m - f)})
     uint32_t encz[kMaxSym];           // EncFast12: s | bias << 17
     uint4 encq[kMaxSym];              // EncQuad records {M, f << t | s, m - f, bias}
+    uint4 encqx[kMaxSym];             // EncQuadX records {magic, f << t | l, m - f, cum}
     uint32_t packed[1 << kPackedMaxBits];  // sym | bias << 8 | f << 20 (f < 4096)
     uint8_t slot_sym[1 << kMaxScaleBits];
     uint2 packed64[1 << 14];          // 13 <= sb <= 14: {sym | bias << 8, f}
@@ -263,6 +265,24 @@ struct EncQuad {
             sh = c - 1u;
         }
         return make_uint4(M, f << t | sh, m - f, bias);
+    }
+};
+
+// The same 16-byte form for tables with a symbol above m/2 (skewed sources;
+// flag kTabEncQuadX, every f < m): the 32-bit M of EncQuad is not exact
+// there, so the division takes divmagic's 33-bit magic (exact for every
+// x < 2^32): .x = magic, .y = Y = f << t | l, .z = m - f, .w = cum;
+//   q = (umulhi(x, magic) + x) >> l   (33-bit sum: add.cc / addc + shf.r.wrap)
+//   x' = (m - f) q + (x + cum)
+// two more instructions than EncQuad. f = 0 is all zeros (Y = 0 marks it:
+// every valid Y >= 2^t).
+struct EncQuadX {
+    __host__ __device__ static uint4 make(uint32_t f, uint32_t cum, int sb) {
+        const uint32_t m = 1u << sb, t = 32u - static_cast<uint32_t>(sb);
+        if (f == 0 || f >= m) return make_uint4(0u, 0u, 0u, 0u);
+        uint32_t magic, l;
+        divmagic(f, &magic, &l);
+        return make_uint4(magic, f << t | l, m - f, cum);
     }
 };
 

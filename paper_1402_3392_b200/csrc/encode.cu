@@ -65,8 +65,9 @@ constexpr uint32_t kOutRingBytes = kOutRing * 2;
 constexpr int kEncfCopies = 16;  // 8-byte records: a half-warp per wavefront
 constexpr int kEnczCopies = 32;
 constexpr int kEncqCopies = 8;   // 16-byte records (QUAD): a quarter-warp per wavefront
-static_assert(kEncqCopies * sizeof(uint4) == kEncfCopies * sizeof(uint2),
-              "the QUAD copies reuse the fast-record region");
+static_assert(kEncqCopies * sizeof(uint4) == kEncfCopies * sizeof(uint2) &&
+                  kEncqCopies * sizeof(uint4) == kEnczCopies * sizeof(uint32_t),
+              "the QUAD copies reuse the fast-record regions");
 __host__ __device__ constexpr size_t encode_smem_bytes(int warps) {
     return kMaxSym * sizeof(uint2) + size_t(kEncfCopies) * kMaxSym * sizeof(uint2) +
            size_t(kEnczCopies) * kMaxSym * sizeof(uint32_t) + size_t(warps) * kInRing +
@@ -163,6 +164,19 @@ __device__ __forceinline__ void spill_group(uint32_t &x, uint32_t &topb, uint32_
             : "+r"(x), "+r"(topb)
             : "r"(lowm), "r"(key), "r"(lt_mul), "r"(ring_addr), "r"(neg2), "r"(two), "r"(on)
             : "memory");
+}
+
+// The 16-byte records' push (EncQuad, XQ = EncQuadX: exact 33-bit magic).
+template <bool XQ>
+__device__ __forceinline__ uint32_t quad_push(uint32_t x, const uint4 &a) {
+    uint32_t q = __umulhi(x, a.x);
+    if (XQ)  // q = (q + x) >> l as a 33-bit sum
+        asm("{\n\t.reg .u32 lo, hi;\n\tadd.cc.u32 lo, %1, %2;\n\taddc.u32 hi, 0, 0;\n\t"
+            "shf.r.wrap.b32 %0, lo, hi, %3;\n\t}"
+            : "=r"(q) : "r"(q), "r"(x), "r"(a.y));
+    else
+        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
+    return a.z * q + (x + a.w);
 }
 
 // The N = 32 fast loop's spill step with the words stored straight to HBM
@@ -296,11 +310,16 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     const bool fast = !QUAD && !F12 && (tab->flags & kTabEncFast) != 0u;
     const bool fast12 = !QUAD && F12 && (tab->flags & kTabEncFast12) != 0u;
     const bool quad = QUAD && (tab->flags & kTabEncQuad) != 0u;
+    // a symbol above m/2: the exact-magic 16-byte records (EncQuadX)
+    const bool quadx = QUAD && !quad && (tab->flags & kTabEncQuadX) != 0u;
     for (int i = threadIdx.x; i < kMaxSym; i += blockDim.x) enc[i] = tab->enc[i];
     if (QUAD) {
-        uint4 *q = reinterpret_cast<uint4 *>(encf_rep);
-        for (int i = threadIdx.x; i < kEncqCopies * kMaxSym; i += blockDim.x)
-            q[i] = tab->encq[i / kEncqCopies];
+        uint4 *q = reinterpret_cast<uint4 *>(quad ? static_cast<void *>(encf_rep)
+                                                  : static_cast<void *>(encz_rep));
+        const uint4 *src = quad ? tab->encq : tab->encqx;
+        if (quad || quadx)
+            for (int i = threadIdx.x; i < kEncqCopies * kMaxSym; i += blockDim.x)
+                q[i] = src[i / kEncqCopies];
     } else {
         for (int i = threadIdx.x; i < kEncfCopies * kMaxSym; i += blockDim.x)
             encf_rep[i] = tab->encf[i / kEncfCopies];
@@ -312,6 +331,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
     const uint2 *encf = encf_rep + (threadIdx.x & (kEncfCopies - 1));
     const uint32_t *encz = encz_rep + (threadIdx.x & (kEnczCopies - 1));
     const uint4 *encq = reinterpret_cast<const uint4 *>(encf_rep) + (threadIdx.x & (kEncqCopies - 1));
+    const uint4 *encqx = reinterpret_cast<const uint4 *>(encz_rep) + (threadIdx.x & (kEncqCopies - 1));
     const EncCtx ctx(tab->scale_bits);
     const uint32_t lowm = ~0u >> tab->scale_bits;  // 2^t - 1, t = 32 - sb
     const uint32_t t_shift = 32u - tab->scale_bits;
@@ -409,7 +429,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
         const uint8_t *seg_src = g + (issued_lo - 1) * kInSeg + lane * 16;
         const uint32_t ring_sa = smem_addr(ring) + lane * 16;
         Idx b = full - 1;
-        if (MODE == 0 && (fast || fast12 || quad) &&
+        if (MODE == 0 && (fast || fast12 || quad || quadx) &&
             (QUAD || (reinterpret_cast<unsigned long long>(scratch + cbase) >> 32) ==
                          (reinterpret_cast<unsigned long long>(scratch + cbase + len) >> 32))) {
             // Pairs of blocks (32 groups) per iteration: one prefetch point
@@ -429,17 +449,19 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             const unsigned long long top0 = gbase + 2ull * static_cast<unsigned long long>(top);
             uint32_t hi = static_cast<uint32_t>(top0 >> 32);
             uint32_t topb = static_cast<uint32_t>(top0);
-            auto body = [&](auto ng, auto wide, uint32_t hi_sa, uint32_t lo_sa) {
+            auto body = [&](auto ng, auto wide, auto xq, uint32_t hi_sa, uint32_t lo_sa) {
                 constexpr int NG = decltype(ng)::value;  // groups: 32 (hi, lo) or 16 (hi)
                 constexpr bool WIDE = decltype(wide)::value;
+                constexpr bool XQ = decltype(xq)::value;  // EncQuadX records
+                const uint4 *rec = XQ ? encqx : encq;
                 if constexpr (QUAD && WIDE) {
                     unsigned long long t64 = static_cast<unsigned long long>(hi) << 32 | topb;
 #pragma unroll 1
                     for (int gg = NG - 1; gg >= 0; --gg) {
                         const uint32_t sym = lds_u8((gg >= kInSeg / 32 ? hi_sa : lo_sa) +
                                                     (gg % (kInSeg / 32)) * 32);
-                        const uint4 a = encq[sym * kEncqCopies];
-                        if (!COVERED) macc &= a.x;
+                        const uint4 a = rec[sym * kEncqCopies];
+                        if (!COVERED) macc = XQ ? min(macc, a.y) : macc & a.x;
                         const bool p = (x | lowm) >= a.y;
                         const uint32_t mk = __ballot_sync(0xffffffffu, p);
                         t64 -= 2ull * static_cast<unsigned long long>(__popc(mk));
@@ -449,9 +471,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                                 static_cast<uint16_t>(x);
                             x >>= 16;
                         }
-                        uint32_t q = __umulhi(x, a.x);
-                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
-                        x = a.z * q + (x + a.w);
+                        x = quad_push<XQ>(x, a);
                     }
                     topb = static_cast<uint32_t>(t64);
                     hi = static_cast<uint32_t>(t64 >> 32);
@@ -459,24 +479,22 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 }
                 if (QUAD) {
                     uint32_t sym_n = lds_u8(hi_sa + (kInSeg / 32 - 1) * 32);
-                    uint4 a_n = encq[sym_n * kEncqCopies];
+                    uint4 a_n = rec[sym_n * kEncqCopies];
                     sym_n = lds_u8(hi_sa + (kInSeg / 32 - 2) * 32);
 #pragma unroll
                     for (int gg = NG - 1; gg >= 0; --gg) {
                         const uint4 a = a_n;  // {M, Y, m - f, bias}
                         if (gg > 0) {
-                            a_n = encq[sym_n * kEncqCopies];
+                            a_n = rec[sym_n * kEncqCopies];
                             if (gg > 1) {
                                 const int nx = gg - 2;
                                 sym_n = lds_u8((nx >= kInSeg / 32 ? hi_sa : lo_sa) +
                                                (nx % (kInSeg / 32)) * 32);
                             }
                         }
-                        if (!COVERED) macc &= a.x;
+                        if (!COVERED) macc = XQ ? min(macc, a.y) : macc & a.x;
                         spill_group_g<1>(x, topb, hi, lowm, a.y, lt_mul, neg2, two);
-                        uint32_t q = __umulhi(x, a.x);
-                        asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(0u), "r"(a.y));
-                        x = a.z * q + (x + a.w);
+                        x = quad_push<XQ>(x, a);
                     }
                     return;
                 }
@@ -515,7 +533,7 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
             // CHK: the chunk's slot crosses a 4 GiB boundary, so each
             // iteration checks whether it could borrow from the high word
             // (a separate copy of the loop: the others pay nothing for it)
-            auto pairs = [&](auto chk) {
+            auto pairs = [&](auto chk, auto xq) {
             constexpr bool CHK = decltype(chk)::value;
             for (; b >= 1; b -= 2) {
                 __syncwarp();  // every lane is done reading blocks b + 1, b + 2
@@ -553,26 +571,34 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 const uint32_t sa_lo = blk_sa + ((static_cast<uint32_t>(b - 1) & 3u) << 9);
                 if (!CHK || topb >= 2u * 32u * 2u * (kInSeg / 32))
                     body(std::integral_constant<int, 2 * (kInSeg / 32)>{}, std::false_type{},
-                         sa_hi, sa_lo);
+                         xq, sa_hi, sa_lo);
                 else
                     body(std::integral_constant<int, 2 * (kInSeg / 32)>{}, std::true_type{},
-                         sa_hi, sa_lo);
+                         xq, sa_hi, sa_lo);
             }
-            };
-            if (QUAD && (gbase >> 32) != ((gbase + 2ull * static_cast<unsigned long long>(len)) >> 32))
-                pairs(std::true_type{});
-            else
-                pairs(std::false_type{});
             cp_async_wait<0>();
             __syncwarp();
             if (b == 0) {  // an odd last block
                 if (!QUAD || topb >= 32u * 2u * (kInSeg / 32))
-                    body(std::integral_constant<int, kInSeg / 32>{}, std::false_type{}, blk_sa,
-                         blk_sa);
+                    body(std::integral_constant<int, kInSeg / 32>{}, std::false_type{}, xq,
+                         blk_sa, blk_sa);
                 else
-                    body(std::integral_constant<int, kInSeg / 32>{}, std::true_type{}, blk_sa,
-                         blk_sa);
+                    body(std::integral_constant<int, kInSeg / 32>{}, std::true_type{}, xq,
+                         blk_sa, blk_sa);
                 b = -1;
+            }
+            };
+            const bool cross = QUAD && (gbase >> 32) !=
+                                           ((gbase + 2ull * static_cast<unsigned long long>(len)) >> 32);
+            // one copy of the loop per (crossing, record form): only QUAD
+            // kernels instantiate the EncQuadX copies
+            if (QUAD && quadx) {
+                if (cross) pairs(std::true_type{}, std::true_type{});
+                else pairs(std::false_type{}, std::true_type{});
+            } else if (cross) {
+                pairs(std::true_type{}, std::false_type{});
+            } else {
+                pairs(std::false_type{}, std::false_type{});
             }
             top = static_cast<Idx>(
                 ((static_cast<unsigned long long>(hi) << 32 | topb) - gbase) >> 1);
@@ -757,7 +783,9 @@ encode_warp_kernel(const uint8_t *__restrict__ msg, int64_t n, int64_t chunk_len
                 st.drain(top, lane);
             }
         }
-        if ((fast || fast12 || quad) && !bad && __ballot_sync(0xffffffffu, (macc >> 31) == 0u)) {
+        // (EncQuadX: the least Y of the region, 0 iff some f = 0)
+        if ((fast || fast12 || quad || quadx) && !bad &&
+            __ballot_sync(0xffffffffu, quadx ? macc == 0u : (macc >> 31) == 0u)) {
             // rare: some symbol of the fast region has f = 0 (its scratch is
             // garbage but stayed inside the chunk: at most 32 spills per
             // group). The highest offending index, as the reference's

@@ -357,8 +357,10 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
             t->encz[tid] = 0u;
         }
         t->encq[tid] = EncQuad::make(f, cum[tid], scale_bits);
+        t->encqx[tid] = EncQuadX::make(f, cum[tid], scale_bits);
     }
     const int quad_ok = freq[tid] <= (m >> 1) ? 1 : 0;
+    const int quadx_ok = freq[tid] < m ? 1 : 0;
     // fast encoder records: sb <= 13 and no symbol above half the range
     const int fast_ok = (scale_bits <= kEncFastMaxBits || scale_bits == 14 || scale_bits == 15) &&
                         freq[tid] <= (m >> 1) ? 1 : 0;
@@ -431,16 +433,19 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
     __syncthreads();
     // the four "every thread" conditions in one CTA-wide AND
     const uint32_t all = block_and_256(static_cast<uint32_t>((ok ? 1 : 0) | (fast_ok ? 2 : 0) |
-                                                             (ok64 ? 4 : 0) | (quad_ok ? 8 : 0)),
+                                                             (ok64 ? 4 : 0) | (quad_ok ? 8 : 0) |
+                                                             (quadx_ok ? 16 : 0)),
                                        reinterpret_cast<uint32_t *>(red));
     const int all_ok = (all & 1u) != 0u;
     const int all_fast = (all & 2u) != 0u;
     const bool p64 = (all & 4u) != 0u;
     const int all_quad = (all & 8u) != 0u;
+    const int all_quadx = (all & 16u) != 0u;
     if (tid == 0)
         t->flags = (all_ok ? kTabPacked : 0u) |
                    (all_fast ? (scale_bits >= 14 ? kTabEncFast12 : kTabEncFast) : 0u) |
-                   (p64 ? kTabPacked64 : 0u) | (all_quad ? kTabEncQuad : 0u);
+                   (p64 ? kTabPacked64 : 0u) | (all_quad ? kTabEncQuad : 0u) |
+                   (all_quadx ? kTabEncQuadX : 0u);
 }
 
 // mode: counts != nullptr -> quantize(counts) first (alphabet = max+1).

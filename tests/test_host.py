@@ -317,6 +317,37 @@ def test_quad_encoder_record_exact(sb):
         assert np.array_equal((xx | u((1 << t) - 1)) >= u(Y), xx >= u(X)), (sb, f)
 
 
+@pytest.mark.parametrize("sb", [1, 2, 8, 12, 14, 16])
+def test_quadx_encoder_record_exact(sb):
+    """The 16-byte record for tables with a symbol above m/2 (common.cuh
+    EncQuadX, every f < m): {magic, Y = f << t | l, m - f, cum} with divmagic's
+    33-bit magic. (x | 2^t - 1) >= Y is the spill test, q = (umulhi(x, magic)
+    + x) >> (Y & 31) (a 33-bit sum) is x // f and (m - f) q + x + cum the
+    reference push (_core.pyx:36-41), for f above and below m/2."""
+    rng = np.random.default_rng(4)
+    u = np.uint64
+    m, t = 1 << sb, 32 - sb
+    fs = np.arange(1, m)
+    if len(fs) > 3000:
+        fs = np.unique(np.concatenate([fs[:300], fs[-1500:], rng.choice(fs, 1200, replace=False)]))
+    for f in map(int, fs):
+        l = (f - 1).bit_length()
+        magic = ((1 << (32 + l)) // f) + 1 - (1 << 32)
+        Y = (f << t) | l
+        assert 0 <= magic < (1 << 32) and Y < (1 << 32) and (Y & 31) == l and Y >= (1 << t)
+        X = f << t
+        xs = np.concatenate([np.arange(max(0, X - 48), X, dtype=np.uint64),
+                             rng.integers(0, X, 48, dtype=np.uint64)])
+        q = (((xs * u(magic)) >> u(32)) + xs) >> u(Y & 31)
+        assert np.array_equal(q, xs // u(f)), (sb, f)
+        for cum in (0, m - f):
+            x2 = (u(m - f) * q + xs + u(cum)) & u(0xFFFFFFFF)
+            assert np.array_equal(x2, (xs // u(f)) * u(m) + xs % u(f) + u(cum)), (sb, f)
+        xx = np.concatenate([np.arange(max(0, X - 40), min(1 << 32, X + 40), dtype=np.uint64),
+                             rng.integers(0, 1 << 32, 32, dtype=np.uint64)])
+        assert np.array_equal((xx | u((1 << t) - 1)) >= u(Y), xx >= u(X)), (sb, f)
+
+
 def test_synth_host_deterministic_and_zipf():
     a = synth.synth_host(1 << 16, 1.1, seed=7)
     b = synth.synth_host(1 << 16, 1.1, seed=7)
