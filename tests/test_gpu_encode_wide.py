@@ -40,12 +40,14 @@ def _framed(codec, d_msg, n):
             codec.chunk_words[:k].clone())
 
 
-@pytest.mark.parametrize("sb", [12, 14])
-def test_encode_scratch_across_4gib_boundary(sb):
+@pytest.mark.parametrize("sb, zipf_s", [(12, 1.1), (14, 1.1), (12, 2.97)])
+def test_encode_scratch_across_4gib_boundary(sb, zipf_s):
+    """zipf_s = 2.97 (H ~ 1 bit) gives a symbol above m/2: the EncQuadX
+    records (exact 33-bit magic) on the same paths."""
     dev = torch.device("cuda", 0)
     C, N, k = 65536, 32, 6
     n = C * k - 777  # a short last chunk (per-group tail + fast blocks)
-    d_msg = synth_device(n, 1.1, 99, device=dev)
+    d_msg = synth_device(n, zipf_s, 99, device=dev)
     ref = _framed(DeviceCodec(n, C, N, sb, dev), d_msg, n)
     w = ref[3].cpu().numpy().astype(np.int64)  # words per chunk (right-aligned in the slot)
 
