@@ -66,8 +66,12 @@ int sm_count() {
 cudaError_t launch_build_table(const unsigned long long *d_counts, const uint32_t *d_freq,
                                int n_freq, const uint32_t *d_cum, const uint8_t *d_slot,
                                int scale_bits, TableDev *d_table, cudaStream_t stream) {
-    build_table_kernel<<<1, kMaxSym, 0, stream>>>(d_counts, d_freq, n_freq, d_cum, d_slot,
-                                                  scale_bits, d_table);
+    // from counts (cum follows from the quantized freq): the slot tables are
+    // split over several CTAs; drop-in tables (given cum / slot) use one
+    const int parts = d_counts && scale_bits >= 1 && scale_bits <= kMaxScaleBits
+                          ? table_parts(scale_bits) : 1;
+    build_table_kernel<<<parts, kMaxSym, 0, stream>>>(d_counts, d_freq, n_freq, d_cum, d_slot,
+                                                      scale_bits, d_table);
     ilans_note_launch();
     return cudaGetLastError();
 }

@@ -13,6 +13,12 @@ __global__ void build_table_kernel(const unsigned long long *__restrict__ counts
                                    const uint32_t *freq_in, int n_freq, const uint32_t *cum_in,
                                    const uint8_t *slot_in, int scale_bits, TableDev *t);
 
+// CTAs of a table build from counts: the slot tables (>= 1024 slots) are
+// split so each thread writes 4 or more (sb 12: 4 CTAs ... sb >= 14: 16)
+__host__ __device__ constexpr int table_parts(int scale_bits) {
+    return scale_bits >= 14 ? 16 : scale_bits >= 10 ? (1 << (scale_bits - 10)) : 1;
+}
+
 // Host launchers (all asynchronous on `stream`; return cudaError_t).
 cudaError_t launch_histogram(const uint8_t *d_msg, int64_t n, unsigned long long *d_counts,
                              cudaStream_t stream);

@@ -448,6 +448,80 @@ __device__ void fill_tables(TableDev *t, const uint32_t *freq, const uint32_t *c
                    (all_quadx ? kTabEncQuadX : 0u);
 }
 
+// fill_tables for a model quantized from counts (cum is freq's prefix sum,
+// no slot map given) with the slot tables split over gridDim.x CTAs: every
+// CTA quantized the same counts (the same result), CTA b writes the slots
+// [b m / G, (b + 1) m / G) and CTA 0 the per-symbol records and the flags.
+// The packed-entry checks are per symbol here (a slot's bias < f, so the
+// 32-bit entry fits iff every f <= 4095), and the 64-bit entries are only
+// written when the 32-bit ones do not fit (the decoder's fallback).
+__device__ void fill_tables_split(TableDev *t, const uint32_t *freq, const uint32_t *cum,
+                                  int scale_bits, int *red) {
+    const int tid = threadIdx.x;
+    const uint32_t m = 1u << scale_bits;
+    const uint32_t f_me = freq[tid];
+    const bool sb32 = scale_bits <= kPackedMaxBits;
+    const bool sb64 = scale_bits >= kPacked64MinBits && scale_bits <= kPacked64MaxBits;
+    const bool fast_sb = scale_bits <= kEncFastMaxBits || scale_bits == 14 || scale_bits == 15;
+    const uint32_t all = block_and_256(
+        static_cast<uint32_t>((f_me <= 4095u ? 1 : 0) | (fast_sb && f_me <= (m >> 1) ? 2 : 0) |
+                              (f_me <= (m >> 1) ? 8 : 0) | (f_me < m ? 16 : 0)),
+        reinterpret_cast<uint32_t *>(red));
+    const bool fits32 = (all & 1u) != 0u;
+    if (blockIdx.x == 0) {
+        t->freq[tid] = f_me;
+        t->enc[tid] = EncSym::make(f_me, cum[tid], scale_bits);
+        t->dec[tid] = make_uint2(f_me, cum[tid]);
+        if (scale_bits == 14 || scale_bits == 15) {
+            uint2 a;
+            uint32_t z;
+            EncFast12::make(f_me, cum[tid], scale_bits, &a, &z);
+            t->encf[tid] = a;
+            t->encz[tid] = z;
+        } else {
+            t->encf[tid] = EncFast::make(f_me, cum[tid], scale_bits);
+            t->encz[tid] = 0u;
+        }
+        t->encq[tid] = EncQuad::make(f_me, cum[tid], scale_bits);
+        t->encqx[tid] = EncQuadX::make(f_me, cum[tid], scale_bits);
+        if (tid == 0) t->cum[kMaxSym] = cum[kMaxSym];
+        t->cum[tid] = cum[tid];
+        if (tid == 0)
+            t->flags = (sb32 && fits32 ? kTabPacked : 0u) |
+                       ((all & 2u) ? (scale_bits >= 14 ? kTabEncFast12 : kTabEncFast) : 0u) |
+                       (sb64 ? kTabPacked64 : 0u) | ((all & 8u) ? kTabEncQuad : 0u) |
+                       ((all & 16u) ? kTabEncQuadX : 0u);
+    }
+    const bool w64 = sb64 && !fits32;
+    const uint32_t per = m / (kMaxSym * gridDim.x);  // a multiple of 4 (launch)
+    const uint32_t j0 = (blockIdx.x * kMaxSym + tid) * per, j1 = j0 + per;
+    int s_cur = 0;
+    {  // largest s with cum[s] <= j0 (zero-f symbols skip)
+        int lo = 0, hi = kMaxSym - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cum[mid] <= j0) lo = mid; else hi = mid - 1;
+        }
+        s_cur = lo;
+    }
+    for (uint32_t j = j0; j < j1; j += 4) {
+        uint32_t e[4], sy = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t jj = j + q;
+            while (s_cur < kMaxSym - 1 && cum[s_cur + 1] <= jj) ++s_cur;
+            const uint32_t sym = static_cast<uint32_t>(s_cur);
+            const uint32_t f = freq[sym];
+            const uint32_t bias = jj - cum[sym];
+            e[q] = sym | (bias & 0xFFFu) << 8 | (f & 0xFFFu) << 20;
+            sy |= sym << (8 * q);
+            if (w64) t->packed64[jj] = make_uint2(sym | bias << 8, f);
+        }
+        if (sb32) *reinterpret_cast<uint4 *>(t->packed + j) = make_uint4(e[0], e[1], e[2], e[3]);
+        *reinterpret_cast<uint32_t *>(t->slot_sym + j) = sy;
+    }
+}
+
 // mode: counts != nullptr -> quantize(counts) first (alphabet = max+1).
 //       otherwise freq_in/cum_in/slot_in as given (drop-in decode/encode).
 __global__ void __launch_bounds__(kMaxSym)
@@ -663,12 +737,15 @@ build_table_kernel(const unsigned long long *__restrict__ counts, const uint32_t
         if (tid == 0) cum[0] = 0;
         __syncthreads();
     }
-    if (tid == 0) {
+    if (tid == 0 && blockIdx.x == 0) {
         t->scale_bits = scale_bits;
         t->n_sym = n_sym;
         t->status = status_sh;
     }
-    fill_tables(t, freq, cum, slot_in, scale_bits, red);
+    if (gridDim.x > 1)  // model from counts: the slot tables split over the CTAs
+        fill_tables_split(t, freq, cum, scale_bits, red);
+    else
+        fill_tables(t, freq, cum, slot_in, scale_bits, red);
 }
 
 }  // namespace ilans
