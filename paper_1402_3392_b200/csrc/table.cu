@@ -536,10 +536,13 @@ build_table_kernel(const unsigned long long *__restrict__ counts, const uint32_t
     __shared__ int red[8];
     __shared__ int status_sh;
     const int tid = threadIdx.x;
+    // the table's header / status words: written by CTA 0 only (a build
+    // from counts runs several CTAs that reach the same result)
+    const bool lead = blockIdx.x == 0;
     if (tid == 0) status_sh = ILANS_OK;
-    if (tid < 4) t->err_detail[tid] = 0;
+    if (lead && tid < 4) t->err_detail[tid] = 0;
     if (scale_bits < 1 || scale_bits > kMaxScaleBits) {
-        if (tid == 0) { t->status = ILANS_ERR_VALUE; t->err_detail[0] = 1; t->scale_bits = scale_bits; }
+        if (lead && tid == 0) { t->status = ILANS_ERR_VALUE; t->err_detail[0] = 1; t->scale_bits = scale_bits; }
         return;
     }
     const uint32_t m = 1u << scale_bits;
@@ -591,7 +594,7 @@ build_table_kernel(const unsigned long long *__restrict__ counts, const uint32_t
             total = 2;
         }
         if (static_cast<uint32_t>(present) > m) {
-            if (tid == 0) {
+            if (lead && tid == 0) {
                 t->status = ILANS_ERR_VALUE;
                 t->err_detail[0] = 2;
                 t->err_detail[1] = present;
@@ -706,7 +709,7 @@ build_table_kernel(const unsigned long long *__restrict__ counts, const uint32_t
             const long long sum = block_sum_256<long long>(static_cast<long long>(freq[tid]),
                                                            reinterpret_cast<long long *>(red64));
             if (sum != static_cast<long long>(m)) {
-                if (tid == 0) {
+                if (lead && tid == 0) {
                     t->status = ILANS_ERR_VALUE;
                     t->err_detail[0] = 3;
                     t->n_sym = n_sym;
@@ -737,7 +740,7 @@ build_table_kernel(const unsigned long long *__restrict__ counts, const uint32_t
         if (tid == 0) cum[0] = 0;
         __syncthreads();
     }
-    if (tid == 0 && blockIdx.x == 0) {
+    if (lead && tid == 0) {
         t->scale_bits = scale_bits;
         t->n_sym = n_sym;
         t->status = status_sh;
