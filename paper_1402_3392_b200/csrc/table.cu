@@ -489,7 +489,8 @@ __device__ void fill_tables_split(TableDev *t, const uint32_t *freq, const uint3
         if (tid == 0)
             t->flags = (sb32 && fits32 ? kTabPacked : 0u) |
                        ((all & 2u) ? (scale_bits >= 14 ? kTabEncFast12 : kTabEncFast) : 0u) |
-                       (sb64 ? kTabPacked64 : 0u) | ((all & 8u) ? kTabEncQuad : 0u) |
+                       (sb64 && !fits32 ? kTabPacked64 : 0u) |  // written only then (below)
+                       ((all & 8u) ? kTabEncQuad : 0u) |
                        ((all & 16u) ? kTabEncQuadX : 0u);
     }
     const bool w64 = sb64 && !fits32;
